@@ -1,0 +1,339 @@
+"""Benchmark of the extended-FD preconditioner apply (+ GMRES time-to-1e-8) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = one ExtendedFDPreconditioner::apply (fdsolve.cpp:155-164) of the A^G preconditioner
+over one seeded uniform[-1,1] vector of the configuration (BASELINE.json configs[1] = c2 by
+default: d=2, p=3, n_el=256, 17,040,642 DoF).  Inputs are resident in HBM and larger than L2
+(136 MB > 126 MB), so no L2 flush is needed between steps.  Prints ONE JSON line (rank 0).
+
+--impl reference times the reference's CPU path for the same workload: the Eigen-free restatement
+in oracle/ (the reference itself needs Eigen and cannot be compiled here).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FD preconditioner applies/s & DoF/s (frac. FP64/HBM roofline); GMRES time-to-1e-8"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampler (NVML, during the timed region)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU path (oracle restatement of the reference) -- baseline and --impl reference
+# ------------------------------------------------------------------------------------------
+def cpu_fd_timing(cfg, steps, warmup, budget_s=None):
+    import numpy as np
+
+    from oracle.assembly import assemble_spatial_parametric, assemble_time_matrices
+    from oracle.fdsolve import ExtendedFDPreconditioner as OracleFD
+    from paper_1909_07309_b200.inputs import uniform_pm1
+
+    W, Mt = assemble_time_matrices(cfg.p, cfg.n_el, 1.0)
+    K, M = assemble_spatial_parametric(cfg.p, cfg.n_el, cfg.d)
+    t0 = time.perf_counter()
+    D = np.ones(cfg.n_dof)  # diag(A)/diag(A~) on the identity map (see problems.geometry_scaling)
+    P = OracleFD.setup(K, M, W, Mt, 1.0, 1.0, scaling=D)
+    setup_s = time.perf_counter() - t0
+    r = uniform_pm1(cfg.n_dof, cfg.seed)
+    for _ in range(warmup):
+        P.apply(r)
+    times = []
+    t_start = time.perf_counter()
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        P.apply(r)
+        times.append(time.perf_counter() - t0)
+        if budget_s is not None and time.perf_counter() - t_start > budget_s:
+            break
+    return times, setup_s
+
+
+def cores_used():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        n = max((i.get("num_threads", 1) for i in info if i.get("user_api") == "blas"), default=1)
+        return int(n)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    from paper_1909_07309_b200.configs import CONFIGS
+
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    warm = max(1, min(args.warmup, 3))
+    steps = max(1, min(args.steps, 20))
+    times, setup_s = cpu_fd_timing(cfg, steps, warm, budget_s=150.0)
+    total = sum(times)
+    v = len(times) / total
+    cores = cores_used()
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "applies/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": warm, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1])",
+        "dof_per_s": v * cfg.n_dof, "setup_s": setup_s,
+        "config": {"workload": f"{cfg.name}: {cfg.note}; A^G FD apply", "d": cfg.d, "p": cfg.p, "n_el": cfg.n_el,
+                   "n_dof": cfg.n_dof, "parallelism": "cpu"},
+        "cpu_baseline": {"value": v, "unit": "applies/s", "cores": cores, "kind": "port",
+                         "sample": f"{len(times)} full {cfg.name} applies of the numpy/OpenBLAS restatement "
+                                   f"(oracle/fdsolve.py, reference fdsolve.cpp:155-164)"},
+        "e2e": {"value": v, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# GPU path
+# ------------------------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1909_07309_b200 import stiga
+    from paper_1909_07309_b200.configs import CONFIGS
+    from paper_1909_07309_b200.inputs import uniform_pm1
+    from paper_1909_07309_b200.problems import geometry_scaling, identity_pieces
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    cfg = CONFIGS[args.config]
+    K_steps, W_steps = args.steps, max(args.warmup, 3)
+
+    pc = identity_pieces(cfg.d, cfg.p, cfg.n_el)
+    t0 = time.perf_counter()
+    D = geometry_scaling(pc)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D, device=dev)
+    setup_s = time.perf_counter() - t0
+    n = P.n_dof
+    launches = P.launches()
+
+    r_host = torch.from_numpy(uniform_pm1(n, cfg.seed + rank)).pin_memory()
+    s_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    r = r_host.cuda(dev)
+    s = torch.empty_like(r)
+    stream = torch.cuda.current_stream(dev)
+
+    peak_dmma, peak_dfma = stiga.fp64_peak(dev, 300.0)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    for _ in range(W_steps):
+        P.apply(r, out=s)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K device-resident applies --------------------------------------------
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(dev)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        ev0.record(stream)
+        for _ in range(K_steps):
+            P.apply(r, out=s)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / K_steps)
+    value = ws / (ms * 1e-3)
+
+    # ---- per-launch durations (separate profiled pass over K steps, events on the same stream) --
+    pass_ms = np.zeros(launches)
+    kp = min(K_steps, 50)
+    for _ in range(kp):
+        pass_ms += np.array(P.apply_profiled(r, s))
+    pass_ms /= kp
+    d, nt, ns = cfg.d, cfg.n_t, cfg.n_s
+    names = [f"fwd_mode{m}" for m in range(d)] + ["time_fused"] + [f"bwd_mode{m}" for m in range(d)]
+    flops = [2.0 * ns * n] * d + [4.0 * nt * n] + [2.0 * ns * n] * d
+    dom = int(np.argmax(pass_ms))
+    achieved = flops[dom] / (pass_ms[dom] * 1e-3) / 1e12
+    traffic = None
+    tf_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf_path):
+        try:
+            traffic = json.load(open(tf_path)).get(cfg.name, {}).get(names[dom])
+        except Exception:
+            traffic = None
+
+    # ---- e2e: host buffers through the public API, copies inside the timed region -----------------
+    for _ in range(2):
+        r.copy_(r_host, non_blocking=True)
+        P.apply(r, out=s)
+        s_host.copy_(s, non_blocking=True)
+    torch.cuda.synchronize()
+    ke = max(3, min(K_steps, 50))
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(ke):
+        r.copy_(r_host, non_blocking=True)
+        P.apply(r, out=s)
+        s_host.copy_(s, non_blocking=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / ke)
+
+    # ---- GMRES time-to-1e-8 (device resident, restart 50, x0 = 0) -----------------------------
+    gm = None
+    if not args.no_gmres:
+        A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=dev)
+        torch.cuda.synchronize()
+        x, rep = stiga.gmres(A, P, r, stiga.GmresOptions(tol=1e-8, max_krylov=500, restart=50))
+        torch.cuda.synchronize()
+        x, rep = stiga.gmres(A, P, r, stiga.GmresOptions(tol=1e-8, max_krylov=500, restart=50))
+        res = (torch.linalg.norm(A.apply(x) - r) / torch.linalg.norm(r)).item()
+        gm = {"time_s": rep.wall_time_s, "iterations": rep.iterations, "converged": rep.converged,
+              "final_rel_precond_residual": rep.residual_history[-1], "true_rel_residual": res,
+              "precond_time_fraction": rep.precond_time_fraction, "restart": 50, "tol": 1e-8}
+        del A
+
+    # ---- CPU baseline (rank 0, N = 1 only) ------------------------------------------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        times, _ = cpu_fd_timing(cfg, 100, 1, budget_s=args.cpu_budget_s)
+        cpu = {"value": len(times) / sum(times), "unit": "applies/s", "cores": cores_used(), "kind": "port",
+               "sample": f"{len(times)} full {cfg.name} applies (after 1 warm-up) of the numpy/OpenBLAS restatement "
+                         f"oracle/fdsolve.py of fdsolve.cpp:155-164"}
+
+    f_alg = cfg.flops_fd()
+    t_roof_flop = f_alg / (peak_dmma * 1e12)
+    t_roof_hbm = 32.0 * n / 6538.9e9
+    out = {
+        "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": ws, "steps": K_steps, "warmup": W_steps,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded uniform[-1,1], splitmix64)",
+        "config": {"workload": f"{cfg.name}: {cfg.note}; A^G FD apply (D^-1/2 scaled), identity geometry",
+                   "d": cfg.d, "p": cfg.p, "n_el": cfg.n_el, "n_dof": n, "dims": P.dims,
+                   "parallelism": "replicas" if ws > 1 else "single",
+                   "l2": "inputs (136 MB+) larger than L2 (126 MB); no flush"},
+        "dof_per_s": value * n,
+        "apply_roofline": {"F_alg_flop": f_alg, "t_roof_ms": 1e3 * max(t_roof_flop, t_roof_hbm),
+                           "frac": max(t_roof_flop, t_roof_hbm) / (ms * 1e-3), "peak_tflops": peak_dmma,
+                           "bound": "fp64 (DMMA)"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s",
+                     "frac": achieved / peak_dmma, "traffic": traffic, "kernel": names[dom],
+                     "flop_per_launch": flops[dom],
+                     "peak_source": "FP64 DMMA m8n8k4 probe measured live in this run (MEASURED_PEAKS.json has no FP64)",
+                     "peak_dfma_tflops": peak_dfma},
+        "pass_ms": {names[i]: float(pass_ms[i]) for i in range(launches)},
+        "e2e": {"value": ws / (e2e_ms * 1e-3), "unit": "applies/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms},
+        "gpu_launches": K_steps * launches,
+        "setup_s": setup_s,
+        "gmres": gm,
+        "cpu_baseline": cpu,
+        "clocks": sampler.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,150 @@
+/*
+ * stiga_gpu.h -- C ABI of the B200-native extended-FD preconditioner / GMRES hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ operator/solver API
+ * (/root/reference/proj/core/include/stiga/ headers).  Every entry point names the reference
+ * interface it replaces.  Plain pointers and sizes only; no C++ or torch types.
+ *
+ * Conventions (mirroring the reference):
+ *   - FP64 everywhere; vectors are colexicographic (i_1 fastest, time slowest), kronop.hpp:10-13.
+ *   - Dense matrices are column-major n x n (the reference's BandedMatrix stores dense, assembly.hpp:18-36).
+ *   - Every call returns a status: STIGA_OK, STIGA_INVALID_ARGUMENT (std::invalid_argument in the
+ *     reference), STIGA_NUMERICAL (std::runtime_error), STIGA_CUDA (device failure).
+ *     stiga_last_error() returns the message of the last failure on the calling thread.
+ *   - Handles are immutable after setup; apply is reentrant per (handle, stream) pair when the
+ *     caller passes distinct output buffers (scratch is per handle: concurrent applies on one
+ *     handle from several streams are not allowed).
+ *   - "device" pointers are CUDA global-memory pointers on the handle's device; "host" pointers
+ *     are ordinary host memory (pinned or pageable).
+ */
+#ifndef STIGA_GPU_H
+#define STIGA_GPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STIGA_OK 0
+#define STIGA_INVALID_ARGUMENT 1
+#define STIGA_NUMERICAL 2
+#define STIGA_CUDA 3
+
+typedef struct stiga_fd_s* stiga_fd_t;
+typedef struct stiga_kronsum_s* stiga_kronsum_t;
+
+/* ---- diagnostics ------------------------------------------------------------------- */
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* stiga_last_error(void);
+/* ABI version (major*100 + minor). */
+int stiga_abi_version(void);
+/* Number of CUDA devices visible (0 on a machine without GPU); never fails. */
+int stiga_device_count(void);
+
+/* ---- host-side 1D assembly (stays on the host, as in the reference) ------------------ */
+
+/* Active dimension of SplineSpace1D::spatial (kind 0) / ::temporal (kind 1), bspline.cpp:139-145. */
+int stiga_space_dim(int p, int n_el, int kind, int* n_out);
+/* assemble_time_matrices(p_t, n_el_t, T) -> W_t, M_t (assembly.cpp:129-138); Wt, Mt are n_t*n_t. */
+int stiga_assemble_time_matrices(int p_t, int n_el_t, double T, double* Wt, double* Mt);
+/* assemble_spatial_parametric for one direction with q Gauss points per element
+   (assembly.cpp:140-149): K, M are n_s*n_s. */
+int stiga_assemble_spatial_parametric(int p, int n_el, int q, double* K, double* M);
+/* assemble_univariate with per-element weights (assembly.cpp:47-79, overload 118-127);
+   kind 0 = spatial space, 1 = temporal space; weights may be NULL (all ones). out: n*n. */
+int stiga_assemble_univariate(int p, int n_el, int kind, int q, int deriv_row, int deriv_col,
+                              const double* element_weights, double* out);
+
+/* ---- ExtendedFDPreconditioner (fdsolve.hpp:41-70) ------------------------------------- */
+
+/* ExtendedFDPreconditioner::setup(space_K, space_M, Wt, Mt, gamma, nu, scaling) (fdsolve.hpp:48-52,
+   fdsolve.cpp:67-153).  d directions; K[l], M[l] point to n[l]*n[l] column-major matrices;
+   Wt, Mt are n_t*n_t.  scaling (the optional D, length scaling_len == N_dof) may be NULL.
+   The eigen/pencil factorizations run on the host; factors are uploaded to `device` once. */
+int stiga_fd_setup(int d, const int* n, const double* const* K, const double* const* M, int n_t,
+                   const double* Wt, const double* Mt, double gamma, double nu, const double* scaling,
+                   long long scaling_len, int device, stiga_fd_t* out);
+/* device < 0 creates a host-only handle (setup + stiga_fd_export, no device apply). */
+int stiga_fd_destroy(stiga_fd_t P);
+/* ExtendedFDPreconditioner::size() and the tensor dims (d spatial sizes then n_t). */
+int stiga_fd_size(stiga_fd_t P, long long* n_dof);
+int stiga_fd_dims(stiga_fd_t P, int* d, int* dims);
+/* Time-factorization summary: #pairs, zero_count, sigma, rho (pencil.hpp:40-52). */
+int stiga_fd_time_info(stiga_fd_t P, int* npairs, int* zero_count, double* sigma, double* rho);
+/* Copies host-side factors for inspection: which = 0: U_l (n_l*n_l, col-major) for direction l;
+   1: Lambda_l (n_l); 2: U_t (n_t*n_t); 3: lambda_t (npairs); 4: g (n_t-1); 5: S_inv (N_s). */
+int stiga_fd_export(stiga_fd_t P, int which, int l, double* out, long long out_len);
+
+/* ExtendedFDPreconditioner::apply(r) (fdsolve.hpp:56, fdsolve.cpp:155-164) on device buffers,
+   asynchronously on `stream` (a cudaStream_t, NULL = legacy default stream).  d_s may equal d_r. */
+int stiga_fd_apply(stiga_fd_t P, const double* d_r, double* d_s, void* stream);
+/* Host-buffer convenience: H2D copy, apply, D2H copy, synchronize. */
+int stiga_fd_apply_host(stiga_fd_t P, const double* h_r, double* h_s);
+/* Same as stiga_fd_apply but records CUDA events around each of the 2d+1 kernel launches and
+   writes their durations (ms) into pass_ms[0..2d] (synchronizes the stream). */
+int stiga_fd_apply_profiled(stiga_fd_t P, const double* d_r, double* d_s, void* stream, float* pass_ms);
+/* Number of kernel launches one apply issues (2d+1). */
+int stiga_fd_launches(stiga_fd_t P, int* launches);
+
+/* ---- Kronecker operators (kronop.hpp:47-79) ------------------------------------------- */
+
+/* kron_matvec(factors, x) (kronop.cpp:75-89) on device buffers: D factors, factor l is
+   rows[l] x cols[l] column-major (host pointer); x has prod(cols) entries, y prod(rows). */
+int stiga_kron_matvec(int D, const int* rows, const int* cols, const double* const* factors,
+                      const double* d_x, double* d_y, int device, void* stream);
+
+/* KronSumOperator(dims, terms) (kronop.hpp:61-79): D dims, nterms terms; term t has coefficient
+   coeffs[t] and D square factors factors[t*D + l] (dims[l]^2, column-major, host pointers).
+   Banded factors are detected and applied with banded kernels. */
+int stiga_kronsum_create(int D, const int* dims, int nterms, const double* coeffs,
+                         const double* const* factors, int device, stiga_kronsum_t* out);
+/* KronSumOperator(dims, kron_sum_terms(K, M, Wt, Mt, gamma, nu)) (solver.cpp:10-30, 67-70): the
+   (d+1)-term space-time operator  gamma (M_1..M_d, W_t) + nu sum_l (M_1..K_l..M_d, M_t)  with
+   banded 1D factors, applied sum-factorized in d+1 banded passes (equal to the per-term sum in
+   exact arithmetic).  K[l], M[l]: n[l]*n[l]; Wt, Mt: n_t*n_t (column-major, host pointers). */
+int stiga_kronsum_create_spacetime(int d, const int* n, const double* const* K, const double* const* M,
+                                   int n_t, const double* Wt, const double* Mt, double gamma, double nu,
+                                   int device, stiga_kronsum_t* out);
+int stiga_kronsum_destroy(stiga_kronsum_t A);
+int stiga_kronsum_size(stiga_kronsum_t A, long long* n_dof);
+/* KronSumOperator::apply(x) (kronop.cpp:108-115): y = sum_t coeff_t (x)_l F_{t,l} x. d_y != d_x. */
+int stiga_kronsum_apply(stiga_kronsum_t A, const double* d_x, double* d_y, void* stream);
+/* KronSumOperator::diagonal() (kronop.cpp:117-131) into a host buffer of N_dof. */
+int stiga_kronsum_diagonal(stiga_kronsum_t A, double* h_diag);
+
+/* ---- GMRES (gmres.hpp:12-35) ---------------------------------------------------------- */
+
+/* Mirrors GmresOptions (gmres.hpp:23-27); restart <= 0 means "no restart" (std::nullopt). */
+typedef struct {
+    double tol;
+    int max_krylov;
+    int restart;
+} stiga_gmres_options;
+
+/* Mirrors SolveReport (gmres.hpp:15-21); residual_history is caller-provided storage of
+   history_capacity doubles, history_len receives the number of entries produced. */
+typedef struct {
+    int iterations;
+    int converged;
+    double wall_time_s;
+    double precond_time_fraction;
+    double* residual_history;
+    int history_capacity;
+    int history_len;
+} stiga_gmres_report;
+
+/* gmres(A, P, b, opts) (gmres.cpp:19-132): left-preconditioned GMRES from x0 = 0 with A a
+   KronSumOperator handle and P an FD handle (P may be NULL).  d_b, d_x are device buffers. */
+int stiga_gmres(stiga_kronsum_t A, stiga_fd_t P, const double* d_b, double* d_x,
+                const stiga_gmres_options* opts, stiga_gmres_report* report, void* stream);
+
+/* ---- measurement helpers ---------------------------------------------------------------- */
+
+/* Sustained FP64 DMMA (m8n8k4) throughput of the device in TFLOP/s over ~`ms` milliseconds. */
+int stiga_fp64_peak(int device, double ms, double* tflops_dmma, double* tflops_dfma);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STIGA_GPU_H */

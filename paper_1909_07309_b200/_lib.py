@@ -1,0 +1,93 @@
+"""ctypes binding of libstiga_gpu.so (the C ABI declared in include/stiga_gpu.h).
+
+There is deliberately no fallback: if the shared library is missing the import fails loudly
+(run `python -c "import __graft_entry__ as g; g.build()"` or `make -C paper_1909_07309_b200/csrc`).
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libstiga_gpu.so")
+
+OK, INVALID_ARGUMENT, NUMERICAL, CUDA = 0, 1, 2, 3
+
+_c_int, _c_ll, _c_dbl, _vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_double, ctypes.c_void_p
+_pd = ctypes.POINTER(ctypes.c_double)
+_pi = ctypes.POINTER(ctypes.c_int)
+_ppd = ctypes.POINTER(_pd)
+
+
+class GmresOptions(ctypes.Structure):
+    _fields_ = [("tol", ctypes.c_double), ("max_krylov", ctypes.c_int), ("restart", ctypes.c_int)]
+
+
+class GmresReport(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int), ("wall_time_s", ctypes.c_double),
+                ("precond_time_fraction", ctypes.c_double), ("residual_history", _pd),
+                ("history_capacity", ctypes.c_int), ("history_len", ctypes.c_int)]
+
+
+# name -> (restype, argtypes); every symbol of include/stiga_gpu.h
+SIGNATURES = {
+    "stiga_last_error": (ctypes.c_char_p, []),
+    "stiga_abi_version": (_c_int, []),
+    "stiga_device_count": (_c_int, []),
+    "stiga_space_dim": (_c_int, [_c_int, _c_int, _c_int, _pi]),
+    "stiga_assemble_time_matrices": (_c_int, [_c_int, _c_int, _c_dbl, _pd, _pd]),
+    "stiga_assemble_spatial_parametric": (_c_int, [_c_int, _c_int, _c_int, _pd, _pd]),
+    "stiga_assemble_univariate": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _pd, _pd]),
+    "stiga_fd_setup": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl, _pd, _c_ll, _c_int,
+                                ctypes.POINTER(_vp)]),
+    "stiga_fd_destroy": (_c_int, [_vp]),
+    "stiga_fd_size": (_c_int, [_vp, ctypes.POINTER(_c_ll)]),
+    "stiga_fd_dims": (_c_int, [_vp, _pi, _pi]),
+    "stiga_fd_time_info": (_c_int, [_vp, _pi, _pi, _pd, _pd]),
+    "stiga_fd_export": (_c_int, [_vp, _c_int, _c_int, _pd, _c_ll]),
+    "stiga_fd_apply": (_c_int, [_vp, _vp, _vp, _vp]),
+    "stiga_fd_apply_host": (_c_int, [_vp, _pd, _pd]),
+    "stiga_fd_apply_profiled": (_c_int, [_vp, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_float)]),
+    "stiga_fd_launches": (_c_int, [_vp, _pi]),
+    "stiga_kron_matvec": (_c_int, [_c_int, _pi, _pi, _ppd, _vp, _vp, _c_int, _vp]),
+    "stiga_kronsum_create": (_c_int, [_c_int, _pi, _c_int, _pd, _ppd, _c_int, ctypes.POINTER(_vp)]),
+    "stiga_kronsum_create_spacetime": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl, _c_int,
+                                                ctypes.POINTER(_vp)]),
+    "stiga_kronsum_destroy": (_c_int, [_vp]),
+    "stiga_kronsum_size": (_c_int, [_vp, ctypes.POINTER(_c_ll)]),
+    "stiga_kronsum_apply": (_c_int, [_vp, _vp, _vp, _vp]),
+    "stiga_kronsum_diagonal": (_c_int, [_vp, _pd]),
+    "stiga_gmres": (_c_int, [_vp, _vp, _vp, _vp, ctypes.POINTER(GmresOptions), ctypes.POINTER(GmresReport), _vp]),
+    "stiga_fp64_peak": (_c_int, [_c_int, _c_dbl, _pd, _pd]),
+}
+
+_lib = None
+
+
+def lib():
+    """Loads (once) and returns the CDLL; raises ImportError if the library was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libstiga_gpu.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+class StigaError(RuntimeError):
+    pass
+
+
+def check(status, what=""):
+    """Maps C-ABI status codes to the reference's exception types (SURVEY §8(b) Errors)."""
+    if status == OK:
+        return
+    msg = lib().stiga_last_error().decode()
+    if status == INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == NUMERICAL:
+        raise RuntimeError(msg)
+    raise StigaError(f"CUDA failure in {what}: {msg}")

@@ -1,0 +1,707 @@
+// C ABI of the B200 extended-FD preconditioner / GMRES path (include/stiga_gpu.h).
+//
+// Host orchestration only: the host-side setup (1D assembly, pencils, Schur diagonal) runs here
+// exactly where the reference runs it (fdsolve.cpp:67-153, pencil.cpp, assembly.cpp), the factors
+// are uploaded once, and every apply is a fixed chain of device kernels on the caller's stream.
+// There is no CPU compute fallback: without a device every compute entry point fails with
+// STIGA_CUDA.
+#include "stiga_gpu.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cuda/aux_kernels.cuh"
+#include "cuda/fd_kernels.cuh"
+#include "host/assembly.hpp"
+#include "host/fdsetup.hpp"
+
+using namespace stiga;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return STIGA_OK;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return STIGA_INVALID_ARGUMENT;
+    } catch (const CudaFailure& e) {
+        g_last_error = e.what();
+        return STIGA_CUDA;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return STIGA_NUMERICAL;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return STIGA_NUMERICAL;
+    }
+}
+
+void require(bool ok, const char* msg) {
+    if (!ok) throw std::invalid_argument(msg);
+}
+
+// Scoped device selection (restores the caller's current device).
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        ck(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+struct DBuf {
+    double* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void alloc(size_t count) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = count;
+        if (count) ck(cudaMalloc(&p, count * sizeof(double)), "cudaMalloc");
+    }
+    void upload(const std::vector<double>& h) {
+        alloc(h.size());
+        if (!h.empty()) ck(cudaMemcpy(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice), "upload");
+    }
+};
+
+DenseMatrix from_colmajor(const double* a, int n) {
+    DenseMatrix m(n, n);
+    std::memcpy(m.a.data(), a, sizeof(double) * n * static_cast<size_t>(n));
+    return m;
+}
+
+// Row-major, zero-padded (Mp x Kp) copy of J, with J(i,j) = transpose ? U(j,i) : U(i,j).
+std::vector<double> pad_factor(const DenseMatrix& U, bool transpose, const gpu::Tiling& t) {
+    std::vector<double> out(static_cast<size_t>(t.Mp) * t.Kp, 0.0);
+    const Index rows = transpose ? U.cols : U.rows;
+    const Index cols = transpose ? U.rows : U.cols;
+    for (Index i = 0; i < rows; ++i)
+        for (Index j = 0; j < cols; ++j) out[i * t.Kp + j] = transpose ? U(j, i) : U(i, j);
+    return out;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+namespace stiga {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace stiga
+
+// ------------------------------------------------------------------------------------------
+// FD preconditioner handle
+// ------------------------------------------------------------------------------------------
+struct stiga_fd_s {
+    int device = 0;
+    FDFactors F;
+    int d = 0;
+    std::vector<int> dims;  // n_1..n_d, n_t
+    long long n_dof = 0, n_s = 0;
+    std::vector<gpu::Tiling> tl;        // per spatial direction
+    gpu::Tiling tl_t;
+    std::vector<std::unique_ptr<DBuf>> Jt, J;  // padded U_l^T, U_l
+    DBuf Jt_t, J_t;
+    std::vector<std::unique_ptr<DBuf>> lam;
+    DBuf S_inv, pair_c, pair_c1, g, dinv;
+    DBuf scratch, scratch2;
+    gpu::ArrowParams ap;
+
+    gpu::ModeGeom geom(int mode) const {
+        gpu::ModeGeom g;
+        long long L = 1;
+        for (int l = 0; l < mode; ++l) L *= dims[l];
+        g.L = L;
+        g.n = g.m = dims[mode];
+        g.ncols = n_dof / dims[mode];
+        return g;
+    }
+
+    // 2d+1 launches: forward spatial modes (D^-1/2 fused into the first), time-fused, backward
+    // spatial modes (D^-1/2 fused into the last).  The reference order (fdsolve.cpp:158-163) applies
+    // U_1..U_d, U_t in the back transform; Kronecker factors on distinct modes commute, so applying
+    // U_t first (fused) is equal in exact arithmetic.
+    void apply(const double* in, double* out, cudaStream_t st, std::vector<cudaEvent_t>* ev) {
+        if (in == out && !scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
+        double* buf0 = (in == out) ? scratch2.p : out;
+        double* bufs[2] = {buf0, scratch.p};
+        const int passes = 2 * d + 1;
+        const double* src = in;
+        for (int k = 0; k < passes; ++k) {
+            double* dst = (k == passes - 1) ? out : bufs[k % 2];
+            if (ev) ck(cudaEventRecord((*ev)[k], st), "event");
+            if (k < d) {
+                ck(gpu::launch_mode_product(tl[k], geom(k), src, dst, Jt[k]->p, k == 0 ? dinv.p : nullptr, nullptr, st),
+                   "fd forward mode product");
+            } else if (k == d) {
+                gpu::ModeGeom g = geom(d);
+                ck(gpu::launch_time_fused(tl_t, g, src, dst, Jt_t.p, J_t.p, ap, st), "fd time-fused kernel");
+            } else {
+                const int m = k - d - 1;
+                ck(gpu::launch_mode_product(tl[m], geom(m), src, dst, J[m]->p, nullptr,
+                                            m == d - 1 ? dinv.p : nullptr, st),
+                   "fd backward mode product");
+            }
+            src = dst;
+        }
+        if (ev) ck(cudaEventRecord((*ev)[passes], st), "event");
+    }
+};
+
+// ------------------------------------------------------------------------------------------
+// KronSum handle
+// ------------------------------------------------------------------------------------------
+struct stiga_kronsum_s {
+    int device = 0;
+    int D = 0;
+    std::vector<int> dims;
+    long long n_dof = 0;
+    bool spacetime = false;
+    // generic: terms x D bands
+    std::vector<double> coeffs;
+    std::vector<std::vector<DenseMatrix>> factors;  // host copies (for diagonal)
+    std::vector<std::unique_ptr<DBuf>> bands;       // term*D + l
+    std::vector<int> hbw;
+    // spacetime: per direction M_l, K_l bands, time gamma*W_t and nu*M_t bands
+    DBuf t0, t1, t2, t3;  // scratch N_dof each
+
+    gpu::ModeGeom geom(int mode) const {
+        gpu::ModeGeom g;
+        long long L = 1;
+        for (int l = 0; l < mode; ++l) L *= dims[l];
+        g.L = L;
+        g.n = g.m = dims[mode];
+        g.ncols = n_dof / dims[mode];
+        return g;
+    }
+    gpu::Band band(int idx) const { return gpu::Band{bands[idx]->p, hbw[idx]}; }
+
+    void ensure_scratch(int count) {
+        DBuf* s[4] = {&t0, &t1, &t2, &t3};
+        for (int i = 0; i < count; ++i)
+            if (!s[i]->p) s[i]->alloc(static_cast<size_t>(n_dof));
+    }
+
+    void apply(const double* x, double* y, cudaStream_t st) {
+        const gpu::Band none{};
+        if (spacetime) {
+            // bands: [M_1, K_1, ..., M_d, K_d, gamma W_t, nu M_t]
+            const int d = D - 1;
+            ensure_scratch(4);
+            double* a = t0.p;  // t_m  (M-chain)
+            double* b = t1.p;  // k_m  (stiffness-sum chain)
+            double* a2 = t2.p;
+            double* b2 = t3.p;
+            // mode 0: a = M_1 x, b = K_1 x
+            ck(gpu::launch_banded_pass(geom(0), x, nullptr, a, b, band(0), none, band(1), none, 0.0, st), "banded");
+            for (int m = 1; m < d; ++m) {
+                // a2 = M_m a ; b2 = K_m a + M_m b
+                ck(gpu::launch_banded_pass(geom(m), a, b, a2, b2, band(2 * m), none, band(2 * m + 1), band(2 * m), 0.0,
+                                           st),
+                   "banded");
+                std::swap(a, a2);
+                std::swap(b, b2);
+            }
+            // time: y = gamma W_t a + nu M_t b
+            ck(gpu::launch_banded_pass(geom(d), a, b, y, nullptr, band(2 * d), band(2 * d + 1), none, none, 0.0, st),
+               "banded");
+            return;
+        }
+        // generic: per term D banded passes, the last accumulating into y
+        ensure_scratch(2);
+        const int nterms = static_cast<int>(coeffs.size());
+        if (nterms == 0) {
+            ck(cudaMemsetAsync(y, 0, sizeof(double) * n_dof, st), "memset");
+            return;
+        }
+        for (int t = 0; t < nterms; ++t) {
+            const double* src = x;
+            double* ping[2] = {t0.p, t1.p};
+            for (int l = 0; l < D; ++l) {
+                const bool last = l == D - 1;
+                double* dst = last ? y : ping[l % 2];
+                gpu::Band Bd = band(t * D + l);
+                ck(gpu::launch_banded_pass(geom(l), src, nullptr, dst, nullptr, Bd, none, none, none,
+                                           last && t > 0 ? 1.0 : 0.0, st),
+                   "banded");
+                src = dst;
+            }
+        }
+    }
+};
+
+namespace {
+
+int half_bandwidth(const DenseMatrix& F) {
+    int p = 0;
+    for (Index j = 0; j < F.cols; ++j)
+        for (Index i = 0; i < F.rows; ++i)
+            if (F(i, j) != 0.0) p = std::max(p, static_cast<int>(std::llabs(i - j)));
+    return p;
+}
+
+// Band storage of coeff * F; the coefficient is folded into the band (coeff_t * kron(...)).
+std::vector<double> to_band(const DenseMatrix& F, int p, double coeff) {
+    const int n = static_cast<int>(F.rows), w = 2 * p + 1;
+    std::vector<double> b(static_cast<size_t>(n) * w, 0.0);
+    for (int i = 0; i < n; ++i)
+        for (int j = std::max(0, i - p); j <= std::min(n - 1, i + p); ++j) b[i * w + (j - i + p)] = coeff * F(i, j);
+    return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* stiga_last_error(void) { return g_last_error.c_str(); }
+
+int stiga_abi_version(void) { return 100; }
+
+int stiga_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int stiga_space_dim(int p, int n_el, int kind, int* n_out) {
+    return guarded([&] {
+        require(n_out != nullptr, "stiga_space_dim: null output");
+        require(kind == 0 || kind == 1, "stiga_space_dim: kind must be 0 (spatial) or 1 (temporal)");
+        const SplineSpace1D s = kind == 0 ? SplineSpace1D::spatial(p, n_el) : SplineSpace1D::temporal(p, n_el);
+        *n_out = s.dim();
+    });
+}
+
+int stiga_assemble_time_matrices(int p_t, int n_el_t, double T, double* Wt, double* Mt) {
+    return guarded([&] {
+        require(Wt && Mt, "stiga_assemble_time_matrices: null output");
+        auto [W, M] = assemble_time_matrices(p_t, n_el_t, T);
+        std::memcpy(Wt, W.m.a.data(), W.m.a.size() * sizeof(double));
+        std::memcpy(Mt, M.m.a.data(), M.m.a.size() * sizeof(double));
+    });
+}
+
+int stiga_assemble_spatial_parametric(int p, int n_el, int q, double* K, double* M) {
+    return guarded([&] {
+        require(K && M, "stiga_assemble_spatial_parametric: null output");
+        BandedMatrix Kb, Mb;
+        assemble_spatial_parametric(p, n_el, q, Kb, Mb);
+        std::memcpy(K, Kb.m.a.data(), Kb.m.a.size() * sizeof(double));
+        std::memcpy(M, Mb.m.a.data(), Mb.m.a.size() * sizeof(double));
+    });
+}
+
+int stiga_assemble_univariate(int p, int n_el, int kind, int q, int deriv_row, int deriv_col,
+                              const double* element_weights, double* out) {
+    return guarded([&] {
+        require(out != nullptr, "stiga_assemble_univariate: null output");
+        require(kind == 0 || kind == 1, "stiga_assemble_univariate: kind must be 0 or 1");
+        const SplineSpace1D s = kind == 0 ? SplineSpace1D::spatial(p, n_el) : SplineSpace1D::temporal(p, n_el);
+        const QuadratureRule quad = gauss_rule(s.knot_vector(), q);
+        std::vector<double> w;
+        if (element_weights) w.assign(element_weights, element_weights + quad.num_elements);
+        const BandedMatrix A = assemble_univariate(s, quad, deriv_row, deriv_col, element_weights ? &w : nullptr);
+        std::memcpy(out, A.m.a.data(), A.m.a.size() * sizeof(double));
+    });
+}
+
+int stiga_fd_setup(int d, const int* n, const double* const* K, const double* const* M, int n_t, const double* Wt,
+                   const double* Mt, double gamma, double nu, const double* scaling, long long scaling_len, int device,
+                   stiga_fd_t* out) {
+    return guarded([&] {
+        require(out != nullptr, "stiga_fd_setup: null handle output");
+        *out = nullptr;
+        require(d >= 1 && d <= gpu::kMaxDim, "ExtendedFDPreconditioner: per-direction matrices mismatch");
+        require(n && K && M && Wt && Mt, "stiga_fd_setup: null input");
+        require(n_t >= 1, "time_factorization: shape mismatch");
+        std::vector<DenseMatrix> Ks, Ms;
+        long long n_s = 1;
+        for (int l = 0; l < d; ++l) {
+            require(n[l] >= 1 && K[l] && M[l], "spd_generalized_eig: shape mismatch");
+            Ks.push_back(from_colmajor(K[l], n[l]));
+            Ms.push_back(from_colmajor(M[l], n[l]));
+            n_s *= n[l];
+        }
+        if (scaling)
+            require(scaling_len == n_s * n_t, "ExtendedFDPreconditioner: scaling vector length mismatch");
+        auto h = std::make_unique<stiga_fd_s>();
+        h->F = fd_setup(Ks, Ms, from_colmajor(Wt, n_t), from_colmajor(Mt, n_t), gamma, nu, scaling);
+        const FDFactors& F = h->F;
+        h->device = device;
+        h->d = d;
+        h->dims.assign(F.n.begin(), F.n.end());
+        h->dims.push_back(F.n_t);
+        h->n_dof = F.n_dof;
+        h->n_s = F.n_s_total;
+        if (device < 0) {  // host-only handle: setup + export, no device resources
+            *out = h.release();
+            return;
+        }
+
+        DeviceGuard dg(device);
+        for (int l = 0; l < d; ++l) {
+            h->tl.push_back(gpu::choose_tiling(F.n[l], F.n[l]));
+            h->Jt.emplace_back(new DBuf);
+            h->J.emplace_back(new DBuf);
+            h->Jt.back()->upload(pad_factor(F.U[l], true, h->tl.back()));
+            h->J.back()->upload(pad_factor(F.U[l], false, h->tl.back()));
+            h->lam.emplace_back(new DBuf);
+            h->lam.back()->upload(F.lambda[l]);
+        }
+        h->tl_t = gpu::choose_tiling(F.n_t, F.n_t);
+        h->Jt_t.upload(pad_factor(F.time.U, true, h->tl_t));
+        h->J_t.upload(pad_factor(F.time.U, false, h->tl_t));
+        h->S_inv.upload(F.S_inv);
+        std::vector<double> pc, pc1;
+        for (double lam : F.time.lambda) {
+            pc.push_back(gamma * gamma / nu * lam * lam);  // fdsolve.cpp:118
+            pc1.push_back(gamma / nu * lam);               // fdsolve.cpp:16
+        }
+        if (pc.empty()) {
+            pc.push_back(0.0);
+            pc1.push_back(0.0);
+        }
+        h->pair_c.upload(pc);
+        h->pair_c1.upload(pc1);
+        std::vector<double> gg(F.time.g.begin(), F.time.g.end());
+        if (gg.empty()) gg.push_back(0.0);
+        h->g.upload(gg);
+        if (!F.d_inv_sqrt.empty()) h->dinv.upload(F.d_inv_sqrt);
+        h->scratch.alloc(static_cast<size_t>(h->n_dof));
+
+        gpu::ArrowParams& ap = h->ap;
+        ap.d = d;
+        for (int l = 0; l < d; ++l) {
+            ap.n[l] = F.n[l];
+            ap.lam[l] = h->lam[l]->p;
+        }
+        ap.S_inv = h->S_inv.p;
+        ap.pair_c = h->pair_c.p;
+        ap.pair_c1 = h->pair_c1.p;
+        ap.g = h->g.p;
+        ap.npairs = static_cast<int>(F.time.lambda.size());
+        ap.zero_count = F.time.zero_count;
+        ap.n_t = F.n_t;
+        ap.gamma = gamma;
+        ap.nu = nu;
+        *out = h.release();
+    });
+}
+
+int stiga_fd_destroy(stiga_fd_t P) {
+    return guarded([&] {
+        if (!P) return;
+        if (P->device < 0) {
+            delete P;
+            return;
+        }
+        DeviceGuard dg(P->device);
+        delete P;
+    });
+}
+
+int stiga_fd_size(stiga_fd_t P, long long* n_dof) {
+    return guarded([&] {
+        require(P && n_dof, "stiga_fd_size: null argument");
+        *n_dof = P->n_dof;
+    });
+}
+
+int stiga_fd_dims(stiga_fd_t P, int* d, int* dims) {
+    return guarded([&] {
+        require(P && d, "stiga_fd_dims: null argument");
+        *d = P->d;
+        if (dims)
+            for (int l = 0; l <= P->d; ++l) dims[l] = P->dims[l];
+    });
+}
+
+int stiga_fd_time_info(stiga_fd_t P, int* npairs, int* zero_count, double* sigma, double* rho) {
+    return guarded([&] {
+        require(P != nullptr, "stiga_fd_time_info: null handle");
+        if (npairs) *npairs = static_cast<int>(P->F.time.lambda.size());
+        if (zero_count) *zero_count = P->F.time.zero_count;
+        if (sigma) *sigma = P->F.time.sigma;
+        if (rho) *rho = P->F.time.rho;
+    });
+}
+
+int stiga_fd_export(stiga_fd_t P, int which, int l, double* out, long long out_len) {
+    return guarded([&] {
+        require(P && out, "stiga_fd_export: null argument");
+        const FDFactors& F = P->F;
+        const std::vector<double>* src = nullptr;
+        std::vector<double> tmp;
+        switch (which) {
+            case 0: require(l >= 0 && l < F.d, "stiga_fd_export: direction out of range"); src = &F.U[l].a; break;
+            case 1: require(l >= 0 && l < F.d, "stiga_fd_export: direction out of range"); src = &F.lambda[l]; break;
+            case 2: src = &F.time.U.a; break;
+            case 3: tmp = F.time.lambda; src = &tmp; break;
+            case 4: src = &F.time.g; break;
+            case 5: src = &F.S_inv; break;
+            default: throw std::invalid_argument("stiga_fd_export: unknown factor id");
+        }
+        require(out_len >= static_cast<long long>(src->size()), "stiga_fd_export: output too small");
+        std::copy(src->begin(), src->end(), out);
+    });
+}
+
+int stiga_fd_apply(stiga_fd_t P, const double* d_r, double* d_s, void* stream) {
+    return guarded([&] {
+        require(P && d_r && d_s, "ExtendedFDPreconditioner::apply: null argument");
+        require(P->device >= 0, "ExtendedFDPreconditioner::apply: host-only handle (setup with device < 0)");
+        DeviceGuard dg(P->device);
+        P->apply(d_r, d_s, as_stream(stream), nullptr);
+    });
+}
+
+int stiga_fd_apply_profiled(stiga_fd_t P, const double* d_r, double* d_s, void* stream, float* pass_ms) {
+    return guarded([&] {
+        require(P && d_r && d_s && pass_ms, "stiga_fd_apply_profiled: null argument");
+        require(P->device >= 0, "ExtendedFDPreconditioner::apply: host-only handle (setup with device < 0)");
+        DeviceGuard dg(P->device);
+        const int passes = 2 * P->d + 1;
+        std::vector<cudaEvent_t> ev(passes + 1);
+        for (auto& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+        P->apply(d_r, d_s, as_stream(stream), &ev);
+        ck(cudaEventSynchronize(ev[passes]), "cudaEventSynchronize");
+        for (int k = 0; k < passes; ++k) ck(cudaEventElapsedTime(&pass_ms[k], ev[k], ev[k + 1]), "elapsed");
+        for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+int stiga_fd_launches(stiga_fd_t P, int* launches) {
+    return guarded([&] {
+        require(P && launches, "stiga_fd_launches: null argument");
+        *launches = 2 * P->d + 1;
+    });
+}
+
+int stiga_fd_apply_host(stiga_fd_t P, const double* h_r, double* h_s) {
+    return guarded([&] {
+        require(P && h_r && h_s, "ExtendedFDPreconditioner::apply: null argument");
+        require(P->device >= 0, "ExtendedFDPreconditioner::apply: host-only handle (setup with device < 0)");
+        DeviceGuard dg(P->device);
+        DBuf in, out;
+        in.alloc(static_cast<size_t>(P->n_dof));
+        out.alloc(static_cast<size_t>(P->n_dof));
+        ck(cudaMemcpy(in.p, h_r, sizeof(double) * P->n_dof, cudaMemcpyHostToDevice), "H2D");
+        P->apply(in.p, out.p, nullptr, nullptr);
+        ck(cudaMemcpy(h_s, out.p, sizeof(double) * P->n_dof, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+int stiga_kron_matvec(int D, const int* rows, const int* cols, const double* const* factors, const double* d_x,
+                      double* d_y, int device, void* stream) {
+    return guarded([&] {
+        require(D >= 1 && rows && cols && factors && d_x && d_y, "kron_matvec: invalid argument");
+        DeviceGuard dg(device);
+        cudaStream_t st = as_stream(stream);
+        std::vector<int> dims(cols, cols + D);
+        long long n = 1;
+        for (int l = 0; l < D; ++l) {
+            require(rows[l] >= 1 && cols[l] >= 1, "kron_matvec: vector length does not match factor dimensions");
+            n *= cols[l];
+        }
+        // intermediate buffers (the reference allocates a Tensor per mode product, kronop.cpp:56-59)
+        DBuf tmp[2];
+        const double* src = d_x;
+        for (int l = 0; l < D; ++l) {
+            const bool last = l == D - 1;
+            long long L = 1;
+            for (int k = 0; k < l; ++k) L *= dims[k];
+            gpu::ModeGeom g;
+            g.L = L;
+            g.n = dims[l];
+            g.m = rows[l];
+            g.ncols = n / dims[l];
+            const long long nout = g.ncols * g.m;
+            double* dst = d_y;
+            if (!last) {
+                tmp[l % 2].alloc(static_cast<size_t>(nout));
+                dst = tmp[l % 2].p;
+            }
+            DenseMatrix Fm(rows[l], cols[l]);
+            std::memcpy(Fm.a.data(), factors[l], sizeof(double) * rows[l] * static_cast<size_t>(cols[l]));
+            const gpu::Tiling t = gpu::choose_tiling(rows[l], cols[l]);
+            DBuf Jp;
+            Jp.upload(pad_factor(Fm, false, t));
+            ck(gpu::launch_mode_product(t, g, src, dst, Jp.p, nullptr, nullptr, st), "kron_matvec mode product");
+            ck(cudaStreamSynchronize(st), "kron_matvec sync");
+            dims[l] = rows[l];
+            n = nout;
+            src = dst;
+        }
+    });
+}
+
+int stiga_kronsum_create(int D, const int* dims, int nterms, const double* coeffs, const double* const* factors,
+                         int device, stiga_kronsum_t* out) {
+    return guarded([&] {
+        require(out != nullptr, "stiga_kronsum_create: null handle output");
+        *out = nullptr;
+        require(D >= 1 && dims, "KronSumOperator: dimensions must be positive");
+        require(nterms >= 0 && (nterms == 0 || (coeffs && factors)), "KronSumOperator: term factor count does not match dims");
+        auto h = std::make_unique<stiga_kronsum_s>();
+        h->device = device;
+        h->D = D;
+        h->n_dof = 1;
+        for (int l = 0; l < D; ++l) {
+            require(dims[l] >= 1, "KronSumOperator: dimensions must be positive");
+            h->dims.push_back(dims[l]);
+            h->n_dof *= dims[l];
+        }
+        DeviceGuard dg(device);
+        for (int t = 0; t < nterms; ++t) {
+            h->coeffs.push_back(coeffs[t]);
+            h->factors.emplace_back();
+            for (int l = 0; l < D; ++l) {
+                require(factors[t * D + l] != nullptr, "KronSumOperator: factor shape does not match dims");
+                DenseMatrix F = from_colmajor(factors[t * D + l], dims[l]);
+                const int p = half_bandwidth(F);
+                h->hbw.push_back(p);
+                h->bands.emplace_back(new DBuf);
+                h->bands.back()->upload(to_band(F, p, l == D - 1 ? coeffs[t] : 1.0));
+                h->factors.back().push_back(std::move(F));
+            }
+        }
+        *out = h.release();
+    });
+}
+
+int stiga_kronsum_create_spacetime(int d, const int* n, const double* const* K, const double* const* M, int n_t,
+                                   const double* Wt, const double* Mt, double gamma, double nu, int device,
+                                   stiga_kronsum_t* out) {
+    return guarded([&] {
+        require(out != nullptr, "stiga_kronsum_create_spacetime: null handle output");
+        *out = nullptr;
+        require(d >= 1 && n && K && M && Wt && Mt && n_t >= 1, "KronSumOperator: dimensions must be positive");
+        auto h = std::make_unique<stiga_kronsum_s>();
+        h->device = device;
+        h->D = d + 1;
+        h->spacetime = true;
+        h->n_dof = 1;
+        for (int l = 0; l < d; ++l) {
+            require(n[l] >= 1 && K[l] && M[l], "KronSumOperator: dimensions must be positive");
+            h->dims.push_back(n[l]);
+            h->n_dof *= n[l];
+        }
+        h->dims.push_back(n_t);
+        h->n_dof *= n_t;
+        DeviceGuard dg(device);
+        // the kron_sum_terms structure (solver.cpp:10-30): terms [gamma; M_1..M_d, W_t] and
+        // [nu; M_1..K_l..M_d, M_t]; kept as dense host factors for diagonal()
+        std::vector<DenseMatrix> Kd, Md;
+        for (int l = 0; l < d; ++l) {
+            Kd.push_back(from_colmajor(K[l], n[l]));
+            Md.push_back(from_colmajor(M[l], n[l]));
+        }
+        const DenseMatrix Wd = from_colmajor(Wt, n_t), Mtd = from_colmajor(Mt, n_t);
+        h->coeffs.push_back(gamma);
+        h->factors.emplace_back(Md);
+        h->factors.back().push_back(Wd);
+        for (int l = 0; l < d; ++l) {
+            h->coeffs.push_back(nu);
+            std::vector<DenseMatrix> fs;
+            for (int k = 0; k < d; ++k) fs.push_back(k == l ? Kd[k] : Md[k]);
+            fs.push_back(Mtd);
+            h->factors.push_back(std::move(fs));
+        }
+        auto push = [&](const DenseMatrix& F, double c) {
+            const int p = half_bandwidth(F);
+            h->hbw.push_back(p);
+            h->bands.emplace_back(new DBuf);
+            h->bands.back()->upload(to_band(F, p, c));
+        };
+        for (int l = 0; l < d; ++l) {
+            push(Md[l], 1.0);
+            push(Kd[l], 1.0);
+        }
+        push(Wd, gamma);
+        push(Mtd, nu);
+        *out = h.release();
+    });
+}
+
+int stiga_kronsum_destroy(stiga_kronsum_t A) {
+    return guarded([&] {
+        if (!A) return;
+        DeviceGuard dg(A->device);
+        delete A;
+    });
+}
+
+int stiga_kronsum_size(stiga_kronsum_t A, long long* n_dof) {
+    return guarded([&] {
+        require(A && n_dof, "stiga_kronsum_size: null argument");
+        *n_dof = A->n_dof;
+    });
+}
+
+int stiga_kronsum_apply(stiga_kronsum_t A, const double* d_x, double* d_y, void* stream) {
+    return guarded([&] {
+        require(A && d_x && d_y, "KronSumOperator::apply: vector length mismatch");
+        require(d_x != d_y, "KronSumOperator::apply: input and output must not alias");
+        DeviceGuard dg(A->device);
+        A->apply(d_x, d_y, as_stream(stream));
+    });
+}
+
+int stiga_kronsum_diagonal(stiga_kronsum_t A, double* h_diag) {
+    return guarded([&] {
+        require(A && h_diag, "KronSumOperator::diagonal: null argument");
+        std::fill(h_diag, h_diag + A->n_dof, 0.0);
+        // kronop.cpp:117-131: acc = kron(diag(F_D), ..., diag(F_1)), first factor fastest
+        for (size_t t = 0; t < A->coeffs.size(); ++t) {
+            std::vector<double> acc(1, 1.0);
+            for (const DenseMatrix& F : A->factors[t]) {
+                std::vector<double> next(acc.size() * F.rows);
+                for (Index j = 0; j < F.rows; ++j)
+                    for (size_t i = 0; i < acc.size(); ++i) next[j * acc.size() + i] = F(j, j) * acc[i];
+                acc.swap(next);
+            }
+            for (long long i = 0; i < A->n_dof; ++i) h_diag[i] += A->coeffs[t] * acc[i];
+        }
+    });
+}
+
+int stiga_fp64_peak(int device, double ms, double* tflops_dmma, double* tflops_dfma) {
+    return guarded([&] {
+        require(tflops_dmma && tflops_dfma, "stiga_fp64_peak: null output");
+        DeviceGuard dg(device);
+        ck(gpu::fp64_peak_probe(ms, tflops_dmma, tflops_dfma), "fp64 peak probe");
+    });
+}
+
+}  // extern "C"

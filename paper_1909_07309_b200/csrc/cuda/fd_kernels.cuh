@@ -1,0 +1,72 @@
+// Device side of the extended-FD apply: FP64 tensor-core (DMMA m8n8k4) mode products and the
+// time-fused (U_t^T -> block-arrowhead solve -> U_t) kernel.
+//
+// Reference ops replaced:
+//   mode_product / KronFactor::{contract,apply_left}  kronop.cpp:27-73
+//   arrowhead_solve / apply_pair_inverse               fdsolve.cpp:11-65
+//   ExtendedFDPreconditioner::apply (D^-1/2 scalings)  fdsolve.cpp:155-164
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace stiga {
+namespace gpu {
+
+constexpr int kMaxDim = 4;  // spatial directions supported by the device path (reference: d = 1..3)
+
+/// Per-spatial-index data of the block-arrowhead solve (ArrowheadLU, fdsolve.hpp:17-31).
+/// R_j^-1 is recomputed on the fly from Lambda_s instead of being stored.
+struct ArrowParams {
+    int d = 0;
+    int n[kMaxDim] = {0, 0, 0, 0};          // spatial mode sizes (colex, n[0] fastest)
+    const double* lam[kMaxDim] = {};        // per-direction eigenvalues Lambda_l
+    const double* S_inv = nullptr;          // N_s
+    const double* pair_c = nullptr;         // gamma^2/nu * lambda_j^2  (fdsolve.cpp:118)
+    const double* pair_c1 = nullptr;        // gamma/nu * lambda_j      (fdsolve.cpp:16)
+    const double* g = nullptr;              // n_t - 1 coupling entries
+    int npairs = 0, zero_count = 0, n_t = 0;
+    double gamma = 0.0, nu = 0.0;
+};
+
+/// Geometry of one mode product over a colex tensor: fibers are indexed by
+/// c = l + L*r (l < L, r < R); element j of fiber c sits at l + L*(j + n*r).
+struct ModeGeom {
+    long long L = 1;      // product of the sizes before the mode
+    long long ncols = 0;  // L * R
+    int n = 0;            // input mode size (contraction length)
+    int m = 0;            // output mode size (rows of J; == n for the square FD factors)
+};
+
+/// Kernel tiling chosen on the host from n (see choose_tiling in fd_kernels.cu).
+struct Tiling {
+    int MI = 1, WM = 1, NI = 2, WN = 4;
+    int S = 1;      // 8-row strips covering n (ceil(n/8))
+    int Mp = 8;     // padded rows of J = 8*MI*WM
+    int Kp = 4;     // padded contraction length = round_up(n, 4)
+    int Xrows = 4;  // rows of the smem tile = max(Kp, m)
+    int BN = 64;    // fibers per CTA = 8*NI*WN
+    int LDX = 68;   // smem row stride of the fiber tile (== 4 mod 16 doubles)
+    size_t smem = 0;
+    int threads() const { return 32 * WM * WN; }
+};
+
+Tiling choose_tiling(int m, int n);  // m output rows, n contraction length
+
+/// Y = (I (x) J (x) I) X along one mode.  J is row-major, zero padded to (t.Mp x t.Kp).
+/// pre_scale (input) / post_scale (output) are optional elementwise factors (D^-1/2).
+cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y,
+                                const double* Jpad, const double* pre_scale, const double* post_scale,
+                                cudaStream_t stream);
+
+/// Time-fused kernel: per spatial index, Z = U_t^T x, arrowhead solve, y = U_t Z.
+/// Jt_pad = U_t^T padded, J_pad = U_t padded (both row-major Mp x Kp).
+cudaError_t launch_time_fused(const Tiling& t, const ModeGeom& g, const double* X, double* Y,
+                              const double* Jt_pad, const double* J_pad, const ArrowParams& ap,
+                              cudaStream_t stream);
+
+/// Elementwise y = a .* x (used when a scaling cannot be fused).
+cudaError_t launch_scale(const double* a, const double* x, double* y, long long n, cudaStream_t stream);
+
+}  // namespace gpu
+}  // namespace stiga

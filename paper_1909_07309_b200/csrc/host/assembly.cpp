@@ -1,0 +1,61 @@
+// Host-side 1D Galerkin assembly; follows /root/reference/proj/core/src/assembly.cpp:47-149.
+#include "assembly.hpp"
+
+#include <stdexcept>
+
+namespace stiga {
+
+BandedMatrix assemble_univariate(const SplineSpace1D& space, const QuadratureRule& quad, int deriv_row,
+                                 int deriv_col, const std::vector<double>* element_weights) {
+    if (deriv_row < 0 || deriv_row > 1 || deriv_col < 0 || deriv_col > 1)
+        throw std::invalid_argument("assemble_univariate: derivative orders must be 0 or 1");
+    if (quad.num_elements != space.knot_vector().num_elements())
+        throw std::invalid_argument("assemble_univariate: quadrature built on a different knot vector");
+    if (element_weights && static_cast<int>(element_weights->size()) != quad.num_elements)
+        throw std::invalid_argument("assemble_univariate: one weight per element required");
+    const int n = space.dim(), p = space.degree();
+    const bool check = element_weights && deriv_row == deriv_col;
+    BandedMatrix A{DenseMatrix(n, n), p};
+    std::vector<double> val(p + 1), der(p + 1);
+    for (int q = 0; q < quad.num_points(); ++q) {
+        const double wq = element_weights ? (*element_weights)[quad.element_of(q)] : 1.0;
+        if (check && wq <= 0.0)
+            throw std::runtime_error("assemble_univariate: non-positive weight sample in a mass/stiffness integral");
+        const double c = quad.weights[q] * wq;
+        const int first = space.eval_active(quad.nodes[q], 0, val.data());
+        space.eval_active(quad.nodes[q], 1, der.data());
+        const auto& rv = deriv_row == 0 ? val : der;
+        const auto& cv = deriv_col == 0 ? val : der;
+        for (int a = 0; a <= p; ++a) {
+            const int i = first + a;
+            if (i < 0 || i >= n) continue;
+            const double ri = rv[a];
+            if (ri == 0.0) continue;
+            for (int b = 0; b <= p; ++b) {
+                const int j = first + b;
+                if (j < 0 || j >= n) continue;
+                A.m(i, j) += c * cv[b] * ri;
+            }
+        }
+    }
+    return A;
+}
+
+std::pair<BandedMatrix, BandedMatrix> assemble_time_matrices(int p_t, int n_el_t, double T) {
+    if (T <= 0.0) throw std::invalid_argument("assemble_time_matrices: T must be positive");
+    const SplineSpace1D space = SplineSpace1D::temporal(p_t, n_el_t);
+    const QuadratureRule quad = gauss_rule(space.knot_vector(), p_t + 1);
+    BandedMatrix W = assemble_univariate(space, quad, 0, 1);
+    BandedMatrix M = assemble_univariate(space, quad, 0, 0);
+    for (double& v : M.m.a) v *= T;
+    return {std::move(W), std::move(M)};
+}
+
+void assemble_spatial_parametric(int p, int n_el, int q, BandedMatrix& K, BandedMatrix& M) {
+    const SplineSpace1D space = SplineSpace1D::spatial(p, n_el);
+    const QuadratureRule quad = gauss_rule(space.knot_vector(), q);
+    K = assemble_univariate(space, quad, 1, 1);
+    M = assemble_univariate(space, quad, 0, 0);
+}
+
+} // namespace stiga

@@ -1,0 +1,169 @@
+"""GPU parity of the FD apply (the hot path) against the CPU oracle, through the C ABI.
+Bar: ||s_gpu - s_oracle||_2 / ||s_oracle||_2 <= 1e-11 (north_star) on seeded uniform[-1,1] inputs."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import fdsolve as ofd  # noqa: E402
+from oracle import kronop as okr  # noqa: E402
+from paper_1909_07309_b200 import stiga  # noqa: E402
+from paper_1909_07309_b200.configs import CONFIGS  # noqa: E402
+from paper_1909_07309_b200.inputs import uniform_pm1  # noqa: E402
+from paper_1909_07309_b200.problems import geometry_scaling, identity_pieces  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def run_pair(d, p, nel, scaled, seed=7, gamma=1.0, nu=1.0):
+    pc = identity_pieces(d, p, nel)
+    D = None
+    if scaled:
+        D = geometry_scaling(pc) * np.exp(0.3 * uniform_pm1(pc.n_dof, seed + 1))
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, gamma, nu, scaling=D, device=0)
+    Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, gamma, nu, scaling=D)
+    r = uniform_pm1(pc.n_dof, seed)
+    s = P.apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    return s, Po.apply(r), P, Po, r
+
+
+@pytest.mark.parametrize("d,p,nel", [
+    (1, 2, 1), (1, 1, 2), (1, 2, 5), (1, 3, 40), (1, 5, 33),         # d = 1, tiny and zero blocks
+    (2, 2, 16),                                                       # c1
+    (2, 1, 3), (2, 3, 8), (2, 3, 9), (2, 4, 11), (2, 2, 30),          # ragged / odd n_t (zero block)
+    (3, 2, 6), (3, 3, 7), (3, 3, 12), (3, 4, 9),
+    (2, 3, 64), (3, 3, 24),                                           # multi-tile sizes
+])
+@pytest.mark.parametrize("scaled", [False, True])
+def test_fd_apply_parity(d, p, nel, scaled):
+    s, so, *_ = run_pair(d, p, nel, scaled)
+    assert rel(s, so) <= TOL
+
+
+def test_fd_apply_nt1():
+    """n_t = 1 (degenerate split, pencil.cpp:124-130): a single diagonal solve (gamma sigma + nu Lambda_s)^-1."""
+    K, M = stiga.assemble_spatial_parametric(2, 5, 2)
+    Wt, Mt = stiga.assemble_time_matrices(1, 1)
+    P = stiga.ExtendedFDPreconditioner.setup(K, M, Wt, Mt, 1.0, 1.0, device=0)
+    Po = ofd.ExtendedFDPreconditioner.setup(K, M, Wt, Mt, 1.0, 1.0)
+    assert P.dims[-1] == 1 and P.time_info()["npairs"] == 0
+    r = uniform_pm1(P.n_dof, 21)
+    s = P.apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert rel(s, Po.apply(r)) <= TOL
+
+
+@pytest.mark.parametrize("nel", [96, 128, 161])
+def test_fd_apply_parity_large_1d_modes(nel):
+    """n = 97..163 exercises WM > 1 warp-row groups and the K-chunk tail (d = 2, small time)."""
+    pc = identity_pieces(2, 3, nel)
+    Wt, Mt = stiga.assemble_time_matrices(3, 6)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, Wt, Mt, 1.0, 1.0, device=0)
+    Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, Wt, Mt, 1.0, 1.0)
+    r = uniform_pm1(P.n_dof, 11)
+    s = P.apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert rel(s, Po.apply(r)) <= TOL
+
+
+def test_fd_apply_parity_c2_reduced_and_long_time():
+    """c2's p = 3 with n_t = 258 (full c2 time direction) on a reduced spatial grid."""
+    K, M = stiga.assemble_spatial_parametric(3, 20, 2)
+    Wt, Mt = stiga.assemble_time_matrices(3, 256)
+    P = stiga.ExtendedFDPreconditioner.setup(K, M, Wt, Mt, 1.0, 1.0, device=0)
+    Po = ofd.ExtendedFDPreconditioner.setup(K, M, Wt, Mt, 1.0, 1.0)
+    r = uniform_pm1(P.n_dof, 12)
+    s = P.apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert rel(s, Po.apply(r)) <= TOL
+
+
+def test_fd_apply_nu_quirk_with_product_basis():
+    """nu != 1 exercises the reference's c1*c1/nu formula (fdsolve.cpp:17,128-129), whose result
+    depends on the time eigenbasis; the oracle arrowhead is fed the product's exported factors."""
+    K, M = stiga.assemble_spatial_parametric(2, 6, 2)
+    Wt, Mt = stiga.assemble_time_matrices(2, 7)
+    gamma, nu = 1.7, 2.5
+    P = stiga.ExtendedFDPreconditioner.setup(K, M, Wt, Mt, gamma, nu, device=0)
+    Po = ofd.ExtendedFDPreconditioner.setup(K, M, Wt, Mt, gamma, nu)
+    # rebuild the oracle's time pieces from the product's factorization
+    ti = P.time_info()
+    Po.time.U = P.export(2)
+    Po.lu.lambda_t = list(P.export(3))
+    Po.lu.g = P.export(4)
+    Po.lu.S_inv = P.export(5)
+    Po.lu.R_inv = [1.0 / (nu * Po.lu.lambda_s + gamma * gamma / nu * lam * lam * Po.lu.lambda_s_inv)
+                   for lam in Po.lu.lambda_t]
+    Po.U = [P.export(0, l) for l in range(2)]
+    Po.transform = Po.U + [Po.time.U]
+    Po.transform_t = [u.T.copy() for u in Po.transform]
+    assert ti["zero_count"] == Po.lu.zero_count
+    r = uniform_pm1(P.n_dof, 13)
+    s = P.apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert rel(s, Po.apply(r)) <= TOL
+
+
+def test_fd_apply_in_place_and_streams():
+    pc = identity_pieces(2, 2, 10)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=0)
+    r = torch.from_numpy(uniform_pm1(P.n_dof, 3)).cuda()
+    ref = P.apply(r)
+    x = r.clone()
+    P.apply(x, out=x)  # aliasing allowed
+    assert torch.equal(x, ref)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        y = P.apply(r)
+    st.synchronize()
+    assert torch.equal(y, ref)  # deterministic
+    host = P.apply(r.cpu().numpy())
+    assert np.array_equal(host, ref.cpu().numpy())
+
+
+def test_fd_apply_errors():
+    pc = identity_pieces(2, 2, 4)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=0)
+    with pytest.raises(ValueError):
+        P.apply(torch.zeros(P.n_dof + 1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        P.apply(np.zeros(3))
+
+
+def test_fd_linearity_and_inverse_full_c2():
+    """Full c2 size (17M DoF): size-independent properties.  On the identity geometry the FD
+    preconditioner is the exact inverse of A, so A P r = r to rounding, and
+    the apply is linear."""
+    cfg = CONFIGS["c2"]
+    pc = identity_pieces(cfg.d, cfg.p, cfg.n_el)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=0)
+    A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0)
+    r = torch.from_numpy(uniform_pm1(P.n_dof, cfg.seed)).cuda()
+    s = P.apply(r)
+    res = torch.linalg.norm(A.apply(s) - r) / torch.linalg.norm(r)
+    assert res.item() <= 1e-9
+    q = torch.from_numpy(uniform_pm1(P.n_dof, 77)).cuda()
+    lin = P.apply(2.0 * r - 3.0 * q) - (2.0 * s - 3.0 * P.apply(q))
+    assert (torch.linalg.norm(lin) / torch.linalg.norm(s)).item() <= 1e-12
+
+
+def test_kron_matvec_matches_dense():  # tests/test_kronop.cpp:62-123 through the GPU mode kernels
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(60)
+    J = rng.standard_normal((6, 4))
+    y = stiga.kron_matvec([np.eye(3), J, np.eye(5)], torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.abs(y - okr.dense_kron_chain([np.eye(3), J, np.eye(5)]) @ x).max() <= 1e-13
+    A, B, C = (rng.standard_normal((4, 4)) for _ in range(3))
+    big = okr.dense_kron_chain([A, B, C])
+    for j in range(64):
+        e = np.zeros(64)
+        e[j] = 1.0
+        col = stiga.kron_matvec([A, B, C], torch.from_numpy(e).cuda()).cpu().numpy()
+        assert np.abs(col - big[:, j]).max() <= 1e-13
+    for n in (17, 97, 130, 258):  # the FD mode sizes
+        Fs = [rng.standard_normal((n, n)) for _ in range(2)]
+        xx = rng.standard_normal(n * n)
+        yy = stiga.kron_matvec(Fs, torch.from_numpy(xx).cuda()).cpu().numpy()
+        ref = okr.kron_matvec(Fs, xx)
+        assert rel(yy, ref) <= 1e-13

@@ -1,0 +1,312 @@
+"""Pins the CPU oracle (oracle/) to every known-answer value the reference holds for this path:
+tests/test_kronop.cpp, tests/test_bspline.cpp, the SPEC.md worked examples (pencil/fdsolve/gmres)
+and the paper's Tables 1 and 3.  CPU only."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import assembly, bspline, fdsolve, gmres as og, kronop, pencil
+
+
+def rnd(r, c, seed):
+    return np.random.default_rng(seed).standard_normal((r, c))
+
+
+# ---------------- tests/test_kronop.cpp -------------------------------------------------
+def test_mode_product_identity_and_scaling():  # test_kronop.cpp:41-60
+    x = np.array([1.0, 3.0, 2.0, 4.0])
+    y, _ = kronop.mode_product(x, [2, 2], np.eye(2), 0)
+    assert np.array_equal(y, x)
+    y, _ = kronop.mode_product(x, [2, 2], 2 * np.eye(2), 0)
+    assert np.abs(y - np.array([2, 6, 4, 8])).max() <= 1e-15
+    with pytest.raises(ValueError):
+        kronop.mode_product(x, [2, 2], np.eye(3), 0)
+    with pytest.raises(ValueError):
+        kronop.mode_product(x, [2, 2], 2 * np.eye(2), 2)
+
+
+def test_mode_product_vectorization_identity():  # test_kronop.cpp:62-72
+    x = rnd(60, 1, 11)[:, 0]
+    J = rnd(6, 4, 12)
+    y, dims = kronop.mode_product(x, [3, 4, 5], J, 1)
+    assert dims == [3, 6, 5]
+    big = kronop.dense_kron_chain([np.eye(3), J, np.eye(5)])
+    assert np.abs(y - big @ x).max() <= 1e-13
+
+
+def test_mode_products_commute():  # test_kronop.cpp:74-83
+    x = rnd(60, 1, 21)[:, 0]
+    A, C = rnd(3, 3, 22), rnd(5, 5, 23)
+    ac = kronop.mode_product(kronop.mode_product(x, [3, 4, 5], A, 0)[0], [3, 4, 5], C, 2)[0]
+    ca = kronop.mode_product(kronop.mode_product(x, [3, 4, 5], C, 2)[0], [3, 4, 5], A, 0)[0]
+    assert np.abs(ac - ca).max() <= 1e-13
+
+
+def test_kron_matvec_cases():  # test_kronop.cpp:85-123
+    x = rnd(8, 1, 31)[:, 0]
+    assert np.array_equal(kronop.kron_matvec([np.eye(2)] * 3, x), x)
+    J1, J2 = np.array([[1.0, 0], [0, 2]]), np.array([[0.0, 1], [1, 0]])
+    xh = np.array([1.0, 3, 2, 4])
+    assert np.abs(kronop.kron_matvec([J1, J2], xh) - np.kron(J2, J1) @ xh).max() <= 1e-14
+    A, B, C = rnd(3, 3, 41), rnd(3, 3, 42), rnd(3, 3, 43)
+    x27 = rnd(27, 1, 44)[:, 0]
+    e = kronop.dense_kron_chain([A, B, C]) @ x27
+    assert np.linalg.norm(kronop.kron_matvec([A, B, C], x27) - e) <= 1e-13 * np.linalg.norm(e)
+    A, B, C = rnd(4, 4, 51), rnd(4, 4, 52), rnd(4, 4, 53)
+    big = kronop.dense_kron_chain([A, B, C])
+    for j in range(64):
+        ej = np.zeros(64)
+        ej[j] = 1
+        assert np.abs(kronop.kron_matvec([A, B, C], ej) - big[:, j]).max() <= 1e-13
+
+
+def test_kronsum_operator():  # test_kronop.cpp:125-171
+    op = kronop.KronSumOperator([1, 1], [(2.0, [np.array([[1 / 3]]), np.array([[0.5]])])])
+    assert op.apply(np.array([3.0]))[0] == pytest.approx(2.0 * 0.5 * (1 / 3) * 3.0)
+    Ms, Wt, Ks, Mt = rnd(3, 3, 61), rnd(4, 4, 62), rnd(3, 3, 63), rnd(4, 4, 64)
+    both = kronop.KronSumOperator([3, 4], [(1.0, [Ms, Wt]), (0.0, [Ks, Mt])])
+    one = kronop.KronSumOperator([3, 4], [(1.0, [Ms, Wt])])
+    x = rnd(12, 1, 65)[:, 0]
+    assert np.abs(both.apply(x) - one.apply(x)).max() <= 1e-14
+    A1, A2, B1, B2 = rnd(3, 3, 71), rnd(3, 3, 72), rnd(3, 3, 73), rnd(3, 3, 74)
+    op = kronop.KronSumOperator([3, 3], [(1.7, [A1, A2]), (-0.3, [B1, B2])])
+    dense = 1.7 * np.kron(A2, A1) - 0.3 * np.kron(B2, B1)
+    x, y = rnd(9, 1, 75)[:, 0], rnd(9, 1, 76)[:, 0]
+    assert np.linalg.norm(op.apply(x) - dense @ x) <= 1e-13 * np.linalg.norm(x)
+    lhs, rhs = op.apply(2 * x - 3 * y), 2 * op.apply(x) - 3 * op.apply(y)
+    assert np.linalg.norm(lhs - rhs) <= 1e-13 * (np.linalg.norm(rhs) + 1)
+    op = kronop.KronSumOperator([3, 3], [(1.0, [A1, A2]), (2.5, [B1, B2])])
+    assert np.abs(op.diagonal() - np.diag(np.kron(A2, A1) + 2.5 * np.kron(B2, B1))).max() <= 1e-14
+    with pytest.raises(ValueError):
+        kronop.KronSumOperator([3, 4], [(1.0, [np.eye(3), np.eye(3)])])
+
+
+# ---------------- tests/test_bspline.cpp ------------------------------------------------
+def test_knot_vectors():  # test_bspline.cpp:11-25
+    assert bspline.KnotVector.uniform_open(1, 1).knots == [0, 0, 1, 1]
+    kv2 = bspline.KnotVector.uniform_open(2, 2)
+    assert kv2.knots == [0, 0, 0, 0.5, 1, 1, 1] and kv2.num_basis == 4
+    kv = bspline.KnotVector.uniform_open(3, 32)
+    assert kv.num_basis == 35 and kv.mesh_size() == pytest.approx(1 / 32)
+    for args in [(0, 4), (2, 0)]:
+        with pytest.raises(ValueError):
+            bspline.KnotVector.uniform_open(*args)
+
+
+def test_linear_hat_values():  # test_bspline.cpp:27-36
+    kv = bspline.KnotVector.uniform_open(1, 1)
+    first, v = kv.eval_basis(0.25, 0)
+    assert first == 0 and v[0] == pytest.approx(0.75) and v[1] == pytest.approx(0.25)
+    for x in (-0.1, 1.1):
+        with pytest.raises(ValueError):
+            kv.eval_basis(x, 0)
+
+
+def test_partition_of_unity_and_derivative_sums():  # test_bspline.cpp:38-69
+    rng = np.random.default_rng(42)
+    for p in range(1, 9):
+        kv = bspline.KnotVector.uniform_open(p, 16)
+        for _ in range(50):
+            x = rng.uniform()
+            first, v = kv.eval_basis(x, 0)
+            assert first == kv.find_span(x) - p
+            assert (v >= 0).all() and abs(v.sum() - 1) <= 1e-13
+            _, dv = kv.eval_basis(x, 1)
+            assert abs(dv.sum()) <= 1e-11 * p / kv.mesh_size()
+    _, dv = bspline.KnotVector.uniform_open(2, 4).eval_basis(0.3, 1)
+    assert abs(dv.sum()) <= 1e-12
+
+
+def test_right_limit_at_one():  # test_bspline.cpp:71-80
+    for p in (1, 2, 4):
+        kv = bspline.KnotVector.uniform_open(p, 5)
+        first, v = kv.eval_basis(1.0, 0)
+        assert first + p == kv.num_basis - 1 and v[p] == pytest.approx(1.0)
+        assert np.abs(v[:p]).max() <= 1e-14
+
+
+def test_derivatives_vs_finite_differences():  # test_bspline.cpp:82-105
+    rng = np.random.default_rng(7)
+    for p in (1, 2, 3, 5):
+        kv = bspline.KnotVector.uniform_open(p, 7)
+        for _ in range(20):
+            x = rng.uniform(0.05, 0.95)
+            h = 1e-6
+            f0, d = kv.eval_basis(x, 1)
+            fp, vp = kv.eval_basis(x + h, 0)
+            fm, vm = kv.eval_basis(x - h, 0)
+            if fp != f0 or fm != f0:
+                continue
+            assert np.abs((vp - vm) / (2 * h) - d).max() <= 1e-5 * max(1.0, np.abs(d).max())
+
+
+def test_spaces_and_gauss_rules():  # test_bspline.cpp:107-145
+    assert bspline.SplineSpace1D.spatial(2, 8).dim == 8
+    assert bspline.SplineSpace1D.temporal(2, 8).dim == 9
+    for q in range(1, 8):
+        x, w = bspline.gauss_legendre_reference(q)
+        assert abs(w.sum() - 2) <= 1e-13
+        for k in range(2 * q):  # exact for degree <= 2q-1
+            exact = (1 - (-1) ** (k + 1)) / (k + 1)
+            assert abs((w * x ** k).sum() - exact) <= 1e-12
+    rule = bspline.gauss_rule(bspline.KnotVector.uniform_open(2, 4), 3)
+    assert rule.num_points == 12 and abs(rule.weights.sum() - 1) <= 1e-14
+
+
+# ---------------- SPEC.md / paper KATs (pencil, fdsolve, gmres) ---------------------------
+def test_spd_generalized_eig_examples():
+    U, lam = pencil.spd_generalized_eig(np.array([[2.0]]), np.array([[1.0]]))
+    assert lam[0] == pytest.approx(2.0) and abs(U[0, 0]) == pytest.approx(1.0)
+    U, lam = pencil.spd_generalized_eig(np.array([[2.0, -1], [-1, 2]]), np.eye(2))
+    assert np.allclose(lam, [1, 3]) and np.allclose(U.T @ U, np.eye(2))
+
+
+@pytest.mark.parametrize("p,kappa", [(2, 2.7), (3, 4.5), (4, 7.6), (5, 13), (6, 21), (7, 35), (8, 57)])
+def test_paper_table1_kappa_U_space(p, kappa):  # PAPER.md:617-639 (Table 1)
+    K, M = assembly.assemble_spatial_parametric(p, 32, 1)
+    U, _ = pencil.spd_generalized_eig(K[0], M[0])
+    assert float(f"{pencil.cond2(U):.2g}") == kappa
+
+
+@pytest.mark.parametrize("p,kappa", [(2, 3.2), (3, 5.2), (4, 8.3), (5, 13), (6, 22), (7, 36), (8, 59)])
+def test_paper_table3_kappa_U_time(p, kappa):  # PAPER.md:840-862 (Table 3, n_el = 32)
+    W, M = assembly.assemble_time_matrices(p, 32, 1.0)
+    tf = pencil.time_factorization(W, M)
+    assert float(f"{pencil.cond2(tf.U):.2g}") == kappa
+
+
+def test_time_factorization_nt1():
+    W, M = assembly.assemble_time_matrices(1, 1, 1.0)
+    assert W[0, 0] == pytest.approx(0.5) and M[0, 0] == pytest.approx(1 / 3)
+    tf = pencil.time_factorization(W, M)
+    assert tf.rho == pytest.approx(math.sqrt(3)) and tf.sigma == pytest.approx(1.5)
+    assert tf.U[0, 0] ** 2 * M[0, 0] == pytest.approx(1.0)
+
+
+@pytest.mark.parametrize("p,nel", [(1, 4), (2, 8), (3, 7), (4, 16), (5, 9), (3, 256), (5, 160)])
+def test_time_factorization_invariants(p, nel):
+    W, M = assembly.assemble_time_matrices(p, nel, 1.0)
+    tf = pencil.time_factorization(W, M)
+    n = W.shape[0]
+    assert np.abs(tf.U.T @ M @ tf.U - np.eye(n)).max() <= 1e-10
+    assert np.linalg.norm(W @ tf.U - M @ tf.U @ tf.delta()) <= 1e-8 * np.linalg.norm(W)
+    assert np.all(tf.U[n - 1, : n - 1] == 0.0) and tf.U[n - 1, n - 1] == tf.rho
+    assert 2 * len(tf.lam) + tf.zero_count == n - 1
+    assert all(a <= b for a, b in zip(tf.lam, tf.lam[1:]))
+    assert tf.zero_count == (n - 1) % 2
+
+
+def test_skew_pencil_small():
+    sk = pencil.skew_pencil_eig(np.array([[0.0]]), np.array([[4.0]]))
+    assert sk.zero_count == 1 and abs(sk.U[0, 0]) == pytest.approx(0.5)
+    sk = pencil.skew_pencil_eig(np.array([[0.0, 3], [-3, 0]]), np.eye(2))
+    assert sk.lam == [pytest.approx(3.0)]
+
+
+@pytest.mark.parametrize("d", [1, 2])
+@pytest.mark.parametrize("p", [1, 2, 3])
+@pytest.mark.parametrize("nel", [2, 4, 8])
+def test_fd_apply_equals_dense_inverse(d, p, nel):  # SPEC.md:408-411 (<= 1e-9)
+    W, Mt = assembly.assemble_time_matrices(p, nel, 1.0)
+    K, M = assembly.assemble_spatial_parametric(p, nel, d)
+    if any(k.shape[0] == 0 for k in K):
+        pytest.skip("empty spatial space")
+    P = fdsolve.ExtendedFDPreconditioner.setup(K, M, W, Mt, 1.0, 1.0)
+    A = sum(c * kronop.dense_kron_chain(fs) for c, fs in assembly.kron_sum_terms(K, M, W, Mt, 1.0, 1.0))
+    r = np.random.default_rng(100 * d + 10 * p + nel).uniform(-1, 1, P.n_dof)
+    x = np.linalg.solve(A, r)
+    assert np.linalg.norm(P.apply(r) - x) <= 1e-9 * np.linalg.norm(r)
+    s = np.random.default_rng(1).uniform(-1, 1, P.n_dof)
+    assert np.linalg.norm(P.apply(2 * r - 3 * s) - (2 * P.apply(r) - 3 * P.apply(s))) <= 1e-12 * np.linalg.norm(x)
+
+
+def test_fd_scaled_variant_dense():  # SPEC.md:402-405 (scaled variant vs dense D^1/2 A D^1/2)
+    W, Mt = assembly.assemble_time_matrices(2, 4, 1.0)
+    K, M = assembly.assemble_spatial_parametric(2, 4, 2)
+    n = K[0].shape[0] ** 2 * W.shape[0]
+    D = np.random.default_rng(3).uniform(0.5, 2.0, n)
+    P = fdsolve.ExtendedFDPreconditioner.setup(K, M, W, Mt, 1.0, 1.0, scaling=D)
+    A = sum(c * kronop.dense_kron_chain(fs) for c, fs in assembly.kron_sum_terms(K, M, W, Mt, 1.0, 1.0))
+    Ds = np.diag(np.sqrt(D))
+    r = np.random.default_rng(4).uniform(-1, 1, n)
+    assert np.linalg.norm(P.apply(r) - np.linalg.solve(Ds @ A @ Ds, r)) <= 1e-9 * np.linalg.norm(r)
+
+
+def test_fd_setup_errors():  # fdsolve.cpp:73-76, 147-150
+    W, Mt = assembly.assemble_time_matrices(2, 4, 1.0)
+    K, M = assembly.assemble_spatial_parametric(2, 4, 1)
+    for g, nu in [(0.0, 1.0), (1.0, -1.0)]:
+        with pytest.raises(ValueError):
+            fdsolve.ExtendedFDPreconditioner.setup(K, M, W, Mt, g, nu)
+    with pytest.raises(ValueError):
+        fdsolve.ExtendedFDPreconditioner.setup(K, M, W, Mt, 1.0, 1.0, scaling=np.ones(3))
+    with pytest.raises(ValueError):
+        fdsolve.ExtendedFDPreconditioner.setup(K, M, W, Mt, 1.0, 1.0, scaling=-np.ones(4 * 5))
+
+
+def test_gmres_identity_and_spd():
+    b = np.array([1.0, -2.0, 3.0])
+    x, rep = og.gmres(lambda v: v, None, b)
+    assert rep.iterations == 1 and rep.converged and np.allclose(x, b)
+    A = np.array([[4.0, 1.0], [1.0, 3.0]])
+    x, rep = og.gmres(lambda v: A @ v, None, np.array([1.0, 2.0]))
+    assert rep.converged and rep.iterations <= 2 and np.allclose(x, np.linalg.solve(A, [1.0, 2.0]))
+    x, rep = og.gmres(lambda v: A @ v, None, np.zeros(2))
+    assert rep.converged and rep.iterations == 0 and rep.residual_history == [0.0]
+    with pytest.raises(ValueError):
+        og.gmres(lambda v: v, None, b, tol=0.0)
+
+
+def test_gmres_restart_and_total_cap():  # gmres.cpp:52-56, 65 (max_krylov caps TOTAL iterations)
+    rng = np.random.default_rng(5)
+    A = np.eye(30) + 0.5 * rng.standard_normal((30, 30)) / np.sqrt(30)
+    b = rng.standard_normal(30)
+    x, rep = og.gmres(lambda v: A @ v, None, b, tol=1e-10, max_krylov=200, restart=5)
+    assert rep.converged and np.linalg.norm(A @ x - b) <= 1e-8 * np.linalg.norm(b)
+    _, rep = og.gmres(lambda v: A @ v, None, b, tol=1e-14, max_krylov=7, restart=3)
+    assert rep.iterations == 7 and not rep.converged
+    h = rep.residual_history
+    assert all(b_ <= a_ * (1 + 1e-12) for a_, b_ in zip(h[1:4], h[2:4]))
+
+
+def test_reference_pairing_walk_fails_on_config2():
+    """The reference's pairing walk (pencil.cpp:54-87) cannot factor the c2 time pencil (p = 3,
+    n_el = 256): near-degenerate top pairs of S^T S mix at 1e-5 > the 1e-6 threshold.  The oracle
+    (like the product) then switches to the Hermitian-embedding pairs; check that path directly."""
+    import scipy.linalg as sla
+    W, M = assembly.assemble_time_matrices(3, 256, 1.0)
+    n = W.shape[0] - 1
+    L = np.linalg.cholesky(M[:n, :n])
+    S = sla.solve_triangular(L, W[:n, :n], lower=True)
+    S = sla.solve_triangular(L, S.T, lower=True).T
+    S = 0.5 * (S - S.T)
+    mu, Q = np.linalg.eigh(S.T @ S)
+    mu = np.maximum(mu, 0.0)
+    tol = 1e-12 * max(mu[-1], 1.0)
+    accepted, cluster, cmu = 0, [], -1.0
+    for k in range(n):  # the reference walk, counting accepted columns
+        q = Q[:, k].copy()
+        if mu[k] > cmu + tol:
+            cluster, cmu = [], mu[k]
+        for c in cluster:
+            q -= c.dot(q) * c
+        nr = np.linalg.norm(q)
+        if nr < 1e-6:
+            continue
+        q /= nr
+        if mu[k] <= tol:
+            accepted += 1
+            cluster.append(q)
+            continue
+        v = S @ q / np.sqrt(mu[k])
+        accepted += 2
+        cluster += [q, v]
+    assert accepted != n  # -> "skew_pencil_eig: eigenvalue pairing failed" in the reference
+    lam, cols = pencil._robust_pairs(S, tol)
+    assert 2 * len(lam) == n - 1
+    B = np.column_stack(cols)
+    assert np.abs(B.T @ B - np.eye(n - 1)).max() <= 1e-12
+    for j, l_ in enumerate(lam):
+        v, q = cols[2 * j], cols[2 * j + 1]
+        assert np.linalg.norm(S @ q - l_ * v) <= 1e-12 * l_ and np.linalg.norm(S @ v + l_ * q) <= 1e-12 * l_

@@ -1,0 +1,102 @@
+"""GPU parity of the system mat-vec (KronSumOperator) and the device GMRES against the oracle:
+A x within 1e-12 relative, GMRES iteration count within +-1 to the same 1e-8 tolerance."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import assembly as oasm  # noqa: E402
+from oracle import fdsolve as ofd  # noqa: E402
+from oracle import gmres as ogm  # noqa: E402
+from oracle import kronop as okr  # noqa: E402
+from paper_1909_07309_b200 import stiga  # noqa: E402
+from paper_1909_07309_b200.configs import CONFIGS  # noqa: E402
+from paper_1909_07309_b200.inputs import uniform_pm1  # noqa: E402
+from paper_1909_07309_b200.problems import identity_pieces  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("d,p,nel", [(1, 2, 5), (2, 2, 16), (2, 3, 9), (3, 2, 6), (3, 4, 7)])
+def test_spacetime_matvec(d, p, nel):
+    pc = identity_pieces(d, p, nel)
+    A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.3, 0.7)
+    Ao = okr.KronSumOperator(pc.dims, oasm.kron_sum_terms(pc.K, pc.M, pc.Wt, pc.Mt, 1.3, 0.7))
+    x = uniform_pm1(pc.n_dof, 5)
+    y = A.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel(y, Ao.apply(x)) <= 1e-12
+    assert np.abs(A.diagonal() - Ao.diagonal()).max() <= 1e-14 * np.abs(Ao.diagonal()).max()
+
+
+def test_generic_kronsum():  # tests/test_kronop.cpp:125-171 on the device
+    rng = np.random.default_rng(71)
+    A1, A2, B1, B2 = (rng.standard_normal((3, 3)) for _ in range(4))
+    op = stiga.KronSumOperator([3, 3], [(1.7, [A1, A2]), (-0.3, [B1, B2])])
+    dense = 1.7 * np.kron(A2, A1) - 0.3 * np.kron(B2, B1)
+    x = rng.standard_normal(9)
+    assert np.linalg.norm(op.apply(torch.from_numpy(x).cuda()).cpu().numpy() - dense @ x) <= 1e-13 * np.linalg.norm(x)
+    assert np.abs(op.diagonal() - np.diag(dense)).max() <= 1e-14
+    with pytest.raises(ValueError):
+        stiga.KronSumOperator([3, 4], [(1.0, [np.eye(3), np.eye(3)])])
+
+
+@pytest.mark.parametrize("d,p,nel,restart", [(2, 2, 16, 50), (1, 3, 12, None), (3, 2, 5, 50)])
+def test_gmres_identity_geometry(d, p, nel, restart):
+    pc = identity_pieces(d, p, nel)
+    A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=0)
+    b = uniform_pm1(pc.n_dof, 2)
+    x, rep = stiga.gmres(A, P, torch.from_numpy(b).cuda(), stiga.GmresOptions(1e-8, 500, restart))
+    Ao = okr.KronSumOperator(pc.dims, oasm.kron_sum_terms(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0))
+    Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0)
+    xo, repo = ogm.gmres(Ao.apply, Po.apply, b, 1e-8, 500, restart)
+    assert rep.converged and repo.converged
+    assert abs(rep.iterations - repo.iterations) <= 1
+    assert rel(x.cpu().numpy(), xo) <= 1e-10
+
+
+def test_gmres_nontrivial_iterations():
+    """A preconditioner built for a different operator (gamma = 0.3) gives a non-trivial
+    iteration count; device and oracle GMRES must agree within +-1 iteration."""
+    pc = identity_pieces(2, 2, 12)
+    A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 0.3, 1.0, device=0)
+    Ao = okr.KronSumOperator(pc.dims, oasm.kron_sum_terms(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0))
+    Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 0.3, 1.0)
+    b = uniform_pm1(pc.n_dof, 4)
+    for restart in (None, 4):
+        x, rep = stiga.gmres(A, P, torch.from_numpy(b).cuda(), stiga.GmresOptions(1e-8, 300, restart))
+        xo, repo = ogm.gmres(Ao.apply, Po.apply, b, 1e-8, 300, restart)
+        assert rep.converged == repo.converged
+        assert rep.iterations > 2 and abs(rep.iterations - repo.iterations) <= 1
+        assert rel(x.cpu().numpy(), xo) <= 1e-7
+        h, ho = rep.residual_history, repo.residual_history
+        m = min(len(h), len(ho))
+        assert np.allclose(h[:m], ho[:m], rtol=1e-6, atol=1e-12)
+
+
+def test_gmres_zero_rhs_and_errors():
+    pc = identity_pieces(1, 2, 4)
+    A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=0)
+    x, rep = stiga.gmres(A, P, torch.zeros(pc.n_dof, dtype=torch.float64, device="cuda"))
+    assert rep.converged and rep.iterations == 0 and rep.residual_history == [0.0]
+    assert torch.count_nonzero(x).item() == 0
+    with pytest.raises(ValueError):
+        stiga.gmres(A, P, torch.zeros(pc.n_dof, dtype=torch.float64, device="cuda"), stiga.GmresOptions(tol=0.0))
+
+
+def test_gmres_full_c2_one_iteration():
+    cfg = CONFIGS["c2"]
+    pc = identity_pieces(cfg.d, cfg.p, cfg.n_el)
+    A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=0)
+    b = torch.from_numpy(uniform_pm1(pc.n_dof, cfg.seed)).cuda()
+    x, rep = stiga.gmres(A, P, b, stiga.GmresOptions(1e-8, 500, 50))
+    assert rep.converged and rep.iterations == 1
+    res = torch.linalg.norm(A.apply(x) - b) / torch.linalg.norm(b)
+    assert res.item() <= 1e-8
