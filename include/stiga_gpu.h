@@ -80,10 +80,10 @@ int stiga_fd_export(stiga_fd_t P, int which, int l, double* out, long long out_l
 int stiga_fd_apply(stiga_fd_t P, const double* d_r, double* d_s, void* stream);
 /* Host-buffer convenience: H2D copy, apply, D2H copy, synchronize. */
 int stiga_fd_apply_host(stiga_fd_t P, const double* h_r, double* h_s);
-/* Same as stiga_fd_apply but records CUDA events around each of the 2d+1 kernel launches and
-   writes their durations (ms) into pass_ms[0..2d] (synchronizes the stream). */
+/* Same as stiga_fd_apply but records CUDA events around each of the kernel launches (2d+1, +1 post-scale with D) and
+   writes their durations (ms) into pass_ms[0..launches-1] (synchronizes the stream). */
 int stiga_fd_apply_profiled(stiga_fd_t P, const double* d_r, double* d_s, void* stream, float* pass_ms);
-/* Number of kernel launches one apply issues (2d+1). */
+/* Number of kernel launches one apply issues (2d+1, +1 when scaled by D). */
 int stiga_fd_launches(stiga_fd_t P, int* launches);
 
 /* ---- Kronecker operators (kronop.hpp:47-79) ------------------------------------------- */

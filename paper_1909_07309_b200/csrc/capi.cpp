@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -100,12 +101,14 @@ DenseMatrix from_colmajor(const double* a, int n) {
 }
 
 // Row-major, zero-padded (Mp x Kp) copy of J, with J(i,j) = transpose ? U(j,i) : U(i,j).
-std::vector<double> pad_factor(const DenseMatrix& U, bool transpose, const gpu::Tiling& t) {
-    std::vector<double> out(static_cast<size_t>(t.Mp) * t.Kp, 0.0);
+std::vector<double> pad_factor(const DenseMatrix& U, bool transpose, int Mp, int Kp) {
+    std::vector<double> out(static_cast<size_t>(Mp) * Kp, 0.0);
     const Index rows = transpose ? U.cols : U.rows;
     const Index cols = transpose ? U.rows : U.cols;
+    if (rows > Mp || cols > Kp || Mp < 1)
+        throw std::runtime_error("internal: no kernel tiling for a factor of size " + std::to_string(rows));
     for (Index i = 0; i < rows; ++i)
-        for (Index j = 0; j < cols; ++j) out[i * t.Kp + j] = transpose ? U(j, i) : U(i, j);
+        for (Index j = 0; j < cols; ++j) out[i * Kp + j] = transpose ? U(j, i) : U(i, j);
     return out;
 }
 
@@ -127,6 +130,7 @@ struct stiga_fd_s {
     std::vector<int> dims;  // n_1..n_d, n_t
     long long n_dof = 0, n_s = 0;
     std::vector<gpu::Tiling> tl;        // per spatial direction
+    gpu::Tiling tl_pre;                 // direction 0 with the D^-1/2 pre-scale staged in smem
     gpu::Tiling tl_t;
     std::vector<std::unique_ptr<DBuf>> Jt, J;  // padded U_l^T, U_l
     DBuf Jt_t, J_t;
@@ -145,34 +149,39 @@ struct stiga_fd_s {
         return g;
     }
 
-    // 2d+1 launches: forward spatial modes (D^-1/2 fused into the first), time-fused, backward
-    // spatial modes (D^-1/2 fused into the last).  The reference order (fdsolve.cpp:158-163) applies
-    // U_1..U_d, U_t in the back transform; Kronecker factors on distinct modes commute, so applying
-    // U_t first (fused) is equal in exact arithmetic.
+    int launches() const { return 2 * d + 1 + (dinv.p ? 1 : 0); }
+
+    // 2d+1 GEMM launches: forward spatial modes (D^-1/2 staged into the first), the time-fused
+    // kernel, backward spatial modes; then the D^-1/2 post-scale (fdsolve.cpp:158-163).  The
+    // reference back transform applies U_1..U_d, U_t; Kronecker factors on distinct modes commute,
+    // so applying U_t first (fused with the arrowhead) is equal in exact arithmetic.
     void apply(const double* in, double* out, cudaStream_t st, std::vector<cudaEvent_t>* ev) {
         if (in == out && !scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
-        double* buf0 = (in == out) ? scratch2.p : out;
-        double* bufs[2] = {buf0, scratch.p};
-        const int passes = 2 * d + 1;
+        double* bufs[2] = {(in == out) ? scratch2.p : out, scratch.p};
+        const bool scaled = dinv.p != nullptr;
+        const int gemm_passes = 2 * d + 1;
         const double* src = in;
-        for (int k = 0; k < passes; ++k) {
-            double* dst = (k == passes - 1) ? out : bufs[k % 2];
-            if (ev) ck(cudaEventRecord((*ev)[k], st), "event");
+        int e = 0;
+        for (int k = 0; k < gemm_passes; ++k) {
+            double* dst = (k == gemm_passes - 1 && !scaled) ? out : bufs[k % 2];
+            if (ev) ck(cudaEventRecord((*ev)[e++], st), "event");
             if (k < d) {
-                ck(gpu::launch_mode_product(tl[k], geom(k), src, dst, Jt[k]->p, k == 0 ? dinv.p : nullptr, nullptr, st),
+                const bool pre = (k == 0) && scaled;
+                ck(gpu::launch_mode_product(pre ? tl_pre : tl[k], geom(k), src, dst, Jt[k]->p, pre ? dinv.p : nullptr, st),
                    "fd forward mode product");
             } else if (k == d) {
-                gpu::ModeGeom g = geom(d);
-                ck(gpu::launch_time_fused(tl_t, g, src, dst, Jt_t.p, J_t.p, ap, st), "fd time-fused kernel");
+                ck(gpu::launch_time_fused(tl_t, geom(d), src, dst, Jt_t.p, J_t.p, ap, st), "fd time-fused kernel");
             } else {
                 const int m = k - d - 1;
-                ck(gpu::launch_mode_product(tl[m], geom(m), src, dst, J[m]->p, nullptr,
-                                            m == d - 1 ? dinv.p : nullptr, st),
-                   "fd backward mode product");
+                ck(gpu::launch_mode_product(tl[m], geom(m), src, dst, J[m]->p, nullptr, st), "fd backward mode product");
             }
             src = dst;
         }
-        if (ev) ck(cudaEventRecord((*ev)[passes], st), "event");
+        if (scaled) {
+            if (ev) ck(cudaEventRecord((*ev)[e++], st), "event");
+            ck(gpu::launch_scale(dinv.p, src, out, n_dof, st), "fd post-scale");
+        }
+        if (ev) ck(cudaEventRecord((*ev)[e], st), "event");
     }
 };
 
@@ -370,18 +379,20 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         }
 
         DeviceGuard dg(device);
+        h->tl_pre = gpu::choose_mode_tiling(F.n[0], F.n[0], true);
         for (int l = 0; l < d; ++l) {
-            h->tl.push_back(gpu::choose_tiling(F.n[l], F.n[l]));
+            h->tl.push_back(gpu::choose_mode_tiling(F.n[l], F.n[l], false));
+            const int rows = std::max(h->tl.back().Mp, l == 0 ? h->tl_pre.Mp : 0);
             h->Jt.emplace_back(new DBuf);
             h->J.emplace_back(new DBuf);
-            h->Jt.back()->upload(pad_factor(F.U[l], true, h->tl.back()));
-            h->J.back()->upload(pad_factor(F.U[l], false, h->tl.back()));
+            h->Jt.back()->upload(pad_factor(F.U[l], true, rows, h->tl.back().Kp));
+            h->J.back()->upload(pad_factor(F.U[l], false, rows, h->tl.back().Kp));
             h->lam.emplace_back(new DBuf);
             h->lam.back()->upload(F.lambda[l]);
         }
-        h->tl_t = gpu::choose_tiling(F.n_t, F.n_t);
-        h->Jt_t.upload(pad_factor(F.time.U, true, h->tl_t));
-        h->J_t.upload(pad_factor(F.time.U, false, h->tl_t));
+        h->tl_t = gpu::choose_time_tiling(F.n_t);
+        h->Jt_t.upload(pad_factor(F.time.U, true, h->tl_t.Mp, h->tl_t.Kp));
+        h->J_t.upload(pad_factor(F.time.U, false, h->tl_t.Mp, h->tl_t.Kp));
         h->S_inv.upload(F.S_inv);
         std::vector<double> pc, pc1;
         for (double lam : F.time.lambda) {
@@ -415,6 +426,7 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         ap.n_t = F.n_t;
         ap.gamma = gamma;
         ap.nu = nu;
+        if (const char* dbg = std::getenv("STIGA_DEBUG_ARROW")) ap.debug = std::atoi(dbg);
         *out = h.release();
     });
 }
@@ -491,7 +503,7 @@ int stiga_fd_apply_profiled(stiga_fd_t P, const double* d_r, double* d_s, void* 
         require(P && d_r && d_s && pass_ms, "stiga_fd_apply_profiled: null argument");
         require(P->device >= 0, "ExtendedFDPreconditioner::apply: host-only handle (setup with device < 0)");
         DeviceGuard dg(P->device);
-        const int passes = 2 * P->d + 1;
+        const int passes = P->launches();
         std::vector<cudaEvent_t> ev(passes + 1);
         for (auto& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
         P->apply(d_r, d_s, as_stream(stream), &ev);
@@ -504,7 +516,7 @@ int stiga_fd_apply_profiled(stiga_fd_t P, const double* d_r, double* d_s, void* 
 int stiga_fd_launches(stiga_fd_t P, int* launches) {
     return guarded([&] {
         require(P && launches, "stiga_fd_launches: null argument");
-        *launches = 2 * P->d + 1;
+        *launches = P->launches();
     });
 }
 
@@ -554,10 +566,10 @@ int stiga_kron_matvec(int D, const int* rows, const int* cols, const double* con
             }
             DenseMatrix Fm(rows[l], cols[l]);
             std::memcpy(Fm.a.data(), factors[l], sizeof(double) * rows[l] * static_cast<size_t>(cols[l]));
-            const gpu::Tiling t = gpu::choose_tiling(rows[l], cols[l]);
+            const gpu::Tiling t = gpu::choose_mode_tiling(rows[l], cols[l], false);
             DBuf Jp;
-            Jp.upload(pad_factor(Fm, false, t));
-            ck(gpu::launch_mode_product(t, g, src, dst, Jp.p, nullptr, nullptr, st), "kron_matvec mode product");
+            Jp.upload(pad_factor(Fm, false, t.Mp, t.Kp));
+            ck(gpu::launch_mode_product(t, g, src, dst, Jp.p, nullptr, st), "kron_matvec mode product");
             ck(cudaStreamSynchronize(st), "kron_matvec sync");
             dims[l] = rows[l];
             n = nout;

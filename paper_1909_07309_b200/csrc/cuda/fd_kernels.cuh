@@ -7,6 +7,7 @@
 //   ExtendedFDPreconditioner::apply (D^-1/2 scalings)  fdsolve.cpp:155-164
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -27,6 +28,7 @@ struct ArrowParams {
     const double* g = nullptr;              // n_t - 1 coupling entries
     int npairs = 0, zero_count = 0, n_t = 0;
     double gamma = 0.0, nu = 0.0;
+    int debug = 0;  // bit 0: skip the arrowhead (Y = U_t U_t^T X); debugging aid
 };
 
 /// Geometry of one mode product over a colex tensor: fibers are indexed by
@@ -38,26 +40,34 @@ struct ModeGeom {
     int m = 0;            // output mode size (rows of J; == n for the square FD factors)
 };
 
-/// Kernel tiling chosen on the host from n (see choose_tiling in fd_kernels.cu).
+/// Kernel tiling chosen on the host (choose_mode_tiling / choose_time_tiling).
+/// One CTA computes MI*WM*8 rows (a "row block") x BN fibers; warps are WM x WN, each owning
+/// MI 8-row strips x NI 8-fiber tiles.  J is streamed in 16-column chunks through `nstage`
+/// cp.async stages together with the matching 16-row chunk of the fiber tile.
 struct Tiling {
     int MI = 1, WM = 1, NI = 2, WN = 4;
-    int S = 1;      // 8-row strips covering n (ceil(n/8))
-    int Mp = 8;     // padded rows of J = 8*MI*WM
-    int Kp = 4;     // padded contraction length = round_up(n, 4)
-    int Xrows = 4;  // rows of the smem tile = max(Kp, m)
-    int BN = 64;    // fibers per CTA = 8*NI*WN
-    int LDX = 68;   // smem row stride of the fiber tile (== 4 mod 16 doubles)
+    int S = 1;        // 8-row strips covering m (ceil(m/8))
+    int RB = 1;       // row blocks (mode kernel only; the time kernel keeps all rows in one CTA)
+    int MpB = 8;      // J rows per CTA = 8*MI*WM
+    int Mp = 8;       // padded rows of the uploaded J = RB*MpB
+    int Kp = 4;       // padded contraction length = round_up(n, 4)
+    int BN = 64;      // fibers per CTA = 8*NI*WN (power of two)
+    int LDX = 68;     // smem row stride of a fiber chunk (== 4 mod 16 doubles)
+    int Zrows = 0;    // time kernel: rows of the resident Z tile (= Kp)
+    int nstage = 3;
+    bool prescale = false;  // mode kernel: D^-1/2 staged through smem with the fiber chunk
     size_t smem = 0;
+    int ctas_per_sm = 1;
     int threads() const { return 32 * WM * WN; }
 };
 
-Tiling choose_tiling(int m, int n);  // m output rows, n contraction length
+Tiling choose_mode_tiling(int m, int n, bool prescale);  // m output rows, n contraction length
+Tiling choose_time_tiling(int n_t);
 
 /// Y = (I (x) J (x) I) X along one mode.  J is row-major, zero padded to (t.Mp x t.Kp).
-/// pre_scale (input) / post_scale (output) are optional elementwise factors (D^-1/2).
+/// pre_scale (optional, requires t.prescale) multiplies X elementwise before the product.
 cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y,
-                                const double* Jpad, const double* pre_scale, const double* post_scale,
-                                cudaStream_t stream);
+                                const double* Jpad, const double* pre_scale, cudaStream_t stream);
 
 /// Time-fused kernel: per spatial index, Z = U_t^T x, arrowhead solve, y = U_t Z.
 /// Jt_pad = U_t^T padded, J_pad = U_t padded (both row-major Mp x Kp).
@@ -65,7 +75,7 @@ cudaError_t launch_time_fused(const Tiling& t, const ModeGeom& g, const double* 
                               const double* Jt_pad, const double* J_pad, const ArrowParams& ap,
                               cudaStream_t stream);
 
-/// Elementwise y = a .* x (used when a scaling cannot be fused).
+/// Elementwise y = a .* x (the D^-1/2 post-scale of the last backward pass).
 cudaError_t launch_scale(const double* a, const double* x, double* y, long long n, cudaStream_t stream);
 
 }  // namespace gpu
