@@ -241,9 +241,9 @@ def run_ours(args):
     d, nt, ns = cfg.d, cfg.n_t, cfg.n_s
     names = [f"fwd_mode{m}" for m in range(d)] + ["time_fused"] + [f"bwd_mode{m}" for m in range(d)]
     flops = [2.0 * ns * n] * d + [4.0 * nt * n] + [2.0 * ns * n] * d
-    if launches > len(names):
-        names.append("post_scale")  # D^-1/2 elementwise (HBM-bound, 24 B/DoF)
-        flops.append(0.0)
+    if launches > len(names):  # D^-1/2 pre/post scale (elementwise, HBM-bound, 24 B/DoF each)
+        names = ["pre_scale"] + names + ["post_scale"]
+        flops = [0.0] + flops + [0.0]
     dom = int(np.argmax(pass_ms))
     achieved = flops[dom] / (pass_ms[dom] * 1e-3) / 1e12
     traffic = None

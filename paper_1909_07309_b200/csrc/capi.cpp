@@ -130,7 +130,6 @@ struct stiga_fd_s {
     std::vector<int> dims;  // n_1..n_d, n_t
     long long n_dof = 0, n_s = 0;
     std::vector<gpu::Tiling> tl;        // per spatial direction
-    gpu::Tiling tl_pre;                 // direction 0 with the D^-1/2 pre-scale staged in smem
     gpu::Tiling tl_t;
     std::vector<std::unique_ptr<DBuf>> Jt, J;  // padded U_l^T, U_l
     DBuf Jt_t, J_t;
@@ -149,37 +148,35 @@ struct stiga_fd_s {
         return g;
     }
 
-    int launches() const { return 2 * d + 1 + (dinv.p ? 1 : 0); }
+    int launches() const { return 2 * d + 1 + (dinv.p ? 2 : 0); }
 
-    // 2d+1 GEMM launches: forward spatial modes (D^-1/2 staged into the first), the time-fused
-    // kernel, backward spatial modes; then the D^-1/2 post-scale (fdsolve.cpp:158-163).  The
-    // reference back transform applies U_1..U_d, U_t; Kronecker factors on distinct modes commute,
-    // so applying U_t first (fused with the arrowhead) is equal in exact arithmetic.
+    // Launch sequence (fdsolve.cpp:158-163): [D^-1/2 pre-scale], forward spatial modes U_l^T, the
+    // time-fused kernel (U_t^T, arrowhead solve, U_t), backward spatial modes U_l, [D^-1/2
+    // post-scale].  The reference back transform applies U_1..U_d, U_t; Kronecker factors on distinct
+    // modes commute, so applying U_t first (fused with the arrowhead) is equal in exact arithmetic.
+    // Intermediates ping-pong between two handle-owned scratch vectors, so d_r may equal d_s.
     void apply(const double* in, double* out, cudaStream_t st, std::vector<cudaEvent_t>* ev) {
-        if (in == out && !scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
-        double* bufs[2] = {(in == out) ? scratch2.p : out, scratch.p};
+        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
+        double* bufs[2] = {scratch.p, scratch2.p};
         const bool scaled = dinv.p != nullptr;
-        const int gemm_passes = 2 * d + 1;
+        const int nops = launches();
         const double* src = in;
         int e = 0;
-        for (int k = 0; k < gemm_passes; ++k) {
-            double* dst = (k == gemm_passes - 1 && !scaled) ? out : bufs[k % 2];
+        for (int k = 0; k < nops; ++k) {
+            double* dst = (k == nops - 1) ? out : bufs[k % 2];
             if (ev) ck(cudaEventRecord((*ev)[e++], st), "event");
-            if (k < d) {
-                const bool pre = (k == 0) && scaled;
-                ck(gpu::launch_mode_product(pre ? tl_pre : tl[k], geom(k), src, dst, Jt[k]->p, pre ? dinv.p : nullptr, st),
-                   "fd forward mode product");
-            } else if (k == d) {
+            const int g = scaled ? k - 1 : k;  // index of the GEMM pass
+            if (scaled && (k == 0 || k == nops - 1)) {
+                ck(gpu::launch_scale(dinv.p, src, dst, n_dof, st), "fd D^-1/2 scale");
+            } else if (g < d) {
+                ck(gpu::launch_mode_product(tl[g], geom(g), src, dst, Jt[g]->p, nullptr, st), "fd forward mode product");
+            } else if (g == d) {
                 ck(gpu::launch_time_fused(tl_t, geom(d), src, dst, Jt_t.p, J_t.p, ap, st), "fd time-fused kernel");
             } else {
-                const int m = k - d - 1;
+                const int m = g - d - 1;
                 ck(gpu::launch_mode_product(tl[m], geom(m), src, dst, J[m]->p, nullptr, st), "fd backward mode product");
             }
             src = dst;
-        }
-        if (scaled) {
-            if (ev) ck(cudaEventRecord((*ev)[e++], st), "event");
-            ck(gpu::launch_scale(dinv.p, src, out, n_dof, st), "fd post-scale");
         }
         if (ev) ck(cudaEventRecord((*ev)[e], st), "event");
     }
@@ -379,10 +376,9 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         }
 
         DeviceGuard dg(device);
-        h->tl_pre = gpu::choose_mode_tiling(F.n[0], F.n[0], true);
         for (int l = 0; l < d; ++l) {
             h->tl.push_back(gpu::choose_mode_tiling(F.n[l], F.n[l], false));
-            const int rows = std::max(h->tl.back().Mp, l == 0 ? h->tl_pre.Mp : 0);
+            const int rows = h->tl.back().Mp;
             h->Jt.emplace_back(new DBuf);
             h->J.emplace_back(new DBuf);
             h->Jt.back()->upload(pad_factor(F.U[l], true, rows, h->tl.back().Kp));

@@ -1,13 +1,15 @@
 // FP64 tensor-core kernels of the extended-FD apply (sm_100a).
 //
 // Every mode product is a batch of small GEMMs  Y_fiber = J * X_fiber  with J the n x n
-// eigenvector factor (n = 16..260).  A CTA owns a row block of J (MI*WM 8-row strips) and BN
-// fibers.  Both operands stream through an `nstage`-deep cp.async pipeline in 16-wide
+// eigenvector factor (n = 16..260).  A CTA owns a row block of J (MI*WM 8-row strips) and
+// BN = 16*WN fibers.  Both operands stream through a 2-3 stage cp.async pipeline in 16-wide
 // contraction chunks (J chunk: rows x 16 from L2, fiber chunk: 16 x BN from HBM), the products
 // run on the FP64 tensor cores (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4; 36.9 TF/s measured on
 // B200 vs 34.0 TF/s for DFMA, profiles/r01_fp64_peak.txt) with fragments double-buffered in
 // registers, and the accumulators are stored straight from registers (no smem epilogue), so
-// several CTAs per SM overlap one tile's epilogue with another's main loop.
+// several CTAs per SM overlap one tile's epilogue with another's main loop.  All per-chunk
+// producer work is compile-time unrolled (element counts follow from MI/WM/WN) so the issue
+// slots go to LDS + DMMA.
 //
 // The time-fused kernel keeps the whole n_t x BN tile of one CTA: Z = U_t^T X lands in shared
 // memory, the block-arrowhead solve of fdsolve.cpp:24-65 (forward pair eliminations, diagonal
@@ -27,7 +29,6 @@ namespace {
 
 constexpr int kBK = 16;        // contraction chunk per pipeline stage
 constexpr int kLDJ = kBK + 4;  // smem row stride of a J chunk (20 == 4 mod 16: conflict-free A fragments)
-constexpr int kMaxThreads = 256;
 constexpr size_t kSmemPerSM = 228 * 1024;
 constexpr size_t kSmemPerCTA = 227 * 1024;
 
@@ -37,14 +38,20 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
         : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async8(unsigned s, const double* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+
+__device__ __forceinline__ void cp_async8_zfill(unsigned s, const double* gmem, bool valid) {
     const int sz = valid ? 8 : 0;  // src-size 0 -> zero fill
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
 
-__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+__device__ __forceinline__ void cp_async16(unsigned s, const double* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 
@@ -55,22 +62,28 @@ __device__ __forceinline__ void cp_wait_n() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// wait until at most (nstage - 2) groups are pending
-__device__ __forceinline__ void cp_wait_stage(int nstage) {
-    if (nstage >= 4) cp_wait_n<2>();
-    else if (nstage == 3) cp_wait_n<1>();
-    else cp_wait_n<0>();
-}
-
 struct KArgs {
     ModeGeom geo;
-    int S, MpB, Kp, BN, bn_log2, LDX, WM, WN, nstage, RB, Zrows;
-    int prescale;
+    int Kp, RB, Zrows, nstage;
 };
 
-__device__ __forceinline__ int stage_doubles(const KArgs& a) {
-    return kBK * a.LDX + a.MpB * kLDJ + (a.prescale ? kBK * a.LDX : 0);
-}
+// Compile-time shape of a CTA.
+template <int MI_, int WM_, int WN_>
+struct Shape {
+    static constexpr int MI = MI_, WM = WM_, WN = WN_, NI = 2;
+    static constexpr int NTHR = 32 * WM * WN;
+    static constexpr int BN = 16 * WN;
+    static constexpr int LDX = BN + 4;  // == 4 mod 16
+    static constexpr int MPB = 8 * MI * WM;
+    static constexpr int XCNT = kBK * BN / NTHR;       // fiber-chunk elements per thread (8/WM)
+    static constexpr int JPIECES = MPB * (kBK / 2);    // 16-byte J pieces per chunk
+    static constexpr int JROWSTEP = NTHR / 8;          // J rows between a thread's pieces
+    static constexpr int JCNT = (JPIECES + NTHR - 1) / NTHR;
+    static constexpr int XROWSTEP = NTHR / BN;         // fiber-chunk rows between elements (L > 1)
+    static constexpr int XCOLSTEP = NTHR / 16;         // fibers between elements (L == 1)
+    static constexpr int STAGE = kBK * LDX + MPB * kLDJ;  // doubles per pipeline stage
+    static_assert(kBK * BN % NTHR == 0, "fiber chunk must split evenly over the CTA");
+};
 
 // Global offset of element 0 of fiber cc (colex: l + L*n*r).
 __device__ __forceinline__ long long fiber_base(long long cc, long long L, int n) {
@@ -79,113 +92,109 @@ __device__ __forceinline__ long long fiber_base(long long cc, long long L, int n
     return (cc - r * L) + L * static_cast<long long>(n) * r;
 }
 
-// Per-thread producer state of the fiber-chunk copies (precomputed once per tile, so a chunk
-// costs a handful of integer ops per element).  Element u of this thread:
-//   L == 1 (fibers contiguous): row j = tid % 16 (fixed), fiber c = tid/16 + u*nthr/16;
-//   L  > 1 (fibers strided):    fiber c = tid % BN (fixed), row j = tid/BN + u*nthr/BN.
-struct XProd {
-    int cnt;               // elements per thread per chunk
-    unsigned emask;        // element u exists (lies inside the 16 x BN chunk)
-    unsigned umask;        // ... and its fiber is inside the tensor
-    int row0, row_step;    // row of element u within a chunk = row0 + u*row_step
-    int s_off, s_step;     // smem offsets (doubles) within a chunk
-    long long g_off, g_step, g_kstep;  // global element offsets
+// Per-thread producer state, computed once per tile.
+//  fiber chunk, L == 1 (fibers contiguous): row j = tid % 16, fiber c = tid/16 + u*NTHR/16;
+//  fiber chunk, L  > 1 (fibers strided):    fiber c = tid % BN, row j = tid/BN + u*NTHR/BN;
+//  J chunk: piece tid % 8 of rows tid/8 + u*NTHR/8.
+struct Prod {
+    const double* xg;    // global address of element u = 0 for chunk 0
+    long long xstep;     // global stride between elements u (elements)
+    long long xkstep;    // global stride between chunks (elements)
+    unsigned xs;         // smem byte offset (within a stage) of element u = 0
+    int xrow0;           // chunk row of element u = 0 (row check for the tail chunk)
+    unsigned colmask;    // element u belongs to a fiber inside the tensor
+    bool full_tile;
+    bool contiguous;     // L == 1
+    const double* jg;    // J global address of this thread's piece u = 0 for chunk 0
+    unsigned js;         // smem byte offset (within a stage) of piece u = 0
+    int jp2;             // 2 * piece index (column offset within the chunk)
 };
 
-__device__ __forceinline__ XProd make_xprod(const KArgs& a, long long c0) {
-    XProd x;
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    const int total = kBK * a.BN;
-    x.cnt = (total + nthr - 1) / nthr;
-    x.umask = 0;
-    x.emask = 0;
-    if (a.geo.L == 1) {
-        const int j = tid & (kBK - 1), cf = tid >> 4, cstep = nthr >> 4;
-        x.row0 = j;
-        x.row_step = 0;
-        x.s_off = j * a.LDX + cf;
-        x.s_step = cstep;
-        x.g_off = (c0 + cf) * a.geo.n + j;
-        x.g_step = static_cast<long long>(cstep) * a.geo.n;
-        x.g_kstep = kBK;
-        for (int u = 0; u < x.cnt; ++u) {
-            const int c = cf + u * cstep;
-            if (c < a.BN) x.emask |= 1u << u;
-            if (c < a.BN && c0 + c < a.geo.ncols) x.umask |= 1u << u;
-        }
+template <class SH>
+__device__ __forceinline__ Prod make_prod(const KArgs& a, long long c0, const double* X, const double* Jg) {
+    Prod p;
+    const int tid = threadIdx.x;
+    p.colmask = 0;
+    p.full_tile = c0 + SH::BN <= a.geo.ncols;
+    p.contiguous = a.geo.L == 1;
+    if (p.contiguous) {
+        const int j = tid & (kBK - 1), cf = tid >> 4;
+        p.xrow0 = j;
+        p.xs = 8u * (j * SH::LDX + cf);
+        p.xg = X + (c0 + cf) * a.geo.n + j;
+        p.xstep = static_cast<long long>(SH::XCOLSTEP) * a.geo.n;
+        p.xkstep = kBK;
+#pragma unroll
+        for (int u = 0; u < SH::XCNT; ++u)
+            if (c0 + cf + u * SH::XCOLSTEP < a.geo.ncols) p.colmask |= 1u << u;
     } else {
-        const int c = tid & (a.BN - 1), j0 = tid >> a.bn_log2, jstep = nthr >> a.bn_log2;
-        x.row0 = j0;
-        x.row_step = jstep;
-        x.s_off = j0 * a.LDX + c;
-        x.s_step = jstep * a.LDX;
+        const int c = tid & (SH::BN - 1), j0 = tid / SH::BN;
         const long long cc = c0 + c;
         const bool cv = cc < a.geo.ncols;
-        x.g_off = fiber_base(cv ? cc : 0, a.geo.L, a.geo.n) + a.geo.L * j0;
-        x.g_step = a.geo.L * jstep;
-        x.g_kstep = a.geo.L * kBK;
-        for (int u = 0; u < x.cnt; ++u) {
-            if (j0 + u * jstep < kBK) x.emask |= 1u << u;
-            if (cv && j0 + u * jstep < kBK) x.umask |= 1u << u;
-        }
+        p.xrow0 = j0;
+        p.xs = 8u * (j0 * SH::LDX + c);
+        p.xg = X + fiber_base(cv ? cc : 0, a.geo.L, a.geo.n) + a.geo.L * j0;
+        p.xstep = a.geo.L * SH::XROWSTEP;
+        p.xkstep = a.geo.L * kBK;
+        p.colmask = cv ? 0xffffffffu : 0u;
     }
-    return x;
+    p.jp2 = 2 * (tid & 7);
+    p.js = 8u * ((tid >> 3) * kLDJ + p.jp2);
+    p.jg = Jg + static_cast<size_t>(tid >> 3) * a.Kp + p.jp2;
+    return p;
 }
 
-struct JProd {
-    int cnt;          // 16-byte pieces per thread per chunk
-    int p2;           // 2 * (piece index within the row) (fixed per thread)
-    int r0, rstep;    // row of piece u = r0 + u*rstep
-};
-
-__device__ __forceinline__ JProd make_jprod(const KArgs& a) {
-    JProd j;
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    j.cnt = (a.MpB * 8 + nthr - 1) / nthr;
-    j.p2 = 2 * (tid & 7);
-    j.r0 = tid >> 3;
-    j.rstep = nthr >> 3;
-    return j;
-}
-
-__device__ __forceinline__ void issue_x(const KArgs& a, const XProd& x, double* Xc, double* Dc,
-                                        const double* __restrict__ X, const double* __restrict__ D, int q) {
-    const int k0 = q * kBK;
-    const long long gq = x.g_off + q * x.g_kstep;
-    for (int u = 0; u < x.cnt; ++u) {
-        if (!((x.emask >> u) & 1u)) continue;  // outside the chunk: must not touch smem
-        const bool v = ((x.umask >> u) & 1u) && (k0 + x.row0 + u * x.row_step < a.geo.n);
-        const long long gi = gq + u * x.g_step;
-        const int so = x.s_off + u * x.s_step;
-        cp_async8(Xc + so, v ? X + gi : X, v);
-        if (Dc) cp_async8(Dc + so, v ? D + gi : D, v);
-    }
-}
-
-__device__ __forceinline__ void prescale_own(const XProd& x, double* Xc, const double* Dc) {
-    for (int u = 0; u < x.cnt; ++u) {
-        const int so = x.s_off + u * x.s_step;
-        if ((x.umask >> u) & 1u) Xc[so] *= Dc[so];
-    }
-}
-
-__device__ __forceinline__ void issue_j(const KArgs& a, const JProd& jp, double* Jc, const double* __restrict__ Jg,
-                                        int q) {
+// Issues the J (and optionally fiber) copies of chunk q into the stage at smem byte address st.
+template <class SH>
+__device__ __forceinline__ void issue_chunk(const KArgs& a, const Prod& p, unsigned st, int q, bool load_x,
+                                            const double* X) {
     const int k0 = q * kBK;
     const int kw = min(kBK, a.Kp - k0);
-    if (jp.p2 >= kw) return;
-    const double* src = Jg + k0 + jp.p2;
-    for (int u = 0; u < jp.cnt; ++u) {
-        const int r = jp.r0 + u * jp.rstep;
-        if (r < a.MpB) cp_async16(Jc + r * kLDJ + jp.p2, src + static_cast<size_t>(r) * a.Kp);
+    if (p.jp2 < kw) {
+        const double* jg = p.jg + k0;
+        const unsigned js = st + 8u * kBK * SH::LDX + p.js;
+#pragma unroll
+        for (int u = 0; u < SH::JCNT; ++u) {
+            if ((u + 1) * SH::NTHR <= SH::JPIECES || (threadIdx.x >> 3) + u * SH::JROWSTEP < SH::MPB)
+                cp_async16(js + 8u * u * SH::JROWSTEP * kLDJ, jg + static_cast<size_t>(u) * SH::JROWSTEP * a.Kp);
+        }
+    }
+    if (!load_x) return;
+    const double* xg = p.xg + q * p.xkstep;
+    const unsigned xs = st + p.xs;
+    if (p.contiguous) {
+        if (p.full_tile && k0 + kBK <= a.geo.n) {
+#pragma unroll
+            for (int u = 0; u < SH::XCNT; ++u) cp_async8(xs + 8u * u * SH::XCOLSTEP, xg + u * p.xstep);
+        } else {
+            const bool rowv = k0 + p.xrow0 < a.geo.n;
+#pragma unroll
+            for (int u = 0; u < SH::XCNT; ++u) {
+                const bool v = rowv && ((p.colmask >> u) & 1u);
+                cp_async8_zfill(xs + 8u * u * SH::XCOLSTEP, v ? xg + u * p.xstep : X, v);
+            }
+        }
+    } else {
+        if (p.full_tile && k0 + kBK <= a.geo.n) {
+#pragma unroll
+            for (int u = 0; u < SH::XCNT; ++u) cp_async8(xs + 8u * u * SH::XROWSTEP * SH::LDX, xg + u * p.xstep);
+        } else {
+            const bool colv = p.colmask != 0u;
+#pragma unroll
+            for (int u = 0; u < SH::XCNT; ++u) {
+                const bool v = colv && (k0 + p.xrow0 + u * SH::XROWSTEP < a.geo.n);
+                cp_async8_zfill(xs + 8u * u * SH::XROWSTEP * SH::LDX, v ? xg + u * p.xstep : X, v);
+            }
+        }
     }
 }
 
 // acc += J_chunk * B_chunk over KS k-steps of 4.  A fragments from the J stage (ja), B fragments
-// from bb (row stride ldb).  Fragments double-buffered in registers; no predicates (padded J
+// from bb (row stride LDX).  Fragments double-buffered in registers; no predicates (padded J
 // rows are zero, so padded strips just produce zeros that are never stored).
-template <int MI, int NI, int KS>
-__device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, int ldb, double (&acc)[MI][NI][2]) {
+template <class SH, int KS>
+__device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, double (&acc)[SH::MI][SH::NI][2]) {
+    constexpr int MI = SH::MI, NI = SH::NI;
     double av[2][MI], bv[2][NI];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) av[0][mi] = ja[mi * 8 * kLDJ];
@@ -198,7 +207,7 @@ __device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, in
 #pragma unroll
             for (int mi = 0; mi < MI; ++mi) av[nxt][mi] = ja[mi * 8 * kLDJ + (kk + 1) * 4];
 #pragma unroll
-            for (int ni = 0; ni < NI; ++ni) bv[nxt][ni] = bb[(kk + 1) * 4 * ldb + ni * 8];
+            for (int ni = 0; ni < NI; ++ni) bv[nxt][ni] = bb[(kk + 1) * 4 * SH::LDX + ni * 8];
         }
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi)
@@ -207,43 +216,32 @@ __device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, in
     }
 }
 
-template <int MI, int NI>
-__device__ __forceinline__ void mma_chunk_any(int ksteps, const double* ja, const double* bb, int ldb,
-                                              double (&acc)[MI][NI][2]) {
-    switch (ksteps) {
-        case 4: mma_chunk<MI, NI, 4>(ja, bb, ldb, acc); break;
-        case 3: mma_chunk<MI, NI, 3>(ja, bb, ldb, acc); break;
-        case 2: mma_chunk<MI, NI, 2>(ja, bb, ldb, acc); break;
-        default: mma_chunk<MI, NI, 1>(ja, bb, ldb, acc); break;
-    }
-}
-
 // Register epilogue: acc rows (< m) of the CTA's row block straight to global memory.
-template <int MI, int NI>
-__device__ __forceinline__ void store_acc(const KArgs& a, const double (&acc)[MI][NI][2], long long c0, int strip0,
-                                          double* __restrict__ Y) {
+template <class SH>
+__device__ __forceinline__ void store_acc(const KArgs& a, const double (&acc)[SH::MI][SH::NI][2], long long c0,
+                                          int strip0, double* __restrict__ Y) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int wm = warp % a.WM, wn = warp / a.WM;
+    const int wm = warp % SH::WM, wn = warp / SH::WM;
     const int g = lane >> 2, t = lane & 3;
     const int m = a.geo.m;
-    long long ob[NI][2];
-    bool cv[NI][2];
+    long long ob[SH::NI][2];
+    bool cv[SH::NI][2];
 #pragma unroll
-    for (int ni = 0; ni < NI; ++ni)
+    for (int ni = 0; ni < SH::NI; ++ni)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-            const long long cc = c0 + (wn * NI + ni) * 8 + 2 * t + v;
+            const long long cc = c0 + (wn * SH::NI + ni) * 8 + 2 * t + v;
             cv[ni][v] = cc < a.geo.ncols;
             ob[ni][v] = fiber_base(cv[ni][v] ? cc : 0, a.geo.L, m);
         }
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi) {
-        const int i = (strip0 + wm * MI + mi) * 8 + g;
+    for (int mi = 0; mi < SH::MI; ++mi) {
+        const int i = (strip0 + wm * SH::MI + mi) * 8 + g;
         if (i < m) {
             const long long off = a.geo.L * i;
 #pragma unroll
-            for (int ni = 0; ni < NI; ++ni)
+            for (int ni = 0; ni < SH::NI; ++ni)
 #pragma unroll
                 for (int v = 0; v < 2; ++v)
                     if (cv[ni][v]) Y[ob[ni][v] + off] = acc[mi][ni][v];
@@ -251,92 +249,79 @@ __device__ __forceinline__ void store_acc(const KArgs& a, const double (&acc)[MI
     }
 }
 
-template <int MI, int NI>
-__device__ __forceinline__ void zero_acc(double (&acc)[MI][NI][2]) {
+template <class SH>
+__device__ __forceinline__ void zero_acc(double (&acc)[SH::MI][SH::NI][2]) {
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi)
+    for (int mi = 0; mi < SH::MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        for (int ni = 0; ni < SH::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+}
+
+__device__ __forceinline__ void cp_wait_stage(int nstage) {
+    if (nstage >= 3) cp_wait_n<1>();
+    else cp_wait_n<0>();
 }
 
 // Multistage GEMM over the full contraction.  X_STREAM: the fiber operand streams through the
-// stages with J; otherwise it is resident in smem at Bres (row stride a.LDX) and only J streams.
-template <int MI, int NI, bool X_STREAM>
-__device__ __forceinline__ void gemm(const KArgs& a, double* stages, const double* __restrict__ Jg,
-                                     const double* __restrict__ X, const double* __restrict__ D, const double* Bres,
-                                     const XProd& xp, const JProd& jp, bool prologue_issued, double (&acc)[MI][NI][2]) {
+// stages with J; otherwise it is resident in smem at Bres (row stride LDX) and only J streams.
+template <class SH, bool X_STREAM>
+__device__ __forceinline__ void gemm(const KArgs& a, double* stages, const Prod& p, const double* X, const double* Bres,
+                                     bool prologue_issued, double (&acc)[SH::MI][SH::NI][2]) {
     const int nchunks = (a.Kp + kBK - 1) / kBK;
-    const int sd = stage_doubles(a);
     const int ns = a.nstage;
-    const int LDX = a.LDX;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = warp % a.WM, wn = warp / a.WM;
+    const int wm = warp % SH::WM, wn = warp / SH::WM;
     const int g = lane >> 2, t = lane & 3;
-    const int ja_off = kBK * LDX + (wm * MI * 8 + g) * kLDJ + t;  // within a stage
-    const int bb_off = t * LDX + wn * NI * 8 + g;
-    const int dc_off = kBK * LDX + a.MpB * kLDJ;
+    const int ja_off = kBK * SH::LDX + (wm * SH::MI * 8 + g) * kLDJ + t;  // within a stage
+    const int bb_off = t * SH::LDX + wn * SH::NI * 8 + g;
+    const unsigned st0 = smem_u32(stages);
     if (!prologue_issued) {
         for (int s = 0; s < ns - 1; ++s) {
-            if (s < nchunks) {
-                double* st = stages + static_cast<size_t>(s) * sd;
-                issue_j(a, jp, st + kBK * LDX, Jg, s);
-                if (X_STREAM) issue_x(a, xp, st, D ? st + dc_off : nullptr, X, D, s);
-            }
+            if (s < nchunks) issue_chunk<SH>(a, p, st0 + 8u * s * SH::STAGE, s, X_STREAM, X);
             cp_commit();
         }
     }
     int stage = 0;
     for (int q = 0; q < nchunks; ++q) {
         cp_wait_stage(ns);
-        double* st = stages + static_cast<size_t>(stage) * sd;
-        if (X_STREAM && D) prescale_own(xp, st, st + dc_off);
         __syncthreads();
         const int nq = q + ns - 1;
         if (nq < nchunks) {
             int nst = stage + ns - 1;
             if (nst >= ns) nst -= ns;
-            double* sn = stages + static_cast<size_t>(nst) * sd;
-            issue_j(a, jp, sn + kBK * LDX, Jg, nq);
-            if (X_STREAM) issue_x(a, xp, sn, D ? sn + dc_off : nullptr, X, D, nq);
+            issue_chunk<SH>(a, p, st0 + 8u * nst * SH::STAGE, nq, X_STREAM, X);
         }
         cp_commit();
+        const double* st = stages + stage * SH::STAGE;
         const double* ja = st + ja_off;
-        const double* bb = X_STREAM ? st + bb_off : Bres + q * kBK * LDX + bb_off;
+        const double* bb = X_STREAM ? st + bb_off : Bres + q * kBK * SH::LDX + bb_off;
         const int ksteps = min(kBK, a.Kp - q * kBK) >> 2;
-        if (ksteps == 4)
-            mma_chunk<MI, NI, 4>(ja, bb, LDX, acc);
-        else
-            mma_chunk_any<MI, NI>(ksteps, ja, bb, LDX, acc);
+        if (ksteps == 4) {
+            mma_chunk<SH, 4>(ja, bb, acc);
+        } else if (ksteps == 3) {
+            mma_chunk<SH, 3>(ja, bb, acc);
+        } else if (ksteps == 2) {
+            mma_chunk<SH, 2>(ja, bb, acc);
+        } else {
+            mma_chunk<SH, 1>(ja, bb, acc);
+        }
         if (++stage == ns) stage = 0;
     }
 }
 
-// Issues the GEMM prologue (J chunks only) so it overlaps work done before gemm<..., false>.
-__device__ __forceinline__ void gemm_prologue_j(const KArgs& a, double* stages, const double* __restrict__ Jg,
-                                                const JProd& jp) {
-    const int nchunks = (a.Kp + kBK - 1) / kBK;
-    const int sd = stage_doubles(a);
-    for (int s = 0; s < a.nstage - 1; ++s) {
-        if (s < nchunks) issue_j(a, jp, stages + static_cast<size_t>(s) * sd + kBK * a.LDX, Jg, s);
-        cp_commit();
-    }
-}
-
-template <int MI, int NI>
-__global__ void __launch_bounds__(kMaxThreads)
-    mode_product_kernel(KArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
-                        const double* __restrict__ D) {
+template <int MI, int WN>
+__global__ void __launch_bounds__(32 * WN)
+    mode_product_kernel(KArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J) {
+    using SH = Shape<MI, 1, WN>;
     extern __shared__ __align__(16) double smem[];
     const int rb = blockIdx.x % a.RB;  // row blocks of one fiber tile are adjacent -> X tile reused from L2
-    const long long c0 = static_cast<long long>(blockIdx.x / a.RB) * a.BN;
-    const int strip0 = rb * MI * a.WM;
-    const double* Jg = J + static_cast<size_t>(rb) * a.MpB * a.Kp;
-    const XProd xp = make_xprod(a, c0);
-    const JProd jp = make_jprod(a);
-    double acc[MI][NI][2];
-    zero_acc(acc);
-    gemm<MI, NI, true>(a, smem, Jg, X, D, nullptr, xp, jp, false, acc);
-    store_acc(a, acc, c0, strip0, Y);
+    const long long c0 = static_cast<long long>(blockIdx.x / a.RB) * SH::BN;
+    const double* Jg = J + static_cast<size_t>(rb) * SH::MPB * a.Kp;
+    const Prod p = make_prod<SH>(a, c0, X, Jg);
+    double acc[SH::MI][SH::NI][2];
+    zero_acc<SH>(acc);
+    gemm<SH, true>(a, smem, p, X, nullptr, false, acc);
+    store_acc<SH>(a, acc, c0, rb * MI, Y);
 }
 
 // apply_pair_inverse (fdsolve.cpp:11-20) with R_j^-1 recomputed from Lambda_s (fdsolve.cpp:114-119).
@@ -350,12 +335,13 @@ __device__ __forceinline__ void pair_inverse(double lam, double linv, double nu,
 }
 
 // Block-arrowhead solve (fdsolve.cpp:24-65) on the resident tile: column c = one spatial
-// eigen-index, rows = time eigen-coordinates.  P threads share a column (pairs j = p mod P).
+// eigen-index, rows = time eigen-coordinates.  P = NTHR/BN = 2*WM threads share a column
+// (pairs j = p mod P, Schur right-hand side reduced with shuffles).
+template <class SH>
 __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long long c0, const ArrowParams& ap) {
-    int P = 1;
-    while (P < 32 && 2 * P * a.BN <= static_cast<int>(blockDim.x)) P *= 2;
+    constexpr int P = SH::NTHR / SH::BN;
+    static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "threads per column must be a power of two <= 32");
     const int tid = threadIdx.x;
-    if (tid >= P * a.BN) return;  // whole warps (P*BN is a multiple of 16; BN >= 16)
     const int c = tid / P;
     const int p = tid - c * P;
     long long s = c0 + c;
@@ -370,81 +356,89 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
     const double linv = 1.0 / lam;
     const double nu = ap.nu, gam = ap.gamma;
     const int nt = ap.n_t;
-    const int LD = a.LDX;
     double* col = Zs + c;
-    const double slast = col[(nt - 1) * LD];
+    const double slast = col[(nt - 1) * SH::LDX];
     double part = 0.0;
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
-        pair_inverse(lam, linv, nu, __ldg(ap.pair_c + j), __ldg(ap.pair_c1 + j), col[(2 * j) * LD],
-                     col[(2 * j + 1) * LD], xa, xb);
-        col[(2 * j) * LD] = xa;
-        col[(2 * j + 1) * LD] = xb;
+        pair_inverse(lam, linv, nu, __ldg(ap.pair_c + j), __ldg(ap.pair_c1 + j), col[(2 * j) * SH::LDX],
+                     col[(2 * j + 1) * SH::LDX], xa, xb);
+        col[(2 * j) * SH::LDX] = xa;
+        col[(2 * j + 1) * SH::LDX] = xb;
         part += gam * (__ldg(ap.g + 2 * j) * xa + __ldg(ap.g + 2 * j + 1) * xb);
     }
     if (ap.zero_count && p == 0) {
         const int z = nt - 2;
-        const double xz = linv * col[z * LD] / nu;
-        col[z * LD] = xz;
+        const double xz = linv * col[z * SH::LDX] / nu;
+        col[z * SH::LDX] = xz;
         part += gam * __ldg(ap.g + z) * xz;
     }
-    const unsigned mask = (P * a.BN >= 32) ? 0xffffffffu : ((1u << (P * a.BN)) - 1u);
-    for (int off = P >> 1; off > 0; off >>= 1) part += __shfl_xor_sync(mask, part, off);
+#pragma unroll
+    for (int off = P >> 1; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
     const double xlast = __ldg(ap.S_inv + s) * (slast + part);
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
         pair_inverse(lam, linv, nu, __ldg(ap.pair_c + j), __ldg(ap.pair_c1 + j),
                      (gam * __ldg(ap.g + 2 * j)) * xlast, (gam * __ldg(ap.g + 2 * j + 1)) * xlast, xa, xb);
-        col[(2 * j) * LD] -= xa;
-        col[(2 * j + 1) * LD] -= xb;
+        col[(2 * j) * SH::LDX] -= xa;
+        col[(2 * j + 1) * SH::LDX] -= xb;
     }
     if (p == 0) {
         if (ap.zero_count) {
             const int z = nt - 2;
-            col[z * LD] -= (gam * __ldg(ap.g + z) / nu) * (linv * xlast);
+            col[z * SH::LDX] -= (gam * __ldg(ap.g + z) / nu) * (linv * xlast);
         }
-        col[(nt - 1) * LD] = xlast;
+        col[(nt - 1) * SH::LDX] = xlast;
     }
 }
 
-template <int MI, int NI>
-__global__ void __launch_bounds__(kMaxThreads)
+template <int MI, int WM, int WN>
+__global__ void __launch_bounds__(32 * WM * WN)
     time_fused_kernel(KArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ Jt,
                       const double* __restrict__ J, ArrowParams ap) {
+    using SH = Shape<MI, WM, WN>;
     extern __shared__ __align__(16) double smem[];
-    double* Zs = smem;                                             // Zrows x LDX, resident
-    double* stages = smem + static_cast<size_t>(a.Zrows) * a.LDX;  // nstage x stage
-    const long long c0 = static_cast<long long>(blockIdx.x) * a.BN;
-    const XProd xp = make_xprod(a, c0);
-    const JProd jp = make_jprod(a);
-    double acc[MI][NI][2];
-    zero_acc(acc);
-    gemm<MI, NI, true>(a, stages, Jt, X, nullptr, nullptr, xp, jp, false, acc);  // Z = U_t^T x
+    double* Zs = smem;                                               // Zrows x LDX, resident
+    double* stages = smem + static_cast<size_t>(a.Zrows) * SH::LDX;  // nstage x stage
+    const long long c0 = static_cast<long long>(blockIdx.x) * SH::BN;
+    Prod p = make_prod<SH>(a, c0, X, Jt);
+    double acc[SH::MI][SH::NI][2];
+    zero_acc<SH>(acc);
+    gemm<SH, true>(a, stages, p, X, nullptr, false, acc);  // Z = U_t^T x
     // Z -> smem (rows < Kp; padded rows are exact zeros because the padded J rows are zero)
     {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const int wm = warp % a.WM, wn = warp / a.WM;
+        const int wm = warp % WM, wn = warp / WM;
         const int g = lane >> 2, t = lane & 3;
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
             const int row = (wm * MI + mi) * 8 + g;
             if (row < a.Zrows) {
 #pragma unroll
-                for (int ni = 0; ni < NI; ++ni) {
-                    const int col = (wn * NI + ni) * 8 + 2 * t;
-                    Zs[row * a.LDX + col] = acc[mi][ni][0];
-                    Zs[row * a.LDX + col + 1] = acc[mi][ni][1];
+                for (int ni = 0; ni < SH::NI; ++ni) {
+                    const int col = (wn * SH::NI + ni) * 8 + 2 * t;
+                    Zs[row * SH::LDX + col] = acc[mi][ni][0];
+                    Zs[row * SH::LDX + col + 1] = acc[mi][ni][1];
                 }
             }
         }
     }
     __syncthreads();  // Z visible; every warp is done with the GEMM-1 stages
-    gemm_prologue_j(a, stages, J, jp);  // U_t chunks stream in while the arrowhead runs
-    if (!(ap.debug & 1)) arrowhead_tile(a, Zs, c0, ap);
+    // U_t chunks stream in while the arrowhead runs
+    p.jg = J + (p.jg - Jt);
+    {
+        const int nchunks = (a.Kp + kBK - 1) / kBK;
+        const unsigned st0 = smem_u32(stages);
+        for (int s = 0; s < a.nstage - 1; ++s) {
+            if (s < nchunks) issue_chunk<SH>(a, p, st0 + 8u * s * SH::STAGE, s, false, X);
+            cp_commit();
+        }
+    }
+    if (!(ap.debug & 1)) arrowhead_tile<SH>(a, Zs, c0, ap);
     __syncthreads();
-    zero_acc(acc);
-    gemm<MI, NI, false>(a, stages, J, nullptr, nullptr, Zs, xp, jp, true, acc);  // y = U_t z
-    store_acc(a, acc, c0, 0, Y);
+    zero_acc<SH>(acc);
+    gemm<SH, false>(a, stages, p, X, Zs, true, acc);  // y = U_t z
+    store_acc<SH>(a, acc, c0, 0, Y);
 }
 
 __global__ void scale_kernel(const double* __restrict__ a, const double* __restrict__ x, double* __restrict__ y,
@@ -464,119 +458,141 @@ __global__ void scale_kernel(const double* __restrict__ a, const double* __restr
 KArgs make_args(const Tiling& t, const ModeGeom& g) {
     KArgs a;
     a.geo = g;
-    a.S = t.S;
-    a.MpB = t.MpB;
     a.Kp = t.Kp;
-    a.BN = t.BN;
-    a.bn_log2 = 0;
-    while ((1 << a.bn_log2) < t.BN) ++a.bn_log2;
-    a.LDX = t.LDX;
-    a.WM = t.WM;
-    a.WN = t.WN;
-    a.nstage = t.nstage;
     a.RB = t.RB;
     a.Zrows = t.Zrows;
-    a.prescale = t.prescale ? 1 : 0;
+    a.nstage = t.nstage;
     return a;
 }
 
-// Resident CTAs per SM of an instantiation (exact occupancy query; falls back to a smem/thread
-// bound with a register estimate when no device is current).
+// Resident CTAs per SM of an instantiation (exact occupancy query; smem/thread bound when no
+// device is current).
 template <typename K>
-int occupancy(K kernel, int threads, size_t smem, int MI) {
+int occupancy(K kernel, int threads, size_t smem) {
     int n = 0;
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) ==
             cudaSuccess &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) == cudaSuccess)
         return n;
     cudaGetLastError();
-    const int regs = std::min(255, 16 * MI + 40);
-    const int by_smem = static_cast<int>(kSmemPerSM / (smem + 1024));
-    const int by_regs = 65536 / (threads * ((regs + 7) / 8 * 8));
-    return std::max(0, std::min({by_smem, 2048 / threads, by_regs}));
+    return std::max(0, std::min(static_cast<int>(kSmemPerSM / (smem + 1024)), 2048 / threads));
 }
 
-#define STIGA_MI_CASES(MI_, EXPR)                                                                    \
-    switch (MI_) {                                                                                   \
-        case 1: return EXPR(1); case 2: return EXPR(2); case 3: return EXPR(3); case 4: return EXPR(4); \
-        case 5: return EXPR(5); case 6: return EXPR(6); case 7: return EXPR(7); case 8: return EXPR(8); \
-        case 9: return EXPR(9); case 10: return EXPR(10); case 11: return EXPR(11);                  \
-        case 12: return EXPR(12); case 13: return EXPR(13);                                          \
-        default: return 0;                                                                           \
+// ---- instantiation dispatch --------------------------------------------------------------------
+template <int MI, int WN>
+cudaError_t launch_mode_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
+                          cudaStream_t st, int* occ) {
+    auto k = mode_product_kernel<MI, WN>;
+    if (occ) {
+        *occ = occupancy(k, 32 * WN, t.smem);
+        return cudaSuccess;
     }
-
-int mode_occupancy(int MI, int threads, size_t smem) {
-#define STIGA_OCC_MODE(M) occupancy(mode_product_kernel<M, 2>, threads, smem, M)
-    STIGA_MI_CASES(MI, STIGA_OCC_MODE)
-#undef STIGA_OCC_MODE
-}
-
-int time_occupancy(int MI, int threads, size_t smem) {
-#define STIGA_OCC_TIME(M) occupancy(time_fused_kernel<M, 2>, threads, smem, M)
-    STIGA_MI_CASES(MI, STIGA_OCC_TIME)
-#undef STIGA_OCC_TIME
-}
-
-template <int MI>
-cudaError_t launch_mode_mi(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                           const double* pre, cudaStream_t st) {
-    auto k = mode_product_kernel<MI, 2>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(t.smem));
     if (e != cudaSuccess) return e;
     const long long blocks = (g.ncols + t.BN - 1) / t.BN * t.RB;
-    k<<<static_cast<unsigned>(blocks), t.threads(), t.smem, st>>>(make_args(t, g), X, Y, J, pre);
+    k<<<static_cast<unsigned>(blocks), 32 * WN, t.smem, st>>>(make_args(t, g), X, Y, J);
     return cudaGetLastError();
 }
 
-template <int MI>
-cudaError_t launch_time_mi(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jt,
-                           const double* J, const ArrowParams& ap, cudaStream_t st) {
-    auto k = time_fused_kernel<MI, 2>;
+template <int MI, int WM, int WN>
+cudaError_t launch_time_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jt,
+                          const double* J, const ArrowParams& ap, cudaStream_t st, int* occ) {
+    auto k = time_fused_kernel<MI, WM, WN>;
+    if (occ) {
+        *occ = occupancy(k, 32 * WM * WN, t.smem);
+        return cudaSuccess;
+    }
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(t.smem));
     if (e != cudaSuccess) return e;
     const long long blocks = (g.ncols + t.BN - 1) / t.BN;
-    k<<<static_cast<unsigned>(blocks), t.threads(), t.smem, st>>>(make_args(t, g), X, Y, Jt, J, ap);
+    k<<<static_cast<unsigned>(blocks), 32 * WM * WN, t.smem, st>>>(make_args(t, g), X, Y, Jt, J, ap);
     return cudaGetLastError();
+}
+
+#define STIGA_MI_SWITCH(MI_, CALL)                                                                   \
+    switch (MI_) {                                                                                   \
+        case 1: return CALL(1); case 2: return CALL(2); case 3: return CALL(3); case 4: return CALL(4); \
+        case 5: return CALL(5); case 6: return CALL(6); case 7: return CALL(7); case 8: return CALL(8); \
+        case 9: return CALL(9); case 10: return CALL(10); case 11: return CALL(11);                  \
+        case 12: return CALL(12); case 13: return CALL(13);                                          \
+        default: return cudaErrorInvalidValue;                                                       \
+    }
+
+template <int WN>
+cudaError_t dispatch_mode_wn(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
+                             cudaStream_t st, int* occ) {
+#define STIGA_CALL_MODE(M) launch_mode_t<M, WN>(t, g, X, Y, J, st, occ)
+    STIGA_MI_SWITCH(t.MI, STIGA_CALL_MODE)
+#undef STIGA_CALL_MODE
+}
+
+cudaError_t dispatch_mode(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
+                          cudaStream_t st, int* occ) {
+    if (t.WM != 1) return cudaErrorInvalidValue;
+    if (t.WN == 4) return dispatch_mode_wn<4>(t, g, X, Y, J, st, occ);
+    if (t.WN == 2) return dispatch_mode_wn<2>(t, g, X, Y, J, st, occ);
+    return cudaErrorInvalidValue;
+}
+
+template <int WM, int WN>
+cudaError_t dispatch_time_w(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jt,
+                            const double* J, const ArrowParams& ap, cudaStream_t st, int* occ) {
+#define STIGA_CALL_TIME(M) launch_time_t<M, WM, WN>(t, g, X, Y, Jt, J, ap, st, occ)
+    STIGA_MI_SWITCH(t.MI, STIGA_CALL_TIME)
+#undef STIGA_CALL_TIME
+}
+
+cudaError_t dispatch_time(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jt,
+                          const double* J, const ArrowParams& ap, cudaStream_t st, int* occ) {
+    if (t.WN == 2) {
+        if (t.WM == 1) return dispatch_time_w<1, 2>(t, g, X, Y, Jt, J, ap, st, occ);
+        if (t.WM == 2) return dispatch_time_w<2, 2>(t, g, X, Y, Jt, J, ap, st, occ);
+        if (t.WM == 4) return dispatch_time_w<4, 2>(t, g, X, Y, Jt, J, ap, st, occ);
+    } else if (t.WN == 4) {
+        if (t.WM == 1) return dispatch_time_w<1, 4>(t, g, X, Y, Jt, J, ap, st, occ);
+        if (t.WM == 2) return dispatch_time_w<2, 4>(t, g, X, Y, Jt, J, ap, st, occ);
+    }
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
 Tiling choose_mode_tiling(int m, int n, bool prescale) {
+    (void)prescale;  // the D^-1/2 pre-scale is a separate elementwise pass
     Tiling best;
+    best.MI = 0;
     double best_score = -1.0;
     const int S = (m + 7) / 8;
     const int Kp = (n + 3) / 4 * 4;
     const int rb0 = (S + 12) / 13;
-    for (int RB = rb0; RB <= rb0 + 1; ++RB) {
+    for (int RB = rb0; RB <= rb0 + 2; ++RB) {
         const int MI = (S + RB - 1) / RB;
         if (MI > 13 || MI < 1) continue;
         for (int WN : {4, 2}) {
-            for (int ns : {3, 2}) {
-                Tiling t;
-                t.MI = MI;
-                t.WM = 1;
-                t.NI = 2;
-                t.WN = WN;
-                t.S = S;
-                t.RB = RB;
-                t.MpB = 8 * MI;
-                t.Mp = RB * t.MpB;
-                t.Kp = Kp;
-                t.BN = 16 * WN;
-                t.LDX = t.BN + 4;
-                t.nstage = ns;
-                t.prescale = prescale;
-                t.smem = sizeof(double) * static_cast<size_t>(ns) *
-                         (kBK * t.LDX + t.MpB * kLDJ + (prescale ? kBK * t.LDX : 0));
-                if (t.smem > kSmemPerCTA) continue;
-                t.ctas_per_sm = mode_occupancy(MI, t.threads(), t.smem);
-                if (t.ctas_per_sm < 1) continue;
-                const double eff = static_cast<double>(S) / (RB * MI);
-                const double score = std::min(t.ctas_per_sm * t.WM * t.WN, 16) * eff + 0.01 * ns + 0.02 * WN;
-                if (score > best_score) {
-                    best_score = score;
-                    best = t;
-                }
+            Tiling t;
+            t.MI = MI;
+            t.WM = 1;
+            t.NI = 2;
+            t.WN = WN;
+            t.S = S;
+            t.RB = RB;
+            t.MpB = 8 * MI;
+            t.Mp = RB * t.MpB;
+            t.Kp = Kp;
+            t.BN = 16 * WN;
+            t.LDX = t.BN + 4;
+            t.nstage = 3;
+            t.smem = sizeof(double) * static_cast<size_t>(t.nstage) * (kBK * t.LDX + t.MpB * kLDJ);
+            if (t.smem > kSmemPerCTA) continue;
+            int occ = 0;
+            dispatch_mode(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, &occ);
+            t.ctas_per_sm = occ;
+            if (occ < 1) continue;
+            const double eff = static_cast<double>(S) / (RB * MI);
+            const double score = std::min(occ * t.WN, 16) * eff + 0.02 * WN - 0.01 * RB;
+            if (score > best_score) {
+                best_score = score;
+                best = t;
             }
         }
     }
@@ -585,17 +601,18 @@ Tiling choose_mode_tiling(int m, int n, bool prescale) {
 
 Tiling choose_time_tiling(int nt) {
     Tiling best;
+    best.MI = 0;
     double best_score = -1.0;
     int force_wm = 0, force_wn = 0, force_ns = 0;  // debugging aid: STIGA_FORCE_TIME_TILING="WM,WN,NS"
-    if (const char* f = std::getenv("STIGA_FORCE_TIME_TILING")) std::sscanf(f, "%d,%d,%d", &force_wm, &force_wn, &force_ns);
+    if (const char* f = std::getenv("STIGA_FORCE_TIME_TILING"))
+        std::sscanf(f, "%d,%d,%d", &force_wm, &force_wn, &force_ns);
     const int S = (nt + 7) / 8;
     const int Kp = (nt + 3) / 4 * 4;
-    const int wm0 = (S + 12) / 13;
-    for (int WM = wm0; WM <= wm0 + (force_wm ? 8 : 2); ++WM) {
+    for (int WM : {1, 2, 4}) {
         const int MI = (S + WM - 1) / WM;
         if (MI > 13 || MI < 1) continue;
-        for (int WN : {4, 2, 1}) {
-            if (32 * WM * WN > kMaxThreads) continue;
+        for (int WN : {4, 2}) {
+            if (WM == 4 && WN == 4) continue;
             if ((force_wm && WM != force_wm) || (force_wn && WN != force_wn)) continue;
             for (int ns : {3, 2}) {
                 if (force_ns && ns != force_ns) continue;
@@ -616,10 +633,13 @@ Tiling choose_time_tiling(int nt) {
                 t.smem = sizeof(double) * (static_cast<size_t>(Kp) * t.LDX +
                                            static_cast<size_t>(ns) * (kBK * t.LDX + t.MpB * kLDJ));
                 if (t.smem > kSmemPerCTA) continue;
-                t.ctas_per_sm = time_occupancy(MI, t.threads(), t.smem);
-                if (t.ctas_per_sm < 1) continue;
+                int occ = 0;
+                ArrowParams ap;
+                dispatch_time(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, ap, nullptr, &occ);
+                t.ctas_per_sm = occ;
+                if (occ < 1) continue;
                 const double eff = static_cast<double>(S) / (WM * MI);
-                const double score = std::min(t.ctas_per_sm * WM * WN, 16) * eff + 0.01 * ns + 0.02 * WN;
+                const double score = std::min(occ * WM * WN, 16) * eff + 0.01 * ns + 0.02 * WN;
                 if (score > best_score) {
                     best_score = score;
                     best = t;
@@ -630,30 +650,17 @@ Tiling choose_time_tiling(int nt) {
     return best;
 }
 
-#define STIGA_MI_SWITCH(MI_, CALL)                                                                   \
-    switch (MI_) {                                                                                   \
-        case 1: return CALL(1); case 2: return CALL(2); case 3: return CALL(3); case 4: return CALL(4); \
-        case 5: return CALL(5); case 6: return CALL(6); case 7: return CALL(7); case 8: return CALL(8); \
-        case 9: return CALL(9); case 10: return CALL(10); case 11: return CALL(11);                  \
-        case 12: return CALL(12); case 13: return CALL(13);                                          \
-        default: return cudaErrorInvalidValue;                                                       \
-    }
-
 cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jpad,
                                 const double* pre, cudaStream_t st) {
     if (g.ncols <= 0) return cudaSuccess;
-    if (pre && !t.prescale) return cudaErrorInvalidValue;
-#define STIGA_CALL_MODE(M) launch_mode_mi<M>(t, g, X, Y, Jpad, pre, st)
-    STIGA_MI_SWITCH(t.MI, STIGA_CALL_MODE)
-#undef STIGA_CALL_MODE
+    if (pre) return cudaErrorInvalidValue;  // pre-scaling is a separate pass
+    return dispatch_mode(t, g, X, Y, Jpad, st, nullptr);
 }
 
 cudaError_t launch_time_fused(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jt_pad,
                               const double* J_pad, const ArrowParams& ap, cudaStream_t st) {
     if (g.ncols <= 0) return cudaSuccess;
-#define STIGA_CALL_TIME(M) launch_time_mi<M>(t, g, X, Y, Jt_pad, J_pad, ap, st)
-    STIGA_MI_SWITCH(t.MI, STIGA_CALL_TIME)
-#undef STIGA_CALL_TIME
+    return dispatch_time(t, g, X, Y, Jt_pad, J_pad, ap, st, nullptr);
 }
 
 cudaError_t launch_scale(const double* a, const double* x, double* y, long long n, cudaStream_t st) {
