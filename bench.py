@@ -238,12 +238,9 @@ def run_ours(args):
     for _ in range(kp):
         pass_ms += np.array(P.apply_profiled(r, s))
     pass_ms /= kp
-    d, nt, ns = cfg.d, cfg.n_t, cfg.n_s
-    names = [f"fwd_mode{m}" for m in range(d)] + ["time_fused"] + [f"bwd_mode{m}" for m in range(d)]
-    flops = [2.0 * ns * n] * d + [4.0 * nt * n] + [2.0 * ns * n] * d
-    if launches > len(names):  # D^-1/2 pre/post scale (elementwise, HBM-bound, 24 B/DoF each)
-        names = ["pre_scale"] + names + ["post_scale"]
-        flops = [0.0] + flops + [0.0]
+    info = P.launch_info()
+    names = [nm for nm, _ in info]
+    flops = [fl for _, fl in info]
     dom = int(np.argmax(pass_ms))
     achieved = flops[dom] / (pass_ms[dom] * 1e-3) / 1e12
     traffic = None

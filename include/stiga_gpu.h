@@ -85,6 +85,9 @@ int stiga_fd_apply_host(stiga_fd_t P, const double* h_r, double* h_s);
 int stiga_fd_apply_profiled(stiga_fd_t P, const double* d_r, double* d_s, void* stream, float* pass_ms);
 /* Number of kernel launches one apply issues (2d+1, +1 when scaled by D). */
 int stiga_fd_launches(stiga_fd_t P, int* launches);
+/* Name (e.g. "fwd_mode0", "time_fused", "arrowhead") and algorithmic FP64 flops of launch i of an
+   apply (the dense mode-product flops 2 n N_dof per product; 0 for elementwise passes). */
+int stiga_fd_launch_info(stiga_fd_t P, int i, char* name, int name_len, double* flops);
 
 /* ---- Kronecker operators (kronop.hpp:47-79) ------------------------------------------- */
 

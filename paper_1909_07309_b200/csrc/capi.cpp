@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -148,34 +149,96 @@ struct stiga_fd_s {
         return g;
     }
 
-    int launches() const { return 2 * d + 1 + (dinv.p ? 2 : 0); }
+    bool time_split = false;            // time direction as U_t^T GEMM + arrowhead + U_t GEMM
+
+    // Picks the faster time-direction variant by timing both once on the scratch vectors
+    // (STIGA_TIME_VARIANT=fused|split forces one).  The fused kernel needs a tiling that holds all
+    // n_t rows in one CTA; when none exists only the split path is available.
+    void choose_time_variant() {
+        const char* force = std::getenv("STIGA_TIME_VARIANT");
+        const bool fused_ok = tl_t.MI > 0;
+        if (force && std::string(force) == "split") { time_split = true; return; }
+        if (force && std::string(force) == "fused" && fused_ok) { time_split = false; return; }
+        if (!fused_ok) { time_split = true; return; }
+        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
+        ck(cudaMemset(scratch.p, 0, sizeof(double) * n_dof), "memset");
+        cudaEvent_t e0, e1;
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        float best[2] = {0.f, 0.f};
+        for (int v = 0; v < 2; ++v) {
+            for (int rep = 0; rep < 3; ++rep) {
+                ck(cudaEventRecord(e0, nullptr), "event");
+                if (v == 0) {
+                    ck(gpu::launch_time_fused(tl_t, geom(d), scratch.p, scratch2.p, Jt_t.p, J_t.p, ap, nullptr), "tune");
+                } else {
+                    ck(gpu::launch_mode_product(tl_ts, geom(d), scratch.p, scratch2.p, Jt_t.p, nullptr, nullptr), "tune");
+                    ck(gpu::launch_arrowhead(scratch2.p, scratch.p, n_s, ap, nullptr), "tune");
+                    ck(gpu::launch_mode_product(tl_ts, geom(d), scratch.p, scratch2.p, J_t.p, nullptr, nullptr), "tune");
+                }
+                ck(cudaEventRecord(e1, nullptr), "event");
+                ck(cudaEventSynchronize(e1), "event");
+                float ms = 0.f;
+                ck(cudaEventElapsedTime(&ms, e0, e1), "event");
+                if (rep > 0) best[v] = (rep == 1) ? ms : std::min(best[v], ms);
+            }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        time_split = best[1] < best[0];
+    }
+    gpu::Tiling tl_ts;                  // mode-kernel tiling of the split time products
+
+    int launches() const { return 2 * d + (time_split ? 3 : 1) + (dinv.p ? 1 : 0); }
 
     // Launch sequence (fdsolve.cpp:158-163): [D^-1/2 pre-scale], forward spatial modes U_l^T, the
-    // time-fused kernel (U_t^T, arrowhead solve, U_t), backward spatial modes U_l, [D^-1/2
-    // post-scale].  The reference back transform applies U_1..U_d, U_t; Kronecker factors on distinct
-    // modes commute, so applying U_t first (fused with the arrowhead) is equal in exact arithmetic.
-    // Intermediates ping-pong between two handle-owned scratch vectors, so d_r may equal d_s.
+    // time direction (fused U_t^T / arrowhead / U_t kernel, or the three as separate passes),
+    // backward spatial modes U_l with the D^-1/2 post-scale fused into the last epilogue.  The
+    // reference back transform applies U_1..U_d, U_t; Kronecker factors on distinct modes commute,
+    // so applying U_t first is equal in exact arithmetic.  Intermediates ping-pong between two
+    // handle-owned scratch vectors, so d_r may equal d_s.
     void apply(const double* in, double* out, cudaStream_t st, std::vector<cudaEvent_t>* ev) {
         if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
         double* bufs[2] = {scratch.p, scratch2.p};
         const bool scaled = dinv.p != nullptr;
         const int nops = launches();
         const double* src = in;
-        int e = 0;
-        for (int k = 0; k < nops; ++k) {
+        int e = 0, k = 0;
+        auto next = [&]() -> double* {
             double* dst = (k == nops - 1) ? out : bufs[k % 2];
             if (ev) ck(cudaEventRecord((*ev)[e++], st), "event");
-            const int g = scaled ? k - 1 : k;  // index of the GEMM pass
-            if (scaled && (k == 0 || k == nops - 1)) {
-                ck(gpu::launch_scale(dinv.p, src, dst, n_dof, st), "fd D^-1/2 scale");
-            } else if (g < d) {
-                ck(gpu::launch_mode_product(tl[g], geom(g), src, dst, Jt[g]->p, nullptr, st), "fd forward mode product");
-            } else if (g == d) {
-                ck(gpu::launch_time_fused(tl_t, geom(d), src, dst, Jt_t.p, J_t.p, ap, st), "fd time-fused kernel");
-            } else {
-                const int m = g - d - 1;
-                ck(gpu::launch_mode_product(tl[m], geom(m), src, dst, J[m]->p, nullptr, st), "fd backward mode product");
-            }
+            ++k;
+            return dst;
+        };
+        if (scaled) {
+            double* dst = next();
+            ck(gpu::launch_scale(dinv.p, src, dst, n_dof, st), "fd D^-1/2 pre-scale");
+            src = dst;
+        }
+        for (int l = 0; l < d; ++l) {
+            double* dst = next();
+            ck(gpu::launch_mode_product(tl[l], geom(l), src, dst, Jt[l]->p, nullptr, st), "fd forward mode product");
+            src = dst;
+        }
+        if (time_split) {
+            double* dst = next();
+            ck(gpu::launch_mode_product(tl_ts, geom(d), src, dst, Jt_t.p, nullptr, st), "fd time U_t^T product");
+            src = dst;
+            dst = next();
+            ck(gpu::launch_arrowhead(src, dst, n_s, ap, st), "fd arrowhead solve");
+            src = dst;
+            dst = next();
+            ck(gpu::launch_mode_product(tl_ts, geom(d), src, dst, J_t.p, nullptr, st), "fd time U_t product");
+            src = dst;
+        } else {
+            double* dst = next();
+            ck(gpu::launch_time_fused(tl_t, geom(d), src, dst, Jt_t.p, J_t.p, ap, st), "fd time-fused kernel");
+            src = dst;
+        }
+        for (int l = 0; l < d; ++l) {
+            double* dst = next();
+            ck(gpu::launch_mode_product(tl[l], geom(l), src, dst, J[l]->p, (l == d - 1 && scaled) ? dinv.p : nullptr, st),
+               "fd backward mode product");
             src = dst;
         }
         if (ev) ck(cudaEventRecord((*ev)[e], st), "event");
@@ -387,8 +450,10 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
             h->lam.back()->upload(F.lambda[l]);
         }
         h->tl_t = gpu::choose_time_tiling(F.n_t);
-        h->Jt_t.upload(pad_factor(F.time.U, true, h->tl_t.Mp, h->tl_t.Kp));
-        h->J_t.upload(pad_factor(F.time.U, false, h->tl_t.Mp, h->tl_t.Kp));
+        h->tl_ts = gpu::choose_mode_tiling(F.n_t, F.n_t, false);
+        const int trows = std::max(h->tl_t.Mp, h->tl_ts.Mp);
+        h->Jt_t.upload(pad_factor(F.time.U, true, trows, h->tl_t.Kp));
+        h->J_t.upload(pad_factor(F.time.U, false, trows, h->tl_t.Kp));
         h->S_inv.upload(F.S_inv);
         std::vector<double> pc, pc1;
         for (double lam : F.time.lambda) {
@@ -423,6 +488,7 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         ap.gamma = gamma;
         ap.nu = nu;
         if (const char* dbg = std::getenv("STIGA_DEBUG_ARROW")) ap.debug = std::atoi(dbg);
+        h->choose_time_variant();
         *out = h.release();
     });
 }
@@ -506,6 +572,30 @@ int stiga_fd_apply_profiled(stiga_fd_t P, const double* d_r, double* d_s, void* 
         ck(cudaEventSynchronize(ev[passes]), "cudaEventSynchronize");
         for (int k = 0; k < passes; ++k) ck(cudaEventElapsedTime(&pass_ms[k], ev[k], ev[k + 1]), "elapsed");
         for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+int stiga_fd_launch_info(stiga_fd_t P, int i, char* name, int name_len, double* flops) {
+    return guarded([&] {
+        require(P && name && name_len > 0 && flops, "stiga_fd_launch_info: null argument");
+        require(i >= 0 && i < P->launches(), "stiga_fd_launch_info: launch index out of range");
+        std::vector<std::pair<std::string, double>> L;
+        const double N = static_cast<double>(P->n_dof);
+        if (P->dinv.p) L.emplace_back("pre_scale", 0.0);
+        for (int l = 0; l < P->d; ++l) L.emplace_back("fwd_mode" + std::to_string(l), 2.0 * P->dims[l] * N);
+        const double nt = P->dims[P->d];
+        if (P->time_split) {
+            L.emplace_back("time_UtT", 2.0 * nt * N);
+            L.emplace_back("arrowhead", 0.0);
+            L.emplace_back("time_Ut", 2.0 * nt * N);
+        } else {
+            L.emplace_back("time_fused", 4.0 * nt * N);
+        }
+        for (int l = 0; l < P->d; ++l)
+            L.emplace_back("bwd_mode" + std::to_string(l) + (l == P->d - 1 && P->dinv.p ? "+post_scale" : ""),
+                           2.0 * P->dims[l] * N);
+        std::snprintf(name, static_cast<size_t>(name_len), "%s", L[i].first.c_str());
+        *flops = L[i].second;
     });
 }
 

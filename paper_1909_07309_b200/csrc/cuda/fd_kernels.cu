@@ -219,7 +219,7 @@ __device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, do
 // Register epilogue: acc rows (< m) of the CTA's row block straight to global memory.
 template <class SH>
 __device__ __forceinline__ void store_acc(const KArgs& a, const double (&acc)[SH::MI][SH::NI][2], long long c0,
-                                          int strip0, double* __restrict__ Y) {
+                                          int strip0, double* __restrict__ Y, const double* __restrict__ post) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int wm = warp % SH::WM, wn = warp / SH::WM;
@@ -235,6 +235,31 @@ __device__ __forceinline__ void store_acc(const KArgs& a, const double (&acc)[SH
             cv[ni][v] = cc < a.geo.ncols;
             ob[ni][v] = fiber_base(cv[ni][v] ? cc : 0, a.geo.L, m);
         }
+    if (post) {  // fused D^-1/2 post-scale: all scale loads issued before the first store
+        double sc[SH::MI][SH::NI][2];
+#pragma unroll
+        for (int mi = 0; mi < SH::MI; ++mi) {
+            const int i = (strip0 + wm * SH::MI + mi) * 8 + g;
+            const long long off = a.geo.L * i;
+#pragma unroll
+            for (int ni = 0; ni < SH::NI; ++ni)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) sc[mi][ni][v] = (i < m && cv[ni][v]) ? __ldg(post + ob[ni][v] + off) : 0.0;
+        }
+#pragma unroll
+        for (int mi = 0; mi < SH::MI; ++mi) {
+            const int i = (strip0 + wm * SH::MI + mi) * 8 + g;
+            if (i < m) {
+                const long long off = a.geo.L * i;
+#pragma unroll
+                for (int ni = 0; ni < SH::NI; ++ni)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v)
+                        if (cv[ni][v]) Y[ob[ni][v] + off] = sc[mi][ni][v] * acc[mi][ni][v];
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int mi = 0; mi < SH::MI; ++mi) {
         const int i = (strip0 + wm * SH::MI + mi) * 8 + g;
@@ -311,7 +336,8 @@ __device__ __forceinline__ void gemm(const KArgs& a, double* stages, const Prod&
 
 template <int MI, int WN>
 __global__ void __launch_bounds__(32 * WN)
-    mode_product_kernel(KArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J) {
+    mode_product_kernel(KArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
+                        const double* __restrict__ post) {
     using SH = Shape<MI, 1, WN>;
     extern __shared__ __align__(16) double smem[];
     const int rb = blockIdx.x % a.RB;  // row blocks of one fiber tile are adjacent -> X tile reused from L2
@@ -321,7 +347,7 @@ __global__ void __launch_bounds__(32 * WN)
     double acc[SH::MI][SH::NI][2];
     zero_acc<SH>(acc);
     gemm<SH, true>(a, smem, p, X, nullptr, false, acc);
-    store_acc<SH>(a, acc, c0, rb * MI, Y);
+    store_acc<SH>(a, acc, c0, rb * MI, Y, post);
 }
 
 // apply_pair_inverse (fdsolve.cpp:11-20) with R_j^-1 recomputed from Lambda_s (fdsolve.cpp:114-119).
@@ -438,7 +464,69 @@ __global__ void __launch_bounds__(32 * WM * WN)
     __syncthreads();
     zero_acc<SH>(acc);
     gemm<SH, false>(a, stages, p, X, Zs, true, acc);  // y = U_t z
-    store_acc<SH>(a, acc, c0, 0, Y);
+    store_acc<SH>(a, acc, c0, 0, Y, nullptr);
+}
+
+// Standalone block-arrowhead solve (fdsolve.cpp:24-65) between two time-mode products.  Block =
+// 32 consecutive spatial indices (one per lane, coalesced) x P warps; warp w handles pairs
+// j = w mod P.  Forward pass: pair eliminations accumulate the Schur right-hand side (reduced over
+// the P warps in smem); second pass recomputes y_j from Z instead of storing it (24 B/DoF of HBM
+// traffic instead of 32) and writes x_j = y_j - H_j^-1 B_j x_last.
+template <int P>
+__global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restrict__ Z, double* __restrict__ Xo,
+                                                           long long Ns, ArrowParams ap) {
+    __shared__ double part_s[P][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long s0 = static_cast<long long>(blockIdx.x) * 32 + lane;
+    const bool valid = s0 < Ns;
+    const long long s = valid ? s0 : Ns - 1;
+    double lam = 0.0;  // ((0 + lambda_1) + lambda_2) + ... (fdsolve.cpp:91-99)
+    long long rem = s;
+    for (int l = 0; l < ap.d; ++l) {
+        const long long q = rem / ap.n[l];
+        lam = lam + __ldg(ap.lam[l] + (rem - q * ap.n[l]));
+        rem = q;
+    }
+    const double linv = 1.0 / lam;
+    const double nu = ap.nu, gam = ap.gamma;
+    const int nt = ap.n_t;
+    const double* zc = Z + s;
+    double part = 0.0;
+#pragma unroll 4
+    for (int j = w; j < ap.npairs; j += P) {
+        double xa, xb;
+        pair_inverse(lam, linv, nu, __ldg(ap.pair_c + j), __ldg(ap.pair_c1 + j), __ldg(zc + (2 * j) * Ns),
+                     __ldg(zc + (2 * j + 1) * Ns), xa, xb);
+        part += gam * (__ldg(ap.g + 2 * j) * xa + __ldg(ap.g + 2 * j + 1) * xb);
+    }
+    double xz = 0.0;
+    const int z = nt - 2;
+    if (ap.zero_count && w == P - 1) {
+        xz = linv * __ldg(zc + z * Ns) / nu;
+        part += gam * __ldg(ap.g + z) * xz;
+    }
+    part_s[w][lane] = part;
+    __syncthreads();
+    double srhs = __ldg(zc + (nt - 1) * Ns);
+#pragma unroll
+    for (int k = 0; k < P; ++k) srhs += part_s[k][lane];
+    const double xlast = __ldg(ap.S_inv + s) * srhs;
+    if (!valid) return;
+    double* xo = Xo + s;
+#pragma unroll 4
+    for (int j = w; j < ap.npairs; j += P) {
+        const double cj = __ldg(ap.pair_c + j), c1 = __ldg(ap.pair_c1 + j);
+        double ya, yb, ca, cb;
+        pair_inverse(lam, linv, nu, cj, c1, __ldg(zc + (2 * j) * Ns), __ldg(zc + (2 * j + 1) * Ns), ya, yb);
+        pair_inverse(lam, linv, nu, cj, c1, (gam * __ldg(ap.g + 2 * j)) * xlast, (gam * __ldg(ap.g + 2 * j + 1)) * xlast,
+                     ca, cb);
+        xo[(2 * j) * Ns] = ya - ca;
+        xo[(2 * j + 1) * Ns] = yb - cb;
+    }
+    if (w == P - 1) {
+        if (ap.zero_count) xo[z * Ns] = xz - (gam * __ldg(ap.g + z) / nu) * (linv * xlast);
+        xo[(nt - 1) * Ns] = xlast;
+    }
 }
 
 __global__ void scale_kernel(const double* __restrict__ a, const double* __restrict__ x, double* __restrict__ y,
@@ -481,7 +569,7 @@ int occupancy(K kernel, int threads, size_t smem) {
 // ---- instantiation dispatch --------------------------------------------------------------------
 template <int MI, int WN>
 cudaError_t launch_mode_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                          cudaStream_t st, int* occ) {
+                          const double* post, cudaStream_t st, int* occ) {
     auto k = mode_product_kernel<MI, WN>;
     if (occ) {
         *occ = occupancy(k, 32 * WN, t.smem);
@@ -490,7 +578,7 @@ cudaError_t launch_mode_t(const Tiling& t, const ModeGeom& g, const double* X, d
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(t.smem));
     if (e != cudaSuccess) return e;
     const long long blocks = (g.ncols + t.BN - 1) / t.BN * t.RB;
-    k<<<static_cast<unsigned>(blocks), 32 * WN, t.smem, st>>>(make_args(t, g), X, Y, J);
+    k<<<static_cast<unsigned>(blocks), 32 * WN, t.smem, st>>>(make_args(t, g), X, Y, J, post);
     return cudaGetLastError();
 }
 
@@ -520,17 +608,17 @@ cudaError_t launch_time_t(const Tiling& t, const ModeGeom& g, const double* X, d
 
 template <int WN>
 cudaError_t dispatch_mode_wn(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                             cudaStream_t st, int* occ) {
-#define STIGA_CALL_MODE(M) launch_mode_t<M, WN>(t, g, X, Y, J, st, occ)
+                             const double* post, cudaStream_t st, int* occ) {
+#define STIGA_CALL_MODE(M) launch_mode_t<M, WN>(t, g, X, Y, J, post, st, occ)
     STIGA_MI_SWITCH(t.MI, STIGA_CALL_MODE)
 #undef STIGA_CALL_MODE
 }
 
 cudaError_t dispatch_mode(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                          cudaStream_t st, int* occ) {
+                          const double* post, cudaStream_t st, int* occ) {
     if (t.WM != 1) return cudaErrorInvalidValue;
-    if (t.WN == 4) return dispatch_mode_wn<4>(t, g, X, Y, J, st, occ);
-    if (t.WN == 2) return dispatch_mode_wn<2>(t, g, X, Y, J, st, occ);
+    if (t.WN == 4) return dispatch_mode_wn<4>(t, g, X, Y, J, post, st, occ);
+    if (t.WN == 2) return dispatch_mode_wn<2>(t, g, X, Y, J, post, st, occ);
     return cudaErrorInvalidValue;
 }
 
@@ -585,7 +673,7 @@ Tiling choose_mode_tiling(int m, int n, bool prescale) {
             t.smem = sizeof(double) * static_cast<size_t>(t.nstage) * (kBK * t.LDX + t.MpB * kLDJ);
             if (t.smem > kSmemPerCTA) continue;
             int occ = 0;
-            dispatch_mode(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, &occ);
+            dispatch_mode(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, nullptr, &occ);
             t.ctas_per_sm = occ;
             if (occ < 1) continue;
             const double eff = static_cast<double>(S) / (RB * MI);
@@ -651,16 +739,23 @@ Tiling choose_time_tiling(int nt) {
 }
 
 cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jpad,
-                                const double* pre, cudaStream_t st) {
+                                const double* post_scale, cudaStream_t st) {
     if (g.ncols <= 0) return cudaSuccess;
-    if (pre) return cudaErrorInvalidValue;  // pre-scaling is a separate pass
-    return dispatch_mode(t, g, X, Y, Jpad, st, nullptr);
+    return dispatch_mode(t, g, X, Y, Jpad, post_scale, st, nullptr);
 }
 
 cudaError_t launch_time_fused(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jt_pad,
                               const double* J_pad, const ArrowParams& ap, cudaStream_t st) {
     if (g.ncols <= 0) return cudaSuccess;
     return dispatch_time(t, g, X, Y, Jt_pad, J_pad, ap, st, nullptr);
+}
+
+cudaError_t launch_arrowhead(const double* Z, double* X, long long Ns, const ArrowParams& ap, cudaStream_t st) {
+    if (Ns <= 0) return cudaSuccess;
+    constexpr int P = 8;
+    const long long blocks = (Ns + 31) / 32;
+    arrowhead_kernel<P><<<static_cast<unsigned>(blocks), 32 * P, 0, st>>>(Z, X, Ns, ap);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_scale(const double* a, const double* x, double* y, long long n, cudaStream_t st) {

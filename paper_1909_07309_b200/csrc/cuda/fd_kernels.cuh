@@ -65,9 +65,14 @@ Tiling choose_mode_tiling(int m, int n, bool prescale);  // m output rows, n con
 Tiling choose_time_tiling(int n_t);
 
 /// Y = (I (x) J (x) I) X along one mode.  J is row-major, zero padded to (t.Mp x t.Kp).
-/// pre_scale (optional, requires t.prescale) multiplies X elementwise before the product.
+/// post_scale (optional) multiplies Y elementwise in the register epilogue (the D^-1/2 post-scale).
 cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y,
-                                const double* Jpad, const double* pre_scale, cudaStream_t stream);
+                                const double* Jpad, const double* post_scale, cudaStream_t stream);
+
+/// Standalone block-arrowhead solve X = (gamma Delta_t (x) I + nu I (x) Lambda_s)^-1 Z on the
+/// time-eigen-coordinate tensor (N_s x n_t, time slowest); used when the time direction runs as
+/// three passes (U_t^T product, arrowhead, U_t product) instead of the fused kernel.
+cudaError_t launch_arrowhead(const double* Z, double* X, long long Ns, const ArrowParams& ap, cudaStream_t stream);
 
 /// Time-fused kernel: per spatial index, Z = U_t^T x, arrowhead solve, y = U_t Z.
 /// Jt_pad = U_t^T padded, J_pad = U_t padded (both row-major Mp x Kp).

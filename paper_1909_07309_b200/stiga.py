@@ -203,6 +203,16 @@ class ExtendedFDPreconditioner:
         check(lib().stiga_fd_launches(self._h, ctypes.byref(n)), "fd_launches")
         return n.value
 
+    def launch_info(self):
+        """[(name, algorithmic flops)] of the kernel launches of one apply."""
+        out = []
+        buf = ctypes.create_string_buffer(64)
+        for i in range(self.launches()):
+            f = ctypes.c_double()
+            check(lib().stiga_fd_launch_info(self._h, i, buf, 64, ctypes.byref(f)), "fd_launch_info")
+            out.append((buf.value.decode(), f.value))
+        return out
+
     def apply(self, r, out=None, stream=None):
         """r -> A^-1 r (fdsolve.cpp:155-164).  torch CUDA tensor in -> tensor out (device path);
         numpy in -> numpy out (host path with H2D/D2H)."""

@@ -167,3 +167,14 @@ def test_kron_matvec_matches_dense():  # tests/test_kronop.cpp:62-123 through th
         yy = stiga.kron_matvec(Fs, torch.from_numpy(xx).cuda()).cpu().numpy()
         ref = okr.kron_matvec(Fs, xx)
         assert rel(yy, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("variant", ["fused", "split"])
+@pytest.mark.parametrize("d,p,nel", [(1, 2, 5), (2, 3, 9), (2, 3, 30), (3, 3, 7), (1, 3, 256)])
+def test_time_variants(variant, d, p, nel, monkeypatch):
+    """Both time-direction paths (fused kernel / U_t^T + arrowhead + U_t passes) match the oracle."""
+    monkeypatch.setenv("STIGA_TIME_VARIANT", variant)
+    s, so, P, *_ = run_pair(d, p, nel, scaled=True, seed=31)
+    names = [nm for nm, _ in P.launch_info()]
+    assert ("time_fused" in names) == (variant == "fused")
+    assert rel(s, so) <= TOL
