@@ -135,7 +135,7 @@ struct stiga_fd_s {
     std::vector<std::unique_ptr<DBuf>> Jt, J;  // padded U_l^T, U_l
     DBuf Jt_t, J_t;
     std::vector<std::unique_ptr<DBuf>> lam;
-    DBuf S_inv, pair_c, pair_c1, g, dinv;
+    DBuf S_inv, pair_c, pair_c1, pair_c1sq, pair_gg, g, dinv;
     DBuf scratch, scratch2;
     gpu::ArrowParams ap;
 
@@ -455,17 +455,26 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         h->Jt_t.upload(pad_factor(F.time.U, true, trows, h->tl_t.Kp));
         h->J_t.upload(pad_factor(F.time.U, false, trows, h->tl_t.Kp));
         h->S_inv.upload(F.S_inv);
-        std::vector<double> pc, pc1;
-        for (double lam : F.time.lambda) {
+        std::vector<double> pc, pc1, pc1sq, pgg;
+        for (size_t j = 0; j < F.time.lambda.size(); ++j) {
+            const double lam = F.time.lambda[j];
             pc.push_back(gamma * gamma / nu * lam * lam);  // fdsolve.cpp:118
-            pc1.push_back(gamma / nu * lam);               // fdsolve.cpp:16
+            const double c1 = gamma / nu * lam;            // fdsolve.cpp:16
+            pc1.push_back(c1);
+            pc1sq.push_back(c1 * c1 / nu);                 // fdsolve.cpp:17 (exact only at nu = 1)
+            pgg.push_back(gamma * F.time.g[2 * j]);        // fdsolve.cpp:57-58
+            pgg.push_back(gamma * F.time.g[2 * j + 1]);
         }
         if (pc.empty()) {
             pc.push_back(0.0);
             pc1.push_back(0.0);
+            pc1sq.push_back(0.0);
+            pgg.assign(2, 0.0);
         }
         h->pair_c.upload(pc);
         h->pair_c1.upload(pc1);
+        h->pair_c1sq.upload(pc1sq);
+        h->pair_gg.upload(pgg);
         std::vector<double> gg(F.time.g.begin(), F.time.g.end());
         if (gg.empty()) gg.push_back(0.0);
         h->g.upload(gg);
@@ -481,12 +490,15 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         ap.S_inv = h->S_inv.p;
         ap.pair_c = h->pair_c.p;
         ap.pair_c1 = h->pair_c1.p;
+        ap.pair_c1sq = h->pair_c1sq.p;
+        ap.pair_gg = h->pair_gg.p;
         ap.g = h->g.p;
         ap.npairs = static_cast<int>(F.time.lambda.size());
         ap.zero_count = F.time.zero_count;
         ap.n_t = F.n_t;
         ap.gamma = gamma;
         ap.nu = nu;
+        ap.inv_nu = 1.0 / nu;
         if (const char* dbg = std::getenv("STIGA_DEBUG_ARROW")) ap.debug = std::atoi(dbg);
         h->choose_time_variant();
         *out = h.release();

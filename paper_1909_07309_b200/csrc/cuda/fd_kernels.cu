@@ -350,13 +350,28 @@ __global__ void __launch_bounds__(32 * WN)
     store_acc<SH>(a, acc, c0, rb * MI, Y, post);
 }
 
-// apply_pair_inverse (fdsolve.cpp:11-20) with R_j^-1 recomputed from Lambda_s (fdsolve.cpp:114-119).
-__device__ __forceinline__ void pair_inverse(double lam, double linv, double nu, double cj, double c1, double u,
-                                             double w, double& xa, double& xb) {
-    const double rinv = 1.0 / (nu * lam + cj * linv);
+// 1/x to ~1 ulp: float reciprocal seed + two Newton steps (fused multiply-adds only; the IEEE
+// division subroutine would cost ~10x more issue slots in the arrowhead passes).
+__device__ __forceinline__ double rcp(double x) {
+    double r = static_cast<double>(__frcp_rn(static_cast<float>(x)));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+// apply_pair_inverse (fdsolve.cpp:11-20) with R_j^-1 = 1/(nu Lambda_s + c_j Lambda_s^-1) recomputed
+// from Lambda_s (fdsolve.cpp:114-119).  Same expression tree as the reference, with x/nu evaluated
+// as x*(1/nu) (exact at nu = 1, within 1 ulp otherwise) and c1*c1/nu precomputed per pair.
+__device__ __forceinline__ double pair_rinv(double lam, double linv, double nu, double cj) {
+    return rcp(nu * lam + cj * linv);
+}
+
+__device__ __forceinline__ void pair_apply(double rinv, double linv, double inv_nu, double c1, double c1sq_nu,
+                                           double u, double w, double& xa, double& xb) {
     const double luiu = linv * u;
     const double riluiu = rinv * luiu;
-    xa = luiu / nu - (c1 * c1 / nu) * (linv * riluiu) - c1 * (linv * (rinv * w));
+    xa = luiu * inv_nu - c1sq_nu * (linv * riluiu) - c1 * (linv * (rinv * w));
     xb = c1 * riluiu + rinv * w;
 }
 
@@ -380,22 +395,23 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
         rem = q;
     }
     const double linv = 1.0 / lam;
-    const double nu = ap.nu, gam = ap.gamma;
+    const double nu = ap.nu, inv_nu = ap.inv_nu, gam = ap.gamma;
     const int nt = ap.n_t;
     double* col = Zs + c;
     const double slast = col[(nt - 1) * SH::LDX];
     double part = 0.0;
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
-        pair_inverse(lam, linv, nu, __ldg(ap.pair_c + j), __ldg(ap.pair_c1 + j), col[(2 * j) * SH::LDX],
-                     col[(2 * j + 1) * SH::LDX], xa, xb);
+        const double rinv = pair_rinv(lam, linv, nu, __ldg(ap.pair_c + j));
+        pair_apply(rinv, linv, inv_nu, __ldg(ap.pair_c1 + j), __ldg(ap.pair_c1sq + j), col[(2 * j) * SH::LDX],
+                   col[(2 * j + 1) * SH::LDX], xa, xb);
         col[(2 * j) * SH::LDX] = xa;
         col[(2 * j + 1) * SH::LDX] = xb;
         part += gam * (__ldg(ap.g + 2 * j) * xa + __ldg(ap.g + 2 * j + 1) * xb);
     }
     if (ap.zero_count && p == 0) {
         const int z = nt - 2;
-        const double xz = linv * col[z * SH::LDX] / nu;
+        const double xz = linv * col[z * SH::LDX] * inv_nu;
         col[z * SH::LDX] = xz;
         part += gam * __ldg(ap.g + z) * xz;
     }
@@ -404,15 +420,16 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
     const double xlast = __ldg(ap.S_inv + s) * (slast + part);
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
-        pair_inverse(lam, linv, nu, __ldg(ap.pair_c + j), __ldg(ap.pair_c1 + j),
-                     (gam * __ldg(ap.g + 2 * j)) * xlast, (gam * __ldg(ap.g + 2 * j + 1)) * xlast, xa, xb);
+        const double rinv = pair_rinv(lam, linv, nu, __ldg(ap.pair_c + j));
+        pair_apply(rinv, linv, inv_nu, __ldg(ap.pair_c1 + j), __ldg(ap.pair_c1sq + j), __ldg(ap.pair_gg + 2 * j) * xlast,
+                   __ldg(ap.pair_gg + 2 * j + 1) * xlast, xa, xb);
         col[(2 * j) * SH::LDX] -= xa;
         col[(2 * j + 1) * SH::LDX] -= xb;
     }
     if (p == 0) {
         if (ap.zero_count) {
             const int z = nt - 2;
-            col[z * SH::LDX] -= (gam * __ldg(ap.g + z) / nu) * (linv * xlast);
+            col[z * SH::LDX] -= (gam * __ldg(ap.g + z) * inv_nu) * (linv * xlast);
         }
         col[(nt - 1) * SH::LDX] = xlast;
     }
@@ -488,21 +505,22 @@ __global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restr
         rem = q;
     }
     const double linv = 1.0 / lam;
-    const double nu = ap.nu, gam = ap.gamma;
+    const double nu = ap.nu, inv_nu = ap.inv_nu, gam = ap.gamma;
     const int nt = ap.n_t;
     const double* zc = Z + s;
     double part = 0.0;
 #pragma unroll 4
     for (int j = w; j < ap.npairs; j += P) {
         double xa, xb;
-        pair_inverse(lam, linv, nu, __ldg(ap.pair_c + j), __ldg(ap.pair_c1 + j), __ldg(zc + (2 * j) * Ns),
-                     __ldg(zc + (2 * j + 1) * Ns), xa, xb);
+        const double rinv = pair_rinv(lam, linv, nu, __ldg(ap.pair_c + j));
+        pair_apply(rinv, linv, inv_nu, __ldg(ap.pair_c1 + j), __ldg(ap.pair_c1sq + j), __ldg(zc + (2 * j) * Ns),
+                   __ldg(zc + (2 * j + 1) * Ns), xa, xb);
         part += gam * (__ldg(ap.g + 2 * j) * xa + __ldg(ap.g + 2 * j + 1) * xb);
     }
     double xz = 0.0;
     const int z = nt - 2;
     if (ap.zero_count && w == P - 1) {
-        xz = linv * __ldg(zc + z * Ns) / nu;
+        xz = linv * __ldg(zc + z * Ns) * inv_nu;
         part += gam * __ldg(ap.g + z) * xz;
     }
     part_s[w][lane] = part;
@@ -515,16 +533,17 @@ __global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restr
     double* xo = Xo + s;
 #pragma unroll 4
     for (int j = w; j < ap.npairs; j += P) {
-        const double cj = __ldg(ap.pair_c + j), c1 = __ldg(ap.pair_c1 + j);
+        const double c1 = __ldg(ap.pair_c1 + j), c1sq = __ldg(ap.pair_c1sq + j);
+        const double rinv = pair_rinv(lam, linv, nu, __ldg(ap.pair_c + j));
         double ya, yb, ca, cb;
-        pair_inverse(lam, linv, nu, cj, c1, __ldg(zc + (2 * j) * Ns), __ldg(zc + (2 * j + 1) * Ns), ya, yb);
-        pair_inverse(lam, linv, nu, cj, c1, (gam * __ldg(ap.g + 2 * j)) * xlast, (gam * __ldg(ap.g + 2 * j + 1)) * xlast,
-                     ca, cb);
+        pair_apply(rinv, linv, inv_nu, c1, c1sq, __ldg(zc + (2 * j) * Ns), __ldg(zc + (2 * j + 1) * Ns), ya, yb);
+        pair_apply(rinv, linv, inv_nu, c1, c1sq, __ldg(ap.pair_gg + 2 * j) * xlast, __ldg(ap.pair_gg + 2 * j + 1) * xlast,
+                   ca, cb);
         xo[(2 * j) * Ns] = ya - ca;
         xo[(2 * j + 1) * Ns] = yb - cb;
     }
     if (w == P - 1) {
-        if (ap.zero_count) xo[z * Ns] = xz - (gam * __ldg(ap.g + z) / nu) * (linv * xlast);
+        if (ap.zero_count) xo[z * Ns] = xz - (gam * __ldg(ap.g + z) * inv_nu) * (linv * xlast);
         xo[(nt - 1) * Ns] = xlast;
     }
 }

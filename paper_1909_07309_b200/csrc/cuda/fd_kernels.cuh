@@ -25,9 +25,11 @@ struct ArrowParams {
     const double* S_inv = nullptr;          // N_s
     const double* pair_c = nullptr;         // gamma^2/nu * lambda_j^2  (fdsolve.cpp:118)
     const double* pair_c1 = nullptr;        // gamma/nu * lambda_j      (fdsolve.cpp:16)
+    const double* pair_c1sq = nullptr;      // c1 * c1 / nu             (fdsolve.cpp:17, the reference's quirk)
+    const double* pair_gg = nullptr;        // gamma * g[2j], gamma * g[2j+1] (2 per pair)
     const double* g = nullptr;              // n_t - 1 coupling entries
     int npairs = 0, zero_count = 0, n_t = 0;
-    double gamma = 0.0, nu = 0.0;
+    double gamma = 0.0, nu = 0.0, inv_nu = 0.0;
     int debug = 0;  // bit 0: skip the arrowhead (Y = U_t U_t^T X); debugging aid
 };
 
