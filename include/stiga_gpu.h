@@ -89,6 +89,21 @@ int stiga_fd_launches(stiga_fd_t P, int* launches);
    apply (the dense mode-product flops 2 n N_dof per product; 0 for elementwise passes). */
 int stiga_fd_launch_info(stiga_fd_t P, int i, char* name, int name_len, double* flops);
 
+/* ---- distributed (time-sharded) apply building blocks, DESIGN.md §6 ------------------------ */
+
+/* Spatial half of the apply on a time slab (time slices [t0, t0+nt_local), a contiguous piece of
+   the colex vector): forward = D^-1/2 pre-scale of the slab (when scaled) + U_1^T..U_d^T;
+   backward = U_1..U_d with the D^-1/2 post-scale fused.  d_in != d_out. */
+int stiga_fd_apply_space(stiga_fd_t P, int backward, long long t0, long long nt_local, const double* d_in,
+                         double* d_out, void* stream);
+/* Time direction (U_t^T, arrowhead_solve fdsolve.cpp:24-65, U_t) on a spatial slab: ns_local spatial
+   eigen-indices starting at global index s0, stored ns_local x n_t colexicographically. */
+int stiga_fd_apply_time(stiga_fd_t P, long long s0, long long ns_local, const double* d_in, double* d_out,
+                        void* stream);
+/* Strided block copy dst[r*dst_ld + c] = src[r*src_ld + c] (pack/unpack around the all-to-alls). */
+int stiga_copy_blocks(const double* d_src, long long src_ld, double* d_dst, long long dst_ld, long long rows,
+                      long long cols, void* stream);
+
 /* ---- Kronecker operators (kronop.hpp:47-79) ------------------------------------------- */
 
 /* kron_matvec(factors, x) (kronop.cpp:75-89) on device buffers: D factors, factor l is

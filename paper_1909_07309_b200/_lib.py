@@ -48,6 +48,9 @@ SIGNATURES = {
     "stiga_fd_apply_profiled": (_c_int, [_vp, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_float)]),
     "stiga_fd_launches": (_c_int, [_vp, _pi]),
     "stiga_fd_launch_info": (_c_int, [_vp, _c_int, ctypes.c_char_p, _c_int, _pd]),
+    "stiga_fd_apply_space": (_c_int, [_vp, _c_int, _c_ll, _c_ll, _vp, _vp, _vp]),
+    "stiga_fd_apply_time": (_c_int, [_vp, _c_ll, _c_ll, _vp, _vp, _vp]),
+    "stiga_copy_blocks": (_c_int, [_vp, _c_ll, _vp, _c_ll, _c_ll, _c_ll, _vp]),
     "stiga_kron_matvec": (_c_int, [_c_int, _pi, _pi, _ppd, _vp, _vp, _c_int, _vp]),
     "stiga_kronsum_create": (_c_int, [_c_int, _pi, _c_int, _pd, _ppd, _c_int, ctypes.POINTER(_vp)]),
     "stiga_kronsum_create_spacetime": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl, _c_int,

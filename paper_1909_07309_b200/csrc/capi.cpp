@@ -148,6 +148,57 @@ struct stiga_fd_s {
         g.ncols = n_dof / dims[mode];
         return g;
     }
+    // spatial mode m of a time slab with nt_local slices
+    gpu::ModeGeom slab_geom(int mode, long long nt_local) const {
+        gpu::ModeGeom g = geom(mode);
+        g.ncols = n_s / dims[mode] * nt_local;
+        return g;
+    }
+    // time mode of a spatial slab with ns_local spatial indices (ns_local x n_t, colex)
+    gpu::ModeGeom time_geom(long long ns_local) const {
+        gpu::ModeGeom g;
+        g.L = ns_local;
+        g.n = g.m = dims[d];
+        g.ncols = ns_local;
+        return g;
+    }
+
+    // Distributed building blocks.
+    void apply_space(bool backward, long long t0, long long nt_local, const double* in, double* out, cudaStream_t st) {
+        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
+        double* bufs[2] = {scratch.p, scratch2.p};
+        const double* dsl = dinv.p ? dinv.p + n_s * t0 : nullptr;
+        const long long nloc = n_s * nt_local;
+        const int nops = d + ((!backward && dsl) ? 1 : 0);
+        int k = 0;
+        const double* src = in;
+        auto next = [&]() -> double* { double* r = (k == nops - 1) ? out : bufs[k % 2]; ++k; return r; };
+        if (!backward && dsl) {
+            double* dst = next();
+            ck(gpu::launch_scale(dsl, src, dst, nloc, st), "slab pre-scale");
+            src = dst;
+        }
+        for (int l = 0; l < d; ++l) {
+            double* dst = next();
+            ck(gpu::launch_mode_product(tl[l], slab_geom(l, nt_local), src, dst, backward ? J[l]->p : Jt[l]->p,
+                                        (backward && l == d - 1) ? dsl : nullptr, st),
+               "slab mode product");
+            src = dst;
+        }
+    }
+    void apply_time(long long s0, long long ns_local, const double* in, double* out, cudaStream_t st) {
+        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
+        gpu::ArrowParams a2 = ap;
+        a2.s_off = s0;
+        const gpu::ModeGeom g = time_geom(ns_local);
+        if (time_split) {
+            ck(gpu::launch_mode_product(tl_ts, g, in, scratch.p, Jt_t.p, nullptr, st), "slab time U_t^T");
+            ck(gpu::launch_arrowhead(scratch.p, scratch2.p, ns_local, a2, st), "slab arrowhead");
+            ck(gpu::launch_mode_product(tl_ts, g, scratch2.p, out, J_t.p, nullptr, st), "slab time U_t");
+        } else {
+            ck(gpu::launch_time_fused(tl_t, g, in, out, Jt_t.p, J_t.p, a2, st), "slab time fused");
+        }
+    }
 
     bool time_split = false;            // time direction as U_t^T GEMM + arrowhead + U_t GEMM
 
@@ -584,6 +635,39 @@ int stiga_fd_apply_profiled(stiga_fd_t P, const double* d_r, double* d_s, void* 
         ck(cudaEventSynchronize(ev[passes]), "cudaEventSynchronize");
         for (int k = 0; k < passes; ++k) ck(cudaEventElapsedTime(&pass_ms[k], ev[k], ev[k + 1]), "elapsed");
         for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+int stiga_fd_apply_space(stiga_fd_t P, int backward, long long t0, long long nt_local, const double* d_in,
+                         double* d_out, void* stream) {
+    return guarded([&] {
+        require(P && d_in && d_out, "stiga_fd_apply_space: null argument");
+        require(P->device >= 0, "stiga_fd_apply_space: host-only handle");
+        require(t0 >= 0 && nt_local >= 1 && t0 + nt_local <= P->dims[P->d], "stiga_fd_apply_space: time slab out of range");
+        require(d_in != d_out, "stiga_fd_apply_space: input and output must not alias");
+        DeviceGuard dg(P->device);
+        P->apply_space(backward != 0, t0, nt_local, d_in, d_out, as_stream(stream));
+    });
+}
+
+int stiga_fd_apply_time(stiga_fd_t P, long long s0, long long ns_local, const double* d_in, double* d_out,
+                        void* stream) {
+    return guarded([&] {
+        require(P && d_in && d_out, "stiga_fd_apply_time: null argument");
+        require(P->device >= 0, "stiga_fd_apply_time: host-only handle");
+        require(s0 >= 0 && ns_local >= 1 && s0 + ns_local <= P->n_s, "stiga_fd_apply_time: spatial slab out of range");
+        require(d_in != d_out, "stiga_fd_apply_time: input and output must not alias");
+        DeviceGuard dg(P->device);
+        P->apply_time(s0, ns_local, d_in, d_out, as_stream(stream));
+    });
+}
+
+int stiga_copy_blocks(const double* d_src, long long src_ld, double* d_dst, long long dst_ld, long long rows,
+                      long long cols, void* stream) {
+    return guarded([&] {
+        require(rows >= 0 && cols >= 0 && (rows == 0 || cols == 0 || (d_src && d_dst)), "stiga_copy_blocks: invalid argument");
+        require(src_ld >= cols && dst_ld >= cols, "stiga_copy_blocks: leading dimension smaller than the row length");
+        ck(gpu::launch_copy_blocks(d_src, src_ld, d_dst, dst_ld, rows, cols, as_stream(stream)), "copy_blocks");
     });
 }
 

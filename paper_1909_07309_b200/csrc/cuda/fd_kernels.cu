@@ -388,7 +388,7 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
     long long s = c0 + c;
     if (s >= a.geo.ncols) s = a.geo.ncols - 1;
     double lam = 0.0;  // ((0 + lambda_1) + lambda_2) + ... (fdsolve.cpp:91-99)
-    long long rem = s;
+    long long rem = s + ap.s_off;  // global spatial index (slab offset in the sharded apply)
     for (int l = 0; l < ap.d; ++l) {
         const long long q = rem / ap.n[l];
         lam = lam + __ldg(ap.lam[l] + (rem - q * ap.n[l]));
@@ -417,7 +417,7 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
     }
 #pragma unroll
     for (int off = P >> 1; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-    const double xlast = __ldg(ap.S_inv + s) * (slast + part);
+    const double xlast = __ldg(ap.S_inv + ap.s_off + s) * (slast + part);
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
         const double rinv = pair_rinv(lam, linv, nu, __ldg(ap.pair_c + j));
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restr
     const bool valid = s0 < Ns;
     const long long s = valid ? s0 : Ns - 1;
     double lam = 0.0;  // ((0 + lambda_1) + lambda_2) + ... (fdsolve.cpp:91-99)
-    long long rem = s;
+    long long rem = s + ap.s_off;  // global spatial index (slab offset in the sharded apply)
     for (int l = 0; l < ap.d; ++l) {
         const long long q = rem / ap.n[l];
         lam = lam + __ldg(ap.lam[l] + (rem - q * ap.n[l]));
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restr
     double srhs = __ldg(zc + (nt - 1) * Ns);
 #pragma unroll
     for (int k = 0; k < P; ++k) srhs += part_s[k][lane];
-    const double xlast = __ldg(ap.S_inv + s) * srhs;
+    const double xlast = __ldg(ap.S_inv + ap.s_off + s) * srhs;
     if (!valid) return;
     double* xo = Xo + s;
 #pragma unroll 4
@@ -550,16 +550,23 @@ __global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restr
 
 __global__ void scale_kernel(const double* __restrict__ a, const double* __restrict__ x, double* __restrict__ y,
                              long long n) {
-    const long long n2 = n >> 1;
-    const double2* a2 = reinterpret_cast<const double2*>(a);
-    const double2* x2 = reinterpret_cast<const double2*>(x);
-    double2* y2 = reinterpret_cast<double2*>(y);
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n2;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const double2 av = a2[i], xv = x2[i];
-        y2[i] = make_double2(av.x * xv.x, av.y * xv.y);
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(x) |
+                           reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
+    if (aligned) {  // 16-byte vector path (slab offsets of the sharded apply can be odd)
+        const long long n2 = n >> 1;
+        const double2* a2 = reinterpret_cast<const double2*>(a);
+        const double2* x2 = reinterpret_cast<const double2*>(x);
+        double2* y2 = reinterpret_cast<double2*>(y);
+        for (long long i = i0; i < n2; i += stride) {
+            const double2 av = a2[i], xv = x2[i];
+            y2[i] = make_double2(av.x * xv.x, av.y * xv.y);
+        }
+        if (i0 == 0 && (n & 1)) y[n - 1] = a[n - 1] * x[n - 1];
+    } else {
+        for (long long i = i0; i < n; i += stride) y[i] = a[i] * x[i];
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) y[n - 1] = a[n - 1] * x[n - 1];
 }
 
 KArgs make_args(const Tiling& t, const ModeGeom& g) {
@@ -774,6 +781,25 @@ cudaError_t launch_arrowhead(const double* Z, double* X, long long Ns, const Arr
     constexpr int P = 8;
     const long long blocks = (Ns + 31) / 32;
     arrowhead_kernel<P><<<static_cast<unsigned>(blocks), 32 * P, 0, st>>>(Z, X, Ns, ap);
+    return cudaGetLastError();
+}
+
+__global__ void copy_blocks_kernel(const double* __restrict__ src, long long sld, double* __restrict__ dst,
+                                   long long dld, long long rows, long long cols) {
+    const long long total = rows * cols;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long r = e / cols, c = e - r * cols;
+        dst[r * dld + c] = src[r * sld + c];
+    }
+}
+
+cudaError_t launch_copy_blocks(const double* src, long long sld, double* dst, long long dld, long long rows,
+                               long long cols, cudaStream_t st) {
+    const long long total = rows * cols;
+    if (total <= 0) return cudaSuccess;
+    const long long blocks = std::min<long long>((total + 255) / 256, 148LL * 16);
+    copy_blocks_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(src, sld, dst, dld, rows, cols);
     return cudaGetLastError();
 }
 

@@ -30,6 +30,7 @@ struct ArrowParams {
     const double* g = nullptr;              // n_t - 1 coupling entries
     int npairs = 0, zero_count = 0, n_t = 0;
     double gamma = 0.0, nu = 0.0, inv_nu = 0.0;
+    long long s_off = 0;  // global index of local spatial index 0 (sharded apply)
     int debug = 0;  // bit 0: skip the arrowhead (Y = U_t U_t^T X); debugging aid
 };
 
@@ -81,6 +82,10 @@ cudaError_t launch_arrowhead(const double* Z, double* X, long long Ns, const Arr
 cudaError_t launch_time_fused(const Tiling& t, const ModeGeom& g, const double* X, double* Y,
                               const double* Jt_pad, const double* J_pad, const ArrowParams& ap,
                               cudaStream_t stream);
+
+/// dst[r*dld + c] = src[r*sld + c] for r < rows, c < cols (pack/unpack of the sharded transposes).
+cudaError_t launch_copy_blocks(const double* src, long long sld, double* dst, long long dld, long long rows,
+                               long long cols, cudaStream_t stream);
 
 /// Elementwise y = a .* x (the D^-1/2 post-scale of the last backward pass).
 cudaError_t launch_scale(const double* a, const double* x, double* y, long long n, cudaStream_t stream);
