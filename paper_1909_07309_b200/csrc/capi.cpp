@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <functional>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -132,6 +133,7 @@ struct stiga_fd_s {
     long long n_dof = 0, n_s = 0;
     std::vector<gpu::Tiling> tl;        // per spatial direction
     gpu::Tiling tl_t;
+    gpu::Tiling tl_ts;                  // mode-kernel tiling of the split time products
     std::vector<std::unique_ptr<DBuf>> Jt, J;  // padded U_l^T, U_l
     DBuf Jt_t, J_t;
     std::vector<std::unique_ptr<DBuf>> lam;
@@ -202,43 +204,85 @@ struct stiga_fd_s {
 
     bool time_split = false;            // time direction as U_t^T GEMM + arrowhead + U_t GEMM
 
-    // Picks the faster time-direction variant by timing both once on the scratch vectors
-    // (STIGA_TIME_VARIANT=fused|split forces one).  The fused kernel needs a tiling that holds all
-    // n_t rows in one CTA; when none exists only the split path is available.
-    void choose_time_variant() {
-        const char* force = std::getenv("STIGA_TIME_VARIANT");
-        const bool fused_ok = tl_t.MI > 0;
-        if (force && std::string(force) == "split") { time_split = true; return; }
-        if (force && std::string(force) == "fused" && fused_ok) { time_split = false; return; }
-        if (!fused_ok) { time_split = true; return; }
-        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
-        ck(cudaMemset(scratch.p, 0, sizeof(double) * n_dof), "memset");
+    // Setup-time autotuning: every candidate tiling of every mode (and both time-direction
+    // variants) is timed once on the scratch vectors at the real tensor geometry and the fastest is
+    // kept.  STIGA_TIME_VARIANT=fused|split forces the time path; STIGA_NO_AUTOTUNE=1 keeps the
+    // heuristic first choices.
+    std::vector<std::vector<gpu::Tiling>> cand_space;
+    std::vector<gpu::Tiling> cand_time, cand_ts;
+
+    float time_once(const std::function<void()>& f) {
         cudaEvent_t e0, e1;
         ck(cudaEventCreate(&e0), "event");
         ck(cudaEventCreate(&e1), "event");
-        float best[2] = {0.f, 0.f};
-        for (int v = 0; v < 2; ++v) {
-            for (int rep = 0; rep < 3; ++rep) {
-                ck(cudaEventRecord(e0, nullptr), "event");
-                if (v == 0) {
-                    ck(gpu::launch_time_fused(tl_t, geom(d), scratch.p, scratch2.p, Jt_t.p, J_t.p, ap, nullptr), "tune");
-                } else {
-                    ck(gpu::launch_mode_product(tl_ts, geom(d), scratch.p, scratch2.p, Jt_t.p, nullptr, nullptr), "tune");
-                    ck(gpu::launch_arrowhead(scratch2.p, scratch.p, n_s, ap, nullptr), "tune");
-                    ck(gpu::launch_mode_product(tl_ts, geom(d), scratch.p, scratch2.p, J_t.p, nullptr, nullptr), "tune");
-                }
-                ck(cudaEventRecord(e1, nullptr), "event");
-                ck(cudaEventSynchronize(e1), "event");
-                float ms = 0.f;
-                ck(cudaEventElapsedTime(&ms, e0, e1), "event");
-                if (rep > 0) best[v] = (rep == 1) ? ms : std::min(best[v], ms);
-            }
+        f();  // warm (sets the smem attribute, loads the module)
+        float best = 1e30f;
+        for (int rep = 0; rep < 2; ++rep) {
+            ck(cudaEventRecord(e0, nullptr), "event");
+            f();
+            ck(cudaEventRecord(e1, nullptr), "event");
+            ck(cudaEventSynchronize(e1), "event");
+            float ms = 0.f;
+            ck(cudaEventElapsedTime(&ms, e0, e1), "event");
+            best = std::min(best, ms);
         }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        time_split = best[1] < best[0];
+        return best;
     }
-    gpu::Tiling tl_ts;                  // mode-kernel tiling of the split time products
+
+    void autotune() {
+        const char* force = std::getenv("STIGA_TIME_VARIANT");
+        const bool no_tune = std::getenv("STIGA_NO_AUTOTUNE") != nullptr;
+        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
+        ck(cudaMemset(scratch.p, 0, sizeof(double) * n_dof), "memset");
+        const size_t kMaxCand = 6;
+        for (int l = 0; l < d; ++l) {
+            tl[l] = cand_space[l].front();
+            if (no_tune) continue;
+            float best = 1e30f;
+            for (size_t c = 0; c < std::min(kMaxCand, cand_space[l].size()); ++c) {
+                const gpu::Tiling& t = cand_space[l][c];
+                const float ms = time_once([&] {
+                    ck(gpu::launch_mode_product(t, geom(l), scratch.p, scratch2.p, Jt[l]->p, nullptr, nullptr), "tune");
+                });
+                if (ms < best) { best = ms; tl[l] = t; }
+            }
+        }
+        const bool fused_ok = !cand_time.empty();
+        tl_t = fused_ok ? cand_time.front() : gpu::Tiling{};
+        tl_ts = cand_ts.front();
+        float best_fused = 1e30f, best_split = 1e30f;
+        if (!no_tune) {
+            if (fused_ok && !(force && std::string(force) == "split")) {
+                for (size_t c = 0; c < std::min(kMaxCand, cand_time.size()); ++c) {
+                    const gpu::Tiling& t = cand_time[c];
+                    const float ms = time_once([&] {
+                        ck(gpu::launch_time_fused(t, geom(d), scratch.p, scratch2.p, Jt_t.p, J_t.p, ap, nullptr), "tune");
+                    });
+                    if (ms < best_fused) { best_fused = ms; tl_t = t; }
+                }
+            }
+            if (!(force && std::string(force) == "fused")) {
+                float best_gemm = 1e30f;
+                for (size_t c = 0; c < std::min(kMaxCand, cand_ts.size()); ++c) {
+                    const gpu::Tiling& t = cand_ts[c];
+                    const float ms = time_once([&] {
+                        ck(gpu::launch_mode_product(t, geom(d), scratch.p, scratch2.p, Jt_t.p, nullptr, nullptr), "tune");
+                    });
+                    if (ms < best_gemm) { best_gemm = ms; tl_ts = t; }
+                }
+                const float arrow = time_once([&] {
+                    ck(gpu::launch_arrowhead(scratch2.p, scratch.p, n_s, ap, nullptr), "tune");
+                });
+                best_split = 2.f * best_gemm + arrow;
+            }
+        }
+        if (force && std::string(force) == "split") time_split = true;
+        else if (force && std::string(force) == "fused" && fused_ok) time_split = false;
+        else if (!fused_ok) time_split = true;
+        else time_split = !no_tune && best_split < best_fused;
+    }
 
     int launches() const { return 2 * d + (time_split ? 3 : 1) + (dinv.p ? 1 : 0); }
 
@@ -491,8 +535,11 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
 
         DeviceGuard dg(device);
         for (int l = 0; l < d; ++l) {
-            h->tl.push_back(gpu::choose_mode_tiling(F.n[l], F.n[l], false));
-            const int rows = h->tl.back().Mp;
+            h->cand_space.push_back(gpu::mode_tiling_candidates(F.n[l], F.n[l]));
+            if (h->cand_space.back().empty()) throw std::runtime_error("internal: no mode-product tiling");
+            h->tl.push_back(h->cand_space.back().front());
+            int rows = 0;
+            for (const auto& t : h->cand_space.back()) rows = std::max(rows, t.Mp);
             h->Jt.emplace_back(new DBuf);
             h->J.emplace_back(new DBuf);
             h->Jt.back()->upload(pad_factor(F.U[l], true, rows, h->tl.back().Kp));
@@ -500,11 +547,15 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
             h->lam.emplace_back(new DBuf);
             h->lam.back()->upload(F.lambda[l]);
         }
-        h->tl_t = gpu::choose_time_tiling(F.n_t);
-        h->tl_ts = gpu::choose_mode_tiling(F.n_t, F.n_t, false);
-        const int trows = std::max(h->tl_t.Mp, h->tl_ts.Mp);
-        h->Jt_t.upload(pad_factor(F.time.U, true, trows, h->tl_t.Kp));
-        h->J_t.upload(pad_factor(F.time.U, false, trows, h->tl_t.Kp));
+        h->cand_time = gpu::time_tiling_candidates(F.n_t);
+        h->cand_ts = gpu::mode_tiling_candidates(F.n_t, F.n_t);
+        if (h->cand_ts.empty()) throw std::runtime_error("internal: no time-product tiling");
+        int trows = 0;
+        for (const auto& t : h->cand_time) trows = std::max(trows, t.Mp);
+        for (const auto& t : h->cand_ts) trows = std::max(trows, t.Mp);
+        const int tKp = h->cand_ts.front().Kp;
+        h->Jt_t.upload(pad_factor(F.time.U, true, trows, tKp));
+        h->J_t.upload(pad_factor(F.time.U, false, trows, tKp));
         h->S_inv.upload(F.S_inv);
         std::vector<double> pc, pc1, pc1sq, pgg;
         for (size_t j = 0; j < F.time.lambda.size(); ++j) {
@@ -551,7 +602,7 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         ap.nu = nu;
         ap.inv_nu = 1.0 / nu;
         if (const char* dbg = std::getenv("STIGA_DEBUG_ARROW")) ap.debug = std::atoi(dbg);
-        h->choose_time_variant();
+        h->autotune();
         *out = h.release();
     });
 }

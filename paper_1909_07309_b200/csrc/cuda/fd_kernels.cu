@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <utility>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 
@@ -671,17 +673,15 @@ cudaError_t dispatch_time(const Tiling& t, const ModeGeom& g, const double* X, d
 
 }  // namespace
 
-Tiling choose_mode_tiling(int m, int n, bool prescale) {
-    (void)prescale;  // the D^-1/2 pre-scale is a separate elementwise pass
-    Tiling best;
-    best.MI = 0;
-    double best_score = -1.0;
+std::vector<Tiling> mode_tiling_candidates(int m, int n) {
+    std::vector<std::pair<double, Tiling>> c;
     const int S = (m + 7) / 8;
     const int Kp = (n + 3) / 4 * 4;
     const int rb0 = (S + 12) / 13;
     for (int RB = rb0; RB <= rb0 + 2; ++RB) {
         const int MI = (S + RB - 1) / RB;
         if (MI > 13 || MI < 1) continue;
+        if (RB > rb0 && (S + rb0 - 1) / rb0 == MI) continue;  // same MI as a smaller RB
         for (int WN : {4, 2}) {
             Tiling t;
             t.MI = MI;
@@ -703,20 +703,28 @@ Tiling choose_mode_tiling(int m, int n, bool prescale) {
             t.ctas_per_sm = occ;
             if (occ < 1) continue;
             const double eff = static_cast<double>(S) / (RB * MI);
-            const double score = std::min(occ * t.WN, 16) * eff + 0.02 * WN - 0.01 * RB;
-            if (score > best_score) {
-                best_score = score;
-                best = t;
-            }
+            c.emplace_back(std::min(occ * t.WN, 16) * eff + 0.02 * WN - 0.01 * RB, t);
         }
     }
-    return best;
+    std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<Tiling> out;
+    for (auto& e : c) out.push_back(e.second);
+    return out;
 }
 
-Tiling choose_time_tiling(int nt) {
-    Tiling best;
-    best.MI = 0;
-    double best_score = -1.0;
+Tiling choose_mode_tiling(int m, int n, bool prescale) {
+    (void)prescale;  // the D^-1/2 pre-scale is a separate elementwise pass
+    const std::vector<Tiling> c = mode_tiling_candidates(m, n);
+    if (c.empty()) {
+        Tiling t;
+        t.MI = 0;
+        return t;
+    }
+    return c.front();
+}
+
+std::vector<Tiling> time_tiling_candidates(int nt) {
+    std::vector<std::pair<double, Tiling>> c;
     int force_wm = 0, force_wn = 0, force_ns = 0;  // debugging aid: STIGA_FORCE_TIME_TILING="WM,WN,NS"
     if (const char* f = std::getenv("STIGA_FORCE_TIME_TILING"))
         std::sscanf(f, "%d,%d,%d", &force_wm, &force_wn, &force_ns);
@@ -753,15 +761,24 @@ Tiling choose_time_tiling(int nt) {
                 t.ctas_per_sm = occ;
                 if (occ < 1) continue;
                 const double eff = static_cast<double>(S) / (WM * MI);
-                const double score = std::min(occ * WM * WN, 16) * eff + 0.01 * ns + 0.02 * WN;
-                if (score > best_score) {
-                    best_score = score;
-                    best = t;
-                }
+                c.emplace_back(std::min(occ * WM * WN, 16) * eff + 0.01 * ns + 0.02 * WN, t);
             }
         }
     }
-    return best;
+    std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<Tiling> out;
+    for (auto& e : c) out.push_back(e.second);
+    return out;
+}
+
+Tiling choose_time_tiling(int nt) {
+    const std::vector<Tiling> c = time_tiling_candidates(nt);
+    if (c.empty()) {
+        Tiling t;
+        t.MI = 0;
+        return t;
+    }
+    return c.front();
 }
 
 cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jpad,

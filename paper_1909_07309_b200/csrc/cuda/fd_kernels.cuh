@@ -11,6 +11,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 namespace stiga {
 namespace gpu {
 
@@ -66,6 +68,9 @@ struct Tiling {
 
 Tiling choose_mode_tiling(int m, int n, bool prescale);  // m output rows, n contraction length
 Tiling choose_time_tiling(int n_t);
+/// All feasible tilings, best heuristic first (setup autotunes over the leading ones).
+std::vector<Tiling> mode_tiling_candidates(int m, int n);
+std::vector<Tiling> time_tiling_candidates(int n_t);
 
 /// Y = (I (x) J (x) I) X along one mode.  J is row-major, zero padded to (t.Mp x t.Kp).
 /// post_scale (optional) multiplies Y elementwise in the register epilogue (the D^-1/2 post-scale).
