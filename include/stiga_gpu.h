@@ -31,6 +31,7 @@ extern "C" {
 
 typedef struct stiga_fd_s* stiga_fd_t;
 typedef struct stiga_kronsum_s* stiga_kronsum_t;
+typedef struct stiga_problem_s* stiga_problem_t;
 
 /* ---- diagnostics ------------------------------------------------------------------- */
 
@@ -54,6 +55,27 @@ int stiga_assemble_spatial_parametric(int p, int n_el, int q, double* K, double*
    kind 0 = spatial space, 1 = temporal space; weights may be NULL (all ones). out: n*n. */
 int stiga_assemble_univariate(int p, int n_el, int kind, int q, int deriv_row, int deriv_col,
                               const double* element_weights, double* out);
+
+/* ---- problems, geometry and the A^G coefficient pieces (host) -------------------------- */
+
+/* make_problem(id) (problems.cpp:244-261), geometry + coefficient part: "identity-interval-1d",
+   "identity-square-2d", "identity-cube-3d", "quarter-annulus-2d", "separable-nu-2d", and the
+   BASELINE config-4 "deformed-cube-3d" (fit_geometry of x + 0.1 sin sin sin (1,1,1) with p_g=3,
+   n_el_g=8; kappa = 1 + 0.5 sin(2 pi x1) cos(2 pi x2); c = 1 + 0.25 x3). */
+int stiga_problem_create(const char* id, stiga_problem_t* out);
+int stiga_problem_destroy(stiga_problem_t P);
+int stiga_problem_dim(stiga_problem_t P, int* d);
+/* GeometryMap::value / ::jacobian (geometry.cpp:41-97); J is column-major d x d, x or J may be NULL. */
+int stiga_problem_eval_geometry(stiga_problem_t P, const double* eta, double* x, double* J);
+/* nu_s(x), gamma_s(x) of the problem (1 when constant). */
+int stiga_problem_eval_fields(stiga_problem_t P, const double* x, double* nu_s, double* gamma_s);
+/* Inputs of make_geometry_preconditioner (solver.cpp:127-144) for degree p / n_el elements in every
+   direction and in time: K~_l, M~_l (d blocks of n_s*n_s, column-major), W_t and the weighted M_t
+   (n_t*n_t), D = diag(A)/diag(A~) (N_dof; NULL skips the physical diagonal quadrature), the separated
+   factors phi, Phi (d*n_el each, may be NULL), the fit residuals (d+1) and ALS sweeps (may be NULL). */
+int stiga_geometry_preconditioner_pieces(stiga_problem_t P, int p, int n_el, double* Kt, double* Mt_s, double* Wt,
+                                         double* Mt, double* D, double* phi, double* Phi, double* residuals,
+                                         int* sweeps);
 
 /* ---- ExtendedFDPreconditioner (fdsolve.hpp:41-70) ------------------------------------- */
 

@@ -36,6 +36,12 @@ SIGNATURES = {
     "stiga_assemble_time_matrices": (_c_int, [_c_int, _c_int, _c_dbl, _pd, _pd]),
     "stiga_assemble_spatial_parametric": (_c_int, [_c_int, _c_int, _c_int, _pd, _pd]),
     "stiga_assemble_univariate": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _pd, _pd]),
+    "stiga_problem_create": (_c_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "stiga_problem_destroy": (_c_int, [_vp]),
+    "stiga_problem_dim": (_c_int, [_vp, _pi]),
+    "stiga_problem_eval_geometry": (_c_int, [_vp, _pd, _pd, _pd]),
+    "stiga_problem_eval_fields": (_c_int, [_vp, _pd, _pd, _pd]),
+    "stiga_geometry_preconditioner_pieces": (_c_int, [_vp, _c_int, _c_int, _pd, _pd, _pd, _pd, _pd, _pd, _pd, _pd, _pi]),
     "stiga_fd_setup": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl, _pd, _c_ll, _c_int,
                                 ctypes.POINTER(_vp)]),
     "stiga_fd_destroy": (_c_int, [_vp]),

@@ -25,6 +25,7 @@
 #include "cuda/fd_kernels.cuh"
 #include "host/assembly.hpp"
 #include "host/fdsetup.hpp"
+#include "host/geometry.hpp"
 
 using namespace stiga;
 
@@ -497,6 +498,71 @@ int stiga_assemble_univariate(int p, int n_el, int kind, int q, int deriv_row, i
         if (element_weights) w.assign(element_weights, element_weights + quad.num_elements);
         const BandedMatrix A = assemble_univariate(s, quad, deriv_row, deriv_col, element_weights ? &w : nullptr);
         std::memcpy(out, A.m.a.data(), A.m.a.size() * sizeof(double));
+    });
+}
+
+struct stiga_problem_s {
+    ProblemSpec spec;
+};
+
+int stiga_problem_create(const char* id, stiga_problem_t* out) {
+    return guarded([&] {
+        require(id && out, "make_problem: null argument");
+        *out = nullptr;
+        auto h = std::make_unique<stiga_problem_s>();
+        h->spec = make_problem(id);
+        *out = h.release();
+    });
+}
+
+int stiga_problem_destroy(stiga_problem_t P) {
+    return guarded([&] { delete P; });
+}
+
+int stiga_problem_dim(stiga_problem_t P, int* d) {
+    return guarded([&] {
+        require(P && d, "stiga_problem_dim: null argument");
+        *d = P->spec.d;
+    });
+}
+
+int stiga_problem_eval_geometry(stiga_problem_t P, const double* eta, double* x, double* J) {
+    return guarded([&] {
+        require(P && eta, "GeometryMap: null argument");
+        if (x) P->spec.geometry.value(eta, x);
+        if (J) P->spec.geometry.jacobian(eta, J);
+    });
+}
+
+int stiga_problem_eval_fields(stiga_problem_t P, const double* x, double* nu_s, double* gamma_s) {
+    return guarded([&] {
+        require(P && x, "stiga_problem_eval_fields: null argument");
+        if (nu_s) *nu_s = P->spec.nu_s ? P->spec.nu_s(x) : 1.0;
+        if (gamma_s) *gamma_s = P->spec.gamma_s ? P->spec.gamma_s(x) : 1.0;
+    });
+}
+
+int stiga_geometry_preconditioner_pieces(stiga_problem_t P, int p, int n_el, double* Kt, double* Mt_s, double* Wt,
+                                         double* Mt, double* D, double* phi, double* Phi, double* residuals,
+                                         int* sweeps) {
+    return guarded([&] {
+        require(P && Kt && Mt_s && Wt && Mt, "make_geometry_preconditioner: null argument");
+        const GeometryPreconditionerPieces g = geometry_preconditioner_pieces(P->spec, p, n_el, D != nullptr);
+        const int d = P->spec.d;
+        const size_t nn = g.Kt[0].a.size();
+        for (int l = 0; l < d; ++l) {
+            std::copy(g.Kt[l].a.begin(), g.Kt[l].a.end(), Kt + l * nn);
+            std::copy(g.Mt_s[l].a.begin(), g.Mt_s[l].a.end(), Mt_s + l * nn);
+        }
+        std::copy(g.Wt.a.begin(), g.Wt.a.end(), Wt);
+        std::copy(g.Mt.a.begin(), g.Mt.a.end(), Mt);
+        if (D) std::copy(g.D.begin(), g.D.end(), D);
+        for (int l = 0; l < d; ++l) {
+            if (phi) std::copy(g.sep.phi[l].begin(), g.sep.phi[l].end(), phi + l * n_el);
+            if (Phi) std::copy(g.sep.Phi[l].begin(), g.sep.Phi[l].end(), Phi + l * n_el);
+        }
+        if (residuals) std::copy(g.sep.residuals.begin(), g.sep.residuals.end(), residuals);
+        if (sweeps) *sweeps = g.sep.sweeps;
     });
 }
 

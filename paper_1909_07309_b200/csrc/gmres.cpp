@@ -34,11 +34,38 @@ void sck(int status, const char* w) {
     if (status != STIGA_OK) throw GFail(std::string(w) + ": " + stiga_last_error());
 }
 
+// Krylov / work vectors come from a per-thread pool keyed by (device, length): large cudaMalloc /
+// cudaFree pairs on every solve cost tens of milliseconds and synchronize the device.
+struct Pool {
+    int device = -1;
+    long long n = -1;
+    std::vector<double*> free_list;
+    ~Pool() {
+        for (double* p : free_list) cudaFree(p);
+    }
+};
+thread_local Pool g_pool;
+
 struct Vec {
     double* p = nullptr;
-    explicit Vec(long long n) { gck(cudaMalloc(&p, sizeof(double) * std::max<long long>(n, 1)), "cudaMalloc"); }
+    explicit Vec(long long n) {
+        int dev = 0;
+        gck(cudaGetDevice(&dev), "cudaGetDevice");
+        if (g_pool.device != dev || g_pool.n != n) {
+            for (double* q : g_pool.free_list) cudaFree(q);
+            g_pool.free_list.clear();
+            g_pool.device = dev;
+            g_pool.n = n;
+        }
+        if (!g_pool.free_list.empty()) {
+            p = g_pool.free_list.back();
+            g_pool.free_list.pop_back();
+        } else {
+            gck(cudaMalloc(&p, sizeof(double) * std::max<long long>(n, 1)), "cudaMalloc");
+        }
+    }
     ~Vec() {
-        if (p) cudaFree(p);
+        if (p) g_pool.free_list.push_back(p);
     }
     Vec(const Vec&) = delete;
     Vec& operator=(const Vec&) = delete;

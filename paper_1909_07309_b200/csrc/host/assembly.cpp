@@ -5,20 +5,39 @@
 
 namespace stiga {
 
+namespace {
+BandedMatrix assemble_impl(const SplineSpace1D& space, const QuadratureRule& quad, int deriv_row, int deriv_col,
+                           const std::function<double(int, double)>& weight_at, bool check);
+}
+
+BandedMatrix assemble_univariate_fn(const SplineSpace1D& space, const QuadratureRule& quad, int deriv_row,
+                                    int deriv_col, const std::function<double(double)>& weight) {
+    return assemble_impl(space, quad, deriv_row, deriv_col, [&](int, double x) { return weight(x); },
+                         deriv_row == deriv_col);
+}
+
 BandedMatrix assemble_univariate(const SplineSpace1D& space, const QuadratureRule& quad, int deriv_row,
                                  int deriv_col, const std::vector<double>* element_weights) {
+    if (element_weights && static_cast<int>(element_weights->size()) != quad.num_elements)
+        throw std::invalid_argument("assemble_univariate: one weight per element required");
+    if (!element_weights)
+        return assemble_impl(space, quad, deriv_row, deriv_col, [](int, double) { return 1.0; }, false);
+    return assemble_impl(space, quad, deriv_row, deriv_col,
+                         [&](int e, double) { return (*element_weights)[e]; }, deriv_row == deriv_col);
+}
+
+namespace {
+BandedMatrix assemble_impl(const SplineSpace1D& space, const QuadratureRule& quad, int deriv_row, int deriv_col,
+                           const std::function<double(int, double)>& weight_at, bool check) {
     if (deriv_row < 0 || deriv_row > 1 || deriv_col < 0 || deriv_col > 1)
         throw std::invalid_argument("assemble_univariate: derivative orders must be 0 or 1");
     if (quad.num_elements != space.knot_vector().num_elements())
         throw std::invalid_argument("assemble_univariate: quadrature built on a different knot vector");
-    if (element_weights && static_cast<int>(element_weights->size()) != quad.num_elements)
-        throw std::invalid_argument("assemble_univariate: one weight per element required");
     const int n = space.dim(), p = space.degree();
-    const bool check = element_weights && deriv_row == deriv_col;
     BandedMatrix A{DenseMatrix(n, n), p};
     std::vector<double> val(p + 1), der(p + 1);
     for (int q = 0; q < quad.num_points(); ++q) {
-        const double wq = element_weights ? (*element_weights)[quad.element_of(q)] : 1.0;
+        const double wq = weight_at(quad.element_of(q), quad.nodes[q]);
         if (check && wq <= 0.0)
             throw std::runtime_error("assemble_univariate: non-positive weight sample in a mass/stiffness integral");
         const double c = quad.weights[q] * wq;
@@ -40,6 +59,7 @@ BandedMatrix assemble_univariate(const SplineSpace1D& space, const QuadratureRul
     }
     return A;
 }
+}  // namespace
 
 std::pair<BandedMatrix, BandedMatrix> assemble_time_matrices(int p_t, int n_el_t, double T) {
     if (T <= 0.0) throw std::invalid_argument("assemble_time_matrices: T must be positive");

@@ -22,6 +22,11 @@ struct BandedMatrix {
 BandedMatrix assemble_univariate(const SplineSpace1D& space, const QuadratureRule& quad, int deriv_row,
                                  int deriv_col, const std::vector<double>* element_weights = nullptr);
 
+/// assemble_univariate with a weight function of the parametric coordinate (assembly.cpp:112-116);
+/// mass/stiffness (deriv_row == deriv_col) require weight > 0 at every quadrature point.
+BandedMatrix assemble_univariate_fn(const SplineSpace1D& space, const QuadratureRule& quad, int deriv_row,
+                                    int deriv_col, const std::function<double(double)>& weight);
+
 /// W_t = [int b'_j b_i], M_t = T * mass on the temporal space (assembly.cpp:129-138).
 std::pair<BandedMatrix, BandedMatrix> assemble_time_matrices(int p_t, int n_el_t, double T);
 

@@ -61,3 +61,77 @@ def geometry_scaling(pc, K_tilde=None, M_tilde=None, Mt_tilde=None):
     At = stiga.kron_sum_terms(K_tilde or pc.K, M_tilde or pc.M, pc.Wt,
                               pc.Mt if Mt_tilde is None else Mt_tilde, 1.0, 1.0)
     return kron_sum_diagonal(A) / kron_sum_diagonal(At)
+
+
+class Problem:
+    """make_problem(id) (problems.cpp:244-261) on the host through the C ABI; the geometry map and
+    coefficient fields are native (they are evaluated at every quadrature point of the setup)."""
+
+    def __init__(self, pid):
+        import ctypes
+
+        from ._lib import check, lib
+
+        self._lib, self._check, self._ct = lib, check, ctypes
+        h = ctypes.c_void_p()
+        check(lib().stiga_problem_create(pid.encode(), ctypes.byref(h)), "make_problem")
+        self._h = h
+        d = ctypes.c_int()
+        check(lib().stiga_problem_dim(h, ctypes.byref(d)), "problem_dim")
+        self.d = d.value
+        self.name = pid
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib().stiga_problem_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def _p(self, a):
+        return a.ctypes.data_as(self._ct.POINTER(self._ct.c_double))
+
+    def geometry(self, eta):
+        eta = np.ascontiguousarray(eta, dtype=np.float64)
+        x = np.zeros(self.d)
+        J = np.zeros(self.d * self.d)
+        self._check(self._lib().stiga_problem_eval_geometry(self._h, self._p(eta), self._p(x), self._p(J)), "geometry")
+        return x, J.reshape(self.d, self.d).T.copy()
+
+    def fields(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        nu, gam = self._ct.c_double(), self._ct.c_double()
+        self._check(self._lib().stiga_problem_eval_fields(self._h, self._p(x), self._ct.byref(nu), self._ct.byref(gam)),
+                    "fields")
+        return nu.value, gam.value
+
+    def geometry_pieces(self, p, n_el, want_D=True):
+        """make_geometry_preconditioner inputs (solver.cpp:127-144): SpaceTimePieces with the
+        separated-coefficient factors K~, M~, W_t, weighted M_t, plus D and phi/Phi."""
+        ns = stiga.space_dim(p, n_el)
+        nt = stiga.space_dim(p, n_el, temporal=True)
+        d = self.d
+        Kt = np.zeros(d * ns * ns)
+        Ms = np.zeros(d * ns * ns)
+        Wt = np.zeros(nt * nt)
+        Mt = np.zeros(nt * nt)
+        D = np.zeros(ns ** d * nt) if want_D else None
+        phi = np.zeros(d * n_el)
+        Phi = np.zeros(d * n_el)
+        res = np.zeros(d + 1)
+        sweeps = self._ct.c_int()
+        self._check(self._lib().stiga_geometry_preconditioner_pieces(
+            self._h, p, n_el, self._p(Kt), self._p(Ms), self._p(Wt), self._p(Mt),
+            self._p(D) if D is not None else None, self._p(phi), self._p(Phi), self._p(res),
+            self._ct.byref(sweeps)), "geometry_preconditioner_pieces")
+        blk = lambda a, l: a[l * ns * ns:(l + 1) * ns * ns].reshape(ns, ns).T.copy()  # noqa: E731
+        pc = SpaceTimePieces(d, p, n_el, [blk(Kt, l) for l in range(d)], [blk(Ms, l) for l in range(d)],
+                             Wt.reshape(nt, nt).T.copy(), Mt.reshape(nt, nt).T.copy())
+        pc.D = D
+        pc.phi = phi.reshape(d, n_el)
+        pc.Phi = Phi.reshape(d, n_el)
+        pc.residuals = res
+        pc.sweeps = sweeps.value
+        return pc
