@@ -145,6 +145,11 @@ int stiga_kronsum_create(int D, const int* dims, int nterms, const double* coeff
 int stiga_kronsum_create_spacetime(int d, const int* n, const double* const* K, const double* const* M,
                                    int n_t, const double* Wt, const double* Mt, double gamma, double nu,
                                    int device, stiga_kronsum_t* out);
+/* SpaceTimeSystem's A_ = M_s (x) W_t + K_s (x) M_t (solver.cpp:58-70) with the physical spatial
+   matrices of `prob` (assemble_spatial_physical, assembly.cpp:151-268) assembled on the device
+   (one CTA per element, stencil storage of the (2p+1)^d tensor B-spline neighbours) for degree p,
+   n_el elements per direction and in time; the time mass carries nu_t/gamma_t. */
+int stiga_kronsum_create_physical(stiga_problem_t prob, int p, int n_el, int device, stiga_kronsum_t* out);
 int stiga_kronsum_destroy(stiga_kronsum_t A);
 int stiga_kronsum_size(stiga_kronsum_t A, long long* n_dof);
 /* KronSumOperator::apply(x) (kronop.cpp:108-115): y = sum_t coeff_t (x)_l F_{t,l} x. d_y != d_x. */

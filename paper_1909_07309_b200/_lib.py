@@ -61,6 +61,7 @@ SIGNATURES = {
     "stiga_kronsum_create": (_c_int, [_c_int, _pi, _c_int, _pd, _ppd, _c_int, ctypes.POINTER(_vp)]),
     "stiga_kronsum_create_spacetime": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl, _c_int,
                                                 ctypes.POINTER(_vp)]),
+    "stiga_kronsum_create_physical": (_c_int, [_vp, _c_int, _c_int, _c_int, ctypes.POINTER(_vp)]),
     "stiga_kronsum_destroy": (_c_int, [_vp]),
     "stiga_kronsum_size": (_c_int, [_vp, ctypes.POINTER(_c_ll)]),
     "stiga_kronsum_apply": (_c_int, [_vp, _vp, _vp, _vp]),

@@ -23,6 +23,7 @@
 
 #include "cuda/aux_kernels.cuh"
 #include "cuda/fd_kernels.cuh"
+#include "cuda/physical.cuh"
 #include "host/assembly.hpp"
 #include "host/fdsetup.hpp"
 #include "host/geometry.hpp"
@@ -357,6 +358,15 @@ struct stiga_kronsum_s {
     std::vector<int> hbw;
     // spacetime: per direction M_l, K_l bands, time gamma*W_t and nu*M_t bands
     DBuf t0, t1, t2, t3;  // scratch N_dof each
+    // physical (geometry-mapped) system: stencil K_s, M_s on the device + time bands
+    bool physical = false;
+    gpu::PhysicalDesc pdesc;
+    DBuf Kst, Mst, cp, qnode, qweight, bval, bder;
+    int* bfirst = nullptr;
+    std::vector<double> time_W, time_M;  // host copies for diagonal()
+    ~stiga_kronsum_s() {
+        if (bfirst) cudaFree(bfirst);
+    }
 
     gpu::ModeGeom geom(int mode) const {
         gpu::ModeGeom g;
@@ -377,6 +387,14 @@ struct stiga_kronsum_s {
 
     void apply(const double* x, double* y, cudaStream_t st) {
         const gpu::Band none{};
+        if (physical) {  // y = M_s X W_t^T + K_s X M_t^T  (solver.cpp:67-70)
+            ensure_scratch(2);
+            const int d = D - 1;
+            ck(gpu::launch_banded_pass(geom(d), x, nullptr, t0.p, t1.p, band(0), none, band(1), none, 0.0, st),
+               "time bands");
+            ck(gpu::launch_stencil_spmm2(pdesc, Mst.p, t0.p, Kst.p, t1.p, y, dims[d], st), "stencil spmm");
+            return;
+        }
         if (spacetime) {
             // bands: [M_1, K_1, ..., M_d, K_d, gamma W_t, nu M_t]
             const int d = D - 1;
@@ -965,6 +983,98 @@ int stiga_kronsum_create_spacetime(int d, const int* n, const double* const* K, 
     });
 }
 
+int stiga_kronsum_create_physical(stiga_problem_t prob, int p, int n_el, int device, stiga_kronsum_t* out) {
+    return guarded([&] {
+        require(prob && out, "stiga_kronsum_create_physical: null argument");
+        *out = nullptr;
+        const ProblemSpec& spec = prob->spec;
+        const int d = spec.d;
+        const SplineSpace1D space = SplineSpace1D::spatial(p, n_el);
+        const int n = space.dim();
+        auto h = std::make_unique<stiga_kronsum_s>();
+        h->device = device;
+        h->D = d + 1;
+        h->physical = true;
+        h->n_dof = 1;
+        for (int l = 0; l < d; ++l) {
+            h->dims.push_back(n);
+            h->n_dof *= n;
+        }
+        DenseMatrix Wt, Mt;
+        time_matrices(spec, p, n_el, Wt, Mt);
+        h->dims.push_back(static_cast<int>(Wt.rows));
+        h->n_dof *= Wt.rows;
+        DeviceGuard dg(device);
+        // time bands (W_t, M_t) for the banded time pass
+        auto push = [&](const DenseMatrix& F) {
+            const int hb = half_bandwidth(F);
+            h->hbw.push_back(hb);
+            h->bands.emplace_back(new DBuf);
+            h->bands.back()->upload(to_band(F, hb, 1.0));
+        };
+        push(Wt);
+        push(Mt);
+        for (Index i = 0; i < Wt.rows; ++i) {
+            h->time_W.push_back(Wt(i, i));
+            h->time_M.push_back(Mt(i, i));
+        }
+        // 1D quadrature tables (q = p + 1 Gauss points per element, solver.cpp:103)
+        const int q = p + 1;
+        const QuadratureRule quad = gauss_rule(space.knot_vector(), q);
+        std::vector<double> nodes(quad.nodes), weights(quad.weights), bv, bd;
+        std::vector<int> bf;
+        std::vector<double> buf(p + 1);
+        for (int qp = 0; qp < quad.num_points(); ++qp) {
+            bf.push_back(space.eval_active(quad.nodes[qp], 0, buf.data()));
+            bv.insert(bv.end(), buf.begin(), buf.end());
+            space.eval_active(quad.nodes[qp], 1, buf.data());
+            bd.insert(bd.end(), buf.begin(), buf.end());
+        }
+        h->qnode.upload(nodes);
+        h->qweight.upload(weights);
+        h->bval.upload(bv);
+        h->bder.upload(bd);
+        ck(cudaMalloc(&h->bfirst, sizeof(int) * bf.size()), "cudaMalloc");
+        ck(cudaMemcpy(h->bfirst, bf.data(), sizeof(int) * bf.size(), cudaMemcpyHostToDevice), "upload");
+        // geometry: uniform open knots of degree pg with neg elements, control points column-major
+        const GeometryMap& F = spec.geometry;
+        const KnotVector& kv0 = F.knot_vectors()[0];
+        for (const KnotVector& kv : F.knot_vectors()) {
+            const KnotVector u = KnotVector::uniform_open(kv.degree(), kv.num_elements());
+            require(kv.knots() == u.knots(), "stiga_kronsum_create_physical: geometry needs uniform open knot vectors");
+            require(kv.degree() == kv0.degree() && kv.num_elements() == kv0.num_elements(),
+                    "stiga_kronsum_create_physical: geometry knot vectors must agree across directions");
+        }
+        h->cp.upload(F.control_points().a);
+        gpu::PhysicalDesc& g = h->pdesc;
+        g.d = d;
+        g.p = p;
+        g.q = q;
+        g.n_el = n_el;
+        g.n = n;
+        g.pg = kv0.degree();
+        g.neg = kv0.num_elements();
+        g.cp = h->cp.p;
+        g.ncp = F.control_points().rows;
+        problem_field_kinds(spec, g.nu_kind, g.gamma_kind);
+        g.qnode = h->qnode.p;
+        g.qweight = h->qweight.p;
+        g.bval = h->bval.p;
+        g.bder = h->bder.p;
+        g.bfirst = h->bfirst;
+        long long S = 1;
+        for (int l = 0; l < d; ++l) S *= 2 * p + 1;
+        const long long Ns = h->n_dof / h->dims[d];
+        h->Kst.alloc(static_cast<size_t>(Ns * S));
+        h->Mst.alloc(static_cast<size_t>(Ns * S));
+        ck(cudaMemset(h->Kst.p, 0, sizeof(double) * Ns * S), "memset");
+        ck(cudaMemset(h->Mst.p, 0, sizeof(double) * Ns * S), "memset");
+        ck(gpu::launch_physical_assembly(g, h->Kst.p, h->Mst.p, nullptr), "physical assembly");
+        ck(cudaDeviceSynchronize(), "physical assembly");
+        *out = h.release();
+    });
+}
+
 int stiga_kronsum_destroy(stiga_kronsum_t A) {
     return guarded([&] {
         if (!A) return;
@@ -993,6 +1103,22 @@ int stiga_kronsum_diagonal(stiga_kronsum_t A, double* h_diag) {
     return guarded([&] {
         require(A && h_diag, "KronSumOperator::diagonal: null argument");
         std::fill(h_diag, h_diag + A->n_dof, 0.0);
+        if (A->physical) {  // diag(M_s) (x) diag(W_t) + diag(K_s) (x) diag(M_t)
+            DeviceGuard dg(A->device);
+            const int d = A->D - 1;
+            const long long Ns = A->n_dof / A->dims[d];
+            DBuf dK, dM;
+            dK.alloc(static_cast<size_t>(Ns));
+            dM.alloc(static_cast<size_t>(Ns));
+            ck(gpu::launch_stencil_diag(A->pdesc, A->Kst.p, A->Mst.p, dK.p, dM.p, nullptr), "stencil diag");
+            std::vector<double> hk(Ns), hm(Ns);
+            ck(cudaMemcpy(hk.data(), dK.p, sizeof(double) * Ns, cudaMemcpyDeviceToHost), "D2H");
+            ck(cudaMemcpy(hm.data(), dM.p, sizeof(double) * Ns, cudaMemcpyDeviceToHost), "D2H");
+            for (int t = 0; t < A->dims[d]; ++t)
+                for (long long i = 0; i < Ns; ++i)
+                    h_diag[t * Ns + i] = hm[i] * A->time_W[t] + hk[i] * A->time_M[t];
+            return;
+        }
         // kronop.cpp:117-131: acc = kron(diag(F_D), ..., diag(F_1)), first factor fastest
         for (size_t t = 0; t < A->coeffs.size(); ++t) {
             std::vector<double> acc(1, 1.0);

@@ -504,6 +504,35 @@ void physical_diagonals(const std::vector<SplineSpace1D>& spaces, const Geometry
         }
 }
 
+void time_matrices(const ProblemSpec& prob, int p, int n_el, DenseMatrix& Wt, DenseMatrix& Mt) {
+    const double T = prob.T;
+    auto [W, Mplain] = assemble_time_matrices(p, n_el, T);
+    Wt = std::move(W.m);
+    const SplineSpace1D tspace = SplineSpace1D::temporal(p, n_el);
+    const QuadratureRule tquad = gauss_rule(tspace.knot_vector(), p + 1);
+    if (prob.nu_t || prob.gamma_t) {  // M_t carries nu_t/gamma_t (solver.cpp:119-125)
+        const auto tw = [&](double tau) {
+            const double nt = prob.nu_t ? prob.nu_t(T * tau) : 1.0;
+            const double gt = prob.gamma_t ? prob.gamma_t(T * tau) : 1.0;
+            return nt / gt;
+        };
+        BandedMatrix Mh = assemble_univariate_fn(tspace, tquad, 0, 0, tw);
+        for (double& v : Mh.m.a) v *= T;
+        Mt = std::move(Mh.m);
+    } else {
+        Mt = std::move(Mplain.m);
+    }
+}
+
+void problem_field_kinds(const ProblemSpec& prob, int& nu_kind, int& gamma_kind) {
+    nu_kind = gamma_kind = 0;  // gpu::kFieldOne
+    if (prob.name == "separable-nu-2d") nu_kind = 1;
+    if (prob.name == "deformed-cube-3d") {
+        nu_kind = 2;
+        gamma_kind = 3;
+    }
+}
+
 GeometryPreconditionerPieces geometry_preconditioner_pieces(const ProblemSpec& prob, int p, int n_el, bool want_D) {
     const int d = prob.d, q = p + 1;
     const double T = prob.T;
@@ -514,23 +543,8 @@ GeometryPreconditionerPieces geometry_preconditioner_pieces(const ProblemSpec& p
         spaces.push_back(SplineSpace1D::spatial(p, n_el));
         kvs.push_back(spaces.back().knot_vector());
     }
-    // time matrices; M_t carries nu_t/gamma_t (solver.cpp:119-125)
-    auto [W, Mplain] = assemble_time_matrices(p, n_el, T);
-    out.Wt = std::move(W.m);
-    const SplineSpace1D tspace = SplineSpace1D::temporal(p, n_el);
-    const QuadratureRule tquad = gauss_rule(tspace.knot_vector(), q);
-    if (prob.nu_t || prob.gamma_t) {
-        const auto tw = [&](double tau) {
-            const double nt = prob.nu_t ? prob.nu_t(T * tau) : 1.0;
-            const double gt = prob.gamma_t ? prob.gamma_t(T * tau) : 1.0;
-            return nt / gt;
-        };
-        BandedMatrix Mh = assemble_univariate_fn(tspace, tquad, 0, 0, tw);
-        for (double& v : Mh.m.a) v *= T;
-        out.Mt = std::move(Mh.m);
-    } else {
-        out.Mt = std::move(Mplain.m);
-    }
+    (void)T;
+    time_matrices(prob, p, n_el, out.Wt, out.Mt);
     // separated coefficients and the weighted 1D factors (solver.cpp:114-119, 130-136)
     std::vector<int> nel(d, n_el);
     out.sep = separate_variables(coefficient_diagonal_samples(kvs, prob.geometry, prob.nu_s, prob.gamma_s), nel);

@@ -92,4 +92,10 @@ struct GeometryPreconditionerPieces {
 };
 GeometryPreconditionerPieces geometry_preconditioner_pieces(const ProblemSpec& prob, int p, int n_el, bool want_D);
 
+/// W_t and the nu_t/gamma_t-weighted M_t of SpaceTimeSystem (solver.cpp:119-125).
+void time_matrices(const ProblemSpec& prob, int p, int n_el, DenseMatrix& Wt, DenseMatrix& Mt);
+
+/// Device field kinds of a catalog problem (nu_s, gamma_s) for the in-kernel physical assembly.
+void problem_field_kinds(const ProblemSpec& prob, int& nu_kind, int& gamma_kind);
+
 }  // namespace stiga

@@ -306,6 +306,15 @@ class KronSumOperator:
               "kronsum_create_spacetime")
         return KronSumOperator(None, None, device, _handle=h.value)
 
+    @staticmethod
+    def physical(problem, p, n_el, device=0):
+        """SpaceTimeSystem's A_ = M_s (x) W_t + K_s (x) M_t (solver.cpp:58-70) with the physical
+        spatial matrices of `problem` (problems.Problem) assembled on the device."""
+        h = ctypes.c_void_p()
+        check(lib().stiga_kronsum_create_physical(problem._h, int(p), int(n_el), int(device), ctypes.byref(h)),
+              "kronsum_create_physical")
+        return KronSumOperator(None, None, device, _handle=h.value)
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:

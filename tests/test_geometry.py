@@ -89,3 +89,41 @@ def test_geometry_preconditioner_apply_gpu(pid, p, nel):
     s = P.apply(torch.from_numpy(r).cuda()).cpu().numpy()
     so = Po.apply(r)
     assert np.linalg.norm(s - so) / np.linalg.norm(so) <= 1e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pid,p,nel", [("identity-cube-3d", 2, 3), ("deformed-cube-3d", 2, 3), ("deformed-cube-3d", 3, 2),
+                                        ("quarter-annulus-2d", 2, 6), ("separable-nu-2d", 3, 5)])
+def test_physical_system_matvec_and_gmres(pid, p, nel):
+    """Device-assembled physical A (stencil SpMM) vs the oracle's assemble_spatial_physical
+    (assembly.cpp:151-268) and GMRES iteration parity (+-1) with the A^G preconditioner."""
+    torch = pytest.importorskip("torch")
+    from oracle import gmres as ogm
+    from oracle.fdsolve import ExtendedFDPreconditioner as OracleFD
+    from paper_1909_07309_b200 import stiga
+    from paper_1909_07309_b200.inputs import uniform_pm1
+
+    prob = Problem(pid)
+    ref = og.geometry_preconditioner_pieces(og.make_problem(pid), p, nel)
+    A = stiga.KronSumOperator.physical(prob, p, nel)
+    Ad = sp_kron(ref)
+    x = uniform_pm1(A.n_dof, 3)
+    y = A.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    yo = Ad @ x
+    assert np.linalg.norm(y - yo) <= 1e-12 * np.linalg.norm(yo)
+    assert np.abs(A.diagonal() - Ad.diagonal()).max() <= 1e-12 * np.abs(Ad.diagonal()).max()
+    pc = prob.geometry_pieces(p, nel)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=pc.D, device=0)
+    Po = OracleFD.setup(ref["Kt"], ref["Mt_s"], ref["Wt"], ref["Mt"], 1.0, 1.0, scaling=ref["D"])
+    b = uniform_pm1(A.n_dof, 4)
+    xg, rep = stiga.gmres(A, P, torch.from_numpy(b).cuda(), stiga.GmresOptions(1e-8, 300, 50))
+    xo, repo = ogm.gmres(lambda v: Ad @ v, Po.apply, b, 1e-8, 300, 50)
+    assert rep.converged and repo.converged
+    assert abs(rep.iterations - repo.iterations) <= 1
+    assert np.linalg.norm(xg.cpu().numpy() - xo) <= 1e-6 * np.linalg.norm(xo)
+
+
+def sp_kron(ref):
+    import scipy.sparse as sp
+
+    return (sp.kron(sp.csr_matrix(ref["Wt"]), ref["Ms"]) + sp.kron(sp.csr_matrix(ref["Mt"]), ref["Ks"])).tocsr()
