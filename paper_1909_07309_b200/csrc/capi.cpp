@@ -236,9 +236,10 @@ struct stiga_fd_s {
     void autotune() {
         const char* force = std::getenv("STIGA_TIME_VARIANT");
         const bool no_tune = std::getenv("STIGA_NO_AUTOTUNE") != nullptr;
+        const bool debug_tune = std::getenv("STIGA_DEBUG_TUNE") != nullptr;
         if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
         ck(cudaMemset(scratch.p, 0, sizeof(double) * n_dof), "memset");
-        const size_t kMaxCand = 6;
+        const size_t kMaxCand = 8;
         for (int l = 0; l < d; ++l) {
             tl[l] = cand_space[l].front();
             if (no_tune) continue;
@@ -249,6 +250,9 @@ struct stiga_fd_s {
                     ck(gpu::launch_mode_product(t, geom(l), scratch.p, scratch2.p, Jt[l]->p, nullptr, nullptr), "tune");
                 });
                 if (ms < best) { best = ms; tl[l] = t; }
+                if (debug_tune)
+                    std::fprintf(stderr, "[stiga tune] mode %d MI=%d WN=%d RB=%d occ=%d: %.4f ms\n", l, t.MI, t.WN,
+                                 t.RB, t.ctas_per_sm, ms);
             }
         }
         const bool fused_ok = !cand_time.empty();
@@ -263,6 +267,9 @@ struct stiga_fd_s {
                         ck(gpu::launch_time_fused(t, geom(d), scratch.p, scratch2.p, Jt_t.p, J_t.p, ap, nullptr), "tune");
                     });
                     if (ms < best_fused) { best_fused = ms; tl_t = t; }
+                    if (debug_tune)
+                        std::fprintf(stderr, "[stiga tune] time fused MI=%d WM=%d WN=%d ns=%d occ=%d: %.4f ms\n", t.MI,
+                                     t.WM, t.WN, t.nstage, t.ctas_per_sm, ms);
                 }
             }
             if (!(force && std::string(force) == "fused")) {
@@ -273,11 +280,15 @@ struct stiga_fd_s {
                         ck(gpu::launch_mode_product(t, geom(d), scratch.p, scratch2.p, Jt_t.p, nullptr, nullptr), "tune");
                     });
                     if (ms < best_gemm) { best_gemm = ms; tl_ts = t; }
+                    if (debug_tune)
+                        std::fprintf(stderr, "[stiga tune] time gemm MI=%d WN=%d RB=%d occ=%d: %.4f ms\n", t.MI, t.WN,
+                                     t.RB, t.ctas_per_sm, ms);
                 }
                 const float arrow = time_once([&] {
                     ck(gpu::launch_arrowhead(scratch2.p, scratch.p, n_s, ap, nullptr), "tune");
                 });
                 best_split = 2.f * best_gemm + arrow;
+                if (debug_tune) std::fprintf(stderr, "[stiga tune] arrowhead: %.4f ms\n", arrow);
             }
         }
         if (force && std::string(force) == "split") time_split = true;
@@ -388,11 +399,13 @@ struct stiga_kronsum_s {
     void apply(const double* x, double* y, cudaStream_t st) {
         const gpu::Band none{};
         if (physical) {  // y = M_s X W_t^T + K_s X M_t^T  (solver.cpp:67-70)
+            // spatial stencils first, as the reference's mode order (kronop.cpp:75-89): MX = M_s X,
+            // KX = K_s X on the tensor cores, then y = MX W_t^T + KX M_t^T in one banded time pass
             ensure_scratch(2);
             const int d = D - 1;
-            ck(gpu::launch_banded_pass(geom(d), x, nullptr, t0.p, t1.p, band(0), none, band(1), none, 0.0, st),
+            ck(gpu::launch_stencil_apply2(pdesc, Mst.p, Kst.p, x, t0.p, t1.p, dims[d], st), "stencil apply");
+            ck(gpu::launch_banded_pass(geom(d), t0.p, t1.p, y, nullptr, band(0), band(1), none, none, 0.0, st),
                "time bands");
-            ck(gpu::launch_stencil_spmm2(pdesc, Mst.p, t0.p, Kst.p, t1.p, y, dims[d], st), "stencil spmm");
             return;
         }
         if (spacetime) {

@@ -67,6 +67,7 @@ __device__ __forceinline__ void cp_wait_n() {
 struct KArgs {
     ModeGeom geo;
     int Kp, RB, Zrows, nstage;
+    int S;  // 8-row strips holding output rows (ceil(rows/8)); strips past S are skipped
 };
 
 // Compile-time shape of a CTA.
@@ -192,14 +193,17 @@ __device__ __forceinline__ void issue_chunk(const KArgs& a, const Prod& p, unsig
 }
 
 // acc += J_chunk * B_chunk over KS k-steps of 4.  A fragments from the J stage (ja), B fragments
-// from bb (row stride LDX).  Fragments double-buffered in registers; no predicates (padded J
-// rows are zero, so padded strips just produce zeros that are never stored).
+// from bb (row stride LDX).  Fragments double-buffered in registers.  Only the warp's first mact
+// strips are computed (warp-uniform predicate): strips wholly past the output rows are skipped, so
+// a row block that overhangs the matrix costs only its live strips; padded rows inside a live
+// strip are zero J rows and produce zeros that are never stored.
 template <class SH, int KS>
-__device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, double (&acc)[SH::MI][SH::NI][2]) {
+__device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, int mact,
+                                          double (&acc)[SH::MI][SH::NI][2]) {
     constexpr int MI = SH::MI, NI = SH::NI;
     double av[2][MI], bv[2][NI];
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi) av[0][mi] = ja[mi * 8 * kLDJ];
+    for (int mi = 0; mi < MI; ++mi) av[0][mi] = mi < mact ? ja[mi * 8 * kLDJ] : 0.0;
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni) bv[0][ni] = bb[ni * 8];
 #pragma unroll
@@ -207,14 +211,15 @@ __device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, do
         const int cur = kk & 1, nxt = cur ^ 1;
         if (kk + 1 < KS) {
 #pragma unroll
-            for (int mi = 0; mi < MI; ++mi) av[nxt][mi] = ja[mi * 8 * kLDJ + (kk + 1) * 4];
+            for (int mi = 0; mi < MI; ++mi) av[nxt][mi] = mi < mact ? ja[mi * 8 * kLDJ + (kk + 1) * 4] : 0.0;
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni) bv[nxt][ni] = bb[(kk + 1) * 4 * SH::LDX + ni * 8];
         }
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[cur][mi], bv[cur][ni]);
+            for (int ni = 0; ni < NI; ++ni)
+                if (mi < mact) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[cur][mi], bv[cur][ni]);
     }
 }
 
@@ -293,7 +298,7 @@ __device__ __forceinline__ void cp_wait_stage(int nstage) {
 // stages with J; otherwise it is resident in smem at Bres (row stride LDX) and only J streams.
 template <class SH, bool X_STREAM>
 __device__ __forceinline__ void gemm(const KArgs& a, double* stages, const Prod& p, const double* X, const double* Bres,
-                                     bool prologue_issued, double (&acc)[SH::MI][SH::NI][2]) {
+                                     bool prologue_issued, int strip0, double (&acc)[SH::MI][SH::NI][2]) {
     const int nchunks = (a.Kp + kBK - 1) / kBK;
     const int ns = a.nstage;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -301,6 +306,7 @@ __device__ __forceinline__ void gemm(const KArgs& a, double* stages, const Prod&
     const int g = lane >> 2, t = lane & 3;
     const int ja_off = kBK * SH::LDX + (wm * SH::MI * 8 + g) * kLDJ + t;  // within a stage
     const int bb_off = t * SH::LDX + wn * SH::NI * 8 + g;
+    const int mact = min(SH::MI, max(0, a.S - (strip0 + wm * SH::MI)));
     const unsigned st0 = smem_u32(stages);
     if (!prologue_issued) {
         for (int s = 0; s < ns - 1; ++s) {
@@ -324,13 +330,13 @@ __device__ __forceinline__ void gemm(const KArgs& a, double* stages, const Prod&
         const double* bb = X_STREAM ? st + bb_off : Bres + q * kBK * SH::LDX + bb_off;
         const int ksteps = min(kBK, a.Kp - q * kBK) >> 2;
         if (ksteps == 4) {
-            mma_chunk<SH, 4>(ja, bb, acc);
+            mma_chunk<SH, 4>(ja, bb, mact, acc);
         } else if (ksteps == 3) {
-            mma_chunk<SH, 3>(ja, bb, acc);
+            mma_chunk<SH, 3>(ja, bb, mact, acc);
         } else if (ksteps == 2) {
-            mma_chunk<SH, 2>(ja, bb, acc);
+            mma_chunk<SH, 2>(ja, bb, mact, acc);
         } else {
-            mma_chunk<SH, 1>(ja, bb, acc);
+            mma_chunk<SH, 1>(ja, bb, mact, acc);
         }
         if (++stage == ns) stage = 0;
     }
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(32 * WN)
     const Prod p = make_prod<SH>(a, c0, X, Jg);
     double acc[SH::MI][SH::NI][2];
     zero_acc<SH>(acc);
-    gemm<SH, true>(a, smem, p, X, nullptr, false, acc);
+    gemm<SH, true>(a, smem, p, X, nullptr, false, rb * MI, acc);
     store_acc<SH>(a, acc, c0, rb * MI, Y, post);
 }
 
@@ -449,7 +455,7 @@ __global__ void __launch_bounds__(32 * WM * WN)
     Prod p = make_prod<SH>(a, c0, X, Jt);
     double acc[SH::MI][SH::NI][2];
     zero_acc<SH>(acc);
-    gemm<SH, true>(a, stages, p, X, nullptr, false, acc);  // Z = U_t^T x
+    gemm<SH, true>(a, stages, p, X, nullptr, false, 0, acc);  // Z = U_t^T x
     // Z -> smem (rows < Kp; padded rows are exact zeros because the padded J rows are zero)
     {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -482,7 +488,7 @@ __global__ void __launch_bounds__(32 * WM * WN)
     if (!(ap.debug & 1)) arrowhead_tile<SH>(a, Zs, c0, ap);
     __syncthreads();
     zero_acc<SH>(acc);
-    gemm<SH, false>(a, stages, p, X, Zs, true, acc);  // y = U_t z
+    gemm<SH, false>(a, stages, p, X, Zs, true, 0, acc);  // y = U_t z
     store_acc<SH>(a, acc, c0, 0, Y, nullptr);
 }
 
@@ -578,6 +584,7 @@ KArgs make_args(const Tiling& t, const ModeGeom& g) {
     a.RB = t.RB;
     a.Zrows = t.Zrows;
     a.nstage = t.nstage;
+    a.S = (g.m + 7) / 8;
     return a;
 }
 
@@ -678,7 +685,7 @@ std::vector<Tiling> mode_tiling_candidates(int m, int n) {
     const int S = (m + 7) / 8;
     const int Kp = (n + 3) / 4 * 4;
     const int rb0 = (S + 12) / 13;
-    for (int RB = rb0; RB <= rb0 + 2; ++RB) {
+    for (int RB = rb0; RB <= std::min(S, rb0 + 3); ++RB) {
         const int MI = (S + RB - 1) / RB;
         if (MI > 13 || MI < 1) continue;
         if (RB > rb0 && (S + rb0 - 1) / rb0 == MI) continue;  // same MI as a smaller RB
@@ -702,8 +709,10 @@ std::vector<Tiling> mode_tiling_candidates(int m, int n) {
             dispatch_mode(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, nullptr, &occ);
             t.ctas_per_sm = occ;
             if (occ < 1) continue;
-            const double eff = static_cast<double>(S) / (RB * MI);
-            c.emplace_back(std::min(occ * t.WN, 16) * eff + 0.02 * WN - 0.01 * RB, t);
+            // strips past S are skipped, so padding costs only imbalance; each extra row block
+            // re-stages the fiber tile
+            const double eff = 0.85 + 0.15 * static_cast<double>(S) / (RB * MI);
+            c.emplace_back(std::min(occ * t.WN, 16) * eff + 0.02 * WN - 0.05 * RB, t);
         }
     }
     std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
@@ -760,7 +769,7 @@ std::vector<Tiling> time_tiling_candidates(int nt) {
                 dispatch_time(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, ap, nullptr, &occ);
                 t.ctas_per_sm = occ;
                 if (occ < 1) continue;
-                const double eff = static_cast<double>(S) / (WM * MI);
+                const double eff = 0.85 + 0.15 * static_cast<double>(S) / (WM * MI);
                 c.emplace_back(std::min(occ * WM * WN, 16) * eff + 0.01 * ns + 0.02 * WN, t);
             }
         }

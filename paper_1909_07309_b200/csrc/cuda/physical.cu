@@ -2,7 +2,11 @@
 // and the stencil SpMM of the space-time system mat-vec.  See physical.cuh.
 #include "physical.cuh"
 
+#include <cuda.h>
+
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 
 namespace stiga {
 namespace gpu {
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(256) physical_assembly_kernel(PhysicalDesc g, 
             s *= g.n;
         }
     }
-    const long long S = ostride[D - 1] * W;
+    const long long Ns = nstride[D - 1] * g.n;
     for (int pair = threadIdx.x; pair < LD * LD; pair += blockDim.x) {
         const int ia = pair % LD, ib = pair / LD;
         int a[D], b[D], ga[D], gb[D];
@@ -250,74 +254,278 @@ __global__ void __launch_bounds__(256) physical_assembly_kernel(PhysicalDesc g, 
             row += ga[l] * nstride[l];
             off += (gb[l] - ga[l] + g.p) * ostride[l];
         }
-        atomicAdd(Kst + row * S + off, kab);
-        atomicAdd(Mst + row * S + off, mab);
+        atomicAdd(Kst + off * Ns + row, kab);  // offset-major: rows of one offset contiguous
+        atomicAdd(Mst + off * Ns + row, mab);
     }
 }
 
-// y[i, t] = sum_o Mst[i][o] P[j(i,o), t] + Kst[i][o] Q[j(i,o), t] for TB time columns per thread.
-template <int D, int TB>
-__global__ void __launch_bounds__(128) stencil_spmm2_kernel(PhysicalDesc g, const double* __restrict__ Mst,
-                                                            const double* __restrict__ P, const double* __restrict__ Kst,
-                                                            const double* __restrict__ Q, double* __restrict__ y,
-                                                            long long n_t) {
-    long long Ns = 1;
-    for (int l = 0; l < D; ++l) Ns *= g.n;
-    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    const long long t0 = static_cast<long long>(blockIdx.y) * TB;
-    if (i >= Ns) return;
-    const int W = 2 * g.p + 1;
-    int il[D], lo[D], hi[D];
-    long long nstride[D], ostride[D];
-    {
-        long long rem = i, s = 1, o = 1;
-        for (int l = 0; l < D; ++l) {
-            il[l] = static_cast<int>(rem % g.n);
-            rem /= g.n;
-            lo[l] = max(0, il[l] - g.p) - il[l] + g.p;
-            hi[l] = min(g.n - 1, il[l] + g.p) - il[l] + g.p;
-            nstride[l] = s;
-            ostride[l] = o;
-            s *= g.n;
-            o *= W;
+// MX = M_s X and KX = K_s X for X (N_s x n_t, colex) on the FP64 tensor cores (DMMA m8n8k4).
+//
+// The stencil rows of 8 consecutive i_1 (fixed i_2.., one neighbour-line offset (o_2, o_3)) touch the
+// window of 8 + 2p neighbours j_1 = i_1 - p .. i_1 + 7 + p, so for that offset the contribution is a
+// dense 8 x 4KS block (the band, zero outside |j_1 - i_1| <= p) times the window of the neighbour
+// line: y[8 rows, t] += A_band (8 x 4KS) * X[window, t].  One CTA owns a segment of up to 8*NW rows
+// of one line (consumer warp w = rows 8w..8w+7) and the t of its chunk, and walks the (2p+1)^(d-1)
+// neighbour lines: each step stages one neighbour-line segment (+-p halo) x t-chunk [t][row] (row
+// pitch == 4 mod 16 doubles: conflict-free B fragments) and the segment's band values [o_1][row].
+// M and K share the staged X, so each B fragment feeds two DMMAs.
+//
+// Two stagings: (a) n even (TMA-legal strides): one producer lane issues three TMA tensor loads
+// per step (X box, M and K band boxes; out-of-range rows / t zero-filled by the TMA unit) into a
+// kStages ring guarded by full / empty mbarriers, consumers never meet a CTA barrier;
+// (b) otherwise every thread stages with 8-byte cp.async (double buffered, one CTA barrier a step).
+constexpr int kTT = 9;          // 8-column time tiles per chunk (72 columns)
+constexpr int kMaxWarps = 12;   // consumer warps (row blocks) per CTA (96 rows)
+constexpr int kStages = 3;
+
+__device__ __forceinline__ void sdmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void scp8(unsigned dst, const double* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mb_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mb_expect(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma3(unsigned dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma2(unsigned dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
+        : "memory");
+}
+
+struct StencilGeo {
+    int n, p, W, d;
+    long long Ns;
+    int n_t;
+    int nseg, seg_rows;  // segments per line, rows per segment (multiple of 8)
+    int SR, LDR;         // staged rows per neighbour line and their smem pitch (== 4 mod 16)
+    int BR;              // band smem pitch (rows) == seg_rows
+    int nsteps;          // W^(d-1) neighbour-line offsets
+    int xstage, bstage;  // doubles per X / band stage (multiples of 16: 128-byte aligned stages)
+    int shift;           // staged window starts at row seg0 - p - shift (TMA: even start coordinate)
+};
+
+struct LineCtx {
+    int lc[2];
+    long long line;
+    int seg0, t0, tcols;
+};
+
+__device__ __forceinline__ LineCtx line_ctx(const StencilGeo& sg) {
+    LineCtx c;
+    c.line = blockIdx.x / sg.nseg;  // i_2 + n i_3 (0 for d = 1)
+    c.seg0 = static_cast<int>(blockIdx.x % sg.nseg) * sg.seg_rows;
+    c.t0 = blockIdx.y * (8 * kTT);
+    c.tcols = min(8 * kTT, sg.n_t - c.t0);
+    c.lc[0] = c.lc[1] = 0;
+    long long r = c.line;
+    for (int l = 0; l < sg.d - 1; ++l) {
+        c.lc[l] = static_cast<int>(r % sg.n);
+        r /= sg.n;
+    }
+    return c;
+}
+
+// neighbour line of step s (offsets o_2 + W o_3), -1 when it falls outside the patch
+__device__ __forceinline__ long long nb_line(const StencilGeo& sg, const LineCtx& c, int s) {
+    long long nl = 0, stride = 1;
+    int rem = s;
+    for (int l = 0; l < sg.d - 1; ++l) {
+        const int o = rem % sg.W;
+        rem /= sg.W;
+        const int j = c.lc[l] + o - sg.p;
+        if (j < 0 || j >= sg.n) return -1;
+        nl += j * stride;
+        stride *= sg.n;
+    }
+    return nl;
+}
+__device__ __forceinline__ int next_step(const StencilGeo& sg, const LineCtx& c, int s) {
+    while (s < sg.nsteps && nb_line(sg, c, s) < 0) ++s;
+    return s;
+}
+
+// One step of a consumer warp: accumulate the band of offset step into (accm, acck).
+template <int KS>
+__device__ __forceinline__ void stencil_step(const StencilGeo& sg, const double* xs, const double* bm, int ntiles,
+                                             double (&accm)[kTT][2], double (&acck)[kTT][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const double* bs = xs + g * sg.LDR + sg.shift + 8 * warp + t4;
+    const double* bmr = bm + 8 * warp + g;
+    const double* bkr = bmr + sg.bstage;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+        const int o1 = 4 * kk + t4 - g;
+        const bool av = o1 >= 0 && o1 < sg.W;
+        const int oc = av ? o1 * sg.BR : 0;  // clamped: the loads are issued unconditionally
+        const double am = av ? bmr[oc] : 0.0;
+        const double ak = av ? bkr[oc] : 0.0;
+#pragma unroll
+        for (int tt = 0; tt < kTT; ++tt) {
+            if (tt < ntiles) {
+                const double b = bs[tt * 8 * sg.LDR + 4 * kk];
+                sdmma(accm[tt][0], accm[tt][1], am, b);
+                sdmma(acck[tt][0], acck[tt][1], ak, b);
+            }
         }
     }
-    const long long S = ostride[D - 1] * W;
-    const int tb = static_cast<int>(min(static_cast<long long>(TB), n_t - t0));
-    double acc[TB];
+}
+
+__device__ __forceinline__ void stencil_store(const StencilGeo& sg, const LineCtx& c, const double (&accm)[kTT][2],
+                                              const double (&acck)[kTT][2], double* MX, double* KX) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int i1 = c.seg0 + 8 * warp + g;
+    if (i1 >= sg.n) return;
+    const long long irow = i1 + sg.n * c.line;
+    // C fragment: row g, columns 2 t4 + {0, 1} of tile tt
 #pragma unroll
-    for (int k = 0; k < TB; ++k) acc[k] = 0.0;
-    const double* mrow = Mst + i * S;
-    const double* krow = Kst + i * S;
-    int o[D];
-    for (int l = 0; l < D; ++l) o[l] = lo[l];
-    while (true) {
-        long long off = 0, j = 0;
-        for (int l = 0; l < D; ++l) {
-            off += o[l] * ostride[l];
-            j += (il[l] + o[l] - g.p) * nstride[l];
-        }
-        const double mv = __ldg(mrow + off), kv = __ldg(krow + off);
-        const double* pc = P + j + Ns * t0;
-        const double* qc = Q + j + Ns * t0;
-        if (tb == TB) {
+    for (int tt = 0; tt < kTT; ++tt) {
 #pragma unroll
-            for (int k = 0; k < TB; ++k) acc[k] += mv * __ldg(pc + Ns * k) + kv * __ldg(qc + Ns * k);
-        } else {
-#pragma unroll
-            for (int k = 0; k < TB; ++k)
-                if (k < tb) acc[k] += mv * __ldg(pc + Ns * k) + kv * __ldg(qc + Ns * k);
+        for (int v = 0; v < 2; ++v) {
+            const int tc = 8 * tt + 2 * t4 + v;
+            if (tc < c.tcols) {
+                const long long o = irow + sg.Ns * (c.t0 + tc);
+                MX[o] = accm[tt][v];
+                KX[o] = acck[tt][v];
+            }
         }
-        int l = 0;
-        while (l < D && ++o[l] > hi[l]) {
-            o[l] = lo[l];
-            ++l;
-        }
-        if (l == D) break;
     }
+}
+
+// (a) TMA staging, warp-specialized: warps 0..nwc-1 consume, warp nwc produces.
+template <int KS>
+__global__ void __launch_bounds__(32 * (kMaxWarps + 1))
+    stencil_tma_kernel(StencilGeo sg, const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapM,
+                       const __grid_constant__ CUtensorMap mapK, double* __restrict__ MX, double* __restrict__ KX) {
+    extern __shared__ __align__(128) double sx[];
+    double* xs = sx;                         // kStages x xstage
+    double* bsm = xs + kStages * sg.xstage;  // kStages x (M, K) x bstage
+    uint64_t* full = reinterpret_cast<uint64_t*>(bsm + kStages * 2 * sg.bstage);
+    uint64_t* empty = full + kStages;
+    const int nwc = blockDim.x / 32 - 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const LineCtx c = line_ctx(sg);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mb_init(full + s, 1);
+            mb_init(empty + s, nwc);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == nwc) {
+        if (lane != 0) return;
+        const unsigned bytes = 8u * (8 * kTT * sg.LDR + 2 * sg.W * sg.BR);
+        const int row0 = static_cast<int>(c.seg0 + sg.n * c.line);
+        int k = 0;
+        for (int s = next_step(sg, c, 0); s < sg.nsteps; s = next_step(sg, c, s + 1), ++k) {
+            const int st = k % kStages;
+            if (k >= kStages) mb_wait(empty + st, ((k / kStages) - 1) & 1);
+            mb_expect(full + st, bytes);
+            tma3(su32(xs + st * sg.xstage), &mapX, c.seg0 - sg.p - sg.shift, static_cast<int>(nb_line(sg, c, s)), c.t0,
+                 full + st);
+            tma2(su32(bsm + (st * 2) * sg.bstage), &mapM, row0, sg.W * s, full + st);
+            tma2(su32(bsm + (st * 2 + 1) * sg.bstage), &mapK, row0, sg.W * s, full + st);
+        }
+        return;
+    }
+    const int ntiles = (c.tcols + 7) >> 3;
+    double accm[kTT][2], acck[kTT][2];
 #pragma unroll
-    for (int k = 0; k < TB; ++k)
-        if (k < tb) y[i + Ns * (t0 + k)] = acc[k];
+    for (int t = 0; t < kTT; ++t) accm[t][0] = accm[t][1] = acck[t][0] = acck[t][1] = 0.0;
+    int k = 0;
+    for (int s = next_step(sg, c, 0); s < sg.nsteps; s = next_step(sg, c, s + 1), ++k) {
+        const int st = k % kStages;
+        mb_wait(full + st, (k / kStages) & 1);
+        stencil_step<KS>(sg, xs + st * sg.xstage, bsm + (st * 2) * sg.bstage, ntiles, accm, acck);
+        __syncwarp();
+        if (lane == 0) mb_arrive(empty + st);
+    }
+    stencil_store(sg, c, accm, acck, MX, KX);
+}
+
+// (b) cp.async staging by all threads (warp = column group, lane = rows), double buffered.
+template <int KS>
+__global__ void __launch_bounds__(32 * kMaxWarps)
+    stencil_sync_kernel(StencilGeo sg, const double* __restrict__ Mst, const double* __restrict__ Kst,
+                        const double* __restrict__ X, double* __restrict__ MX, double* __restrict__ KX) {
+    extern __shared__ __align__(128) double sx[];
+    double* xs = sx;                   // 2 x xstage
+    double* bsm = xs + 2 * sg.xstage;  // 2 x (M, K) x bstage
+    const int nw = blockDim.x / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const LineCtx c = line_ctx(sg);
+    const int rows_seg = min(sg.seg_rows, sg.n - c.seg0);
+    auto issue = [&](int s, int buf) {
+        const long long nl = nb_line(sg, c, s);
+        const double* src = X + (c.seg0 - sg.p) + sg.n * nl + sg.Ns * c.t0;
+        const unsigned dst = su32(xs + buf * sg.xstage);
+        for (int col = warp; col < c.tcols; col += nw) {
+            const double* sc = src + sg.Ns * col;
+            const unsigned dc = dst + 8u * col * sg.LDR;
+            for (int r = lane; r < sg.SR; r += 32) {
+                const int j1 = c.seg0 - sg.p + r;
+                const bool v = j1 >= 0 && j1 < sg.n;
+                scp8(dc + 8u * r, v ? sc + r : X, v);
+            }
+        }
+        const long long row0 = c.seg0 + sg.n * c.line;
+        for (int mo = warp; mo < 2 * sg.W; mo += nw) {
+            const int mat = mo / sg.W, o1 = mo - mat * sg.W;
+            const double* bsrc = (mat ? Kst : Mst) + (o1 + static_cast<long long>(sg.W) * s) * sg.Ns + row0;
+            const unsigned bd = su32(bsm + (buf * 2 + mat) * sg.bstage + o1 * sg.BR);
+            for (int r = lane; r < sg.seg_rows; r += 32) scp8(bd + 8u * r, r < rows_seg ? bsrc + r : X, r < rows_seg);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    const int ntiles = (c.tcols + 7) >> 3;
+    double accm[kTT][2], acck[kTT][2];
+#pragma unroll
+    for (int t = 0; t < kTT; ++t) accm[t][0] = accm[t][1] = acck[t][0] = acck[t][1] = 0.0;
+    int s = next_step(sg, c, 0);
+    if (s < sg.nsteps) issue(s, 0);
+    int buf = 0;
+    while (s < sg.nsteps) {
+        const int sn = next_step(sg, c, s + 1);
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();  // stage buf landed for all; the other buffer is free again
+        if (sn < sg.nsteps) issue(sn, buf ^ 1);
+        stencil_step<KS>(sg, xs + buf * sg.xstage, bsm + (buf * 2) * sg.bstage, ntiles, accm, acck);
+        s = sn;
+        buf ^= 1;
+    }
+    stencil_store(sg, c, accm, acck, MX, KX);
 }
 
 template <int D>
@@ -331,8 +539,8 @@ __global__ void stencil_diag_kernel(PhysicalDesc g, const double* Kst, const dou
     S = o;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < Ns;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        dK[i] = Kst[i * S + c];
-        dM[i] = Mst[i * S + c];
+        dK[i] = Kst[c * Ns + i];
+        dM[i] = Mst[c * Ns + i];
     }
 }
 
@@ -353,15 +561,52 @@ cudaError_t assembly_d(const PhysicalDesc& g, double* Kst, double* Mst, cudaStre
     return cudaGetLastError();
 }
 
-template <int D>
-cudaError_t spmm_d(const PhysicalDesc& g, const double* Mst, const double* P, const double* Kst, const double* Q,
-                   double* y, long long n_t, cudaStream_t st) {
-    constexpr int TB = 24;
-    long long Ns = 1;
-    for (int l = 0; l < D; ++l) Ns *= g.n;
-    dim3 grid(static_cast<unsigned>((Ns + 127) / 128), static_cast<unsigned>((n_t + TB - 1) / TB));
-    stencil_spmm2_kernel<D, TB><<<grid, 128, 0, st>>>(g, Mst, P, Kst, Q, y, n_t);
+template <int KS>
+cudaError_t stencil_launch(const StencilGeo& sg, bool tma, dim3 grid, int nwc, const double* Mst, const double* Kst,
+                           const double* X, const CUtensorMap* maps, double* MX, double* KX, cudaStream_t st) {
+    if (tma) {
+        const size_t smem = sizeof(double) * kStages * (sg.xstage + 2 * sg.bstage) + 2 * kStages * sizeof(uint64_t);
+        cudaError_t e = cudaFuncSetAttribute(stencil_tma_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        stencil_tma_kernel<KS><<<grid, 32 * (nwc + 1), smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX);
+    } else {
+        const size_t smem = sizeof(double) * 2 * (sg.xstage + 2 * sg.bstage);
+        cudaError_t e = cudaFuncSetAttribute(stencil_sync_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        stencil_sync_kernel<KS><<<grid, 32 * nwc, smem, st>>>(sg, Mst, Kst, X, MX, KX);
+    }
     return cudaGetLastError();
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+bool encode(CUtensorMap* m, const double* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+            const cuuint32_t* box) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -376,12 +621,62 @@ cudaError_t launch_physical_assembly(const PhysicalDesc& g, double* Kst, double*
     }
 }
 
-cudaError_t launch_stencil_spmm2(const PhysicalDesc& g, const double* Mst, const double* P, const double* Kst,
-                                 const double* Q, double* y, long long n_t, cudaStream_t st) {
-    switch (g.d) {
-        case 1: return spmm_d<1>(g, Mst, P, Kst, Q, y, n_t, st);
-        case 2: return spmm_d<2>(g, Mst, P, Kst, Q, y, n_t, st);
-        case 3: return spmm_d<3>(g, Mst, P, Kst, Q, y, n_t, st);
+cudaError_t launch_stencil_apply2(const PhysicalDesc& g, const double* Mst, const double* Kst, const double* X,
+                                  double* MX, double* KX, long long n_t, cudaStream_t st) {
+    if (g.d < 1 || g.d > 3 || g.n <= 0 || n_t <= 0) return cudaErrorInvalidValue;
+    StencilGeo sg;
+    sg.n = g.n;
+    sg.p = g.p;
+    sg.W = 2 * g.p + 1;
+    sg.d = g.d;
+    sg.Ns = 1;
+    long long lines = 1;
+    sg.nsteps = 1;
+    for (int l = 0; l < g.d; ++l) sg.Ns *= g.n;
+    for (int l = 1; l < g.d; ++l) {
+        lines *= g.n;
+        sg.nsteps *= sg.W;
+    }
+    sg.n_t = static_cast<int>(n_t);
+    const int KS = (8 + 2 * g.p + 3) / 4;
+    const int blocks8 = (g.n + 7) / 8;
+    sg.nseg = (blocks8 + kMaxWarps - 1) / kMaxWarps;
+    const int wpc = (blocks8 + sg.nseg - 1) / sg.nseg;  // warps (row blocks) per segment
+    sg.seg_rows = 8 * wpc;
+    sg.SR = 8 * wpc - 8 + 4 * KS;
+    // TMA boxes start on an even row: a box at an odd (negative) start coordinate faults, so odd p
+    // stages one extra leading row
+    const int shift = g.p & 1;
+    sg.LDR = (sg.SR + shift + 11) / 16 * 16 + 4;
+    if (sg.LDR - 16 >= sg.SR + shift) sg.LDR -= 16;
+    sg.BR = sg.seg_rows;
+    sg.xstage = (8 * kTT * sg.LDR + 15) / 16 * 16;
+    sg.bstage = (sg.W * sg.BR + 15) / 16 * 16;
+    dim3 grid(static_cast<unsigned>(lines * sg.nseg), static_cast<unsigned>((n_t + 8 * kTT - 1) / (8 * kTT)));
+    // TMA staging needs 16-byte strides / base addresses (n even) and boxes <= 256 per dimension
+    CUtensorMap maps[3];
+    bool tma = g.n % 2 == 0 && sg.LDR <= 256 && sg.W <= 256 && sg.BR <= 256 && !std::getenv("STIGA_STENCIL_NO_TMA") &&
+               ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Mst) | reinterpret_cast<uintptr_t>(Kst)) &
+                15u) == 0;
+    if (tma) {
+        const cuuint64_t dx[3] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(sg.Ns / g.n),
+                                  static_cast<cuuint64_t>(n_t)};
+        const cuuint64_t sx[2] = {static_cast<cuuint64_t>(g.n) * 8, static_cast<cuuint64_t>(sg.Ns) * 8};
+        const cuuint32_t bx[3] = {static_cast<cuuint32_t>(sg.LDR), 1, 8 * kTT};
+        long long planes = 1;
+        for (int l = 0; l < g.d; ++l) planes *= sg.W;
+        const cuuint64_t db[2] = {static_cast<cuuint64_t>(sg.Ns), static_cast<cuuint64_t>(planes)};
+        const cuuint64_t sb[1] = {static_cast<cuuint64_t>(sg.Ns) * 8};
+        const cuuint32_t bb[2] = {static_cast<cuuint32_t>(sg.BR), static_cast<cuuint32_t>(sg.W)};
+        tma = encode(&maps[0], X, 3, dx, sx, bx) && encode(&maps[1], Mst, 2, db, sb, bb) &&
+              encode(&maps[2], Kst, 2, db, sb, bb);
+    }
+    sg.shift = tma ? shift : 0;
+    switch (KS) {
+        case 3: return stencil_launch<3>(sg, tma, grid, wpc, Mst, Kst, X, maps, MX, KX, st);
+        case 4: return stencil_launch<4>(sg, tma, grid, wpc, Mst, Kst, X, maps, MX, KX, st);
+        case 5: return stencil_launch<5>(sg, tma, grid, wpc, Mst, Kst, X, maps, MX, KX, st);
+        case 6: return stencil_launch<6>(sg, tma, grid, wpc, Mst, Kst, X, maps, MX, KX, st);
         default: return cudaErrorInvalidValue;
     }
 }

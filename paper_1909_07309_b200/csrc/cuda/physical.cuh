@@ -39,13 +39,13 @@ struct PhysicalDesc {
     const int* bfirst = nullptr;
 };
 
-/// Stencil-format assembly: Kst / Mst have N_s rows of (2p+1)^d doubles (zeroed by the caller);
-/// entry [i][o] couples row i with the neighbour at offset o = sum_l (j_l - i_l + p)(2p+1)^l.
+/// Stencil-format assembly: Kst / Mst hold (2p+1)^d offset planes of N_s doubles (zeroed by the
+/// caller); entry [o][i] couples row i with the neighbour at offset o = sum_l (j_l - i_l + p)(2p+1)^l.
 cudaError_t launch_physical_assembly(const PhysicalDesc& desc, double* Kst, double* Mst, cudaStream_t st);
 
-/// y (N_s x n_t) = Mst-stencil * P + Kst-stencil * Q, P and Q (N_s x n_t) colex (space fastest).
-cudaError_t launch_stencil_spmm2(const PhysicalDesc& desc, const double* Mst, const double* P, const double* Kst,
-                                 const double* Q, double* y, long long n_t, cudaStream_t st);
+/// MX = M_s X and KX = K_s X, X / MX / KX (N_s x n_t) colex (space fastest), on the FP64 tensor cores.
+cudaError_t launch_stencil_apply2(const PhysicalDesc& desc, const double* Mst, const double* Kst, const double* X,
+                                  double* MX, double* KX, long long n_t, cudaStream_t st);
 
 /// Diagonal entries of the two stencils (the centre offset), N_s each.
 cudaError_t launch_stencil_diag(const PhysicalDesc& desc, const double* Kst, const double* Mst, double* dK, double* dM,

@@ -127,3 +127,26 @@ def sp_kron(ref):
     import scipy.sparse as sp
 
     return (sp.kron(sp.csr_matrix(ref["Wt"]), ref["Ms"]) + sp.kron(sp.csr_matrix(ref["Mt"]), ref["Ks"])).tocsr()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pid,p,nel", [("identity-interval-1d", 5, 200), ("identity-interval-1d", 1, 150),
+                                        ("identity-interval-1d", 2, 90), ("quarter-annulus-2d", 4, 9),
+                                        ("separable-nu-2d", 5, 4)])
+def test_physical_matvec_tiling_edges(pid, p, nel):
+    """Tensor-core stencil mat-vec at sizes that exercise its tiling: several 96-row segments per
+    line and several 72-column time chunks (1D, n up to 203), every band width KS = 3..5 (p = 1..5),
+    and partial row blocks / time tiles; against the oracle's assembled A (solver.cpp:67-70)."""
+    torch = pytest.importorskip("torch")
+    from paper_1909_07309_b200 import stiga
+    from paper_1909_07309_b200.inputs import uniform_pm1
+
+    prob = Problem(pid)
+    ref = og.geometry_preconditioner_pieces(og.make_problem(pid), p, nel)
+    A = stiga.KronSumOperator.physical(prob, p, nel)
+    Ad = sp_kron(ref)
+    for seed in (5, 6):
+        x = uniform_pm1(A.n_dof, seed)
+        y = A.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        yo = Ad @ x
+        assert np.linalg.norm(y - yo) <= 1e-12 * np.linalg.norm(yo)
