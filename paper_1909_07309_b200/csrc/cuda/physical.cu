@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256) physical_assembly_kernel(PhysicalDesc g, 
 // kStages ring guarded by full / empty mbarriers, consumers never meet a CTA barrier;
 // (b) otherwise every thread stages with 8-byte cp.async (double buffered, one CTA barrier a step).
 constexpr int kTT = 9;          // 8-column time tiles per chunk (72 columns)
-constexpr int kMaxWarps = 12;   // consumer warps (row blocks) per CTA (96 rows)
+constexpr int kMaxWarps = 12;   // row blocks per CTA (96 rows); two consumer warps (M, K) each
 constexpr int kStages = 3;
 
 __device__ __forceinline__ void sdmma(double& c0, double& c1, double a, double b) {
@@ -332,6 +332,8 @@ struct StencilGeo {
     int nsteps;          // W^(d-1) neighbour-line offsets
     int xstage, bstage;  // doubles per X / band stage (multiples of 16: 128-byte aligned stages)
     int shift;           // staged window starts at row seg0 - p - shift (TMA: even start coordinate)
+    int nst;             // TMA ring depth
+    int boxt;            // time columns per TMA box (min(72, n_t))
 };
 
 struct LineCtx {
@@ -375,37 +377,38 @@ __device__ __forceinline__ int next_step(const StencilGeo& sg, const LineCtx& c,
 }
 
 // One step of a consumer warp: accumulate the band of offset step into (accm, acck).
-template <int KS>
-__device__ __forceinline__ void stencil_step(const StencilGeo& sg, const double* xs, const double* bm, int ntiles,
-                                             double (&accm)[kTT][2], double (&acck)[kTT][2]) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// One step of consumer warp (row block rb, matrix mat): acc += band(mat) x staged window.
+template <int KS, bool FULL>
+__device__ __forceinline__ void stencil_step_t(const StencilGeo& sg, const double* xs, const double* bm, int rb,
+                                               int ntiles, double (&acc)[kTT][2]) {
+    const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
-    const double* bs = xs + g * sg.LDR + sg.shift + 8 * warp + t4;
-    const double* bmr = bm + 8 * warp + g;
-    const double* bkr = bmr + sg.bstage;
+    const double* bs = xs + g * sg.LDR + sg.shift + 8 * rb + t4;
+    const double* br = bm + 8 * rb + g;
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
         const int o1 = 4 * kk + t4 - g;
         const bool av = o1 >= 0 && o1 < sg.W;
-        const int oc = av ? o1 * sg.BR : 0;  // clamped: the loads are issued unconditionally
-        const double am = av ? bmr[oc] : 0.0;
-        const double ak = av ? bkr[oc] : 0.0;
+        const double a = av ? br[av ? o1 * sg.BR : 0] : 0.0;  // clamped index: the load is unconditional
 #pragma unroll
         for (int tt = 0; tt < kTT; ++tt) {
-            if (tt < ntiles) {
-                const double b = bs[tt * 8 * sg.LDR + 4 * kk];
-                sdmma(accm[tt][0], accm[tt][1], am, b);
-                sdmma(acck[tt][0], acck[tt][1], ak, b);
-            }
+            if (FULL || tt < ntiles) sdmma(acc[tt][0], acc[tt][1], a, bs[tt * 8 * sg.LDR + 4 * kk]);
         }
     }
 }
 
-__device__ __forceinline__ void stencil_store(const StencilGeo& sg, const LineCtx& c, const double (&accm)[kTT][2],
-                                              const double (&acck)[kTT][2], double* MX, double* KX) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <int KS>
+__device__ __forceinline__ void stencil_step(const StencilGeo& sg, const double* xs, const double* bm, int rb,
+                                             int ntiles, double (&acc)[kTT][2]) {
+    if (ntiles == kTT) stencil_step_t<KS, true>(sg, xs, bm, rb, ntiles, acc);
+    else stencil_step_t<KS, false>(sg, xs, bm, rb, ntiles, acc);
+}
+
+__device__ __forceinline__ void stencil_store(const StencilGeo& sg, const LineCtx& c, int rb,
+                                              const double (&acc)[kTT][2], double* Y) {
+    const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
-    const int i1 = c.seg0 + 8 * warp + g;
+    const int i1 = c.seg0 + 8 * rb + g;
     if (i1 >= sg.n) return;
     const long long irow = i1 + sg.n * c.line;
     // C fragment: row g, columns 2 t4 + {0, 1} of tile tt
@@ -414,30 +417,28 @@ __device__ __forceinline__ void stencil_store(const StencilGeo& sg, const LineCt
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
             const int tc = 8 * tt + 2 * t4 + v;
-            if (tc < c.tcols) {
-                const long long o = irow + sg.Ns * (c.t0 + tc);
-                MX[o] = accm[tt][v];
-                KX[o] = acck[tt][v];
-            }
+            if (tc < c.tcols) Y[irow + sg.Ns * (c.t0 + tc)] = acc[tt][v];
         }
     }
 }
 
-// (a) TMA staging, warp-specialized: warps 0..nwc-1 consume, warp nwc produces.
+// (a) TMA staging, warp-specialized: warps 0..nwc-1 consume (row block w % nrb, matrix w / nrb),
+// warp nwc produces.
 template <int KS>
-__global__ void __launch_bounds__(32 * (kMaxWarps + 1))
+__global__ void __launch_bounds__(32 * (2 * kMaxWarps + 1))
     stencil_tma_kernel(StencilGeo sg, const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapM,
                        const __grid_constant__ CUtensorMap mapK, double* __restrict__ MX, double* __restrict__ KX) {
     extern __shared__ __align__(128) double sx[];
-    double* xs = sx;                         // kStages x xstage
-    double* bsm = xs + kStages * sg.xstage;  // kStages x (M, K) x bstage
-    uint64_t* full = reinterpret_cast<uint64_t*>(bsm + kStages * 2 * sg.bstage);
-    uint64_t* empty = full + kStages;
+    const int nst = sg.nst;
+    double* xs = sx;                     // nst x xstage
+    double* bsm = xs + nst * sg.xstage;  // nst x (M, K) x bstage
+    uint64_t* full = reinterpret_cast<uint64_t*>(bsm + nst * 2 * sg.bstage);
+    uint64_t* empty = full + nst;
     const int nwc = blockDim.x / 32 - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const LineCtx c = line_ctx(sg);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < nst; ++s) {
             mb_init(full + s, 1);
             mb_init(empty + s, nwc);
         }
@@ -446,12 +447,12 @@ __global__ void __launch_bounds__(32 * (kMaxWarps + 1))
     __syncthreads();
     if (warp == nwc) {
         if (lane != 0) return;
-        const unsigned bytes = 8u * (8 * kTT * sg.LDR + 2 * sg.W * sg.BR);
+        const unsigned bytes = 8u * (sg.boxt * sg.LDR + 2 * sg.W * sg.BR);
         const int row0 = static_cast<int>(c.seg0 + sg.n * c.line);
         int k = 0;
         for (int s = next_step(sg, c, 0); s < sg.nsteps; s = next_step(sg, c, s + 1), ++k) {
-            const int st = k % kStages;
-            if (k >= kStages) mb_wait(empty + st, ((k / kStages) - 1) & 1);
+            const int st = k % nst;
+            if (k >= nst) mb_wait(empty + st, ((k / nst) - 1) & 1);
             mb_expect(full + st, bytes);
             tma3(su32(xs + st * sg.xstage), &mapX, c.seg0 - sg.p - sg.shift, static_cast<int>(nb_line(sg, c, s)), c.t0,
                  full + st);
@@ -460,24 +461,25 @@ __global__ void __launch_bounds__(32 * (kMaxWarps + 1))
         }
         return;
     }
+    const int nrb = nwc / 2, rb = warp % nrb, mat = warp / nrb;
     const int ntiles = (c.tcols + 7) >> 3;
-    double accm[kTT][2], acck[kTT][2];
+    double acc[kTT][2];
 #pragma unroll
-    for (int t = 0; t < kTT; ++t) accm[t][0] = accm[t][1] = acck[t][0] = acck[t][1] = 0.0;
+    for (int t = 0; t < kTT; ++t) acc[t][0] = acc[t][1] = 0.0;
     int k = 0;
     for (int s = next_step(sg, c, 0); s < sg.nsteps; s = next_step(sg, c, s + 1), ++k) {
-        const int st = k % kStages;
-        mb_wait(full + st, (k / kStages) & 1);
-        stencil_step<KS>(sg, xs + st * sg.xstage, bsm + (st * 2) * sg.bstage, ntiles, accm, acck);
+        const int st = k % nst;
+        mb_wait(full + st, (k / nst) & 1);
+        stencil_step<KS>(sg, xs + st * sg.xstage, bsm + (st * 2 + mat) * sg.bstage, rb, ntiles, acc);
         __syncwarp();
         if (lane == 0) mb_arrive(empty + st);
     }
-    stencil_store(sg, c, accm, acck, MX, KX);
+    stencil_store(sg, c, rb, acc, mat ? KX : MX);
 }
 
 // (b) cp.async staging by all threads (warp = column group, lane = rows), double buffered.
 template <int KS>
-__global__ void __launch_bounds__(32 * kMaxWarps)
+__global__ void __launch_bounds__(32 * 2 * kMaxWarps)
     stencil_sync_kernel(StencilGeo sg, const double* __restrict__ Mst, const double* __restrict__ Kst,
                         const double* __restrict__ X, double* __restrict__ MX, double* __restrict__ KX) {
     extern __shared__ __align__(128) double sx[];
@@ -509,10 +511,11 @@ __global__ void __launch_bounds__(32 * kMaxWarps)
         }
         asm volatile("cp.async.commit_group;\n" ::);
     };
+    const int nrb = nw / 2, rb = warp % nrb, mat = warp / nrb;
     const int ntiles = (c.tcols + 7) >> 3;
-    double accm[kTT][2], acck[kTT][2];
+    double acc[kTT][2];
 #pragma unroll
-    for (int t = 0; t < kTT; ++t) accm[t][0] = accm[t][1] = acck[t][0] = acck[t][1] = 0.0;
+    for (int t = 0; t < kTT; ++t) acc[t][0] = acc[t][1] = 0.0;
     int s = next_step(sg, c, 0);
     if (s < sg.nsteps) issue(s, 0);
     int buf = 0;
@@ -521,22 +524,21 @@ __global__ void __launch_bounds__(32 * kMaxWarps)
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();  // stage buf landed for all; the other buffer is free again
         if (sn < sg.nsteps) issue(sn, buf ^ 1);
-        stencil_step<KS>(sg, xs + buf * sg.xstage, bsm + (buf * 2) * sg.bstage, ntiles, accm, acck);
+        stencil_step<KS>(sg, xs + buf * sg.xstage, bsm + (buf * 2 + mat) * sg.bstage, rb, ntiles, acc);
         s = sn;
         buf ^= 1;
     }
-    stencil_store(sg, c, accm, acck, MX, KX);
+    stencil_store(sg, c, rb, acc, mat ? KX : MX);
 }
 
 template <int D>
 __global__ void stencil_diag_kernel(PhysicalDesc g, const double* Kst, const double* Mst, double* dK, double* dM) {
-    long long Ns = 1, S = 1, c = 0, o = 1;
+    long long Ns = 1, c = 0, o = 1;
     for (int l = 0; l < D; ++l) {
         Ns *= g.n;
         c += g.p * o;
         o *= 2 * g.p + 1;
     }
-    S = o;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < Ns;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         dK[i] = Kst[c * Ns + i];
@@ -565,17 +567,17 @@ template <int KS>
 cudaError_t stencil_launch(const StencilGeo& sg, bool tma, dim3 grid, int nwc, const double* Mst, const double* Kst,
                            const double* X, const CUtensorMap* maps, double* MX, double* KX, cudaStream_t st) {
     if (tma) {
-        const size_t smem = sizeof(double) * kStages * (sg.xstage + 2 * sg.bstage) + 2 * kStages * sizeof(uint64_t);
+        const size_t smem = sizeof(double) * sg.nst * (sg.xstage + 2 * sg.bstage) + 2 * sg.nst * sizeof(uint64_t);
         cudaError_t e = cudaFuncSetAttribute(stencil_tma_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        stencil_tma_kernel<KS><<<grid, 32 * (nwc + 1), smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX);
+        stencil_tma_kernel<KS><<<grid, 32 * (2 * nwc + 1), smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX);
     } else {
         const size_t smem = sizeof(double) * 2 * (sg.xstage + 2 * sg.bstage);
         cudaError_t e = cudaFuncSetAttribute(stencil_sync_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        stencil_sync_kernel<KS><<<grid, 32 * nwc, smem, st>>>(sg, Mst, Kst, X, MX, KX);
+        stencil_sync_kernel<KS><<<grid, 64 * nwc, smem, st>>>(sg, Mst, Kst, X, MX, KX);
     }
     return cudaGetLastError();
 }
@@ -649,9 +651,12 @@ cudaError_t launch_stencil_apply2(const PhysicalDesc& g, const double* Mst, cons
     const int shift = g.p & 1;
     sg.LDR = (sg.SR + shift + 11) / 16 * 16 + 4;
     if (sg.LDR - 16 >= sg.SR + shift) sg.LDR -= 16;
-    sg.BR = sg.seg_rows;
+    sg.BR = (sg.seg_rows + 11) / 16 * 16 + 4;  // == 4 mod 16: conflict-free band fragments
+    if (sg.BR - 16 >= sg.seg_rows) sg.BR -= 16;
     sg.xstage = (8 * kTT * sg.LDR + 15) / 16 * 16;
     sg.bstage = (sg.W * sg.BR + 15) / 16 * 16;
+    sg.boxt = static_cast<int>(std::min<long long>(8 * kTT, n_t));
+    sg.nst = kStages;
     dim3 grid(static_cast<unsigned>(lines * sg.nseg), static_cast<unsigned>((n_t + 8 * kTT - 1) / (8 * kTT)));
     // TMA staging needs 16-byte strides / base addresses (n even) and boxes <= 256 per dimension
     CUtensorMap maps[3];
@@ -662,7 +667,7 @@ cudaError_t launch_stencil_apply2(const PhysicalDesc& g, const double* Mst, cons
         const cuuint64_t dx[3] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(sg.Ns / g.n),
                                   static_cast<cuuint64_t>(n_t)};
         const cuuint64_t sx[2] = {static_cast<cuuint64_t>(g.n) * 8, static_cast<cuuint64_t>(sg.Ns) * 8};
-        const cuuint32_t bx[3] = {static_cast<cuuint32_t>(sg.LDR), 1, 8 * kTT};
+        const cuuint32_t bx[3] = {static_cast<cuuint32_t>(sg.LDR), 1, static_cast<cuuint32_t>(sg.boxt)};
         long long planes = 1;
         for (int l = 0; l < g.d; ++l) planes *= sg.W;
         const cuuint64_t db[2] = {static_cast<cuuint64_t>(sg.Ns), static_cast<cuuint64_t>(planes)};
@@ -672,6 +677,16 @@ cudaError_t launch_stencil_apply2(const PhysicalDesc& g, const double* Mst, cons
               encode(&maps[2], Kst, 2, db, sb, bb);
     }
     sg.shift = tma ? shift : 0;
+    if (tma) {  // deepest ring that fits: X boxes of boxt columns (columns past n_t are never stored)
+        sg.xstage = (sg.boxt * sg.LDR + 15) / 16 * 16;
+        const size_t per = sizeof(double) * (sg.xstage + 2 * sg.bstage) + 2 * sizeof(uint64_t);
+        sg.nst = static_cast<int>(std::min<size_t>(4, (227 * 1024) / per));
+        if (sg.nst < 2) tma = false;
+    }
+    if (!tma) {
+        sg.xstage = (8 * kTT * sg.LDR + 15) / 16 * 16;
+        sg.shift = 0;
+    }
     switch (KS) {
         case 3: return stencil_launch<3>(sg, tma, grid, wpc, Mst, Kst, X, maps, MX, KX, st);
         case 4: return stencil_launch<4>(sg, tma, grid, wpc, Mst, Kst, X, maps, MX, KX, st);
