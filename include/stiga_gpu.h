@@ -152,10 +152,32 @@ int stiga_kronsum_create_spacetime(int d, const int* n, const double* const* K, 
 int stiga_kronsum_create_physical(stiga_problem_t prob, int p, int n_el, int device, stiga_kronsum_t* out);
 int stiga_kronsum_destroy(stiga_kronsum_t A);
 int stiga_kronsum_size(stiga_kronsum_t A, long long* n_dof);
+/* Tensor dimensions [n_1 .. n_d, n_t] (*D entries; cap = capacity of dims). */
+int stiga_kronsum_dims(stiga_kronsum_t A, int* D, int* dims, int cap);
 /* KronSumOperator::apply(x) (kronop.cpp:108-115): y = sum_t coeff_t (x)_l F_{t,l} x. d_y != d_x. */
 int stiga_kronsum_apply(stiga_kronsum_t A, const double* d_x, double* d_y, void* stream);
 /* KronSumOperator::diagonal() (kronop.cpp:117-131) into a host buffer of N_dof. */
 int stiga_kronsum_diagonal(stiga_kronsum_t A, double* h_diag);
+
+/* Time-sharded mat-vec building blocks, for the space-time (identity geometry) and
+   physical systems: A x = W~ (x) a(x) + M~ (x) b(x) with a, b the spatial halves.
+   apply_space: on a slab of nt_local time slices (N_s x nt_local colex), d_a = a(x), d_b = b(x)
+     (spacetime: a = (M_d .. M_1) x, b = sum_l (M_d .. K_l .. M_1) x; physical: a = M_s x, b = K_s x).
+   apply_time: d_y (slices t0 .. t0+nt_local) = W~ a + M~ b with the time bands (gamma W_t, nu M_t /
+     W_t, M_t), where d_a, d_b hold slices [t0 - halo_lo, t0 + nt_local + halo_hi) and each halo is
+     min(p, slices that exist) wide (p from stiga_kronsum_time_halfband).  Generic-term operators
+     (stiga_kronsum_create) are rejected with STIGA_INVALID. */
+int stiga_kronsum_time_halfband(stiga_kronsum_t A, int* p);
+int stiga_kronsum_apply_space(stiga_kronsum_t A, long long nt_local, const double* d_x, double* d_a, double* d_b,
+                              void* stream);
+int stiga_kronsum_apply_time(stiga_kronsum_t A, long long t0, long long nt_local, int halo_lo, int halo_hi,
+                             const double* d_a, const double* d_b, double* d_y, void* stream);
+
+/* GMRES BLAS-1 on the device (gmres.cpp:76-85, 121), for the distributed solver above the ABI:
+   deterministic dot into *d_result (device scalar), y += alpha x, y = alpha x. */
+int stiga_vec_dot(const double* d_x, const double* d_y, long long n, double* d_result, void* stream);
+int stiga_vec_axpy(double alpha, const double* d_x, double* d_y, long long n, void* stream);
+int stiga_vec_scal(double alpha, const double* d_x, double* d_y, long long n, void* stream);
 
 /* ---- GMRES (gmres.hpp:12-35) ---------------------------------------------------------- */
 

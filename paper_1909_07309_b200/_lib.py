@@ -68,6 +68,13 @@ SIGNATURES = {
     "stiga_kronsum_diagonal": (_c_int, [_vp, _pd]),
     "stiga_gmres": (_c_int, [_vp, _vp, _vp, _vp, ctypes.POINTER(GmresOptions), ctypes.POINTER(GmresReport), _vp]),
     "stiga_fp64_peak": (_c_int, [_c_int, _c_dbl, _pd, _pd]),
+    "stiga_kronsum_time_halfband": (_c_int, [_vp, _pi]),
+    "stiga_kronsum_dims": (_c_int, [_vp, _pi, _pi, _c_int]),
+    "stiga_kronsum_apply_space": (_c_int, [_vp, _c_ll, _vp, _vp, _vp, _vp]),
+    "stiga_kronsum_apply_time": (_c_int, [_vp, _c_ll, _c_ll, _c_int, _c_int, _vp, _vp, _vp, _vp]),
+    "stiga_vec_dot": (_c_int, [_vp, _vp, _c_ll, _vp, _vp]),
+    "stiga_vec_axpy": (_c_int, [_c_dbl, _vp, _vp, _c_ll, _vp]),
+    "stiga_vec_scal": (_c_int, [_c_dbl, _vp, _vp, _c_ll, _vp]),
 }
 
 _lib = None

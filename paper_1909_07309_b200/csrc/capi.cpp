@@ -1103,12 +1103,124 @@ int stiga_kronsum_size(stiga_kronsum_t A, long long* n_dof) {
     });
 }
 
+int stiga_kronsum_dims(stiga_kronsum_t A, int* D, int* dims, int cap) {
+    return guarded([&] {
+        require(A && D && dims, "stiga_kronsum_dims: null argument");
+        require(cap >= A->D, "stiga_kronsum_dims: capacity too small");
+        *D = A->D;
+        for (int l = 0; l < A->D; ++l) dims[l] = A->dims[l];
+    });
+}
+
 int stiga_kronsum_apply(stiga_kronsum_t A, const double* d_x, double* d_y, void* stream) {
     return guarded([&] {
         require(A && d_x && d_y, "KronSumOperator::apply: vector length mismatch");
         require(d_x != d_y, "KronSumOperator::apply: input and output must not alias");
         DeviceGuard dg(A->device);
         A->apply(d_x, d_y, as_stream(stream));
+    });
+}
+
+int stiga_kronsum_time_halfband(stiga_kronsum_t A, int* p) {
+    return guarded([&] {
+        require(A && p, "stiga_kronsum_time_halfband: null argument");
+        require(A->physical || A->spacetime, "stiga_kronsum_time_halfband: needs a spacetime or physical operator");
+        const int d = A->D - 1;
+        *p = A->physical ? std::max(A->hbw[0], A->hbw[1]) : std::max(A->hbw[2 * d], A->hbw[2 * d + 1]);
+    });
+}
+
+int stiga_kronsum_apply_space(stiga_kronsum_t A, long long nt_local, const double* d_x, double* d_a, double* d_b,
+                              void* stream) {
+    return guarded([&] {
+        require(A && d_x && d_a && d_b, "stiga_kronsum_apply_space: null argument");
+        require(A->physical || A->spacetime, "stiga_kronsum_apply_space: needs a spacetime or physical operator");
+        const int d = A->D - 1;
+        require(nt_local >= 0 && nt_local <= A->dims[d], "stiga_kronsum_apply_space: slab larger than n_t");
+        require(d_x != d_a && d_x != d_b && d_a != d_b, "stiga_kronsum_apply_space: buffers must not alias");
+        if (nt_local == 0) return;
+        DeviceGuard dg(A->device);
+        cudaStream_t st = as_stream(stream);
+        if (A->physical) {
+            ck(gpu::launch_stencil_apply2(A->pdesc, A->Mst.p, A->Kst.p, d_x, d_a, d_b, nt_local, st), "stencil apply");
+            return;
+        }
+        // spatial chain of the spacetime form over dims [n_1 .. n_d, nt_local]
+        const long long Ns = A->n_dof / A->dims[d];
+        auto geo = [&](int m) {
+            gpu::ModeGeom g;
+            long long L = 1;
+            for (int l = 0; l < m; ++l) L *= A->dims[l];
+            g.L = L;
+            g.n = g.m = A->dims[m];
+            g.ncols = Ns * nt_local / A->dims[m];
+            return g;
+        };
+        const gpu::Band none{};
+        A->ensure_scratch(4);
+        double* bufs[2][2] = {{A->t0.p, A->t1.p}, {A->t2.p, A->t3.p}};
+        double* a = d == 1 ? d_a : bufs[0][0];
+        double* b = d == 1 ? d_b : bufs[0][1];
+        ck(gpu::launch_banded_pass(geo(0), d_x, nullptr, a, b, A->band(0), none, A->band(1), none, 0.0, st), "banded");
+        for (int m = 1; m < d; ++m) {
+            double* a2 = m == d - 1 ? d_a : bufs[m % 2][0];
+            double* b2 = m == d - 1 ? d_b : bufs[m % 2][1];
+            ck(gpu::launch_banded_pass(geo(m), a, b, a2, b2, A->band(2 * m), none, A->band(2 * m + 1), A->band(2 * m), 0.0,
+                                       st),
+               "banded");
+            a = a2;
+            b = b2;
+        }
+    });
+}
+
+int stiga_kronsum_apply_time(stiga_kronsum_t A, long long t0, long long nt_local, int halo_lo, int halo_hi,
+                             const double* d_a, const double* d_b, double* d_y, void* stream) {
+    return guarded([&] {
+        require(A && d_a && d_b && d_y, "stiga_kronsum_apply_time: null argument");
+        require(A->physical || A->spacetime, "stiga_kronsum_apply_time: needs a spacetime or physical operator");
+        const int d = A->D - 1;
+        const int nt = A->dims[d];
+        require(t0 >= 0 && nt_local >= 0 && t0 + nt_local <= nt, "stiga_kronsum_apply_time: slab outside [0, n_t)");
+        const int ia = A->physical ? 0 : 2 * d, ib = ia + 1;
+        const int p = std::max(A->hbw[ia], A->hbw[ib]);
+        require(halo_lo == std::min<long long>(p, t0) && halo_hi == std::min<long long>(p, nt - t0 - nt_local),
+                "stiga_kronsum_apply_time: halo widths must be min(p, slices that exist)");
+        require(d_y != d_a && d_y != d_b, "stiga_kronsum_apply_time: output must not alias the inputs");
+        if (nt_local == 0) return;
+        DeviceGuard dg(A->device);
+        const long long Ns = A->n_dof / nt;
+        ck(gpu::launch_time_band_slab(Ns, nt, t0, nt_local, halo_lo, d_a, d_b, d_y, A->band(ia), A->band(ib),
+                                      as_stream(stream)),
+           "time band slab");
+    });
+}
+
+int stiga_vec_dot(const double* d_x, const double* d_y, long long n, double* d_result, void* stream) {
+    return guarded([&] {
+        require(n >= 0 && d_result && (n == 0 || (d_x && d_y)), "stiga_vec_dot: invalid argument");
+        cudaStream_t st = as_stream(stream);
+        if (n == 0) {
+            ck(cudaMemsetAsync(d_result, 0, sizeof(double), st), "memset");
+            return;
+        }
+        thread_local DBuf partials;
+        if (!partials.p) partials.alloc(static_cast<size_t>(gpu::dot_partials_size()));
+        ck(gpu::launch_dot(d_x, d_y, n, partials.p, d_result, st), "dot");
+    });
+}
+
+int stiga_vec_axpy(double alpha, const double* d_x, double* d_y, long long n, void* stream) {
+    return guarded([&] {
+        require(n >= 0 && (n == 0 || (d_x && d_y)), "stiga_vec_axpy: invalid argument");
+        ck(gpu::launch_axpy(alpha, d_x, d_y, n, as_stream(stream)), "axpy");
+    });
+}
+
+int stiga_vec_scal(double alpha, const double* d_x, double* d_y, long long n, void* stream) {
+    return guarded([&] {
+        require(n >= 0 && (n == 0 || (d_x && d_y)), "stiga_vec_scal: invalid argument");
+        ck(gpu::launch_scal(alpha, d_x, d_y, n, as_stream(stream)), "scal");
     });
 }
 

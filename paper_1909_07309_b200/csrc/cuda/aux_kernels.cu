@@ -57,6 +57,25 @@ __global__ void banded_pass_kernel(ModeGeom g, const double* __restrict__ in0, c
     }
 }
 
+// Time-banded pass on a time slab with halos (sharded system mat-vec):
+// y[s, r] = sum_j A[t0 + r][j] a[s, j - t0 + hl] + B[t0 + r][j] b[s, j - t0 + hl], |j - (t0 + r)| <= p.
+__global__ void time_band_slab_kernel(long long Ns, int nt, long long t0, long long ntl, int hl,
+                                      const double* __restrict__ a, const double* __restrict__ b,
+                                      double* __restrict__ y, Band A, Band B) {
+    const long long total = Ns * ntl;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long r = e / Ns;
+        const long long s = e - r * Ns;
+        const int i = static_cast<int>(t0 + r);
+        const long long base = s + Ns * (hl - t0);  // a[s, j - t0 + hl] = a[base + Ns j]
+        double v = 0.0;
+        if (A.band) v += band_row(A, a, base, Ns, i, nt);
+        if (B.band) v += band_row(B, b, base, Ns, i, nt);
+        y[e] = v;
+    }
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
@@ -155,6 +174,14 @@ cudaError_t launch_banded_pass(const ModeGeom& g, const double* in0, const doubl
     const long long total = g.ncols * g.n;
     if (total <= 0) return cudaSuccess;
     banded_pass_kernel<<<grid_for(total), kThreads, 0, st>>>(g, in0, in1, out0, out1, A, B, C, D, beta0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_time_band_slab(long long Ns, int nt, long long t0, long long ntl, int hl, const double* a,
+                                  const double* b, double* y, Band A, Band B, cudaStream_t st) {
+    const long long total = Ns * ntl;
+    if (total <= 0) return cudaSuccess;
+    time_band_slab_kernel<<<grid_for(total), kThreads, 0, st>>>(Ns, nt, t0, ntl, hl, a, b, y, A, B);
     return cudaGetLastError();
 }
 

@@ -20,6 +20,12 @@ struct Band {
 cudaError_t launch_banded_pass(const ModeGeom& g, const double* in0, const double* in1, double* out0, double* out1,
                                Band A, Band B, Band C, Band D, double beta0, cudaStream_t st);
 
+/// Time-banded pass on a slab of ntl time slices starting at global slice t0 (colex, N_s fastest):
+/// y = A a + B b with A, B the global n_t x n_t bands; a, b hold slices [t0 - hl, ...) (the halo
+/// of p slices on each side that exists).
+cudaError_t launch_time_band_slab(long long Ns, int nt, long long t0, long long ntl, int hl, const double* a,
+                                  const double* b, double* y, Band A, Band B, cudaStream_t st);
+
 /// Deterministic dot product: partials (grid-sized) then a single-block finish into *d_result.
 cudaError_t launch_dot(const double* x, const double* y, long long n, double* d_partials, double* d_result,
                        cudaStream_t st);

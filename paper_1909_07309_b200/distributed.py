@@ -171,3 +171,288 @@ class ShardedExtendedFD:
             return
         self.dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits,
                                     group=self.group)
+
+
+# ---- time-sharded system mat-vec and GMRES --------------------------------------
+
+
+class DeviceSystemBackend:
+    """Spatial / time halves of a spacetime or physical KronSumOperator through the C ABI."""
+
+    def __init__(self, A, stream=None):
+        self.A = A
+        self.stream = stream
+
+    def _st(self):
+        import torch
+
+        s = self.stream or torch.cuda.current_stream()
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def halfband(self):
+        p = ctypes.c_int()
+        check(lib().stiga_kronsum_time_halfband(self.A.handle, ctypes.byref(p)), "kronsum_time_halfband")
+        return p.value
+
+    def space(self, x, a, b, ntl):
+        check(lib().stiga_kronsum_apply_space(self.A.handle, ntl, ctypes.c_void_p(x.data_ptr()),
+                                              ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                                              self._st()), "kronsum_apply_space")
+
+    def time(self, a_ext, b_ext, y, t0, ntl, hl, hh):
+        check(lib().stiga_kronsum_apply_time(self.A.handle, t0, ntl, hl, hh, ctypes.c_void_p(a_ext.data_ptr()),
+                                             ctypes.c_void_p(b_ext.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                             self._st()), "kronsum_apply_time")
+
+
+class ShardedSystem:
+    """Time-sharded SpaceTimeSystem mat-vec A x = W~(x)a(x) + M~(x)b(x) (solver.cpp:58-70).
+
+    The spatial halves a, b are local to the time slab; the banded time factors (half-bandwidth p)
+    couple p slices across a slab boundary, so a and b are computed straight into halo-extended
+    buffers and the p edge slices are exchanged with the time neighbours (point-to-point, not an
+    all-to-all)."""
+
+    def __init__(self, backend, dims, group=None, world=None, rank=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.backend = backend
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.plan = ShardPlan.make(list(dims), world, rank)
+        self.p = backend.halfband()
+        pl = self.plan
+        t0, ntl = pl.t_off[rank], pl.t_len[rank]
+        self.hl = min(self.p, t0)
+        self.hh = min(self.p, pl.n_t - t0 - ntl)
+        for q in range(world - 1):  # a halo never spans more than one neighbouring slab
+            if pl.t_len[q] < self.p or pl.t_len[q + 1] < self.p:
+                raise ValueError("ShardedSystem: every time slab needs at least p slices")
+        self._bufs = None
+
+    def _buffers(self, like):
+        import torch
+
+        pl = self.plan
+        n_ext = pl.n_s * (pl.t_len[pl.rank] + self.hl + self.hh)
+        if self._bufs is None or self._bufs[0].device != like.device:
+            self._bufs = tuple(torch.empty(n_ext, dtype=torch.float64, device=like.device) for _ in range(2))
+        return self._bufs
+
+    def stage_space(self, x_local):
+        pl = self.plan
+        a, b = self._buffers(x_local)
+        ntl = pl.t_len[pl.rank]
+        o, e = self.hl * pl.n_s, (self.hl + ntl) * pl.n_s
+        self.backend.space(x_local, a[o:e], b[o:e], ntl)
+        return a, b
+
+    def halo_views(self):
+        """(send_lo, send_hi, recv_lo, recv_hi) slices of the extended a/b buffers (None if absent)."""
+        pl = self.plan
+        ns, ntl = pl.n_s, pl.t_len[pl.rank]
+        a, b = self._bufs
+        out = []
+        for buf in (a, b):
+            o = self.hl * ns
+            out.append(dict(
+                send_lo=buf[o:o + self.hl * ns] if self.hl else None,
+                send_hi=buf[o + (ntl - self.hh) * ns:o + ntl * ns] if self.hh else None,
+                recv_lo=buf[:o] if self.hl else None,
+                recv_hi=buf[o + ntl * ns:] if self.hh else None))
+        return out
+
+    def stage_time(self, out):
+        pl = self.plan
+        a, b = self._bufs
+        self.backend.time(a, b, out, pl.t_off[pl.rank], pl.t_len[pl.rank], self.hl, self.hh)
+        return out
+
+    def exchange_halos(self):
+        """Send my first hl / last hh slices of a and b to the lower / upper time neighbour and
+        receive theirs (the lower neighbour's last p slices are my lower halo, and so on)."""
+        pl = self.plan
+        if pl.world == 1:
+            return
+        dist, r = self.dist, pl.rank
+        ops = []
+        for v in self.halo_views():
+            if v["recv_lo"] is not None:
+                ops.append(dist.P2POp(dist.irecv, v["recv_lo"], r - 1, self.group))
+                ops.append(dist.P2POp(dist.isend, v["send_lo"], r - 1, self.group))
+            if v["recv_hi"] is not None:
+                ops.append(dist.P2POp(dist.irecv, v["recv_hi"], r + 1, self.group))
+                ops.append(dist.P2POp(dist.isend, v["send_hi"], r + 1, self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def apply(self, x_local, out=None):
+        self.stage_space(x_local)
+        self.exchange_halos()
+        return self.stage_time(out if out is not None else x_local.new_empty(x_local.shape))
+
+
+class DeviceVec:
+    """GMRES BLAS-1 on this rank's device slab through the C ABI; dots are reduced over the group."""
+
+    def __init__(self, group=None, stream=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.stream = stream
+        self._scalar = None
+
+    def _st(self):
+        import torch
+
+        s = self.stream or torch.cuda.current_stream()
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def dot(self, x, y):
+        import torch
+
+        if self._scalar is None or self._scalar.device != x.device:
+            self._scalar = torch.zeros(1, dtype=torch.float64, device=x.device)
+        check(lib().stiga_vec_dot(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), x.numel(),
+                                  ctypes.c_void_p(self._scalar.data_ptr()), self._st()), "vec_dot")
+        if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
+            self.dist.all_reduce(self._scalar, group=self.group)
+        return float(self._scalar.item())
+
+    def axpy(self, alpha, x, y):
+        check(lib().stiga_vec_axpy(float(alpha), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                   x.numel(), self._st()), "vec_axpy")
+
+    def scal(self, alpha, x, y):
+        check(lib().stiga_vec_scal(float(alpha), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                   x.numel(), self._st()), "vec_scal")
+
+
+class SolveReport:
+    """gmres.hpp:15-21 (replicated on every rank)."""
+
+    def __init__(self):
+        self.iterations = 0
+        self.residual_history = []
+        self.converged = False
+        self.wall_time_s = 0.0
+        self.precond_time_fraction = 0.0
+
+
+def sharded_gmres(A, P, b, vec, tol=1e-8, max_krylov=100, restart=None):
+    """Left-preconditioned GMRES (gmres.cpp:19-132) on time-sharded vectors.
+
+    A and P expose apply(x_local, out) (ShardedSystem / ShardedExtendedFD, or any rank-local
+    operator); `vec` supplies dot (all-reduced over the group), axpy and scal on the local slabs.
+    Same control flow as the reference: x0 = 0, beta0 = ||P b||, MGS Arnoldi (k+1 sequential
+    all-reduced dots per iteration), Givens on the replicated host Hessenberg, breakdown
+    H(k+1,k) <= 1e-14 beta0 -> converged, true preconditioned residual at each restart, and
+    `max_krylov` capping the TOTAL iteration count across restarts (gmres.cpp:52-56, 65)."""
+    import math
+    import time
+
+    import torch
+
+    if tol <= 0.0:
+        raise ValueError("gmres: tolerance must be positive")
+    if max_krylov < 1:
+        raise ValueError("gmres: max_krylov must be >= 1")
+    if restart is not None and restart < 1:
+        raise ValueError("gmres: restart cycle must be >= 1")
+    t_start = time.perf_counter()
+    ptime = [0.0]
+
+    def apply_P(v, out):
+        if P is None:
+            out.copy_(v)
+            return out
+        t = time.perf_counter()
+        P.apply(v, out)
+        ptime[0] += time.perf_counter() - t
+        return out
+
+    def norm(v):
+        return math.sqrt(max(vec.dot(v, v), 0.0))
+
+    rep = SolveReport()
+    x = torch.zeros_like(b)
+    z0 = apply_P(b, torch.empty_like(b))
+    beta0 = norm(z0)
+    rep.residual_history.append(1.0)
+    if beta0 == 0.0:
+        rep.converged = True
+        rep.residual_history[-1] = 0.0
+        rep.wall_time_s = time.perf_counter() - t_start
+        return x, rep
+    cycle = min(restart, max_krylov) if restart is not None else max_krylov
+    total = 0
+    done = False
+    w = torch.empty_like(b)
+    tmp = torch.empty_like(b)
+    while not done and total < max_krylov:
+        if total == 0:
+            z = z0
+        else:  # true preconditioned residual P(b - A x) at the restart (gmres.cpp:58-63)
+            A.apply(x, tmp)
+            vec.scal(-1.0, tmp, tmp)
+            vec.axpy(1.0, b, tmp)
+            z = apply_P(tmp, torch.empty_like(b))
+        beta = norm(z)
+        if beta / beta0 <= tol:
+            rep.converged = True
+            break
+        m = min(cycle, max_krylov - total)
+        V = [torch.empty_like(b)]
+        vec.scal(1.0 / beta, z, V[0])
+        H = np.zeros((m + 1, m))
+        cs, sn = np.zeros(m), np.zeros(m)
+        gv = np.zeros(m + 1)
+        gv[0] = beta
+        k = 0
+        while k < m:
+            A.apply(V[k], tmp)
+            apply_P(tmp, w)
+            for i in range(k + 1):
+                H[i, k] = vec.dot(V[i], w)
+                vec.axpy(-H[i, k], V[i], w)
+            H[k + 1, k] = norm(w)
+            tiny = H[k + 1, k] <= 1e-14 * beta0
+            if not tiny:
+                V.append(torch.empty_like(b))
+                vec.scal(1.0 / H[k + 1, k], w, V[-1])
+            for i in range(k):
+                t = cs[i] * H[i, k] + sn[i] * H[i + 1, k]
+                H[i + 1, k] = -sn[i] * H[i, k] + cs[i] * H[i + 1, k]
+                H[i, k] = t
+            denom = math.hypot(H[k, k], H[k + 1, k])
+            cs[k] = H[k, k] / denom
+            sn[k] = H[k + 1, k] / denom
+            H[k, k] = denom
+            H[k + 1, k] = 0.0
+            gv[k + 1] = -sn[k] * gv[k]
+            gv[k] = cs[k] * gv[k]
+            total += 1
+            rel = abs(gv[k + 1]) / beta0
+            rep.residual_history.append(rel)
+            if rel <= tol or tiny:
+                rep.converged = True
+                k += 1
+                done = True
+                break
+            k += 1
+        if k > 0:  # back substitution on the upper-triangular H (gmres.cpp:116-124)
+            y = np.zeros(k)
+            for i in range(k - 1, -1, -1):
+                y[i] = (gv[i] - H[i, i + 1:k].dot(y[i + 1:k])) / H[i, i]
+            for i in range(k):
+                vec.axpy(y[i], V[i], x)
+        if restart is None and not done:
+            break
+    rep.iterations = total
+    rep.wall_time_s = time.perf_counter() - t_start
+    rep.precond_time_fraction = min(1.0, ptime[0] / rep.wall_time_s) if rep.wall_time_s > 0 else 0.0
+    return x, rep

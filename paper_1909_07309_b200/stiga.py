@@ -289,6 +289,10 @@ class KronSumOperator:
         n = ctypes.c_longlong()
         check(lib().stiga_kronsum_size(self._h, ctypes.byref(n)), "kronsum_size")
         self.n_dof = n.value
+        nd = ctypes.c_int()
+        dims_buf = (ctypes.c_int * 8)()
+        check(lib().stiga_kronsum_dims(self._h, ctypes.byref(nd), dims_buf, 8), "kronsum_dims")
+        self.dims = [dims_buf[i] for i in range(nd.value)]
 
     @staticmethod
     def spacetime(K, M, Wt, Mt, gamma, nu, device=0):
