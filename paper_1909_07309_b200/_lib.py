@@ -7,7 +7,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libstiga_gpu.so")
+# STIGA_LIB_PATH: an alternative in-tree build (kernel A/B experiments); default lib/libstiga_gpu.so
+LIB_PATH = os.environ.get("STIGA_LIB_PATH") or os.path.join(_HERE, "lib", "libstiga_gpu.so")
 
 OK, INVALID_ARGUMENT, NUMERICAL, CUDA = 0, 1, 2, 3
 
