@@ -386,8 +386,28 @@ __device__ __forceinline__ void pair_apply(double rinv, double linv, double inv_
 // Block-arrowhead solve (fdsolve.cpp:24-65) on the resident tile: column c = one spatial
 // eigen-index, rows = time eigen-coordinates.  P = NTHR/BN = 2*WM threads share a column
 // (pairs j = p mod P, Schur right-hand side reduced with shuffles).
+// Pair constants staged in smem once per CTA (the 8-byte cp.async fiber copies go through L1 and
+// evict them, and the arrowhead is otherwise latency-bound on their reloads):
+// cs[k * NP + j], k = 0..6: c_j, c1_j, c1_j^2/nu, g[2j], g[2j+1], gamma g[2j], gamma g[2j+1].
+__device__ __forceinline__ int arrow_np(const ArrowParams& ap) { return ap.n_t / 2 + 1; }
+
+__device__ __forceinline__ void stage_arrow_consts(const ArrowParams& ap, double* cs) {
+    const int NP = arrow_np(ap);
+    for (int j = threadIdx.x; j < ap.npairs; j += blockDim.x) {
+        cs[j] = __ldg(ap.pair_c + j);
+        cs[NP + j] = __ldg(ap.pair_c1 + j);
+        cs[2 * NP + j] = __ldg(ap.pair_c1sq + j);
+        cs[3 * NP + j] = __ldg(ap.g + 2 * j);
+        cs[4 * NP + j] = __ldg(ap.g + 2 * j + 1);
+        cs[5 * NP + j] = __ldg(ap.pair_gg + 2 * j);
+        cs[6 * NP + j] = __ldg(ap.pair_gg + 2 * j + 1);
+    }
+}
+
 template <class SH>
-__device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long long c0, const ArrowParams& ap) {
+__device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long long c0, const ArrowParams& ap,
+                                               const double* cs) {
+    const int NP = arrow_np(ap);
     constexpr int P = SH::NTHR / SH::BN;
     static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "threads per column must be a power of two <= 32");
     const int tid = threadIdx.x;
@@ -410,12 +430,12 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
     double part = 0.0;
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
-        const double rinv = pair_rinv(lam, linv, nu, __ldg(ap.pair_c + j));
-        pair_apply(rinv, linv, inv_nu, __ldg(ap.pair_c1 + j), __ldg(ap.pair_c1sq + j), col[(2 * j) * SH::LDX],
-                   col[(2 * j + 1) * SH::LDX], xa, xb);
+        const double rinv = pair_rinv(lam, linv, nu, cs[j]);
+        pair_apply(rinv, linv, inv_nu, cs[NP + j], cs[2 * NP + j], col[(2 * j) * SH::LDX], col[(2 * j + 1) * SH::LDX], xa,
+                   xb);
         col[(2 * j) * SH::LDX] = xa;
         col[(2 * j + 1) * SH::LDX] = xb;
-        part += gam * (__ldg(ap.g + 2 * j) * xa + __ldg(ap.g + 2 * j + 1) * xb);
+        part += gam * (cs[3 * NP + j] * xa + cs[4 * NP + j] * xb);
     }
     if (ap.zero_count && p == 0) {
         const int z = nt - 2;
@@ -428,9 +448,9 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
     const double xlast = __ldg(ap.S_inv + ap.s_off + s) * (slast + part);
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
-        const double rinv = pair_rinv(lam, linv, nu, __ldg(ap.pair_c + j));
-        pair_apply(rinv, linv, inv_nu, __ldg(ap.pair_c1 + j), __ldg(ap.pair_c1sq + j), __ldg(ap.pair_gg + 2 * j) * xlast,
-                   __ldg(ap.pair_gg + 2 * j + 1) * xlast, xa, xb);
+        const double rinv = pair_rinv(lam, linv, nu, cs[j]);
+        pair_apply(rinv, linv, inv_nu, cs[NP + j], cs[2 * NP + j], cs[5 * NP + j] * xlast, cs[6 * NP + j] * xlast, xa,
+                   xb);
         col[(2 * j) * SH::LDX] -= xa;
         col[(2 * j + 1) * SH::LDX] -= xb;
     }
@@ -451,7 +471,9 @@ __global__ void __launch_bounds__(32 * WM * WN)
     extern __shared__ __align__(16) double smem[];
     double* Zs = smem;                                               // Zrows x LDX, resident
     double* stages = smem + static_cast<size_t>(a.Zrows) * SH::LDX;  // nstage x stage
+    double* cs = stages + static_cast<size_t>(a.nstage) * SH::STAGE;    // 7 x (n_t/2 + 1) pair constants
     const long long c0 = static_cast<long long>(blockIdx.x) * SH::BN;
+    stage_arrow_consts(ap, cs);  // visible after the GEMM's first barrier
     Prod p = make_prod<SH>(a, c0, X, Jt);
     double acc[SH::MI][SH::NI][2];
     zero_acc<SH>(acc);
@@ -485,7 +507,7 @@ __global__ void __launch_bounds__(32 * WM * WN)
             cp_commit();
         }
     }
-    if (!(ap.debug & 1)) arrowhead_tile<SH>(a, Zs, c0, ap);
+    if (!(ap.debug & 1)) arrowhead_tile<SH>(a, Zs, c0, ap, cs);
     __syncthreads();
     zero_acc<SH>(acc);
     gemm<SH, false>(a, stages, p, X, Zs, true, 0, acc);  // y = U_t z
@@ -762,7 +784,8 @@ std::vector<Tiling> time_tiling_candidates(int nt) {
                 t.Zrows = Kp;
                 t.nstage = ns;
                 t.smem = sizeof(double) * (static_cast<size_t>(Kp) * t.LDX +
-                                           static_cast<size_t>(ns) * (kBK * t.LDX + t.MpB * kLDJ));
+                                           static_cast<size_t>(ns) * (kBK * t.LDX + t.MpB * kLDJ) +
+                                           7 * static_cast<size_t>(nt / 2 + 1));
                 if (t.smem > kSmemPerCTA) continue;
                 int occ = 0;
                 ArrowParams ap;
