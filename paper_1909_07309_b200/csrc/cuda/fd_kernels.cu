@@ -358,10 +358,12 @@ __global__ void __launch_bounds__(32 * WN)
     store_acc<SH>(a, acc, c0, rb * MI, Y, post);
 }
 
-// 1/x to ~1 ulp: float reciprocal seed + two Newton steps (fused multiply-adds only; the IEEE
-// division subroutine would cost ~10x more issue slots in the arrowhead passes).
+// 1/x to ~1 ulp: MUFU double-precision reciprocal seed (rcp.approx.ftz.f64, full exponent range,
+// no float conversions on the FP64 pipe) + two Newton steps.  The IEEE division subroutine would
+// cost ~10x more FP64 issue slots, and in the arrowhead passes those slots are shared with DMMA.
 __device__ __forceinline__ double rcp(double x) {
-    double r = static_cast<double>(__frcp_rn(static_cast<float>(x)));
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     double e = fma(-x, r, 1.0);
     r = fma(r, e, r);
     e = fma(-x, r, 1.0);
@@ -371,8 +373,8 @@ __device__ __forceinline__ double rcp(double x) {
 // apply_pair_inverse (fdsolve.cpp:11-20) with R_j^-1 = 1/(nu Lambda_s + c_j Lambda_s^-1) recomputed
 // from Lambda_s (fdsolve.cpp:114-119).  Same expression tree as the reference, with x/nu evaluated
 // as x*(1/nu) (exact at nu = 1, within 1 ulp otherwise) and c1*c1/nu precomputed per pair.
-__device__ __forceinline__ double pair_rinv(double lam, double linv, double nu, double cj) {
-    return rcp(nu * lam + cj * linv);
+__device__ __forceinline__ double pair_rinv(double nulam, double linv, double cj) {
+    return rcp(fma(cj, linv, nulam));  // nulam = nu * Lambda_s, hoisted out of the pair loops
 }
 
 __device__ __forceinline__ void pair_apply(double rinv, double linv, double inv_nu, double c1, double c1sq_nu,
@@ -424,18 +426,19 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
     }
     const double linv = 1.0 / lam;
     const double nu = ap.nu, inv_nu = ap.inv_nu, gam = ap.gamma;
+    const double nulam = nu * lam;
     const int nt = ap.n_t;
     double* col = Zs + c;
     const double slast = col[(nt - 1) * SH::LDX];
     double part = 0.0;
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
-        const double rinv = pair_rinv(lam, linv, nu, cs[j]);
+        const double rinv = pair_rinv(nulam, linv, cs[j]);
         pair_apply(rinv, linv, inv_nu, cs[NP + j], cs[2 * NP + j], col[(2 * j) * SH::LDX], col[(2 * j + 1) * SH::LDX], xa,
                    xb);
         col[(2 * j) * SH::LDX] = xa;
         col[(2 * j + 1) * SH::LDX] = xb;
-        part += gam * (cs[3 * NP + j] * xa + cs[4 * NP + j] * xb);
+        part = fma(cs[5 * NP + j], xa, fma(cs[6 * NP + j], xb, part));  // gamma g[2j] x_a + gamma g[2j+1] x_b
     }
     if (ap.zero_count && p == 0) {
         const int z = nt - 2;
@@ -448,7 +451,7 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
     const double xlast = __ldg(ap.S_inv + ap.s_off + s) * (slast + part);
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
-        const double rinv = pair_rinv(lam, linv, nu, cs[j]);
+        const double rinv = pair_rinv(nulam, linv, cs[j]);
         pair_apply(rinv, linv, inv_nu, cs[NP + j], cs[2 * NP + j], cs[5 * NP + j] * xlast, cs[6 * NP + j] * xlast, xa,
                    xb);
         col[(2 * j) * SH::LDX] -= xa;
@@ -536,16 +539,17 @@ __global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restr
     }
     const double linv = 1.0 / lam;
     const double nu = ap.nu, inv_nu = ap.inv_nu, gam = ap.gamma;
+    const double nulam = nu * lam;
     const int nt = ap.n_t;
     const double* zc = Z + s;
     double part = 0.0;
 #pragma unroll 4
     for (int j = w; j < ap.npairs; j += P) {
         double xa, xb;
-        const double rinv = pair_rinv(lam, linv, nu, __ldg(ap.pair_c + j));
+        const double rinv = pair_rinv(nulam, linv, __ldg(ap.pair_c + j));
         pair_apply(rinv, linv, inv_nu, __ldg(ap.pair_c1 + j), __ldg(ap.pair_c1sq + j), __ldg(zc + (2 * j) * Ns),
                    __ldg(zc + (2 * j + 1) * Ns), xa, xb);
-        part += gam * (__ldg(ap.g + 2 * j) * xa + __ldg(ap.g + 2 * j + 1) * xb);
+        part = fma(__ldg(ap.pair_gg + 2 * j), xa, fma(__ldg(ap.pair_gg + 2 * j + 1), xb, part));
     }
     double xz = 0.0;
     const int z = nt - 2;
@@ -564,7 +568,7 @@ __global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restr
 #pragma unroll 4
     for (int j = w; j < ap.npairs; j += P) {
         const double c1 = __ldg(ap.pair_c1 + j), c1sq = __ldg(ap.pair_c1sq + j);
-        const double rinv = pair_rinv(lam, linv, nu, __ldg(ap.pair_c + j));
+        const double rinv = pair_rinv(nulam, linv, __ldg(ap.pair_c + j));
         double ya, yb, ca, cb;
         pair_apply(rinv, linv, inv_nu, c1, c1sq, __ldg(zc + (2 * j) * Ns), __ldg(zc + (2 * j + 1) * Ns), ya, yb);
         pair_apply(rinv, linv, inv_nu, c1, c1sq, __ldg(ap.pair_gg + 2 * j) * xlast, __ldg(ap.pair_gg + 2 * j + 1) * xlast,
