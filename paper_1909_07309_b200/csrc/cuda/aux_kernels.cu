@@ -6,6 +6,7 @@
 #include "aux_kernels.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 
 namespace stiga {
@@ -29,6 +30,183 @@ __device__ __forceinline__ double band_row(const Band& B, const double* __restri
     double s = 0.0;
     for (int j = jlo; j <= jhi; ++j) s += __ldg(row + (j - i + B.p)) * __ldg(in + base + L * j);
     return s;
+}
+
+// Unsigned 32-bit division by a runtime-invariant divisor via multiply-high (Granlund-Montgomery):
+// the colex index decompositions of these streaming kernels would otherwise run the 64-bit
+// division subroutine per element and be issue-bound far below the HBM roofline.
+struct FastDiv {
+    unsigned d = 1, m = 1, s = 0;
+    __host__ __device__ FastDiv() {}
+    __host__ __device__ explicit FastDiv(unsigned dd) : d(dd) {
+        s = 0;
+        while ((1ull << s) < dd) ++s;
+        m = static_cast<unsigned>(((1ull << 32) * ((1ull << s) - dd)) / dd + 1);
+    }
+};
+__device__ __forceinline__ unsigned fdiv(unsigned n, const FastDiv& f) {
+    const unsigned t = __umulhi(n, f.m);
+    return static_cast<unsigned>((static_cast<unsigned long long>(t) + n) >> f.s);
+}
+
+// 32-bit index path (total < 2^32): e = l + L (i + n r) decomposed with two fast divisions.
+__global__ void banded_pass_kernel32(ModeGeom g, FastDiv dLn, FastDiv dL, unsigned total,
+                                     const double* __restrict__ in0, const double* __restrict__ in1,
+                                     double* __restrict__ out0, double* __restrict__ out1, Band A, Band B, Band C,
+                                     Band D, double beta0) {
+    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const unsigned r = fdiv(e, dLn);
+        const unsigned rem = e - r * dLn.d;
+        const unsigned i = fdiv(rem, dL);
+        const unsigned l = rem - i * dL.d;
+        const long long base = l + static_cast<long long>(dLn.d) * r;
+        double s0 = 0.0;
+        if (A.band) s0 += band_row(A, in0, base, g.L, static_cast<int>(i), g.n);
+        if (B.band) s0 += band_row(B, in1, base, g.L, static_cast<int>(i), g.n);
+        if (beta0 != 0.0) s0 += beta0 * out0[e];
+        out0[e] = s0;
+        if (out1) {
+            double s1 = 0.0;
+            if (C.band) s1 += band_row(C, in0, base, g.L, static_cast<int>(i), g.n);
+            if (D.band) s1 += band_row(D, in1, base, g.L, static_cast<int>(i), g.n);
+            out1[e] = s1;
+        }
+    }
+}
+
+// Smem-tiled banded pass: a CTA stages TL whole fibers (all n entries, zero-padded by P on both
+// ends) of each input and the band rows of the pass (widened to 2P+1 with zeros), then computes every
+// output of those fibers with fully unrolled (2P+1)-tap loops, and writes them once: HBM traffic is
+// one read of each input and one write of each output (the per-element kernel re-read up to 2p+1
+// inputs: 3.4x the algorithmic DRAM bytes on the time mode) and no index arithmetic per tap.
+// FIBER_MAJOR (L == 1, fibers contiguous): smem [fiber][i] with pitch n+2P+1; otherwise [i][l] with
+// pitch TL+1 (rows of TL consecutive l are contiguous in HBM).
+struct BandSet {
+    Band b[4];  // A, B (-> out0 from in0, in1), C, D (-> out1 from in0, in1)
+};
+
+__device__ __forceinline__ void cp8(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src));
+}
+
+template <bool FIBER_MAJOR, int P>
+__global__ void __launch_bounds__(256) banded_tile_kernel(ModeGeom g, int TL, long long ntiles_l, FastDiv dn,
+                                                          const double* __restrict__ in0, const double* __restrict__ in1,
+                                                          double* __restrict__ out0, double* __restrict__ out1,
+                                                          BandSet bs, double beta0) {
+    constexpr int W = 2 * P + 1;
+    extern __shared__ double sm[];
+    const int n = g.n;
+    const int np = n + 2 * P;  // padded fiber length
+    const int pitch = FIBER_MAJOR ? np + 1 : TL + 1;
+    const int tsize = FIBER_MAJOR ? TL * pitch : np * pitch;
+    const bool two = in1 != nullptr;
+    const int nin = two ? 2 : 1;
+    double* buf[2] = {sm, sm + nin * tsize};  // double-buffered tiles [in0 | in1]
+    double* bsm = sm + 2 * nin * tsize;       // present bands, n x W each
+    int nb = 0;
+    int slot[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) slot[k] = bs.b[k].band ? nb++ : -1;
+    // bands -> smem, widened to W taps (zeros outside each band's own half-bandwidth)
+    for (int e = threadIdx.x; e < nb * n * W; e += blockDim.x) {
+        const int q = e / (n * W), rem = e - q * n * W;
+        const int i = rem / W, k = rem - i * W;
+        int which = 0;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+            if (slot[kk] == q) which = kk;
+        const Band& B = bs.b[which];
+        const int o = k - P + B.p;  // tap offset inside the stored row of width 2 B.p + 1
+        const int j = i + k - P;
+        bsm[e] = (o >= 0 && o <= 2 * B.p && j >= 0 && j < n) ? __ldg(B.band + static_cast<long long>(i) * (2 * B.p + 1) + o)
+                                                             : 0.0;
+    }
+    auto soff = [&](int ip, int lc) { return FIBER_MAJOR ? lc * pitch + ip : ip * pitch + lc; };  // ip = i + P
+    // zero halo rows (P on each side of every fiber slot) of both buffers; copies never touch them
+    for (int e = threadIdx.x; e < 2 * P * TL; e += blockDim.x) {
+        const int lc = e / (2 * P), h = e - lc * (2 * P);
+        const int ip = h < P ? h : n + h;  // 0..P-1 and n+P..n+2P-1
+        for (int bb = 0; bb < 2; ++bb)
+            for (int q = 0; q < nin; ++q) buf[bb][q * tsize + soff(ip, lc)] = 0.0;
+    }
+    const long long ntiles = FIBER_MAJOR ? ntiles_l : ntiles_l * (g.ncols / g.L);
+    struct TileGeo {
+        long long gbase;
+        int tl;
+    };
+    auto tile_geo = [&](long long bt) {
+        TileGeo t;
+        const long long r = FIBER_MAJOR ? 0 : bt / ntiles_l;
+        const long long l0 = (FIBER_MAJOR ? bt : bt - r * ntiles_l) * TL;
+        t.tl = static_cast<int>(min(static_cast<long long>(TL), (FIBER_MAJOR ? g.ncols : g.L) - l0));
+        t.gbase = FIBER_MAJOR ? l0 * n : l0 + g.L * n * r;
+        return t;
+    };
+    auto goff = [&](int i, int lc) -> long long { return FIBER_MAJOR ? lc * static_cast<long long>(n) + i : lc + g.L * i; };
+    auto split = [&](int o, int tl, int& i, int& lc) {
+        if (FIBER_MAJOR) {
+            lc = static_cast<int>(fdiv(static_cast<unsigned>(o), dn));
+            i = o - lc * n;
+        } else {
+            i = o / tl;
+            lc = o - i * tl;
+        }
+    };
+    auto issue = [&](long long bt, double* dst) {  // cp.async the tile's fibers (HBM order) into dst
+        const TileGeo t = tile_geo(bt);
+        for (int o = threadIdx.x; o < t.tl * n; o += blockDim.x) {
+            int i, lc;
+            split(o, t.tl, i, lc);
+            const long long ga = t.gbase + goff(i, lc);
+            cp8(dst + soff(i + P, lc), in0 + ga);
+            if (two) cp8(dst + tsize + soff(i + P, lc), in1 + ga);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    const double* bA = slot[0] >= 0 ? bsm + slot[0] * n * W : nullptr;
+    const double* bB = slot[1] >= 0 ? bsm + slot[1] * n * W : nullptr;
+    const double* bC = slot[2] >= 0 ? bsm + slot[2] * n * W : nullptr;
+    const double* bD = slot[3] >= 0 ? bsm + slot[3] * n * W : nullptr;
+    const int ti = FIBER_MAJOR ? 1 : pitch;  // smem stride between consecutive i
+    long long bt = blockIdx.x;
+    if (bt < ntiles) issue(bt, buf[0]);
+    int cur = 0;
+    for (; bt < ntiles; bt += gridDim.x) {
+        if (bt + gridDim.x < ntiles) {
+            issue(bt + gridDim.x, buf[cur ^ 1]);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        __syncthreads();  // tile bt (and the bands / halos on the first pass) visible
+        const TileGeo t = tile_geo(bt);
+        const double* t0 = buf[cur];
+        const double* t1 = buf[cur] + tsize;
+        for (int o = threadIdx.x; o < t.tl * n; o += blockDim.x) {
+            int i, lc;
+            split(o, t.tl, i, lc);
+            const long long ga = t.gbase + goff(i, lc);
+            const double* x0 = t0 + soff(i, lc);  // taps i-P .. i+P live at padded rows i .. i+2P
+            const double* x1 = t1 + soff(i, lc);
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const double v0 = x0[k * ti];
+                const double v1 = two ? x1[k * ti] : 0.0;
+                if (bA) s0 = fma(bA[i * W + k], v0, s0);
+                if (bB) s0 = fma(bB[i * W + k], v1, s0);
+                if (bC) s1 = fma(bC[i * W + k], v0, s1);
+                if (bD) s1 = fma(bD[i * W + k], v1, s1);
+            }
+            if (beta0 != 0.0) s0 += beta0 * out0[ga];
+            out0[ga] = s0;
+            if (out1) out1[ga] = s1;
+        }
+        __syncthreads();  // buffer cur is refilled two iterations later
+        cur ^= 1;
+    }
 }
 
 __global__ void banded_pass_kernel(ModeGeom g, const double* __restrict__ in0, const double* __restrict__ in1,
@@ -63,9 +241,11 @@ __global__ void time_band_slab_kernel(long long Ns, int nt, long long t0, long l
                                       const double* __restrict__ a, const double* __restrict__ b,
                                       double* __restrict__ y, Band A, Band B) {
     const long long total = Ns * ntl;
+    const bool small = total < (1ll << 32) && Ns < (1ll << 32);
+    const FastDiv dNs(small ? static_cast<unsigned>(Ns) : 1u);
     for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long r = e / Ns;
+        const long long r = small ? fdiv(static_cast<unsigned>(e), dNs) : e / Ns;
         const long long s = e - r * Ns;
         const int i = static_cast<int>(t0 + r);
         const long long base = s + Ns * (hl - t0);  // a[s, j - t0 + hl] = a[base + Ns j]
@@ -173,7 +353,69 @@ cudaError_t launch_banded_pass(const ModeGeom& g, const double* in0, const doubl
                                Band A, Band B, Band C, Band D, double beta0, cudaStream_t st) {
     const long long total = g.ncols * g.n;
     if (total <= 0) return cudaSuccess;
-    banded_pass_kernel<<<grid_for(total), kThreads, 0, st>>>(g, in0, in1, out0, out1, A, B, C, D, beta0);
+    // tiled path: TL fibers per CTA, as wide as fits 48 KB of smem for the staged inputs + bands
+    const int nin = in1 ? 2 : 1;
+    const bool fm = g.L == 1;
+    const Band bands[4] = {A, B, C, D};
+    int P = 0, nb = 0;
+    for (const Band& b : bands)
+        if (b.band) {
+            P = std::max(P, b.p);
+            ++nb;
+        }
+    P = std::max(P, 1);
+    auto tile_bytes = [&](int tl) {  // two tile buffers + bands
+        const size_t np = g.n + 2 * P;
+        return sizeof(double) *
+               (2 * nin * (fm ? tl * (np + 1) : np * (tl + 1)) + nb * static_cast<size_t>(g.n) * (2 * P + 1));
+    };
+    constexpr size_t kBudget = 72 * 1024;  // 3 CTAs (24 warps) per SM
+    int TL = 32;
+    while (TL > 8 && tile_bytes(TL) > kBudget) TL /= 2;
+    if (P <= 8 && tile_bytes(TL) <= kBudget && !std::getenv("STIGA_BANDED_FLAT")) {
+        const long long ntl = fm ? (g.ncols + TL - 1) / TL : (g.L + TL - 1) / TL;
+        const long long R = fm ? 1 : g.ncols / g.L;
+        const long long blocks = ntl * R;
+        if (blocks < (1ll << 31)) {
+            BandSet bs{{A, B, C, D}};
+            const FastDiv dn(static_cast<unsigned>(g.n));
+            const size_t sm = tile_bytes(TL);
+            const int per_sm = std::max(1, static_cast<int>((227 * 1024) / (sm + 1024)));
+            const unsigned nbk = static_cast<unsigned>(std::min<long long>(blocks, 148LL * std::min(per_sm, 8)));
+#define STIGA_BANDED_CASE(PP)                                                                                      \
+    case PP:                                                                                                       \
+        if (fm) {                                                                                                  \
+            cudaFuncSetAttribute(banded_tile_kernel<true, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                 static_cast<int>(sm));                                                            \
+            banded_tile_kernel<true, PP><<<nbk, 256, sm, st>>>(g, TL, ntl, dn, in0, in1, out0, out1, bs, beta0);    \
+        } else {                                                                                                   \
+            cudaFuncSetAttribute(banded_tile_kernel<false, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                 static_cast<int>(sm));                                                            \
+            banded_tile_kernel<false, PP><<<nbk, 256, sm, st>>>(g, TL, ntl, dn, in0, in1, out0, out1, bs, beta0);   \
+        }                                                                                                          \
+        return cudaGetLastError();
+            switch (P) {
+                STIGA_BANDED_CASE(1)
+                STIGA_BANDED_CASE(2)
+                STIGA_BANDED_CASE(3)
+                STIGA_BANDED_CASE(4)
+                STIGA_BANDED_CASE(5)
+                STIGA_BANDED_CASE(6)
+                STIGA_BANDED_CASE(7)
+                STIGA_BANDED_CASE(8)
+                default: break;
+            }
+#undef STIGA_BANDED_CASE
+        }
+    }
+    if (total < (1ll << 32)) {
+        banded_pass_kernel32<<<grid_for(total), kThreads, 0, st>>>(g, FastDiv(static_cast<unsigned>(g.L * g.n)),
+                                                                   FastDiv(static_cast<unsigned>(g.L)),
+                                                                   static_cast<unsigned>(total), in0, in1, out0, out1,
+                                                                   A, B, C, D, beta0);
+    } else {
+        banded_pass_kernel<<<grid_for(total), kThreads, 0, st>>>(g, in0, in1, out0, out1, A, B, C, D, beta0);
+    }
     return cudaGetLastError();
 }
 

@@ -1,4 +1,4 @@
-"""ncu driver for the physical space-time mat-vec (c4 by default): assemble A on the device, run
+"""ncu driver for the space-time mat-vec (c4 physical by default, Kronecker-sum form for identity configs): run
 `--applies` mat-vecs, bracket the last one with cudaProfilerStart/Stop."""
 import argparse
 import os
@@ -20,7 +20,13 @@ ap.add_argument("--applies", type=int, default=3)
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 t = time.time()
-A = stiga.KronSumOperator.physical(Problem(cfg.problem), cfg.p, cfg.n_el)
+if cfg.problem == "identity":  # Kronecker-sum (banded) form of the space-time system
+    from paper_1909_07309_b200.problems import identity_pieces
+
+    pc = identity_pieces(cfg.d, cfg.p, cfg.n_el)
+    A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0)
+else:
+    A = stiga.KronSumOperator.physical(Problem(cfg.problem), cfg.p, cfg.n_el)
 torch.cuda.synchronize()
 print("assembly_s", time.time() - t)
 x = torch.from_numpy(uniform_pm1(A.n_dof, cfg.seed)).cuda()
