@@ -249,12 +249,17 @@ def run_ours(args):
     sampler = ClockSampler(dev)
     barrier()
     torch.cuda.synchronize()
+    prof_range = os.environ.get("STIGA_PROFILE_RANGE") == "1"  # ncu --profile-from-start off: timed steps only
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStart()
     with sampler:
         ev0.record(stream)
         for _ in range(K_steps):
             apply_fn(r, s)
         ev1.record(stream)
         torch.cuda.synchronize()
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStop()
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / K_steps)
     value = (1 if sharded else ws) / (ms * 1e-3)

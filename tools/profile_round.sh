@@ -11,20 +11,27 @@ python bench.py > $O/${TAG}_bench_c2.log 2>&1 && tail -1 $O/${TAG}_bench_c2.log 
 for c in c3 c4; do
   python bench.py --config $c --steps 100 --no-cpu-baseline > $O/${TAG}_bench_$c.log 2>&1 && tail -1 $O/${TAG}_bench_$c.log > $O/${TAG}_bench_$c.json
 done
-# 2. launch list of the default bench command (cold, serialised; shares only)
-python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-gmres > $O/${TAG}_plain.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${TAG}_launches.csv \
-      python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-gmres > $O/${TAG}_ncu_launches.log 2>&1
-# 3. one apply per config, full set, per-launch raw page
+# 2. launch list of the timed steps of the default bench command (cold, serialised; shares only).
+#    The plain run records its autotuned tilings in a cache that the ncu run replays, and the timed
+#    region is bracketed by cudaProfilerStart/Stop (STIGA_PROFILE_RANGE=1).
+export STIGA_TUNE_CACHE=/tmp/stiga_tune_${TAG}.txt
+rm -f $STIGA_TUNE_CACHE
+STIGA_PROFILE_RANGE=1 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-gmres > $O/${TAG}_plain.log 2>&1 && \
+  STIGA_PROFILE_RANGE=1 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+      --log-file $O/${TAG}_launches.csv \
+      python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-gmres > $O/${TAG}_ncu_launches.log 2>&1
+# 3. one apply per config, full set, per-launch raw page (same tuned tilings as the plain run)
 for c in c2 c3 c4; do
   python tools/profile_fd.py --config $c --names-out $O/${TAG}_names_$c.json > $O/${TAG}_pf_$c.log 2>&1 && \
   ncu --set full --clock-control none --profile-from-start off -o $O/${TAG}_$c \
       python tools/profile_fd.py --config $c > $O/${TAG}_ncu_$c.log 2>&1 && \
   ncu -i $O/${TAG}_$c.ncu-rep --page raw --csv > $O/${TAG}_${c}_raw.csv && rm -f $O/${TAG}_$c.ncu-rep
 done
-# 4. the physical mat-vec of c4 (stencil kernel + banded time pass)
-python tools/profile_matvec.py > $O/${TAG}_pm.log 2>&1 && \
-  ncu --set full --clock-control none --profile-from-start off -o $O/${TAG}_matvec \
-      python tools/profile_matvec.py > $O/${TAG}_ncu_matvec.log 2>&1 && \
-  ncu -i $O/${TAG}_matvec.ncu-rep --page raw --csv > $O/${TAG}_matvec_raw.csv && rm -f $O/${TAG}_matvec.ncu-rep
+# 4. the system mat-vecs: c4 physical (stencil kernel + banded time pass), c3 Kronecker-sum form
+for c in c4 c3; do
+  python tools/profile_matvec.py --config $c > $O/${TAG}_pm_$c.log 2>&1 && \
+  ncu --set full --clock-control none --profile-from-start off -o $O/${TAG}_matvec_$c \
+      python tools/profile_matvec.py --config $c > $O/${TAG}_ncu_matvec_$c.log 2>&1 && \
+  ncu -i $O/${TAG}_matvec_$c.ncu-rep --page raw --csv > $O/${TAG}_matvec_${c}_raw.csv && rm -f $O/${TAG}_matvec_$c.ncu-rep
+done
 ls -la $O | grep $TAG
