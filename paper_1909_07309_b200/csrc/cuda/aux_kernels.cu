@@ -108,14 +108,19 @@ __global__ void __launch_bounds__(256) banded_tile_kernel(ModeGeom g, int TL, lo
     int nb = 0;
     int slot[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) slot[k] = bs.b[k].band ? nb++ : -1;
+    for (int k = 0; k < 4; ++k) {  // identical bands (M applied to both inputs) share one smem copy
+        slot[k] = bs.b[k].band ? nb : -1;
+        for (int q = 0; q < k; ++q)
+            if (bs.b[k].band && bs.b[q].band == bs.b[k].band) slot[k] = slot[q];
+        if (slot[k] == nb) ++nb;
+    }
     // bands -> smem, widened to W taps (zeros outside each band's own half-bandwidth)
     for (int e = threadIdx.x; e < nb * n * W; e += blockDim.x) {
         const int q = e / (n * W), rem = e - q * n * W;
         const int i = rem / W, k = rem - i * W;
         int which = 0;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
+        for (int kk = 3; kk >= 0; --kk)
             if (slot[kk] == q) which = kk;
         const Band& B = bs.b[which];
         const int o = k - P + B.p;  // tap offset inside the stored row of width 2 B.p + 1
@@ -358,10 +363,12 @@ cudaError_t launch_banded_pass(const ModeGeom& g, const double* in0, const doubl
     const bool fm = g.L == 1;
     const Band bands[4] = {A, B, C, D};
     int P = 0, nb = 0;
-    for (const Band& b : bands)
-        if (b.band) {
-            P = std::max(P, b.p);
-            ++nb;
+    for (int k = 0; k < 4; ++k)
+        if (bands[k].band) {
+            P = std::max(P, bands[k].p);
+            bool dup = false;
+            for (int q = 0; q < k; ++q) dup = dup || bands[q].band == bands[k].band;
+            if (!dup) ++nb;
         }
     P = std::max(P, 1);
     auto tile_bytes = [&](int tl) {  // two tile buffers + bands
@@ -369,10 +376,19 @@ cudaError_t launch_banded_pass(const ModeGeom& g, const double* in0, const doubl
         return sizeof(double) *
                (2 * nin * (fm ? tl * (np + 1) : np * (tl + 1)) + nb * static_cast<size_t>(g.n) * (2 * P + 1));
     };
-    constexpr size_t kBudget = 72 * 1024;  // 3 CTAs (24 warps) per SM
+    // 72 KB = 3 CTAs (24 warps) per SM; wide bands at large n (e.g. p = 5, n = 163: 43 KB of bands)
+    // fall back to 2 CTAs, then 1, before the untiled kernel
+    size_t budget = 0;
     int TL = 32;
-    while (TL > 8 && tile_bytes(TL) > kBudget) TL /= 2;
-    if (P <= 8 && tile_bytes(TL) <= kBudget && !std::getenv("STIGA_BANDED_FLAT")) {
+    for (size_t b : {size_t(72) * 1024, size_t(110) * 1024, size_t(220) * 1024}) {
+        TL = 32;
+        while (TL > 8 && tile_bytes(TL) > b) TL /= 2;
+        if (tile_bytes(TL) <= b) {
+            budget = b;
+            break;
+        }
+    }
+    if (P <= 8 && budget > 0 && !std::getenv("STIGA_BANDED_FLAT")) {
         const long long ntl = fm ? (g.ncols + TL - 1) / TL : (g.L + TL - 1) / TL;
         const long long R = fm ? 1 : g.ncols / g.L;
         const long long blocks = ntl * R;
