@@ -173,19 +173,21 @@ struct stiga_fd_s {
         double* bufs[2] = {scratch.p, scratch2.p};
         const double* dsl = dinv.p ? dinv.p + n_s * t0 : nullptr;
         const long long nloc = n_s * nt_local;
-        const int nops = d + ((!backward && dsl) ? 1 : 0);
+        const bool fused_pre = !backward && dsl && fused_prescale();
+        const int nops = d + ((!backward && dsl && !fused_pre) ? 1 : 0);
         int k = 0;
         const double* src = in;
         auto next = [&]() -> double* { double* r = (k == nops - 1) ? out : bufs[k % 2]; ++k; return r; };
-        if (!backward && dsl) {
+        if (!backward && dsl && !fused_pre) {
             double* dst = next();
             ck(gpu::launch_scale(dsl, src, dst, nloc, st), "slab pre-scale");
             src = dst;
         }
         for (int l = 0; l < d; ++l) {
             double* dst = next();
-            ck(gpu::launch_mode_product(tl[l], slab_geom(l, nt_local), src, dst, backward ? J[l]->p : Jt[l]->p,
-                                        (backward && l == d - 1) ? dsl : nullptr, st),
+            ck(gpu::launch_mode_product((!backward && l == 0) ? first_tiling() : tl[l], slab_geom(l, nt_local), src,
+                                        dst, backward ? J[l]->p : Jt[l]->p, (backward && l == d - 1) ? dsl : nullptr, st,
+                                        (fused_pre && l == 0) ? dsl : nullptr),
                "slab mode product");
             src = dst;
         }
@@ -218,8 +220,9 @@ struct stiga_fd_s {
         ck(cudaEventCreate(&e0), "event");
         ck(cudaEventCreate(&e1), "event");
         f();  // warm (sets the smem attribute, loads the module)
+        f();
         float best = 1e30f;
-        for (int rep = 0; rep < 2; ++rep) {
+        for (int rep = 0; rep < 3; ++rep) {
             ck(cudaEventRecord(e0, nullptr), "event");
             f();
             ck(cudaEventRecord(e1, nullptr), "event");
@@ -258,7 +261,7 @@ struct stiga_fd_s {
                 v.push_back(static_cast<int>(x));
                 p = end;
             }
-            if (static_cast<int>(v.size()) != d + 3) continue;
+            if (static_cast<int>(v.size()) != d + 4) continue;
             bool ok = true;
             for (int l = 0; l < d; ++l) ok = ok && v[l] >= 0 && v[l] < static_cast<int>(cand_space[l].size());
             ok = ok && v[d] >= -1 && v[d] < static_cast<int>(cand_time.size()) && v[d + 1] >= 0 &&
@@ -268,6 +271,8 @@ struct stiga_fd_s {
             tl_t = v[d] >= 0 ? cand_time[v[d]] : gpu::Tiling{};
             tl_ts = cand_ts[v[d + 1]];
             time_split = v[d + 2] == 1;
+            use_fused_pre = v[d + 3] >= 0 && v[d + 3] < static_cast<int>(cand_space[0].size());
+            tl_pre = use_fused_pre ? cand_space[0][v[d + 3]] : tl[0];
             found = true;
         }
         std::fclose(f);
@@ -298,6 +303,29 @@ struct stiga_fd_s {
                     std::fprintf(stderr, "[stiga tune] mode %d MI=%d WN=%d RB=%d occ=%d: %.4f ms\n", l, t.MI, t.WN,
                                  t.RB, t.ctas_per_sm, ms);
             }
+        }
+        use_fused_pre = false;
+        tl_pre = tl[0];
+        int pick_pre = -1;
+        if (!no_tune && dinv.p) {
+            const float sep = time_once([&] {
+                ck(gpu::launch_scale(dinv.p, scratch.p, scratch2.p, n_dof, nullptr), "tune");
+                ck(gpu::launch_mode_product(tl[0], geom(0), scratch2.p, scratch.p, Jt[0]->p, nullptr, nullptr), "tune");
+            });
+            float best_fus = 1e30f;
+            for (size_t c = 0; c < std::min(kMaxCand, cand_space[0].size()); ++c) {
+                const gpu::Tiling& t = cand_space[0][c];
+                if (!gpu::prescale_fits(t)) continue;
+                const float ms = time_once([&] {
+                    ck(gpu::launch_mode_product(t, geom(0), scratch.p, scratch2.p, Jt[0]->p, nullptr, nullptr, dinv.p),
+                       "tune");
+                });
+                if (ms < best_fus) { best_fus = ms; tl_pre = t; pick_pre = static_cast<int>(c); }
+            }
+            use_fused_pre = pick_pre >= 0 && best_fus < sep;
+            if (debug_tune)
+                std::fprintf(stderr, "[stiga tune] pre-scale separate %.4f ms, fused %.4f ms (MI=%d RB=%d)\n", sep,
+                             best_fus, tl_pre.MI, tl_pre.RB);
         }
         const bool fused_ok = !cand_time.empty();
         tl_t = fused_ok ? cand_time.front() : gpu::Tiling{};
@@ -344,14 +372,24 @@ struct stiga_fd_s {
                 std::string ln = tune_key() + " |";
                 for (int l = 0; l < d; ++l) ln += " " + std::to_string(pick[l]);
                 ln += " " + std::to_string(fused_ok ? pick[d] : -1) + " " + std::to_string(pick[d + 1]) + " " +
-                      std::to_string(time_split ? 1 : 0) + "\n";
+                      std::to_string(time_split ? 1 : 0) + " " + std::to_string(use_fused_pre ? pick_pre : -1) + "\n";
                 std::fputs(ln.c_str(), f);
                 std::fclose(f);
             }
         }
     }
 
-    int launches() const { return 2 * d + (time_split ? 3 : 1) + (dinv.p ? 1 : 0); }
+    // D^-1/2 pre-scale fused into the first forward mode product when its smem allows (the
+    // separate scale pass otherwise); STIGA_NO_FUSED_PRESCALE=1 forces the separate pass.
+    bool use_fused_pre = false;  // decided by the autotuner (fused vs separate, timed)
+    gpu::Tiling tl_pre;          // tiling of the pre-scaled first forward pass (tuned separately: every
+                                 // row block re-stages the D chunk, so it prefers fewer row blocks)
+    bool fused_prescale() const {
+        static const bool off = std::getenv("STIGA_NO_FUSED_PRESCALE") != nullptr;
+        return dinv.p != nullptr && use_fused_pre && !off && gpu::prescale_fits(tl_pre);
+    }
+    const gpu::Tiling& first_tiling() const { return fused_prescale() ? tl_pre : tl[0]; }
+    int launches() const { return 2 * d + (time_split ? 3 : 1) + (dinv.p && !fused_prescale() ? 1 : 0); }
 
     // Launch sequence (fdsolve.cpp:158-163): [D^-1/2 pre-scale], forward spatial modes U_l^T, the
     // time direction (fused U_t^T / arrowhead / U_t kernel, or the three as separate passes),
@@ -372,14 +410,17 @@ struct stiga_fd_s {
             ++k;
             return dst;
         };
-        if (scaled) {
+        const bool fused_pre = fused_prescale();
+        if (scaled && !fused_pre) {
             double* dst = next();
             ck(gpu::launch_scale(dinv.p, src, dst, n_dof, st), "fd D^-1/2 pre-scale");
             src = dst;
         }
         for (int l = 0; l < d; ++l) {
             double* dst = next();
-            ck(gpu::launch_mode_product(tl[l], geom(l), src, dst, Jt[l]->p, nullptr, st), "fd forward mode product");
+            ck(gpu::launch_mode_product(l == 0 ? first_tiling() : tl[l], geom(l), src, dst, Jt[l]->p, nullptr, st,
+                                        (l == 0 && fused_pre) ? dinv.p : nullptr),
+               "fd forward mode product");
             src = dst;
         }
         if (time_split) {
@@ -879,8 +920,10 @@ int stiga_fd_launch_info(stiga_fd_t P, int i, char* name, int name_len, double* 
         require(i >= 0 && i < P->launches(), "stiga_fd_launch_info: launch index out of range");
         std::vector<std::pair<std::string, double>> L;
         const double N = static_cast<double>(P->n_dof);
-        if (P->dinv.p) L.emplace_back("pre_scale", 0.0);
-        for (int l = 0; l < P->d; ++l) L.emplace_back("fwd_mode" + std::to_string(l), 2.0 * P->dims[l] * N);
+        if (P->dinv.p && !P->fused_prescale()) L.emplace_back("pre_scale", 0.0);
+        for (int l = 0; l < P->d; ++l)
+            L.emplace_back("fwd_mode" + std::to_string(l) + (l == 0 && P->fused_prescale() ? "+pre_scale" : ""),
+                           2.0 * P->dims[l] * N);
         const double nt = P->dims[P->d];
         if (P->time_split) {
             L.emplace_back("time_UtT", 2.0 * nt * N);

@@ -71,9 +71,10 @@ struct KArgs {
 };
 
 // Compile-time shape of a CTA.
-template <int MI_, int WM_, int WN_>
+template <int MI_, int WM_, int WN_, bool PS_ = false>
 struct Shape {
     static constexpr int MI = MI_, WM = WM_, WN = WN_, NI = 2;
+    static constexpr bool PS = PS_;  // fused D^-1/2 pre-scale: a D chunk is staged beside each fiber chunk
     static constexpr int NTHR = 32 * WM * WN;
     static constexpr int BN = 16 * WN;
     static constexpr int LDX = BN + 4;  // == 4 mod 16
@@ -84,7 +85,8 @@ struct Shape {
     static constexpr int JCNT = (JPIECES + NTHR - 1) / NTHR;
     static constexpr int XROWSTEP = NTHR / BN;         // fiber-chunk rows between elements (L > 1)
     static constexpr int XCOLSTEP = NTHR / 16;         // fibers between elements (L == 1)
-    static constexpr int STAGE = kBK * LDX + MPB * kLDJ;  // doubles per pipeline stage
+    static constexpr int DOFF = kBK * LDX + MPB * kLDJ;  // D chunk offset within a stage (PS)
+    static constexpr int STAGE = DOFF + (PS ? kBK * LDX : 0);  // doubles per pipeline stage
     static_assert(kBK * BN % NTHR == 0, "fiber chunk must split evenly over the CTA");
 };
 
@@ -108,6 +110,7 @@ struct Prod {
     unsigned colmask;    // element u belongs to a fiber inside the tensor
     bool full_tile;
     bool contiguous;     // L == 1
+    const double* dg;    // PS: D^-1/2 address of element u = 0 for chunk 0 (same offsets as xg)
     const double* jg;    // J global address of this thread's piece u = 0 for chunk 0
     unsigned js;         // smem byte offset (within a stage) of piece u = 0
     int jp2;             // 2 * piece index (column offset within the chunk)
@@ -163,33 +166,35 @@ __device__ __forceinline__ void issue_chunk(const KArgs& a, const Prod& p, unsig
         }
     }
     if (!load_x) return;
-    const double* xg = p.xg + q * p.xkstep;
-    const unsigned xs = st + p.xs;
-    if (p.contiguous) {
-        if (p.full_tile && k0 + kBK <= a.geo.n) {
+    auto copy_chunk = [&](const double* xg, unsigned xs) {
+        if (p.contiguous) {
+            if (p.full_tile && k0 + kBK <= a.geo.n) {
 #pragma unroll
-            for (int u = 0; u < SH::XCNT; ++u) cp_async8(xs + 8u * u * SH::XCOLSTEP, xg + u * p.xstep);
+                for (int u = 0; u < SH::XCNT; ++u) cp_async8(xs + 8u * u * SH::XCOLSTEP, xg + u * p.xstep);
+            } else {
+                const bool rowv = k0 + p.xrow0 < a.geo.n;
+#pragma unroll
+                for (int u = 0; u < SH::XCNT; ++u) {
+                    const bool v = rowv && ((p.colmask >> u) & 1u);
+                    cp_async8_zfill(xs + 8u * u * SH::XCOLSTEP, v ? xg + u * p.xstep : X, v);
+                }
+            }
         } else {
-            const bool rowv = k0 + p.xrow0 < a.geo.n;
+            if (p.full_tile && k0 + kBK <= a.geo.n) {
 #pragma unroll
-            for (int u = 0; u < SH::XCNT; ++u) {
-                const bool v = rowv && ((p.colmask >> u) & 1u);
-                cp_async8_zfill(xs + 8u * u * SH::XCOLSTEP, v ? xg + u * p.xstep : X, v);
+                for (int u = 0; u < SH::XCNT; ++u) cp_async8(xs + 8u * u * SH::XROWSTEP * SH::LDX, xg + u * p.xstep);
+            } else {
+                const bool colv = p.colmask != 0u;
+#pragma unroll
+                for (int u = 0; u < SH::XCNT; ++u) {
+                    const bool v = colv && (k0 + p.xrow0 + u * SH::XROWSTEP < a.geo.n);
+                    cp_async8_zfill(xs + 8u * u * SH::XROWSTEP * SH::LDX, v ? xg + u * p.xstep : X, v);
+                }
             }
         }
-    } else {
-        if (p.full_tile && k0 + kBK <= a.geo.n) {
-#pragma unroll
-            for (int u = 0; u < SH::XCNT; ++u) cp_async8(xs + 8u * u * SH::XROWSTEP * SH::LDX, xg + u * p.xstep);
-        } else {
-            const bool colv = p.colmask != 0u;
-#pragma unroll
-            for (int u = 0; u < SH::XCNT; ++u) {
-                const bool v = colv && (k0 + p.xrow0 + u * SH::XROWSTEP < a.geo.n);
-                cp_async8_zfill(xs + 8u * u * SH::XROWSTEP * SH::LDX, v ? xg + u * p.xstep : X, v);
-            }
-        }
-    }
+    };
+    copy_chunk(p.xg + q * p.xkstep, st + p.xs);
+    if constexpr (SH::PS) copy_chunk(p.dg + q * p.xkstep, st + 8u * SH::DOFF + p.xs);
 }
 
 // acc += J_chunk * B_chunk over KS k-steps of 4.  A fragments from the J stage (ja), B fragments
@@ -205,7 +210,7 @@ __device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, in
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) av[0][mi] = mi < mact ? ja[mi * 8 * kLDJ] : 0.0;
 #pragma unroll
-    for (int ni = 0; ni < NI; ++ni) bv[0][ni] = bb[ni * 8];
+    for (int ni = 0; ni < NI; ++ni) bv[0][ni] = SH::PS ? bb[ni * 8] * bb[SH::DOFF + ni * 8] : bb[ni * 8];
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
         const int cur = kk & 1, nxt = cur ^ 1;
@@ -213,7 +218,9 @@ __device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, in
 #pragma unroll
             for (int mi = 0; mi < MI; ++mi) av[nxt][mi] = mi < mact ? ja[mi * 8 * kLDJ + (kk + 1) * 4] : 0.0;
 #pragma unroll
-            for (int ni = 0; ni < NI; ++ni) bv[nxt][ni] = bb[(kk + 1) * 4 * SH::LDX + ni * 8];
+            for (int ni = 0; ni < NI; ++ni)
+                bv[nxt][ni] = SH::PS ? bb[(kk + 1) * 4 * SH::LDX + ni * 8] * bb[SH::DOFF + (kk + 1) * 4 * SH::LDX + ni * 8]
+                                     : bb[(kk + 1) * 4 * SH::LDX + ni * 8];
         }
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi)
@@ -342,16 +349,21 @@ __device__ __forceinline__ void gemm(const KArgs& a, double* stages, const Prod&
     }
 }
 
-template <int MI, int WN>
+// PS: Y = (I (x) J (x) I)(pre .* X) -- the D^-1/2 pre-scale of the apply fused into the first forward
+// mode product: each fiber chunk's D^-1/2 chunk is staged beside it by the same cp.async pattern
+// and B fragments are scaled as they are read (two DMULs per k-step on the FP64 pipe, against the
+// separate 24 B/DoF HBM pass of scale_kernel).
+template <int MI, int WN, bool PS>
 __global__ void __launch_bounds__(32 * WN)
     mode_product_kernel(KArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
-                        const double* __restrict__ post) {
-    using SH = Shape<MI, 1, WN>;
+                        const double* __restrict__ post, const double* __restrict__ pre) {
+    using SH = Shape<MI, 1, WN, PS>;
     extern __shared__ __align__(16) double smem[];
     const int rb = blockIdx.x % a.RB;  // row blocks of one fiber tile are adjacent -> X tile reused from L2
     const long long c0 = static_cast<long long>(blockIdx.x / a.RB) * SH::BN;
     const double* Jg = J + static_cast<size_t>(rb) * SH::MPB * a.Kp;
-    const Prod p = make_prod<SH>(a, c0, X, Jg);
+    Prod p = make_prod<SH>(a, c0, X, Jg);
+    if constexpr (PS) p.dg = pre + (p.xg - X);
     double acc[SH::MI][SH::NI][2];
     zero_acc<SH>(acc);
     gemm<SH, true>(a, smem, p, X, nullptr, false, rb * MI, acc);
@@ -630,16 +642,17 @@ int occupancy(K kernel, int threads, size_t smem) {
 // ---- instantiation dispatch --------------------------------------------------------------------
 template <int MI, int WN>
 cudaError_t launch_mode_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                          const double* post, cudaStream_t st, int* occ) {
-    auto k = mode_product_kernel<MI, WN>;
+                          const double* post, const double* pre, cudaStream_t st, int* occ) {
+    auto k = pre ? mode_product_kernel<MI, WN, true> : mode_product_kernel<MI, WN, false>;
+    const size_t smem = pre ? prescale_smem(t) : t.smem;
     if (occ) {
-        *occ = occupancy(k, 32 * WN, t.smem);
+        *occ = occupancy(k, 32 * WN, smem);
         return cudaSuccess;
     }
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(t.smem));
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const long long blocks = (g.ncols + t.BN - 1) / t.BN * t.RB;
-    k<<<static_cast<unsigned>(blocks), 32 * WN, t.smem, st>>>(make_args(t, g), X, Y, J, post);
+    k<<<static_cast<unsigned>(blocks), 32 * WN, smem, st>>>(make_args(t, g), X, Y, J, post, pre);
     return cudaGetLastError();
 }
 
@@ -669,17 +682,17 @@ cudaError_t launch_time_t(const Tiling& t, const ModeGeom& g, const double* X, d
 
 template <int WN>
 cudaError_t dispatch_mode_wn(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                             const double* post, cudaStream_t st, int* occ) {
-#define STIGA_CALL_MODE(M) launch_mode_t<M, WN>(t, g, X, Y, J, post, st, occ)
+                             const double* post, const double* pre, cudaStream_t st, int* occ) {
+#define STIGA_CALL_MODE(M) launch_mode_t<M, WN>(t, g, X, Y, J, post, pre, st, occ)
     STIGA_MI_SWITCH(t.MI, STIGA_CALL_MODE)
 #undef STIGA_CALL_MODE
 }
 
 cudaError_t dispatch_mode(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                          const double* post, cudaStream_t st, int* occ) {
+                          const double* post, const double* pre, cudaStream_t st, int* occ) {
     if (t.WM != 1) return cudaErrorInvalidValue;
-    if (t.WN == 4) return dispatch_mode_wn<4>(t, g, X, Y, J, post, st, occ);
-    if (t.WN == 2) return dispatch_mode_wn<2>(t, g, X, Y, J, post, st, occ);
+    if (t.WN == 4) return dispatch_mode_wn<4>(t, g, X, Y, J, post, pre, st, occ);
+    if (t.WN == 2) return dispatch_mode_wn<2>(t, g, X, Y, J, post, pre, st, occ);
     return cudaErrorInvalidValue;
 }
 
@@ -732,7 +745,7 @@ std::vector<Tiling> mode_tiling_candidates(int m, int n) {
             t.smem = sizeof(double) * static_cast<size_t>(t.nstage) * (kBK * t.LDX + t.MpB * kLDJ);
             if (t.smem > kSmemPerCTA) continue;
             int occ = 0;
-            dispatch_mode(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, nullptr, &occ);
+            dispatch_mode(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &occ);
             t.ctas_per_sm = occ;
             if (occ < 1) continue;
             // strips past S are skipped, so padding costs only imbalance; each extra row block
@@ -817,10 +830,17 @@ Tiling choose_time_tiling(int nt) {
     return c.front();
 }
 
+size_t prescale_smem(const Tiling& t) {
+    return t.smem + sizeof(double) * static_cast<size_t>(t.nstage) * kBK * t.LDX;
+}
+
+bool prescale_fits(const Tiling& t) { return t.WM == 1 && prescale_smem(t) <= kSmemPerCTA; }
+
 cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jpad,
-                                const double* post_scale, cudaStream_t st) {
+                                const double* post_scale, cudaStream_t st, const double* pre_scale) {
     if (g.ncols <= 0) return cudaSuccess;
-    return dispatch_mode(t, g, X, Y, Jpad, post_scale, st, nullptr);
+    if (pre_scale && !prescale_fits(t)) return cudaErrorInvalidValue;
+    return dispatch_mode(t, g, X, Y, Jpad, post_scale, pre_scale, st, nullptr);
 }
 
 cudaError_t launch_time_fused(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jt_pad,

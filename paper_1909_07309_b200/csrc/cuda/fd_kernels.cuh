@@ -74,8 +74,14 @@ std::vector<Tiling> time_tiling_candidates(int n_t);
 
 /// Y = (I (x) J (x) I) X along one mode.  J is row-major, zero padded to (t.Mp x t.Kp).
 /// post_scale (optional) multiplies Y elementwise in the register epilogue (the D^-1/2 post-scale).
+/// pre_scale (optional) multiplies X elementwise before the product (the D^-1/2 pre-scale, staged
+/// beside each fiber chunk); needs prescale_fits(t).
 cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y,
-                                const double* Jpad, const double* post_scale, cudaStream_t stream);
+                                const double* Jpad, const double* post_scale, cudaStream_t stream,
+                                const double* pre_scale = nullptr);
+/// Dynamic smem of the pre-scaled mode kernel for tiling t, and whether it fits one CTA.
+size_t prescale_smem(const Tiling& t);
+bool prescale_fits(const Tiling& t);
 
 /// Standalone block-arrowhead solve X = (gamma Delta_t (x) I + nu I (x) Lambda_s)^-1 Z on the
 /// time-eigen-coordinate tensor (N_s x n_t, time slowest); used when the time direction runs as
