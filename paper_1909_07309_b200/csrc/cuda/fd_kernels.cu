@@ -405,6 +405,27 @@ __device__ __forceinline__ void pair_apply(double rinv, double linv, double inv_
 // cs[k * NP + j], k = 0..6: c_j, c1_j, c1_j^2/nu, g[2j], g[2j+1], gamma g[2j], gamma g[2j+1].
 __device__ __forceinline__ int arrow_np(const ArrowParams& ap) { return ap.n_t / 2 + 1; }
 
+// Per-column constants of the tile (staged during the GEMM prologue, so the arrowhead never waits on
+// global loads): ccol[c] = Lambda_s, ccol[BN + c] = 1/Lambda_s (one IEEE division per column instead
+// of one per thread), ccol[2 BN + c] = S^-1.
+__device__ __forceinline__ void stage_column_consts(const ArrowParams& ap, long long c0, long long ncols, int BN,
+                                                    double* ccol) {
+    for (int c = threadIdx.x; c < BN; c += blockDim.x) {
+        long long s = c0 + c;
+        if (s >= ncols) s = ncols - 1;
+        double lam = 0.0;  // ((0 + lambda_1) + lambda_2) + ... (fdsolve.cpp:91-99)
+        long long rem = s + ap.s_off;  // global spatial index (slab offset in the sharded apply)
+        for (int l = 0; l < ap.d; ++l) {
+            const long long q = rem / ap.n[l];
+            lam = lam + __ldg(ap.lam[l] + (rem - q * ap.n[l]));
+            rem = q;
+        }
+        ccol[c] = lam;
+        ccol[BN + c] = 1.0 / lam;
+        ccol[2 * BN + c] = __ldg(ap.S_inv + ap.s_off + s);
+    }
+}
+
 __device__ __forceinline__ void stage_arrow_consts(const ArrowParams& ap, double* cs) {
     const int NP = arrow_np(ap);
     for (int j = threadIdx.x; j < ap.npairs; j += blockDim.x) {
@@ -420,60 +441,50 @@ __device__ __forceinline__ void stage_arrow_consts(const ArrowParams& ap, double
 
 template <class SH>
 __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long long c0, const ArrowParams& ap,
-                                               const double* cs) {
+                                               const double* cs, const double* ccol) {
     const int NP = arrow_np(ap);
     constexpr int P = SH::NTHR / SH::BN;
     static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "threads per column must be a power of two <= 32");
     const int tid = threadIdx.x;
     const int c = tid / P;
     const int p = tid - c * P;
-    long long s = c0 + c;
-    if (s >= a.geo.ncols) s = a.geo.ncols - 1;
-    double lam = 0.0;  // ((0 + lambda_1) + lambda_2) + ... (fdsolve.cpp:91-99)
-    long long rem = s + ap.s_off;  // global spatial index (slab offset in the sharded apply)
-    for (int l = 0; l < ap.d; ++l) {
-        const long long q = rem / ap.n[l];
-        lam = lam + __ldg(ap.lam[l] + (rem - q * ap.n[l]));
-        rem = q;
-    }
-    const double linv = 1.0 / lam;
+    const double lam = ccol[c], linv = ccol[SH::BN + c];
     const double nu = ap.nu, inv_nu = ap.inv_nu, gam = ap.gamma;
     const double nulam = nu * lam;
     const int nt = ap.n_t;
     double* col = Zs + c;
     const double slast = col[(nt - 1) * SH::LDX];
+    // Forward sweep: Schur right-hand side sum_j gamma g_j . H_j^-1 z_j (fdsolve.cpp:31-47) without
+    // storing H_j^-1 z_j; the back sweep then forms x_j = H_j^-1 (z_j - gamma g_j x_last) from the
+    // untouched z_j -- equal to the reference's y_j - H_j^-1 (gamma g_j x_last) (fdsolve.cpp:52-63)
+    // by linearity, with fewer FP64 instructions (which share the pipe with the DMMAs) and no stores.
     double part = 0.0;
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
         const double rinv = pair_rinv(nulam, linv, cs[j]);
         pair_apply(rinv, linv, inv_nu, cs[NP + j], cs[2 * NP + j], col[(2 * j) * SH::LDX], col[(2 * j + 1) * SH::LDX], xa,
                    xb);
-        col[(2 * j) * SH::LDX] = xa;
-        col[(2 * j + 1) * SH::LDX] = xb;
         part = fma(cs[5 * NP + j], xa, fma(cs[6 * NP + j], xb, part));  // gamma g[2j] x_a + gamma g[2j+1] x_b
     }
+    double xz = 0.0;
     if (ap.zero_count && p == 0) {
-        const int z = nt - 2;
-        const double xz = linv * col[z * SH::LDX] * inv_nu;
-        col[z * SH::LDX] = xz;
-        part += gam * __ldg(ap.g + z) * xz;
+        xz = linv * col[(nt - 2) * SH::LDX] * inv_nu;
+        part += gam * __ldg(ap.g + nt - 2) * xz;
     }
 #pragma unroll
     for (int off = P >> 1; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-    const double xlast = __ldg(ap.S_inv + ap.s_off + s) * (slast + part);
+    const double xlast = ccol[2 * SH::BN + c] * (slast + part);
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;
         const double rinv = pair_rinv(nulam, linv, cs[j]);
-        pair_apply(rinv, linv, inv_nu, cs[NP + j], cs[2 * NP + j], cs[5 * NP + j] * xlast, cs[6 * NP + j] * xlast, xa,
-                   xb);
-        col[(2 * j) * SH::LDX] -= xa;
-        col[(2 * j + 1) * SH::LDX] -= xb;
+        const double u = fma(-cs[5 * NP + j], xlast, col[(2 * j) * SH::LDX]);
+        const double w = fma(-cs[6 * NP + j], xlast, col[(2 * j + 1) * SH::LDX]);
+        pair_apply(rinv, linv, inv_nu, cs[NP + j], cs[2 * NP + j], u, w, xa, xb);
+        col[(2 * j) * SH::LDX] = xa;
+        col[(2 * j + 1) * SH::LDX] = xb;
     }
     if (p == 0) {
-        if (ap.zero_count) {
-            const int z = nt - 2;
-            col[z * SH::LDX] -= (gam * __ldg(ap.g + z) * inv_nu) * (linv * xlast);
-        }
+        if (ap.zero_count) col[(nt - 2) * SH::LDX] = xz - (gam * __ldg(ap.g + nt - 2) * inv_nu) * (linv * xlast);
         col[(nt - 1) * SH::LDX] = xlast;
     }
 }
@@ -487,8 +498,10 @@ __global__ void __launch_bounds__(32 * WM * WN)
     double* Zs = smem;                                               // Zrows x LDX, resident
     double* stages = smem + static_cast<size_t>(a.Zrows) * SH::LDX;  // nstage x stage
     double* cs = stages + static_cast<size_t>(a.nstage) * SH::STAGE;    // 7 x (n_t/2 + 1) pair constants
+    double* ccol = cs + 7 * arrow_np(ap);                               // 3 x BN column constants
     const long long c0 = static_cast<long long>(blockIdx.x) * SH::BN;
     stage_arrow_consts(ap, cs);  // visible after the GEMM's first barrier
+    stage_column_consts(ap, c0, a.geo.ncols, SH::BN, ccol);
     Prod p = make_prod<SH>(a, c0, X, Jt);
     double acc[SH::MI][SH::NI][2];
     zero_acc<SH>(acc);
@@ -522,7 +535,7 @@ __global__ void __launch_bounds__(32 * WM * WN)
             cp_commit();
         }
     }
-    if (!(ap.debug & 1)) arrowhead_tile<SH>(a, Zs, c0, ap, cs);
+    if (!(ap.debug & 1)) arrowhead_tile<SH>(a, Zs, c0, ap, cs, ccol);
     __syncthreads();
     zero_acc<SH>(acc);
     gemm<SH, false>(a, stages, p, X, Zs, true, 0, acc);  // y = U_t z
@@ -802,7 +815,7 @@ std::vector<Tiling> time_tiling_candidates(int nt) {
                 t.nstage = ns;
                 t.smem = sizeof(double) * (static_cast<size_t>(Kp) * t.LDX +
                                            static_cast<size_t>(ns) * (kBK * t.LDX + t.MpB * kLDJ) +
-                                           7 * static_cast<size_t>(nt / 2 + 1));
+                                           7 * static_cast<size_t>(nt / 2 + 1) + 3 * static_cast<size_t>(t.BN));
                 if (t.smem > kSmemPerCTA) continue;
                 int occ = 0;
                 ArrowParams ap;
