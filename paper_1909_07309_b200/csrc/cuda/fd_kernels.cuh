@@ -60,7 +60,6 @@ struct Tiling {
     int LDX = 68;     // smem row stride of a fiber chunk (== 4 mod 16 doubles)
     int Zrows = 0;    // time kernel: rows of the resident Z tile (= Kp)
     int nstage = 3;
-    bool prescale = false;  // mode kernel: D^-1/2 staged through smem with the fiber chunk
     size_t smem = 0;
     int ctas_per_sm = 1;
     int threads() const { return 32 * WM * WN; }

@@ -118,3 +118,39 @@ def test_sharded_gmres_driver_on_device_matches_native():
     assert rep.converged and repn.converged and rep.iterations > 3
     assert abs(rep.iterations - repn.iterations) <= 1
     assert torch.linalg.norm(x - xn) <= 1e-8 * torch.linalg.norm(xn)
+
+
+def test_slab_stage_argument_errors():
+    """The slab stages reject what the reference's operators would reject (invalid_argument ->
+    ValueError): generic-term operators, halo widths other than min(p, slices that exist), slabs
+    outside [0, n_t), aliasing outputs."""
+    import ctypes
+
+    from paper_1909_07309_b200._lib import check, lib
+    from paper_1909_07309_b200.distributed import DeviceSystemBackend
+
+    pc = identity_pieces(2, 2, 6)
+    A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0)
+    be = DeviceSystemBackend(A)
+    p = be.halfband()
+    ns, nt = int(np.prod(A.dims[:-1])), A.dims[-1]
+    x = torch.zeros(ns * nt, dtype=torch.float64, device="cuda")
+    a, b, y = torch.zeros_like(x), torch.zeros_like(x), torch.zeros_like(x)
+    with pytest.raises(ValueError):
+        be.time(a, b, y, 2, 2, p + 1, p)  # wrong lower halo
+    with pytest.raises(ValueError):
+        be.time(a, b, y, nt - 1, 2, p, 0)  # slab past n_t
+    with pytest.raises(ValueError):
+        be.time(a, b, a, 0, 2, 0, p)  # output aliases an input
+    with pytest.raises(ValueError):
+        be.space(x, x, b, nt)  # output aliases the input
+    G = stiga.KronSumOperator(A.dims, [(1.0, [np.eye(n) for n in A.dims])])
+    with pytest.raises(ValueError):
+        DeviceSystemBackend(G).halfband()
+    r = torch.ones(10, dtype=torch.float64, device="cuda")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    check(lib().stiga_vec_dot(ctypes.c_void_p(r.data_ptr()), ctypes.c_void_p(r.data_ptr()), 10,
+                              ctypes.c_void_p(out.data_ptr()), None), "vec_dot")
+    assert out.item() == 10.0
+    with pytest.raises(ValueError):
+        check(lib().stiga_vec_dot(None, None, 10, ctypes.c_void_p(out.data_ptr()), None), "vec_dot")
