@@ -8,9 +8,11 @@ O=gpurun_out
 mkdir -p $O
 # 1. bench lines (default = c2 headline with CPU baseline + GMRES; c3, c4 with GMRES)
 python bench.py > $O/${TAG}_bench_c2.log 2>&1 && tail -1 $O/${TAG}_bench_c2.log > $O/${TAG}_bench_c2.json
-for c in c3 c4; do
-  python bench.py --config $c --steps 100 --no-cpu-baseline > $O/${TAG}_bench_$c.log 2>&1 && tail -1 $O/${TAG}_bench_$c.log > $O/${TAG}_bench_$c.json
+for c in c3 c4 c5p2 c5p4 c5p5; do
+  python bench.py --config $c --steps 50 --no-cpu-baseline > $O/${TAG}_bench_$c.log 2>&1 && tail -1 $O/${TAG}_bench_$c.log > $O/${TAG}_bench_$c.json
 done
+python -m pytest tests -q -m gpu > $O/${TAG}_pytest_gpu.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1
 # 2. launch list of the timed steps of the default bench command (cold, serialised; shares only).
 #    The plain run records its autotuned tilings in a cache that the ncu run replays, and the timed
 #    region is bracketed by cudaProfilerStart/Stop (STIGA_PROFILE_RANGE=1).
