@@ -1301,9 +1301,15 @@ int stiga_vec_dot(const double* d_x, const double* d_y, long long n, double* d_r
             ck(cudaMemsetAsync(d_result, 0, sizeof(double), st), "memset");
             return;
         }
-        thread_local DBuf partials;
-        if (!partials.p) partials.alloc(static_cast<size_t>(gpu::dot_partials_size()));
-        ck(gpu::launch_dot(d_x, d_y, n, partials.p, d_result, st), "dot");
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        thread_local std::vector<std::unique_ptr<DBuf>> partials;  // per device of this host thread
+        if (static_cast<int>(partials.size()) <= dev) partials.resize(dev + 1);
+        if (!partials[dev]) {
+            partials[dev] = std::make_unique<DBuf>();
+            partials[dev]->alloc(static_cast<size_t>(gpu::dot_partials_size()));
+        }
+        ck(gpu::launch_dot(d_x, d_y, n, partials[dev]->p, d_result, st), "dot");
     });
 }
 

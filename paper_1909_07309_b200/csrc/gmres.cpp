@@ -48,8 +48,9 @@ thread_local Pool g_pool;
 
 struct Vec {
     double* p = nullptr;
-    explicit Vec(long long n) {
-        int dev = 0;
+    int dev = 0;
+    long long n = 0;
+    explicit Vec(long long n_) : n(n_) {
         gck(cudaGetDevice(&dev), "cudaGetDevice");
         if (g_pool.device != dev || g_pool.n != n) {
             for (double* q : g_pool.free_list) cudaFree(q);
@@ -64,8 +65,10 @@ struct Vec {
             gck(cudaMalloc(&p, sizeof(double) * std::max<long long>(n, 1)), "cudaMalloc");
         }
     }
-    ~Vec() {
-        if (p) g_pool.free_list.push_back(p);
+    ~Vec() {  // back to the pool only if it still serves this (device, length)
+        if (!p) return;
+        if (g_pool.device == dev && g_pool.n == n) g_pool.free_list.push_back(p);
+        else cudaFree(p);
     }
     Vec(const Vec&) = delete;
     Vec& operator=(const Vec&) = delete;
