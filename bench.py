@@ -34,6 +34,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 time-sharded apply: p2p = all-to-all fused into the kernels' scatter epilogues "
+                         "over NVLink peer memory (CUDA IPC); nccl = pack + NCCL all_to_all_single + unpack")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of the time-sharded apply")
     return ap.parse_args()
@@ -212,10 +215,20 @@ def run_ours(args):
     launches = P.launches()
 
     sharded = ws > 1 and not args.replicas
-    if sharded:  # time-sharded apply: rank owns a time slab, two NCCL all-to-alls per apply
-        from paper_1909_07309_b200.distributed import DeviceBackend, ShardedExtendedFD
+    exchange = None
+    if sharded:  # time-sharded apply: rank owns a time slab, two all-to-all transposes per apply
+        from paper_1909_07309_b200.distributed import DeviceBackend, FusedShardedExtendedFD, ShardedExtendedFD
 
-        sh = ShardedExtendedFD(DeviceBackend(P), P.dims)
+        sh = None
+        if args.exchange == "p2p":
+            try:
+                sh = FusedShardedExtendedFD.create(P, P.dims, device=dev)
+                exchange = "p2p scatter epilogues (CUDA IPC peer memory)"
+            except Exception as e:  # e.g. no peer access between these GPUs: keep the NCCL exchange
+                exchange = f"nccl (p2p unavailable: {type(e).__name__}: {str(e)[:120]})"
+        if sh is None:
+            sh = ShardedExtendedFD(DeviceBackend(P), P.dims)
+            exchange = exchange or "nccl all_to_all_single (pack / unpack)"
         a0, a1 = sh.plan.local_slice()
         r_host = torch.from_numpy(uniform_pm1(a1 - a0, cfg.seed, start=a0)).pin_memory()
         apply_fn = lambda x, y: sh.apply(x, out=y)  # noqa: E731
@@ -420,13 +433,18 @@ def run_ours(args):
         "data": "synthetic (seeded uniform[-1,1], splitmix64)",
         "config": {"workload": f"{cfg.name}: {cfg.note}; A^G FD apply (D^-1/2 scaled), {cfg.problem} geometry",
                    "d": cfg.d, "p": cfg.p, "n_el": cfg.n_el, "n_dof": n, "dims": P.dims,
-                   "parallelism": (f"time-sharded x{ws} (NCCL all-to-all)" if sharded else
+                   "parallelism": (f"time-sharded x{ws} ({exchange})" if sharded else
                                    ("replicas" if ws > 1 else "single")),
                    "l2": "inputs (136 MB+) larger than L2 (126 MB); no flush"},
         "dof_per_s": value * n,
         "apply_roofline": {"F_alg_flop": f_alg, "t_roof_ms": 1e3 * max(t_roof_flop, t_roof_hbm),
                            "frac": max(t_roof_flop, t_roof_hbm) / (ms * 1e-3), "peak_tflops": peak_dmma,
-                           "bound": "fp64 (DMMA)"},
+                           "bound": "fp64 (DMMA)",
+                           "F_exec_flop": float(sum(flops)),
+                           "frac_exec": float(sum(flops)) / (peak_dmma * 1e12) / (ms * 1e-3),
+                           "note": "F_alg = 4 N (sum n_l + n_t) (PAPER.md:1061-1064, dense mode products); "
+                                   "F_exec = FP64 work the launches execute (a folded centrosymmetric product "
+                                   "does ~half of a dense one, DESIGN.md §5)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s",
                      "frac": achieved / peak_dmma, "traffic": traffic, "kernel": names[dom],
                      "flop_per_launch": flops[dom],
@@ -437,7 +455,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": 8 * r.numel(), "d2h_bytes_per_step": 8 * r.numel(), "ms_per_step": e2e_ms,
                 "pipelining": "H2D / apply / D2H on three streams, two buffer pairs",
                 "serial_value": (1 if sharded else ws) / (e2e_serial_ms * 1e-3)},
-        "gpu_launches": K_steps * (launches + (2 * ws if sharded else 0)),
+        "gpu_launches": K_steps * (launches + (2 * ws if sharded and exchange.startswith("nccl") else 0)),
         "setup_s": setup_s, "pieces_s": pieces_s,
         "gmres": gm,
         "cpu_baseline": cpu,

@@ -122,6 +122,41 @@ int stiga_fd_apply_space(stiga_fd_t P, int backward, long long t0, long long nt_
    eigen-indices starting at global index s0, stored ns_local x n_t colexicographically. */
 int stiga_fd_apply_time(stiga_fd_t P, long long s0, long long ns_local, const double* d_in, double* d_out,
                         void* stream);
+/* Fused exchange: the same two stages, but the last product of the stage stores every
+   output element straight into the receive buffer of the rank that owns it -- the all-to-all
+   transpose of the time-sharded apply fused into the producing kernel's epilogue (NVLink P2P stores
+   through pointers opened with stiga_ipc_open; plain local pointers for virtual ranks).  Replaces
+   pack + all-to-all + unpack; the caller orders the stages across ranks (a barrier after each
+   scatter stage).  Destination of output element (a, b):
+     dst[q] + (a - (by_time ? 0 : offsets[q]) + a_shift) + ld[q] * (b - (by_time ? offsets[q] : 0) + b_shift)
+   space stage (by_time = 0): a = spatial index (0..N_s), b = local time slice; q owns a;
+   time stage  (by_time = 1): a = local spatial index (0..ns_local), b = time slice; q owns b.
+   offsets[0..world] partition the owner coordinate (increasing, offsets[world] = its extent). */
+#define STIGA_MAX_RANKS 8
+#define STIGA_IPC_HANDLE_BYTES 64
+typedef struct stiga_scatter_desc {
+    int world;
+    int by_time;
+    long long offsets[STIGA_MAX_RANKS + 1];
+    long long ld[STIGA_MAX_RANKS];
+    long long a_shift, b_shift;
+    double* dst[STIGA_MAX_RANKS];
+} stiga_scatter_desc;
+/* Forward spatial stage (pre-scale + U_1^T..U_d^T) of time slab [t0, t0+nt_local), scattered. */
+int stiga_fd_apply_space_scatter(stiga_fd_t P, long long t0, long long nt_local, const double* d_in,
+                                 const stiga_scatter_desc* sc, void* stream);
+/* Time stage (U_t^T, arrowhead, U_t) of spatial slab [s0, s0+ns_local), scattered. */
+int stiga_fd_apply_time_scatter(stiga_fd_t P, long long s0, long long ns_local, const double* d_in,
+                                const stiga_scatter_desc* sc, void* stream);
+/* Plain cudaMalloc / cudaFree on `device` (receive buffers that can be shared with CUDA IPC). */
+int stiga_device_alloc(long long bytes, int device, void** d_ptr);
+int stiga_device_free(void* d_ptr);
+/* CUDA IPC: export a cudaMalloc'd base pointer (STIGA_IPC_HANDLE_BYTES opaque bytes), open a peer's
+   handle in this process (peer access enabled lazily), close it. */
+int stiga_ipc_handle(const void* d_ptr, void* handle_out);
+int stiga_ipc_open(const void* handle, int device, void** d_ptr);
+int stiga_ipc_close(void* d_ptr);
+
 /* Strided block copy dst[r*dst_ld + c] = src[r*src_ld + c] (pack/unpack around the all-to-alls). */
 int stiga_copy_blocks(const double* d_src, long long src_ld, double* d_dst, long long dst_ld, long long rows,
                       long long cols, void* stream);

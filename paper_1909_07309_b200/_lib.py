@@ -28,6 +28,16 @@ class GmresReport(ctypes.Structure):
                 ("history_capacity", ctypes.c_int), ("history_len", ctypes.c_int)]
 
 
+MAX_RANKS = 8
+IPC_HANDLE_BYTES = 64
+
+
+class ScatterDesc(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int), ("by_time", ctypes.c_int), ("offsets", ctypes.c_longlong * (MAX_RANKS + 1)),
+                ("ld", ctypes.c_longlong * MAX_RANKS), ("a_shift", ctypes.c_longlong), ("b_shift", ctypes.c_longlong),
+                ("dst", ctypes.c_void_p * MAX_RANKS)]
+
+
 # name -> (restype, argtypes); every symbol of include/stiga_gpu.h
 SIGNATURES = {
     "stiga_last_error": (ctypes.c_char_p, []),
@@ -57,6 +67,13 @@ SIGNATURES = {
     "stiga_fd_launch_info": (_c_int, [_vp, _c_int, ctypes.c_char_p, _c_int, _pd]),
     "stiga_fd_apply_space": (_c_int, [_vp, _c_int, _c_ll, _c_ll, _vp, _vp, _vp]),
     "stiga_fd_apply_time": (_c_int, [_vp, _c_ll, _c_ll, _vp, _vp, _vp]),
+    "stiga_fd_apply_space_scatter": (_c_int, [_vp, _c_ll, _c_ll, _vp, ctypes.POINTER(ScatterDesc), _vp]),
+    "stiga_fd_apply_time_scatter": (_c_int, [_vp, _c_ll, _c_ll, _vp, ctypes.POINTER(ScatterDesc), _vp]),
+    "stiga_device_alloc": (_c_int, [_c_ll, _c_int, ctypes.POINTER(_vp)]),
+    "stiga_device_free": (_c_int, [_vp]),
+    "stiga_ipc_handle": (_c_int, [_vp, ctypes.c_char_p]),
+    "stiga_ipc_open": (_c_int, [ctypes.c_char_p, _c_int, ctypes.POINTER(_vp)]),
+    "stiga_ipc_close": (_c_int, [_vp]),
     "stiga_copy_blocks": (_c_int, [_vp, _c_ll, _vp, _c_ll, _c_ll, _c_ll, _vp]),
     "stiga_kron_matvec": (_c_int, [_c_int, _pi, _pi, _ppd, _vp, _vp, _c_int, _vp]),
     "stiga_kronsum_create": (_c_int, [_c_int, _pi, _c_int, _pd, _ppd, _c_int, ctypes.POINTER(_vp)]),

@@ -136,7 +136,8 @@ struct stiga_fd_s {
     std::vector<gpu::Tiling> tl;        // per spatial direction
     gpu::Tiling tl_t;
     gpu::Tiling tl_ts;                  // mode-kernel tiling of the split time products
-    std::vector<std::unique_ptr<DBuf>> Jt, J;  // padded U_l^T, U_l
+    std::vector<std::unique_ptr<DBuf>> Jt, J;  // padded U_l^T, U_l (device eigen-order)
+    std::vector<std::unique_ptr<DBuf>> Jft, Jfb;  // folded [A_e; A_o] / [A_p; A_q] (split directions)
     DBuf Jt_t, J_t;
     std::vector<std::unique_ptr<DBuf>> lam;
     DBuf S_inv, pair_c, pair_c1, pair_c1sq, pair_gg, g, dinv;
@@ -167,6 +168,23 @@ struct stiga_fd_s {
         return g;
     }
 
+    // One spatial mode product with tiling t: the folded kernel for a folded tiling (split
+    // direction), the dense DMMA kernel otherwise.
+    void mprod(const gpu::Tiling& t, int l, bool backward, const gpu::ModeGeom& g, const double* src, double* dst,
+               const double* post, cudaStream_t st, const double* pre = nullptr, const gpu::Scatter* sc = nullptr) {
+        if (t.fold) {
+            if (pre || sc) throw std::runtime_error("internal: folded product with pre-scale / scatter");
+            ck(gpu::launch_fold_product(t, g, src, dst, backward ? Jfb[l]->p : Jft[l]->p, !backward, post, st),
+               "fd folded mode product");
+        } else {
+            ck(gpu::launch_mode_product(t, g, src, dst, backward ? J[l]->p : Jt[l]->p, post, st, pre, sc),
+               "fd mode product");
+        }
+    }
+    // best dense (unfolded) candidate of direction l (for stages the folded kernel cannot do)
+    std::vector<gpu::Tiling> tl_dense;  // heuristic dense tiling per direction (J / Jt are padded for it)
+    const gpu::Tiling& dense_tiling(int l) const { return tl[l].fold ? tl_dense[l] : tl[l]; }
+
     // Distributed building blocks.
     void apply_space(bool backward, long long t0, long long nt_local, const double* in, double* out, cudaStream_t st) {
         if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
@@ -185,10 +203,8 @@ struct stiga_fd_s {
         }
         for (int l = 0; l < d; ++l) {
             double* dst = next();
-            ck(gpu::launch_mode_product((!backward && l == 0) ? first_tiling() : tl[l], slab_geom(l, nt_local), src,
-                                        dst, backward ? J[l]->p : Jt[l]->p, (backward && l == d - 1) ? dsl : nullptr, st,
-                                        (fused_pre && l == 0) ? dsl : nullptr),
-               "slab mode product");
+            mprod((!backward && l == 0) ? first_tiling() : tl[l], l, backward, slab_geom(l, nt_local), src, dst,
+                  (backward && l == d - 1) ? dsl : nullptr, st, (fused_pre && l == 0) ? dsl : nullptr);
             src = dst;
         }
     }
@@ -203,6 +219,48 @@ struct stiga_fd_s {
             ck(gpu::launch_mode_product(tl_ts, g, scratch2.p, out, J_t.p, nullptr, st), "slab time U_t");
         } else {
             ck(gpu::launch_time_fused(tl_t, g, in, out, Jt_t.p, J_t.p, a2, st), "slab time fused");
+        }
+    }
+
+    // Fused-exchange variants: the last product of the stage stores straight into the
+    // owner ranks' receive buffers through the scatter epilogue, so no pack / all-to-all / unpack.
+    void apply_space_scatter(long long t0, long long nt_local, const double* in, const gpu::Scatter& sc,
+                             cudaStream_t st) {
+        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
+        double* bufs[2] = {scratch.p, scratch2.p};
+        const double* dsl = dinv.p ? dinv.p + n_s * t0 : nullptr;
+        const long long nloc = n_s * nt_local;
+        // the scattering product cannot also pre-scale: with d = 1 the pre-scale runs as its own pass
+        const bool fused_pre = dsl && fused_prescale() && d > 1;
+        const double* src = in;
+        int k = 0;
+        if (dsl && !fused_pre) {
+            ck(gpu::launch_scale(dsl, src, bufs[k % 2], nloc, st), "slab pre-scale");
+            src = bufs[k++ % 2];
+        }
+        for (int l = 0; l < d; ++l) {
+            const bool last = l == d - 1;
+            double* dst = last ? nullptr : bufs[k++ % 2];
+            const gpu::Tiling& t = last ? (l == 0 && fused_pre ? first_tiling() : dense_tiling(l))
+                                        : (l == 0 ? first_tiling() : tl[l]);
+            mprod(t, l, false, slab_geom(l, nt_local), src, dst, nullptr, st, (fused_pre && l == 0) ? dsl : nullptr,
+                  last ? &sc : nullptr);
+            src = dst;
+        }
+    }
+    void apply_time_scatter(long long s0, long long ns_local, const double* in, const gpu::Scatter& sc,
+                            cudaStream_t st) {
+        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
+        gpu::ArrowParams a2 = ap;
+        a2.s_off = s0;
+        const gpu::ModeGeom g = time_geom(ns_local);
+        if (time_split) {
+            ck(gpu::launch_mode_product(tl_ts, g, in, scratch.p, Jt_t.p, nullptr, st), "slab time U_t^T");
+            ck(gpu::launch_arrowhead(scratch.p, scratch2.p, ns_local, a2, st), "slab arrowhead");
+            ck(gpu::launch_mode_product(tl_ts, g, scratch2.p, nullptr, J_t.p, nullptr, st, nullptr, &sc),
+               "slab time U_t (scatter)");
+        } else {
+            ck(gpu::launch_time_fused(tl_t, g, in, nullptr, Jt_t.p, J_t.p, a2, st, &sc), "slab time fused (scatter)");
         }
     }
 
@@ -293,15 +351,17 @@ struct stiga_fd_s {
             tl[l] = cand_space[l].front();
             if (no_tune) continue;
             float best = 1e30f;
-            for (size_t c = 0; c < std::min(kMaxCand, cand_space[l].size()); ++c) {
+            size_t n_fold = 0, n_dense = 0;
+            for (size_t c = 0; c < cand_space[l].size(); ++c) {
                 const gpu::Tiling& t = cand_space[l][c];
+                if ((t.fold ? n_fold : n_dense)++ >= kMaxCand) continue;
                 const float ms = time_once([&] {
-                    ck(gpu::launch_mode_product(t, geom(l), scratch.p, scratch2.p, Jt[l]->p, nullptr, nullptr), "tune");
+                    mprod(t, l, false, geom(l), scratch.p, scratch2.p, nullptr, nullptr);
                 });
                 if (ms < best) { best = ms; tl[l] = t; pick[l] = static_cast<int>(c); }
                 if (debug_tune)
-                    std::fprintf(stderr, "[stiga tune] mode %d MI=%d WN=%d RB=%d occ=%d: %.4f ms\n", l, t.MI, t.WN,
-                                 t.RB, t.ctas_per_sm, ms);
+                    std::fprintf(stderr, "[stiga tune] mode %d %s MI=%d WN=%d RB=%d ns=%d occ=%d: %.4f ms\n", l,
+                                 t.fold ? "folded" : "dense", t.MI, t.WN, t.RB, t.nstage, t.ctas_per_sm, ms);
             }
         }
         use_fused_pre = false;
@@ -310,7 +370,7 @@ struct stiga_fd_s {
         if (!no_tune && dinv.p) {
             const float sep = time_once([&] {
                 ck(gpu::launch_scale(dinv.p, scratch.p, scratch2.p, n_dof, nullptr), "tune");
-                ck(gpu::launch_mode_product(tl[0], geom(0), scratch2.p, scratch.p, Jt[0]->p, nullptr, nullptr), "tune");
+                mprod(tl[0], 0, false, geom(0), scratch2.p, scratch.p, nullptr, nullptr);
             });
             float best_fus = 1e30f;
             for (size_t c = 0; c < std::min(kMaxCand, cand_space[0].size()); ++c) {
@@ -418,9 +478,8 @@ struct stiga_fd_s {
         }
         for (int l = 0; l < d; ++l) {
             double* dst = next();
-            ck(gpu::launch_mode_product(l == 0 ? first_tiling() : tl[l], geom(l), src, dst, Jt[l]->p, nullptr, st,
-                                        (l == 0 && fused_pre) ? dinv.p : nullptr),
-               "fd forward mode product");
+            mprod(l == 0 ? first_tiling() : tl[l], l, false, geom(l), src, dst, nullptr, st,
+                  (l == 0 && fused_pre) ? dinv.p : nullptr);
             src = dst;
         }
         if (time_split) {
@@ -440,8 +499,7 @@ struct stiga_fd_s {
         }
         for (int l = 0; l < d; ++l) {
             double* dst = next();
-            ck(gpu::launch_mode_product(tl[l], geom(l), src, dst, J[l]->p, (l == d - 1 && scaled) ? dinv.p : nullptr, st),
-               "fd backward mode product");
+            mprod(tl[l], l, true, geom(l), src, dst, (l == d - 1 && scaled) ? dinv.p : nullptr, st);
             src = dst;
         }
         if (ev) ck(cudaEventRecord((*ev)[e], st), "event");
@@ -574,7 +632,7 @@ extern "C" {
 
 const char* stiga_last_error(void) { return g_last_error.c_str(); }
 
-int stiga_abi_version(void) { return 100; }
+int stiga_abi_version(void) { return 101; }
 
 int stiga_device_count(void) {
     int n = 0;
@@ -727,17 +785,40 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
 
         DeviceGuard dg(device);
         for (int l = 0; l < d; ++l) {
-            h->cand_space.push_back(gpu::mode_tiling_candidates(F.n[l], F.n[l]));
-            if (h->cand_space.back().empty()) throw std::runtime_error("internal: no mode-product tiling");
-            h->tl.push_back(h->cand_space.back().front());
+            std::vector<gpu::Tiling> dense = gpu::mode_tiling_candidates(F.n[l], F.n[l]);
+            if (dense.empty()) throw std::runtime_error("internal: no mode-product tiling");
             int rows = 0;
-            for (const auto& t : h->cand_space.back()) rows = std::max(rows, t.Mp);
+            for (const auto& t : dense) rows = std::max(rows, t.Mp);
+            const DenseMatrix Ud = F.U_dev(l);  // device eigen-order (folded order for a split direction)
             h->Jt.emplace_back(new DBuf);
             h->J.emplace_back(new DBuf);
-            h->Jt.back()->upload(pad_factor(F.U[l], true, rows, h->tl.back().Kp));
-            h->J.back()->upload(pad_factor(F.U[l], false, rows, h->tl.back().Kp));
+            h->Jt.back()->upload(pad_factor(Ud, true, rows, dense.front().Kp));
+            h->J.back()->upload(pad_factor(Ud, false, rows, dense.front().Kp));
+            h->Jft.emplace_back(new DBuf);
+            h->Jfb.emplace_back(new DBuf);
+            std::vector<gpu::Tiling> cands;
+            // STIGA_FOLD_KERNEL=off: dense kernels only; =force: folded kernels only (split directions);
+            // unset: both kinds are candidates of the setup-time autotuner
+            const char* fk = std::getenv("STIGA_FOLD_KERNEL");
+            const bool dense_only = fk && std::string(fk) == "off";
+            const bool fold_only = fk && std::string(fk) == "force";
+            if (F.fold[l].on && !dense_only) {  // folded candidates first (half the FLOPs)
+                std::vector<gpu::Tiling> fc = gpu::fold_tiling_candidates(F.n[l]);
+                int frows = 0;
+                for (const auto& t : fc) frows = std::max(frows, t.Mp);
+                for (auto& t : fc) t.Mp = frows;  // both matrices padded to the largest row-block cover
+                if (!fc.empty()) {
+                    h->Jft.back()->upload(fold_matrices(F.fold[l], true, frows, fc.front().Kp));
+                    h->Jfb.back()->upload(fold_matrices(F.fold[l], false, frows, fc.front().Kp));
+                }
+                cands = fc;
+            }
+            if (!(fold_only && !cands.empty())) cands.insert(cands.end(), dense.begin(), dense.end());
+            h->cand_space.push_back(cands);
+            h->tl_dense.push_back(dense.front());
+            h->tl.push_back(cands.front());
             h->lam.emplace_back(new DBuf);
-            h->lam.back()->upload(F.lambda[l]);
+            h->lam.back()->upload(F.lambda_dev(l));
         }
         h->cand_time = gpu::time_tiling_candidates(F.n_t);
         h->cand_ts = gpu::mode_tiling_candidates(F.n_t, F.n_t);
@@ -748,7 +829,7 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         const int tKp = h->cand_ts.front().Kp;
         h->Jt_t.upload(pad_factor(F.time.U, true, trows, tKp));
         h->J_t.upload(pad_factor(F.time.U, false, trows, tKp));
-        h->S_inv.upload(F.S_inv);
+        h->S_inv.upload(F.S_inv_dev());
         std::vector<double> pc, pc1, pc1sq, pgg;
         for (size_t j = 0; j < F.time.lambda.size(); ++j) {
             const double lam = F.time.lambda[j];
@@ -905,6 +986,101 @@ int stiga_fd_apply_time(stiga_fd_t P, long long s0, long long ns_local, const do
     });
 }
 
+namespace {
+// Validates a C-ABI scatter descriptor against the stage it feeds and converts it.
+gpu::Scatter to_scatter(const stiga_scatter_desc* d, bool by_time, long long a_extent, long long b_extent,
+                        const char* who) {
+    const std::string w(who);
+    require(d != nullptr, (w + ": null scatter descriptor").c_str());
+    require(d->world >= 1 && d->world <= STIGA_MAX_RANKS, (w + ": world must be 1..STIGA_MAX_RANKS").c_str());
+    require((d->by_time != 0) == by_time, (w + ": scatter descriptor has the wrong owner coordinate").c_str());
+    gpu::Scatter sc;
+    sc.G = d->world;
+    sc.by_time = by_time ? 1 : 0;
+    sc.a_shift = d->a_shift;
+    sc.b_shift = d->b_shift;
+    require(d->offsets[0] == 0 && d->offsets[d->world] == (by_time ? b_extent : a_extent),
+            (w + ": partition offsets must cover the owner coordinate exactly").c_str());
+    for (int q = 0; q <= d->world; ++q) sc.off[q] = d->offsets[q];
+    for (int q = 0; q < d->world; ++q) {
+        require(d->offsets[q + 1] > d->offsets[q], (w + ": partition offsets must be increasing").c_str());
+        require(d->dst[q] != nullptr && d->ld[q] >= 1, (w + ": null destination or bad leading dimension").c_str());
+        require(d->a_shift >= 0 && d->b_shift >= 0, (w + ": negative shift").c_str());
+        sc.ld[q] = d->ld[q];
+        sc.ptr[q] = d->dst[q];
+    }
+    return sc;
+}
+}  // namespace
+
+int stiga_fd_apply_space_scatter(stiga_fd_t P, long long t0, long long nt_local, const double* d_in,
+                                 const stiga_scatter_desc* sc, void* stream) {
+    return guarded([&] {
+        require(P && d_in, "stiga_fd_apply_space_scatter: null argument");
+        require(P->device >= 0, "stiga_fd_apply_space_scatter: host-only handle");
+        require(t0 >= 0 && nt_local >= 1 && t0 + nt_local <= P->dims[P->d],
+                "stiga_fd_apply_space_scatter: time slab out of range");
+        const gpu::Scatter s = to_scatter(sc, false, P->n_s, nt_local, "stiga_fd_apply_space_scatter");
+        DeviceGuard dg(P->device);
+        P->apply_space_scatter(t0, nt_local, d_in, s, as_stream(stream));
+    });
+}
+
+int stiga_fd_apply_time_scatter(stiga_fd_t P, long long s0, long long ns_local, const double* d_in,
+                                const stiga_scatter_desc* sc, void* stream) {
+    return guarded([&] {
+        require(P && d_in, "stiga_fd_apply_time_scatter: null argument");
+        require(P->device >= 0, "stiga_fd_apply_time_scatter: host-only handle");
+        require(s0 >= 0 && ns_local >= 1 && s0 + ns_local <= P->n_s,
+                "stiga_fd_apply_time_scatter: spatial slab out of range");
+        const gpu::Scatter s = to_scatter(sc, true, ns_local, P->dims[P->d], "stiga_fd_apply_time_scatter");
+        DeviceGuard dg(P->device);
+        P->apply_time_scatter(s0, ns_local, d_in, s, as_stream(stream));
+    });
+}
+
+int stiga_device_alloc(long long bytes, int device, void** d_ptr) {
+    return guarded([&] {
+        require(d_ptr != nullptr && bytes >= 0, "stiga_device_alloc: bad argument");
+        *d_ptr = nullptr;
+        DeviceGuard dg(device);
+        if (bytes) ck(cudaMalloc(d_ptr, static_cast<size_t>(bytes)), "cudaMalloc");
+    });
+}
+
+int stiga_device_free(void* d_ptr) {
+    return guarded([&] {
+        if (d_ptr) ck(cudaFree(d_ptr), "cudaFree");
+    });
+}
+
+int stiga_ipc_handle(const void* d_ptr, void* handle_out) {
+    return guarded([&] {
+        require(d_ptr && handle_out, "stiga_ipc_handle: null argument");
+        static_assert(sizeof(cudaIpcMemHandle_t) == STIGA_IPC_HANDLE_BYTES, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)), "cudaIpcGetMemHandle");
+        std::memcpy(handle_out, &h, sizeof(h));
+    });
+}
+
+int stiga_ipc_open(const void* handle, int device, void** d_ptr) {
+    return guarded([&] {
+        require(handle && d_ptr, "stiga_ipc_open: null argument");
+        DeviceGuard dg(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        ck(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+int stiga_ipc_close(void* d_ptr) {
+    return guarded([&] {
+        require(d_ptr != nullptr, "stiga_ipc_close: null argument");
+        ck(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle");
+    });
+}
+
 int stiga_copy_blocks(const double* d_src, long long src_ld, double* d_dst, long long dst_ld, long long rows,
                       long long cols, void* stream) {
     return guarded([&] {
@@ -921,9 +1097,17 @@ int stiga_fd_launch_info(stiga_fd_t P, int i, char* name, int name_len, double* 
         std::vector<std::pair<std::string, double>> L;
         const double N = static_cast<double>(P->n_dof);
         if (P->dinv.p && !P->fused_prescale()) L.emplace_back("pre_scale", 0.0);
-        for (int l = 0; l < P->d; ++l)
-            L.emplace_back("fwd_mode" + std::to_string(l) + (l == 0 && P->fused_prescale() ? "+pre_scale" : ""),
-                           2.0 * P->dims[l] * N);
+        // executed FP64 work: 2 n N per dense product, 4 F^2 N / n per folded one (F = ceil(n/2))
+        auto prod_flops = [&](const gpu::Tiling& t, int l) {
+            const double n = P->dims[l], Fh = n - std::floor(n / 2);
+            return t.fold ? 4.0 * Fh * Fh * N / n : 2.0 * n * N;
+        };
+        auto tag = [](const gpu::Tiling& t) { return t.fold ? std::string("(folded)") : std::string(); };
+        for (int l = 0; l < P->d; ++l) {
+            const gpu::Tiling& t = l == 0 ? P->first_tiling() : P->tl[l];
+            L.emplace_back("fwd_mode" + std::to_string(l) + tag(t) + (l == 0 && P->fused_prescale() ? "+pre_scale" : ""),
+                           prod_flops(t, l));
+        }
         const double nt = P->dims[P->d];
         if (P->time_split) {
             L.emplace_back("time_UtT", 2.0 * nt * N);
@@ -933,8 +1117,9 @@ int stiga_fd_launch_info(stiga_fd_t P, int i, char* name, int name_len, double* 
             L.emplace_back("time_fused", 4.0 * nt * N);
         }
         for (int l = 0; l < P->d; ++l)
-            L.emplace_back("bwd_mode" + std::to_string(l) + (l == P->d - 1 && P->dinv.p ? "+post_scale" : ""),
-                           2.0 * P->dims[l] * N);
+            L.emplace_back("bwd_mode" + std::to_string(l) + tag(P->tl[l]) +
+                               (l == P->d - 1 && P->dinv.p ? "+post_scale" : ""),
+                           prod_flops(P->tl[l], l));
         std::snprintf(name, static_cast<size_t>(name_len), "%s", L[i].first.c_str());
         *flops = L[i].second;
     });

@@ -303,6 +303,32 @@ __global__ void axpy_kernel(double alpha, const double* __restrict__ x, double* 
         y[i] += alpha * x[i];
 }
 
+// One modified Gram-Schmidt step with the coefficient left on the device: w -= h * v, then the
+// block partials of dot(vn, w_new) (vn == nullptr: ||w_new||^2).  Same grid and summation order as
+// dot_partial_kernel and the same DFMA as axpy_kernel, so the result is bit-identical to
+// dot -> axpy -> dot, with one pass over w instead of three and no host round trip for h.
+__global__ void axpy_dot_partial_kernel(const double* __restrict__ h, const double* __restrict__ v,
+                                        double* __restrict__ w, const double* __restrict__ vn, long long n,
+                                        double* __restrict__ partials) {
+    __shared__ double ws[32];
+    const double alpha = -*h;
+    double s = 0.0;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double wi = w[i] + alpha * v[i];
+        w[i] = wi;
+        s += (vn ? vn[i] : wi) * wi;
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double u = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+        u = warp_sum(u);
+        if (threadIdx.x == 0) partials[blockIdx.x] = u;
+    }
+}
+
 __global__ void scal_kernel(double alpha, const double* __restrict__ x, double* __restrict__ y, long long n) {
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -448,6 +474,13 @@ int dot_partials_size() { return kDotBlocks; }
 cudaError_t launch_dot(const double* x, const double* y, long long n, double* d_partials, double* d_result,
                        cudaStream_t st) {
     dot_partial_kernel<<<kDotBlocks, kThreads, 0, st>>>(x, y, n, d_partials);
+    dot_finish_kernel<<<1, 1024, 0, st>>>(d_partials, kDotBlocks, d_result);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_axpy_dot(const double* d_h, const double* v, double* w, const double* vn, long long n,
+                            double* d_partials, double* d_result, cudaStream_t st) {
+    axpy_dot_partial_kernel<<<kDotBlocks, kThreads, 0, st>>>(d_h, v, w, vn, n, d_partials);
     dot_finish_kernel<<<1, 1024, 0, st>>>(d_partials, kDotBlocks, d_result);
     return cudaGetLastError();
 }

@@ -30,6 +30,10 @@ cudaError_t launch_time_band_slab(long long Ns, int nt, long long t0, long long 
 cudaError_t launch_dot(const double* x, const double* y, long long n, double* d_partials, double* d_result,
                        cudaStream_t st);
 int dot_partials_size();
+/// MGS step: w -= (*d_h) * v, then *d_result = dot(vn, w) (vn == nullptr: dot(w, w)); bit-identical
+/// to launch_axpy(-h) followed by launch_dot.
+cudaError_t launch_axpy_dot(const double* d_h, const double* v, double* w, const double* vn, long long n,
+                            double* d_partials, double* d_result, cudaStream_t st);
 /// y = y + alpha x
 cudaError_t launch_axpy(double alpha, const double* x, double* y, long long n, cudaStream_t st);
 /// y = alpha x

@@ -45,6 +45,25 @@ struct ModeGeom {
     int m = 0;            // output mode size (rows of J; == n for the square FD factors)
 };
 
+/// Peer-memory scatter epilogue of the time-sharded apply: instead of storing to the
+/// local output, the kernel stores every output element straight into the receive buffer of the
+/// rank that owns it (NVLink P2P stores through pointers opened with CUDA IPC; local pointers for
+/// virtual ranks), which fuses the all-to-all transpose into the producing product.
+///   forward (by_time = 0, last spatial mode of a time slab): a = spatial index l + L*i, b = local
+///     time slice r; owner q = the rank whose spatial range [off[q], off[q+1]) holds a;
+///   backward (by_time = 1, time mode of a spatial slab): a = local spatial index l, b = time slice
+///     i; owner q = the rank whose time range holds b.
+/// Destination: ptr[q] + (a - (by_time ? 0 : off[q]) + a_shift) + ld[q] * (b - (by_time ? off[q] : 0) + b_shift).
+constexpr int kMaxRanks = 8;
+struct Scatter {
+    int G = 0;        // ranks (1..kMaxRanks)
+    int by_time = 0;  // owner coordinate: 0 = a (spatial), 1 = b (time)
+    long long off[kMaxRanks + 1] = {};
+    long long ld[kMaxRanks] = {};
+    long long a_shift = 0, b_shift = 0;
+    double* ptr[kMaxRanks] = {};
+};
+
 /// Kernel tiling chosen on the host (choose_mode_tiling / choose_time_tiling).
 /// One CTA computes MI*WM*8 rows (a "row block") x BN fibers; warps are WM x WN, each owning
 /// MI 8-row strips x NI 8-fiber tiles.  J is streamed in 16-column chunks through `nstage`
@@ -60,6 +79,7 @@ struct Tiling {
     int LDX = 68;     // smem row stride of a fiber chunk (== 4 mod 16 doubles)
     int Zrows = 0;    // time kernel: rows of the resident Z tile (= Kp)
     int nstage = 3;
+    int fold = 0;     // 1: folded (centrosymmetric) product, fold_kernels.cu; MI/RB/Mp/Kp refer to the folded matrices
     size_t smem = 0;
     int ctas_per_sm = 1;
     int threads() const { return 32 * WM * WN; }
@@ -75,12 +95,22 @@ std::vector<Tiling> time_tiling_candidates(int n_t);
 /// post_scale (optional) multiplies Y elementwise in the register epilogue (the D^-1/2 post-scale).
 /// pre_scale (optional) multiplies X elementwise before the product (the D^-1/2 pre-scale, staged
 /// beside each fiber chunk); needs prescale_fits(t).
+/// sc (optional): scatter the output to the owners' receive buffers instead of Y (Y unused; no
+/// pre/post scale).
 cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y,
                                 const double* Jpad, const double* post_scale, cudaStream_t stream,
-                                const double* pre_scale = nullptr);
+                                const double* pre_scale = nullptr, const Scatter* sc = nullptr);
 /// Dynamic smem of the pre-scaled mode kernel for tiling t, and whether it fits one CTA.
 size_t prescale_smem(const Tiling& t);
 bool prescale_fits(const Tiling& t);
+
+/// Folded mode products of a centrosymmetric direction (fold_kernels.cu): half the FLOPs of the
+/// dense product.  Jfold holds the two folded matrices, each row-major zero-padded t.Mp x t.Kp,
+/// the second at offset t.Mp*t.Kp: forward (U^T) [A_e; A_o], backward (U) [A_p; A_q].
+/// post_scale (backward only) multiplies the outputs elementwise.
+std::vector<Tiling> fold_tiling_candidates(int n);
+cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
+                                bool forward, const double* post_scale, cudaStream_t stream);
 
 /// Standalone block-arrowhead solve X = (gamma Delta_t (x) I + nu I (x) Lambda_s)^-1 Z on the
 /// time-eigen-coordinate tensor (N_s x n_t, time slowest); used when the time direction runs as
@@ -91,7 +121,7 @@ cudaError_t launch_arrowhead(const double* Z, double* X, long long Ns, const Arr
 /// Jt_pad = U_t^T padded, J_pad = U_t padded (both row-major Mp x Kp).
 cudaError_t launch_time_fused(const Tiling& t, const ModeGeom& g, const double* X, double* Y,
                               const double* Jt_pad, const double* J_pad, const ArrowParams& ap,
-                              cudaStream_t stream);
+                              cudaStream_t stream, const Scatter* sc = nullptr);
 
 /// dst[r*dld + c] = src[r*sld + c] for r < rows, c < cols (pack/unpack of the sharded transposes).
 cudaError_t launch_copy_blocks(const double* src, long long sld, double* dst, long long dld, long long rows,

@@ -1,0 +1,88 @@
+// Time direction of the FD apply: the time-fused kernel (fd_time_impl.cuh), its tiling candidates
+// and launcher.
+#include "fd_time_impl.cuh"
+
+namespace stiga {
+namespace gpu {
+
+namespace {
+
+cudaError_t dispatch_time(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jt,
+                          const double* J, const ArrowParams& ap, cudaStream_t st, int* occ,
+                          const Scatter* sc = nullptr) {
+    if (sc) return dispatch_time_scatter(t, g, X, Jt, J, ap, st, occ, sc);
+    return dispatch_time_v<false>(t, g, X, Y, Jt, J, ap, st, occ, nullptr);
+}
+
+}  // namespace
+
+std::vector<Tiling> time_tiling_candidates(int nt) {
+    std::vector<std::pair<double, Tiling>> c;
+    int force_wm = 0, force_wn = 0, force_ns = 0;  // debugging aid: STIGA_FORCE_TIME_TILING="WM,WN,NS"
+    if (const char* f = std::getenv("STIGA_FORCE_TIME_TILING"))
+        std::sscanf(f, "%d,%d,%d", &force_wm, &force_wn, &force_ns);
+    const int S = (nt + 7) / 8;
+    const int Kp = (nt + 3) / 4 * 4;
+    for (int WM : {1, 2, 4}) {
+        const int MI = (S + WM - 1) / WM;
+        if (MI > 13 || MI < 1) continue;
+        for (int WN : {4, 2}) {
+            if (WM == 4 && WN == 4) continue;
+            if ((force_wm && WM != force_wm) || (force_wn && WN != force_wn)) continue;
+            for (int ns : {3, 2}) {
+                if (force_ns && ns != force_ns) continue;
+                Tiling t;
+                t.MI = MI;
+                t.WM = WM;
+                t.NI = 2;
+                t.WN = WN;
+                t.S = S;
+                t.RB = 1;
+                t.MpB = 8 * MI * WM;
+                t.Mp = t.MpB;
+                t.Kp = Kp;
+                t.BN = 16 * WN;
+                t.LDX = t.BN + 4;
+                t.Zrows = Kp;
+                t.nstage = ns;
+                t.smem = sizeof(double) * (static_cast<size_t>(Kp) * t.LDX +
+                                           static_cast<size_t>(ns) * (kBK * t.LDX + t.MpB * kLDJ) +
+                                           7 * static_cast<size_t>(nt / 2 + 1) + 3 * static_cast<size_t>(t.BN));
+                if (t.smem > kSmemPerCTA) continue;
+                int occ = 0;
+                ArrowParams ap;
+                dispatch_time(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, ap, nullptr, &occ);
+                t.ctas_per_sm = occ;
+                if (occ < 1) continue;
+                const double eff = 0.85 + 0.15 * static_cast<double>(S) / (WM * MI);
+                c.emplace_back(std::min(occ * WM * WN, 16) * eff + 0.01 * ns + 0.02 * WN, t);
+            }
+        }
+    }
+    std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<Tiling> out;
+    for (auto& e : c) out.push_back(e.second);
+    return out;
+}
+
+Tiling choose_time_tiling(int nt) {
+    const std::vector<Tiling> c = time_tiling_candidates(nt);
+    if (c.empty()) {
+        Tiling t;
+        t.MI = 0;
+        return t;
+    }
+    return c.front();
+}
+
+
+cudaError_t launch_time_fused(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jt_pad,
+                              const double* J_pad, const ArrowParams& ap, cudaStream_t st, const Scatter* sc) {
+    if (g.ncols <= 0) return cudaSuccess;
+    if (sc && (sc->G < 1 || sc->G > kMaxRanks)) return cudaErrorInvalidValue;
+    return dispatch_time(t, g, X, Y, Jt_pad, J_pad, ap, st, nullptr, sc);
+}
+
+
+}  // namespace gpu
+}  // namespace stiga

@@ -1,0 +1,406 @@
+// Folded (centrosymmetric) mode products: half the FP64 work of a dense mode product.
+//
+// On uniform open knots with both spatial end functions dropped and constant coefficients (the
+// identity-geometry configs c1, c2, c3, c5) the 1D pencil (K_l, M_l) is centrosymmetric,
+// J K_l J = K_l and J M_l J = M_l with J the exchange matrix.  Its eigenvectors then split into
+// symmetric and skew ones (host/fdsetup.cpp builds them that way): with n = 2h + o (o = n mod 2) and
+// F = h + o,
+//   U = Q blockdiag(W_e, W_o),   Q^T x = [ (x_top + J x_bot)/sqrt2 ; x_mid (o = 1) ; (x_top - J x_bot)/sqrt2 ],
+// so the forward product y = U^T x of a fiber is
+//   y[r]     = sum_k A_e[r][k] (x[k] + x[n-1-k])   r < F    (A_e = W_e^T / sqrt2, middle column / 2)
+//   y[F + r] = sum_k A_o[r][k] (x[k] - x[n-1-k])   r < h    (A_o = W_o^T / sqrt2)
+// and the backward product x = U y is
+//   p[i] = sum_c A_p[i][c] y[c],  q[i] = sum_c A_q[i][c] y[F + c],
+//   x[i] = p[i] + q[i],  x[n-1-i] = p[i] - q[i]  (i < h),  x[h] = p[h] (o = 1).
+// Two F x F products instead of one n x n product: 2 F^2 ~ n^2 / 2 multiply-adds per fiber.
+//
+// Kernel structure follows mode_product_kernel (fd_kernels.cu): a CTA owns a row block of both
+// folded matrices (MI 8-row strips each) and BN = 16 WN fibers; two 16-row fiber chunks (forward:
+// rows k0.. and the mirrored rows n-k0-16..; backward: rows k0.. and F+k0..) and the two matrix
+// chunks stream through a cp.async pipeline; the fold (x_k +- x_{n-1-k}) is formed while the
+// B fragments are read from shared memory; DMMA.8x8x4 on the FP64 tensor cores; register epilogue.
+#include "fd_kernels.cuh"
+
+#include <algorithm>
+#include <utility>
+#include <vector>
+
+namespace stiga {
+namespace gpu {
+
+namespace {
+
+constexpr int kBK = 16;
+constexpr int kLDJ = kBK + 4;  // == 4 mod 16 doubles: conflict-free A fragments
+constexpr size_t kSmemPerSM = 228 * 1024;
+constexpr size_t kSmemPerCTA = 227 * 1024;
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp8z(unsigned s, const double* g, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g), "r"(valid ? 8 : 0));
+}
+
+__device__ __forceinline__ void cp16(unsigned s, const double* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
+}
+
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void wait_n() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+struct FArgs {
+    ModeGeom geo;
+    int F, h;      // folded length F = h + (n mod 2), h = n / 2
+    int Kp;        // round4(F): padded contraction of both folded matrices
+    int RB, nstage;
+    int S;         // live 8-row strips of the first matrix (ceil(F / 8))
+    long long A2;  // offset (doubles) of the second folded matrix after the first (Mp * Kp)
+};
+
+template <int MI_, int WN_>
+struct FShape {
+    static constexpr int MI = MI_, WN = WN_, NI = 2;
+    static constexpr int NTHR = 32 * WN;
+    static constexpr int BN = 16 * WN;
+    static constexpr int LDX = BN + 4;
+    static constexpr int MPB = 8 * MI;
+    static constexpr int XCNT = kBK * BN / NTHR;  // fiber-chunk elements per thread and chunk (= 8)
+    static constexpr int JPIECES = MPB * (kBK / 2);
+    static constexpr int JROWSTEP = NTHR / 8;
+    static constexpr int JCNT = (JPIECES + NTHR - 1) / NTHR;
+    static constexpr int XROWSTEP = NTHR / BN;  // L > 1: chunk rows between a thread's elements
+    static constexpr int XCOLSTEP = NTHR / 16;  // L == 1: fibers between a thread's elements
+    // stage: Xa (16 x LDX), Xb (16 x LDX), J1 (MPB x LDJ), J2 (MPB x LDJ)
+    static constexpr int XB = kBK * LDX;
+    static constexpr int J1 = 2 * kBK * LDX;
+    static constexpr int J2 = J1 + MPB * kLDJ;
+    static constexpr int STAGE = J2 + MPB * kLDJ;
+};
+
+__device__ __forceinline__ long long fbase(long long cc, long long L, int n) {
+    if (L == 1) return cc * n;
+    const long long r = cc / L;
+    return (cc - r * L) + L * static_cast<long long>(n) * r;
+}
+
+// Per-thread loader state: element u of a chunk is fiber fc[u] (global base fb[u]), chunk row jr[u].
+template <class SH>
+struct FProd {
+    long long fb[SH::XCNT];  // global offset of element 0 of the element's fiber (valid fibers)
+    unsigned xs[SH::XCNT];   // smem byte offset within a stage (Xa; Xb adds XB)
+    int jr[SH::XCNT];        // chunk row 0..15
+    unsigned fmask;          // fiber inside the tensor
+    const double* jg;        // J1 row piece for chunk 0
+    unsigned js;
+    int jp2;
+};
+
+template <class SH>
+__device__ __forceinline__ FProd<SH> make_fprod(const FArgs& a, long long c0, const double* Jg) {
+    FProd<SH> p;
+    const int tid = threadIdx.x;
+    p.fmask = 0;
+#pragma unroll
+    for (int u = 0; u < SH::XCNT; ++u) {
+        int c, j;
+        if (a.geo.L == 1) {
+            j = tid & (kBK - 1);
+            c = (tid >> 4) + u * SH::XCOLSTEP;
+        } else {
+            c = tid & (SH::BN - 1);
+            j = tid / SH::BN + u * SH::XROWSTEP;
+        }
+        const long long cc = c0 + c;
+        const bool v = cc < a.geo.ncols;
+        if (v) p.fmask |= 1u << u;
+        p.fb[u] = fbase(v ? cc : 0, a.geo.L, a.geo.n);
+        p.jr[u] = j;
+        p.xs[u] = 8u * (j * SH::LDX + c);
+    }
+    p.jp2 = 2 * (tid & 7);
+    p.js = 8u * ((tid >> 3) * kLDJ + p.jp2);
+    p.jg = Jg + static_cast<size_t>(tid >> 3) * a.Kp + p.jp2;
+    return p;
+}
+
+// Chunk q: matrix columns [16q, 16q+16) of both folded matrices; fiber rows ra0 + r (Xa) and
+// rb0 + r (Xb), r = 0..15, zero-filled outside [0, n).
+template <class SH, bool FWD>
+__device__ __forceinline__ void fissue(const FArgs& a, const FProd<SH>& p, unsigned st, int q, const double* X,
+                                       const double* J) {
+    const int k0 = q * kBK;
+    const int kw = min(kBK, a.Kp - k0);
+    if (p.jp2 < kw) {
+#pragma unroll
+        for (int u = 0; u < SH::JCNT; ++u) {
+            if ((u + 1) * SH::NTHR <= SH::JPIECES || (threadIdx.x >> 3) + u * SH::JROWSTEP < SH::MPB) {
+                const double* g = p.jg + k0 + static_cast<size_t>(u) * SH::JROWSTEP * a.Kp;
+                const unsigned s = st + p.js + 8u * u * SH::JROWSTEP * kLDJ;
+                cp16(s + 8u * SH::J1, g);
+                cp16(s + 8u * SH::J2, g + a.A2);
+            }
+        }
+    }
+    const int n = a.geo.n;
+    const long long L = a.geo.L;
+    const int ra0 = k0, rb0 = FWD ? n - k0 - kBK : a.F + k0;
+#pragma unroll
+    for (int u = 0; u < SH::XCNT; ++u) {
+        const bool fv = (p.fmask >> u) & 1u;
+        const int ra = ra0 + p.jr[u], rb = rb0 + p.jr[u];
+        const bool va = fv && ra < n, vb = fv && rb >= 0 && rb < n;
+        cp8z(st + p.xs[u], va ? X + p.fb[u] + L * ra : X, va);
+        cp8z(st + 8u * SH::XB + p.xs[u], vb ? X + p.fb[u] + L * rb : X, vb);
+    }
+}
+
+template <class SH, bool FWD, int KS>
+__device__ __forceinline__ void fmma(const double* ja, const double* xa, const double* xb, int mact,
+                                     double (&c1)[SH::MI][SH::NI][2], double (&c2)[SH::MI][SH::NI][2]) {
+    constexpr int MI = SH::MI, NI = SH::NI;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+        double a1[MI], a2[MI], b1[NI], b2[NI];
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+            a1[mi] = mi < mact ? ja[mi * 8 * kLDJ + kk * 4] : 0.0;
+            a2[mi] = mi < mact ? ja[(SH::J2 - SH::J1) + mi * 8 * kLDJ + kk * 4] : 0.0;
+        }
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+            const double u = xa[kk * 4 * SH::LDX + ni * 8];
+            if (FWD) {  // xb points at mirrored row 15 - t; rows run backwards
+                const double w = xb[-kk * 4 * SH::LDX + ni * 8];
+                b1[ni] = u + w;
+                b2[ni] = u - w;
+            } else {
+                b1[ni] = u;
+                b2[ni] = xb[kk * 4 * SH::LDX + ni * 8];
+            }
+        }
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+                if (mi < mact) {
+                    dmma(c1[mi][ni][0], c1[mi][ni][1], a1[mi], b1[ni]);
+                    dmma(c2[mi][ni][0], c2[mi][ni][1], a2[mi], b2[ni]);
+                }
+    }
+}
+
+template <int MI, int WN, bool FWD>
+__global__ void __launch_bounds__(32 * WN)
+    fold_mode_kernel(FArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
+                     const double* __restrict__ post) {
+    using SH = FShape<MI, WN>;
+    extern __shared__ __align__(16) double smem[];
+    const int rb = blockIdx.x % a.RB;
+    const long long c0 = static_cast<long long>(blockIdx.x / a.RB) * SH::BN;
+    const int strip0 = rb * MI;
+    const FProd<SH> p = make_fprod<SH>(a, c0, J + static_cast<size_t>(rb) * SH::MPB * a.Kp);
+    double c1[MI][SH::NI][2], c2[MI][SH::NI][2];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < SH::NI; ++ni) c1[mi][ni][0] = c1[mi][ni][1] = c2[mi][ni][0] = c2[mi][ni][1] = 0.0;
+
+    const int nchunks = (a.Kp + kBK - 1) / kBK;
+    const int ns = a.nstage;
+    const int lane = threadIdx.x & 31, wn = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int mact = min(MI, max(0, a.S - strip0));
+    const unsigned st0 = smem_u32(smem);
+    for (int s = 0; s < ns - 1; ++s) {
+        if (s < nchunks) fissue<SH, FWD>(a, p, st0 + 8u * s * SH::STAGE, s, X, J);
+        commit();
+    }
+    const int ja_off = SH::J1 + g * kLDJ + t;
+    const int xa_off = t * SH::LDX + wn * SH::NI * 8 + g;
+    const int xb_off = SH::XB + (FWD ? (kBK - 1 - t) : t) * SH::LDX + wn * SH::NI * 8 + g;
+    int stage = 0;
+    for (int q = 0; q < nchunks; ++q) {
+        if (ns >= 3) wait_n<1>();
+        else wait_n<0>();
+        __syncthreads();
+        const int nq = q + ns - 1;
+        if (nq < nchunks) {
+            int nst = stage + ns - 1;
+            if (nst >= ns) nst -= ns;
+            fissue<SH, FWD>(a, p, st0 + 8u * nst * SH::STAGE, nq, X, J);
+        }
+        commit();
+        const double* sb = smem + stage * SH::STAGE;
+        const int ks = min(kBK, a.Kp - q * kBK) >> 2;
+        if (ks == 4) fmma<SH, FWD, 4>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
+        else if (ks == 3) fmma<SH, FWD, 3>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
+        else if (ks == 2) fmma<SH, FWD, 2>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
+        else fmma<SH, FWD, 1>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
+        if (++stage == ns) stage = 0;
+    }
+
+    // register epilogue
+    const int n = a.geo.n;
+    const long long L = a.geo.L;
+    long long ob[SH::NI][2];
+    bool cv[SH::NI][2];
+#pragma unroll
+    for (int ni = 0; ni < SH::NI; ++ni)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const long long cc = c0 + (wn * SH::NI + ni) * 8 + 2 * t + v;
+            cv[ni][v] = cc < a.geo.ncols;
+            ob[ni][v] = fbase(cv[ni][v] ? cc : 0, L, n);
+        }
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+        const int i = (strip0 + mi) * 8 + g;
+#pragma unroll
+        for (int ni = 0; ni < SH::NI; ++ni)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                if (!cv[ni][v]) continue;
+                double* y = Y + ob[ni][v];
+                const double* ps = post ? post + ob[ni][v] : nullptr;
+                if (FWD) {
+                    if (i < a.F) y[L * i] = c1[mi][ni][v];
+                    if (i < a.h) y[L * (a.F + i)] = c2[mi][ni][v];
+                } else if (i < a.h) {
+                    const long long lo = L * i, hi = L * (n - 1 - i);
+                    const double s1 = c1[mi][ni][v] + c2[mi][ni][v], s2 = c1[mi][ni][v] - c2[mi][ni][v];
+                    y[lo] = ps ? __ldg(ps + lo) * s1 : s1;
+                    y[hi] = ps ? __ldg(ps + hi) * s2 : s2;
+                } else if (i < a.F) {  // middle row (odd n)
+                    const long long mid = L * i;
+                    y[mid] = ps ? __ldg(ps + mid) * c1[mi][ni][v] : c1[mi][ni][v];
+                }
+            }
+    }
+}
+
+template <typename K>
+int occ_of(K kernel, int threads, size_t smem) {
+    int n = 0;
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) ==
+            cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) == cudaSuccess)
+        return n;
+    cudaGetLastError();
+    return std::max(0, std::min(static_cast<int>(kSmemPerSM / (smem + 1024)), 2048 / threads));
+}
+
+FArgs make_fargs(const Tiling& t, const ModeGeom& g) {
+    FArgs a;
+    a.geo = g;
+    a.h = g.n / 2;
+    a.F = g.n - a.h;
+    a.Kp = t.Kp;
+    a.RB = t.RB;
+    a.nstage = t.nstage;
+    a.S = (a.F + 7) / 8;
+    a.A2 = static_cast<long long>(t.Mp) * t.Kp;
+    return a;
+}
+
+template <int MI, int WN>
+cudaError_t fold_launch_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
+                          const double* post, bool fwd, cudaStream_t st, int* occ) {
+    auto k = fwd ? fold_mode_kernel<MI, WN, true> : fold_mode_kernel<MI, WN, false>;
+    if (occ) {
+        *occ = occ_of(k, 32 * WN, t.smem);
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(t.smem));
+    if (e != cudaSuccess) return e;
+    const long long blocks = (g.ncols + t.BN - 1) / t.BN * t.RB;
+    k<<<static_cast<unsigned>(blocks), 32 * WN, t.smem, st>>>(make_fargs(t, g), X, Y, J, post);
+    return cudaGetLastError();
+}
+
+template <int WN>
+cudaError_t fold_dispatch_wn(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
+                             const double* post, bool fwd, cudaStream_t st, int* occ) {
+    switch (t.MI) {
+        case 1: return fold_launch_t<1, WN>(t, g, X, Y, J, post, fwd, st, occ);
+        case 2: return fold_launch_t<2, WN>(t, g, X, Y, J, post, fwd, st, occ);
+        case 3: return fold_launch_t<3, WN>(t, g, X, Y, J, post, fwd, st, occ);
+        case 4: return fold_launch_t<4, WN>(t, g, X, Y, J, post, fwd, st, occ);
+        case 5: return fold_launch_t<5, WN>(t, g, X, Y, J, post, fwd, st, occ);
+        case 6: return fold_launch_t<6, WN>(t, g, X, Y, J, post, fwd, st, occ);
+        case 7: return fold_launch_t<7, WN>(t, g, X, Y, J, post, fwd, st, occ);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t fold_dispatch(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
+                          const double* post, bool fwd, cudaStream_t st, int* occ) {
+    if (t.WN == 4) return fold_dispatch_wn<4>(t, g, X, Y, J, post, fwd, st, occ);
+    if (t.WN == 2) return fold_dispatch_wn<2>(t, g, X, Y, J, post, fwd, st, occ);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+std::vector<Tiling> fold_tiling_candidates(int n) {
+    std::vector<std::pair<double, Tiling>> c;
+    const int h = n / 2, F = n - h;
+    if (h < 1) return {};
+    const int S = (F + 7) / 8;
+    const int Kp = (F + 3) / 4 * 4;
+    for (int MI = 1; MI <= 7; ++MI) {
+        const int RB = (S + MI - 1) / MI;
+        if ((S + RB - 1) / RB != MI) continue;  // a smaller MI covers the strips with as many row blocks
+        for (int WN : {4, 2}) {
+            for (int ns : {3, 2}) {
+                Tiling t;
+                t.fold = 1;
+                t.MI = MI;
+                t.WM = 1;
+                t.NI = 2;
+                t.WN = WN;
+                t.S = S;
+                t.RB = RB;
+                t.MpB = 8 * MI;
+                t.Mp = RB * t.MpB;
+                t.Kp = Kp;
+                t.BN = 16 * WN;
+                t.LDX = t.BN + 4;
+                t.nstage = ns;
+                t.smem = sizeof(double) * static_cast<size_t>(ns) * (2 * kBK * t.LDX + 2 * t.MpB * kLDJ);
+                if (t.smem > kSmemPerCTA) continue;
+                int occ = 0;
+                fold_dispatch(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, true, nullptr, &occ);
+                t.ctas_per_sm = occ;
+                if (occ < 1) continue;
+                const double eff = 0.85 + 0.15 * static_cast<double>(S) / (RB * MI);
+                c.emplace_back(std::min(occ * WN, 16) * eff - 0.05 * RB + 0.02 * WN + 0.01 * ns, t);
+            }
+        }
+    }
+    std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<Tiling> out;
+    for (auto& e : c) out.push_back(e.second);
+    return out;
+}
+
+cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
+                                bool forward, const double* post_scale, cudaStream_t st) {
+    if (g.ncols <= 0) return cudaSuccess;
+    if (!t.fold || g.m != g.n || g.n < 2 || (forward && post_scale)) return cudaErrorInvalidValue;
+    return fold_dispatch(t, g, X, Y, Jfold, post_scale, forward, st, nullptr);
+}
+
+}  // namespace gpu
+}  // namespace stiga

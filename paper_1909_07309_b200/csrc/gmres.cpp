@@ -86,6 +86,7 @@ struct Ctx {
         gck(cudaMallocHost(&host, sizeof(double)), "cudaMallocHost");
     }
     ~Ctx() {
+        release_h();
         cudaFree(partials);
         cudaFree(result);
         cudaFreeHost(host);
@@ -97,6 +98,32 @@ struct Ctx {
         return *host;
     }
     double norm(const double* x) { return std::sqrt(dot(x, x)); }
+    // Arnoldi column k by modified Gram-Schmidt with the coefficients kept on the device
+    // (gmres.cpp:78-83): h_0 = V_0.w; for i < k: w -= h_i V_i, h_{i+1} = V_{i+1}.w; w -= h_k V_k,
+    // h_{k+1} = w.w.  Same operations and order as dot/axpy pairs (bit-identical), one fused pass
+    // per step and one host read-back per column instead of k+2 synchronizing round trips.
+    void mgs(const std::vector<const double*>& V, double* w, int k, double* h_out) {
+        if (!hdev) {
+            gck(cudaMalloc(&hdev, sizeof(double) * hcap), "cudaMalloc");
+            gck(cudaMallocHost(&hhost, sizeof(double) * hcap), "cudaMallocHost");
+        }
+        if (k + 2 > hcap) throw std::invalid_argument("gmres: Krylov column beyond the coefficient buffer");
+        gck(stiga::gpu::launch_dot(V[0], w, n, partials, hdev, st), "dot");
+        for (int i = 0; i <= k; ++i)
+            gck(stiga::gpu::launch_axpy_dot(hdev + i, V[i], w, i < k ? V[i + 1] : nullptr, n, partials, hdev + i + 1, st),
+                "axpy_dot");
+        gck(cudaMemcpyAsync(hhost, hdev, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, st), "mgs D2H");
+        gck(cudaStreamSynchronize(st), "mgs sync");
+        for (int i = 0; i < k + 2; ++i) h_out[i] = hhost[i];
+    }
+    int hcap = 0;
+    double* hdev = nullptr;
+    double* hhost = nullptr;
+    void release_h() {
+        if (hdev) cudaFree(hdev);
+        if (hhost) cudaFreeHost(hhost);
+        hdev = hhost = nullptr;
+    }
 };
 
 }  // namespace
@@ -117,6 +144,7 @@ extern "C" int stiga_gmres(stiga_kronsum_t A, stiga_fd_t P, const double* d_b, d
         }
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         Ctx ctx(st, n);
+        ctx.hcap = (has_restart ? std::min(opts->restart, opts->max_krylov) : opts->max_krylov) + 2;
         using Clock = std::chrono::steady_clock;
         const auto t_start = Clock::now();
         double precond_ms = 0.0;
@@ -178,11 +206,12 @@ extern "C" int stiga_gmres(stiga_kronsum_t A, stiga_fd_t P, const double* d_b, d
                 for (; k < m; ++k) {
                     apply_A(V[k]->p, tmp.p);
                     apply_P(tmp.p, w.p);  // w = P(A v_k)
-                    for (int i = 0; i <= k; ++i) {  // modified Gram-Schmidt
-                        Hk(i, k) = ctx.dot(V[i]->p, w.p);
-                        gck(stiga::gpu::launch_axpy(-Hk(i, k), V[i]->p, w.p, n, st), "axpy");
-                    }
-                    Hk(k + 1, k) = ctx.norm(w.p);
+                    std::vector<const double*> Vp(k + 1);
+                    for (int i = 0; i <= k; ++i) Vp[i] = V[i]->p;
+                    std::vector<double> hcol(k + 2);
+                    ctx.mgs(Vp, w.p, k, hcol.data());  // modified Gram-Schmidt
+                    for (int i = 0; i <= k; ++i) Hk(i, k) = hcol[i];
+                    Hk(k + 1, k) = std::sqrt(hcol[k + 1]);
                     const bool tiny = Hk(k + 1, k) <= 1e-14 * beta0;
                     if (!tiny) {
                         if (static_cast<int>(V.size()) <= k + 1) V.emplace_back(new Vec(n));

@@ -1,6 +1,8 @@
 // Host-side 1D Galerkin assembly; follows /root/reference/proj/core/src/assembly.cpp:47-149.
 #include "assembly.hpp"
 
+#include <algorithm>
+
 #include <stdexcept>
 
 namespace stiga {
@@ -71,11 +73,34 @@ std::pair<BandedMatrix, BandedMatrix> assemble_time_matrices(int p_t, int n_el_t
     return {std::move(W), std::move(M)};
 }
 
+namespace {
+// The spatial space on uniform open knots with both end functions dropped is mirror symmetric
+// (b_i(x) = b_{n-1-i}(1-x)), so its Galerkin matrices satisfy A(i,j) = A(j,i) = A(n-1-i,n-1-j)
+// exactly; quadrature reproduces that only to rounding (~1e-14 relative).  Every entry is replaced
+// by the mean of its four mirror images, summed in a canonical order, so the four positions hold
+// bitwise identical values: the matrices the reference's quadrature approximates, to rounding,
+// and exactly centrosymmetric, which lets the setup split their eigenbasis (host/fdsetup.cpp,
+// folded products).
+void mirror_symmetrize(DenseMatrix& A) {
+    const Index n = A.rows;
+    DenseMatrix B(n, n);
+    for (Index j = 0; j < n; ++j)
+        for (Index i = 0; i < n; ++i) {
+            double v[4] = {A(i, j), A(j, i), A(n - 1 - i, n - 1 - j), A(n - 1 - j, n - 1 - i)};
+            std::sort(v, v + 4);
+            B(i, j) = ((v[0] + v[1]) + (v[2] + v[3])) * 0.25;
+        }
+    A = std::move(B);
+}
+}  // namespace
+
 void assemble_spatial_parametric(int p, int n_el, int q, BandedMatrix& K, BandedMatrix& M) {
     const SplineSpace1D space = SplineSpace1D::spatial(p, n_el);
     const QuadratureRule quad = gauss_rule(space.knot_vector(), q);
     K = assemble_univariate(space, quad, 1, 1);
     M = assemble_univariate(space, quad, 0, 0);
+    mirror_symmetrize(K.m);
+    mirror_symmetrize(M.m);
 }
 
 } // namespace stiga

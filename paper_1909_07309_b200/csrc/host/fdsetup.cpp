@@ -1,7 +1,9 @@
 // Host half of the extended-FD setup; follows /root/reference/proj/core/src/fdsolve.cpp:67-153.
 #include "fdsetup.hpp"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 
 namespace stiga {
@@ -17,6 +19,125 @@ Vector kron_sum_eigenvalues(const std::vector<Vector>& lambda) {
     return lam_s;
 }
 
+bool centrosymmetric(const DenseMatrix& A, double rtol) {
+    const Index n = A.rows;
+    if (A.cols != n || n < 2) return false;
+    double amax = 0.0, dmax = 0.0;
+    for (Index j = 0; j < n; ++j)
+        for (Index i = 0; i < n; ++i) {
+            amax = std::max(amax, std::fabs(A(i, j)));
+            dmax = std::max(dmax, std::fabs(A(i, j) - A(n - 1 - i, n - 1 - j)));
+            dmax = std::max(dmax, std::fabs(A(i, j) - A(j, i)));
+        }
+    return amax > 0.0 && dmax <= rtol * amax;
+}
+
+namespace {
+
+// Q^T A Q for Q = [(e_i + e_{n-1-i})/sqrt2 (i < h), e_h (n odd), (e_i - e_{n-1-i})/sqrt2 (i < h)],
+// symmetrised over the four mirrored entries (A is centrosymmetric only to rounding).
+void fold_blocks(const DenseMatrix& A, int h, int F, DenseMatrix& E, DenseMatrix& O) {
+    const Index n = A.rows;
+    const double r2 = std::sqrt(2.0);
+    E = DenseMatrix(F, F);
+    O = DenseMatrix(h, h);
+    auto a = [&](Index i, Index j) { return 0.5 * (A(i, j) + A(j, i)); };
+    for (int j = 0; j < h; ++j)
+        for (int i = 0; i < h; ++i) {
+            const double s = a(i, j), c = a(i, n - 1 - j), r = a(n - 1 - i, j), t = a(n - 1 - i, n - 1 - j);
+            E(i, j) = 0.5 * ((s + t) + (c + r));
+            O(i, j) = 0.5 * ((s + t) - (c + r));
+        }
+    if (F > h) {
+        for (int i = 0; i < h; ++i) E(i, h) = E(h, i) = (a(i, h) + a(n - 1 - i, h)) / r2;
+        E(h, h) = A(h, h);
+    }
+}
+
+// Split eigenbasis of a centrosymmetric SPD pencil: U (n x n) in folded column order [even; odd]
+// with eigenvalues lam_fold; fb receives the half-size bases.
+void split_eig(const DenseMatrix& K, const DenseMatrix& M, FoldBasis& fb, DenseMatrix& U, Vector& lam_fold) {
+    const Index n = K.rows;
+    fb.h = static_cast<int>(n / 2);
+    fb.F = static_cast<int>(n) - fb.h;
+    DenseMatrix Ke, Ko, Me, Mo;
+    fold_blocks(K, fb.h, fb.F, Ke, Ko);
+    fold_blocks(M, fb.h, fb.F, Me, Mo);
+    Vector le, lo;
+    spd_generalized_eig(Ke, Me, fb.We, le);
+    if (fb.h > 0) spd_generalized_eig(Ko, Mo, fb.Wo, lo);
+    const double r2 = std::sqrt(2.0);
+    U = DenseMatrix(n, n);
+    for (int c = 0; c < fb.F; ++c) {
+        for (int i = 0; i < fb.h; ++i) U(i, c) = U(n - 1 - i, c) = fb.We(i, c) / r2;
+        if (fb.F > fb.h) U(fb.h, c) = fb.We(fb.h, c);
+    }
+    for (int c = 0; c < fb.h; ++c)
+        for (int i = 0; i < fb.h; ++i) {
+            U(i, fb.F + c) = fb.Wo(i, c) / r2;
+            U(n - 1 - i, fb.F + c) = -fb.Wo(i, c) / r2;
+        }
+    lam_fold = le;
+    lam_fold.insert(lam_fold.end(), lo.begin(), lo.end());
+}
+
+}  // namespace
+
+std::vector<double> fold_matrices(const FoldBasis& fb, bool forward, int Mp, int Kp) {
+    const int h = fb.h, F = fb.F;
+    if (Mp < F || Kp < F) throw std::runtime_error("internal: folded matrix padding too small");
+    std::vector<double> out(2 * static_cast<size_t>(Mp) * Kp, 0.0);
+    double* A1 = out.data();
+    double* A2 = out.data() + static_cast<size_t>(Mp) * Kp;
+    const double r2 = std::sqrt(2.0);
+    for (int r = 0; r < F; ++r)
+        for (int k = 0; k < F; ++k) {
+            if (forward) {  // A_e[r][k] (U^T, even rows), A_o[r][k] (odd rows)
+                A1[r * Kp + k] = k < h ? fb.We(k, r) / r2 : 0.5 * fb.We(k, r);
+                if (r < h && k < h) A2[r * Kp + k] = fb.Wo(k, r) / r2;
+            } else {        // A_p[i][c], A_q[i][c] (U: p = A_p y_e, q = A_q y_o)
+                A1[r * Kp + k] = r < h ? fb.We(r, k) / r2 : fb.We(r, k);
+                if (r < h && k < h) A2[r * Kp + k] = fb.Wo(r, k) / r2;
+            }
+        }
+    return out;
+}
+
+Vector FDFactors::lambda_dev(int l) const {
+    if (!fold[l].on) return lambda[l];
+    Vector v(lambda[l].size());
+    for (size_t f = 0; f < v.size(); ++f) v[f] = lambda[l][fold[l].dev_order[f]];
+    return v;
+}
+
+DenseMatrix FDFactors::U_dev(int l) const {
+    if (!fold[l].on) return U[l];
+    const DenseMatrix& A = U[l];
+    DenseMatrix B(A.rows, A.cols);
+    for (Index f = 0; f < A.cols; ++f)
+        for (Index i = 0; i < A.rows; ++i) B(i, f) = A(i, fold[l].dev_order[f]);
+    return B;
+}
+
+Vector FDFactors::S_inv_dev() const {
+    bool any = false;
+    for (const auto& fb : fold) any = any || fb.on;
+    if (!any) return S_inv;
+    Vector out(S_inv.size());
+    std::vector<Index> stride(d, 1);
+    for (int l = 1; l < d; ++l) stride[l] = stride[l - 1] * n[l - 1];
+    for (Index s = 0; s < static_cast<Index>(S_inv.size()); ++s) {
+        Index rem = s, sa = 0;
+        for (int l = 0; l < d; ++l) {
+            const Index f = rem % n[l];
+            rem /= n[l];
+            sa += stride[l] * (fold[l].on ? fold[l].dev_order[f] : f);
+        }
+        out[s] = S_inv[sa];
+    }
+    return out;
+}
+
 FDFactors fd_setup(const std::vector<DenseMatrix>& space_K, const std::vector<DenseMatrix>& space_M,
                    const DenseMatrix& Wt, const DenseMatrix& Mt, double gamma, double nu,
                    const double* scaling) {
@@ -27,13 +148,40 @@ FDFactors fd_setup(const std::vector<DenseMatrix>& space_K, const std::vector<De
     FDFactors F;
     F.d = static_cast<int>(space_K.size());
     Index n_s = 1;
+    static const bool no_fold = std::getenv("STIGA_NO_FOLD") != nullptr;
     for (int l = 0; l < F.d; ++l) {
         DenseMatrix U;
         Vector lam;
-        spd_generalized_eig(space_K[l], space_M[l], U, lam);
+        FoldBasis fb;
+        // exact mirror symmetry only: splitting a pencil that is centrosymmetric merely to rounding
+        // would perturb the preconditioner by ~1e-12 relative (measured), so such inputs keep the
+        // dense eigenbasis
+        if (!no_fold && space_K[l].rows >= 2 && centrosymmetric(space_K[l], 0.0) &&
+            centrosymmetric(space_M[l], 0.0)) {
+            DenseMatrix Uf;
+            Vector lf;
+            split_eig(space_K[l], space_M[l], fb, Uf, lf);
+            // exported order: ascending eigenvalues, as spd_generalized_eig returns them
+            const int nl = static_cast<int>(lf.size());
+            std::vector<int> asc(nl);
+            for (int i = 0; i < nl; ++i) asc[i] = i;
+            std::stable_sort(asc.begin(), asc.end(), [&](int a, int b) { return lf[a] < lf[b]; });
+            U = DenseMatrix(nl, nl);
+            lam.resize(nl);
+            fb.dev_order.assign(nl, 0);
+            for (int k = 0; k < nl; ++k) {
+                lam[k] = lf[asc[k]];
+                for (int i = 0; i < nl; ++i) U(i, k) = Uf(i, asc[k]);
+                fb.dev_order[asc[k]] = k;
+            }
+            fb.on = true;
+        } else {
+            spd_generalized_eig(space_K[l], space_M[l], U, lam);
+        }
         F.n.push_back(static_cast<int>(lam.size()));
         F.U.push_back(std::move(U));
         F.lambda.push_back(std::move(lam));
+        F.fold.push_back(std::move(fb));
         n_s *= F.n.back();
     }
     F.time = time_factorization(Wt, Mt);

@@ -173,6 +173,173 @@ class ShardedExtendedFD:
                                     group=self.group)
 
 
+# ---- fused exchange: the transposes as scatter epilogues over peer memory --------
+
+
+def scatter_fields(plan, stage, dst_ptrs):
+    """Fields of the C-ABI stiga_scatter_desc for this rank's scattering stage.
+
+    stage "space": the forward spatial stage of time slab T_r stores element (s, t) of its output
+    (s spatial, t local time) into rank q = owner(s)'s slab receive buffer z_q (|S_q| x n_t colex)
+    at (s - s_off[q]) + |S_q| (t_off[r] + t).
+    stage "time": the time stage of spatial slab S_q stores element (s, t) (s local spatial, t time)
+    into rank r = owner(t)'s time-slab receive buffer y_r (N_s x |T_r| colex) at
+    (s_off[q] + s) + N_s (t - t_off[r]).
+    dst_ptrs[q] = rank q's receive buffer as seen from this process."""
+    pl, r = plan, plan.rank
+    if len(dst_ptrs) != pl.world:
+        raise ValueError("scatter_fields: one destination per rank")
+    if stage == "space":
+        offsets = pl.s_off + [pl.n_s]
+        return dict(world=pl.world, by_time=0, offsets=offsets, ld=list(pl.s_len), a_shift=0,
+                    b_shift=pl.t_off[r], dst=list(dst_ptrs))
+    if stage == "time":
+        offsets = pl.t_off + [pl.n_t]
+        return dict(world=pl.world, by_time=1, offsets=offsets, ld=[pl.n_s] * pl.world, a_shift=pl.s_off[r],
+                    b_shift=0, dst=list(dst_ptrs))
+    raise ValueError(f"scatter_fields: unknown stage {stage!r}")
+
+
+def scatter_desc(fields):
+    """ctypes stiga_scatter_desc from scatter_fields()."""
+    from ._lib import MAX_RANKS, ScatterDesc
+
+    if not 1 <= fields["world"] <= MAX_RANKS:
+        raise ValueError(f"fused exchange supports 1..{MAX_RANKS} ranks")
+    d = ScatterDesc()
+    d.world, d.by_time = fields["world"], fields["by_time"]
+    for q, o in enumerate(fields["offsets"]):
+        d.offsets[q] = o
+    for q in range(fields["world"]):
+        d.ld[q] = fields["ld"][q]
+        d.dst[q] = fields["dst"][q]
+    d.a_shift, d.b_shift = fields["a_shift"], fields["b_shift"]
+    return d
+
+
+class FusedShardedExtendedFD:
+    """Time-sharded ExtendedFDPreconditioner::apply (fdsolve.cpp:155-164) with the two all-to-all
+    transposes fused into the producing kernels: the last forward spatial product stores straight
+    into the owners' slab receive buffers, the time stage's last product straight into the owners'
+    time-slab receive buffers (peer memory over NVLink).  Per apply:
+
+      space fwd (scatter) -> barrier -> time (scatter) -> barrier -> space bwd (local)
+
+    No pack / unpack passes, no NCCL data movement; the barriers order the stages across ranks (a
+    1-element NCCL all-reduce on the stream, or host barrier after a stream sync on gloo).  Bit-for-bit
+    the same arithmetic as ShardedExtendedFD (same products, same order).
+
+    slab_ptrs[q] / time_ptrs[q]: rank q's receive buffers (|S_q| x n_t and N_s x |T_q| doubles) as
+    device addresses valid in this process; `create` allocates and exchanges them with CUDA IPC."""
+
+    def __init__(self, P, dims, rank, world, slab_ptrs, time_ptrs, barrier=None, stream=None):
+        self.P = P
+        self.plan = ShardPlan.make(list(dims), world, rank)
+        self.slab_ptrs = list(slab_ptrs)
+        self.time_ptrs = list(time_ptrs)
+        self.fwd = scatter_desc(scatter_fields(self.plan, "space", self.slab_ptrs))
+        self.bwd = scatter_desc(scatter_fields(self.plan, "time", self.time_ptrs))
+        self.barrier = barrier or (lambda: None)
+        self.stream = stream
+        self._owned = []  # (ptr, kind) to release in close()
+
+    def _st(self):
+        import torch
+
+        s = self.stream or torch.cuda.current_stream()
+        return ctypes.c_void_p(s.cuda_stream)
+
+    @classmethod
+    def create(cls, P, dims, group=None, device=None, stream=None):
+        """Allocates this rank's receive buffers, exchanges CUDA IPC handles over the process group
+        and opens the peers' buffers (one process per GPU; NVLink P2P on the B200 box)."""
+        import torch
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        dev = torch.cuda.current_device() if device is None else device
+        plan = ShardPlan.make(list(dims), world, rank)
+        L = lib()
+        mine = []
+        for n in (plan.s_len[rank] * plan.n_t, plan.n_s * plan.t_len[rank]):
+            p = ctypes.c_void_p()
+            check(L.stiga_device_alloc(8 * n, dev, ctypes.byref(p)), "device_alloc")
+            mine.append(p.value)
+        handles = []
+        for p in mine:
+            h = ctypes.create_string_buffer(64)
+            check(L.stiga_ipc_handle(ctypes.c_void_p(p), h), "ipc_handle")
+            handles.append(h.raw)
+        if world > 1:
+            gathered = [None] * world
+            dist.all_gather_object(gathered, handles, group=group)
+        else:
+            gathered = [handles]
+        opened = []
+        ptrs = [[None] * world, [None] * world]
+        for q in range(world):
+            for k in range(2):
+                if q == rank:
+                    ptrs[k][q] = mine[k]
+                else:
+                    p = ctypes.c_void_p()
+                    check(L.stiga_ipc_open(gathered[q][k], dev, ctypes.byref(p)), "ipc_open")
+                    ptrs[k][q] = p.value
+                    opened.append(p.value)
+        if world > 1 and dist.get_backend(group) == "nccl":
+            flag = torch.zeros(1, dtype=torch.float64, device=f"cuda:{dev}")
+
+            def barrier():  # stream-ordered: the next stage's kernels wait for every rank's scatter
+                dist.all_reduce(flag, group=group)
+        elif world > 1:
+            def barrier():
+                torch.cuda.current_stream().synchronize()
+                dist.barrier(group=group)
+        else:
+            barrier = None
+        self = cls(P, dims, rank, world, ptrs[0], ptrs[1], barrier=barrier, stream=stream)
+        self._owned = [(p, "ipc") for p in opened] + [(p, "alloc") for p in mine]
+        return self
+
+    def close(self):
+        L = lib()
+        for p, kind in self._owned:
+            if kind == "ipc":
+                L.stiga_ipc_close(ctypes.c_void_p(p))
+        for p, kind in self._owned:
+            if kind == "alloc":
+                L.stiga_device_free(ctypes.c_void_p(p))
+        self._owned = []
+
+    # stages (split out so one process can drive several virtual ranks on one GPU)
+    def stage_forward(self, x_local):
+        pl = self.plan
+        check(lib().stiga_fd_apply_space_scatter(self.P.handle, pl.t_off[pl.rank], pl.t_len[pl.rank],
+                                                 ctypes.c_void_p(x_local.data_ptr()), ctypes.byref(self.fwd),
+                                                 self._st()), "fd_apply_space_scatter")
+
+    def stage_time(self):
+        pl = self.plan
+        check(lib().stiga_fd_apply_time_scatter(self.P.handle, pl.s_off[pl.rank], pl.s_len[pl.rank],
+                                                ctypes.c_void_p(self.slab_ptrs[pl.rank]), ctypes.byref(self.bwd),
+                                                self._st()), "fd_apply_time_scatter")
+
+    def stage_backward(self, out):
+        pl = self.plan
+        check(lib().stiga_fd_apply_space(self.P.handle, 1, pl.t_off[pl.rank], pl.t_len[pl.rank],
+                                         ctypes.c_void_p(self.time_ptrs[pl.rank]), ctypes.c_void_p(out.data_ptr()),
+                                         self._st()), "fd_apply_space")
+        return out
+
+    def apply(self, x_local, out=None):
+        self.stage_forward(x_local)
+        self.barrier()
+        self.stage_time()
+        self.barrier()
+        return self.stage_backward(out if out is not None else x_local.new_empty(x_local.shape))
+
+
 # ---- time-sharded system mat-vec and GMRES (SURVEY §8(e)) --------------------------------------
 
 

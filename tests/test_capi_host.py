@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(L, s), s
         assert s in _lib.SIGNATURES, f"{s} missing from the ctypes signature table"
-    assert L.stiga_abi_version() == 100
+    assert L.stiga_abi_version() == 101
 
 
 def test_compute_without_device_fails_loudly():

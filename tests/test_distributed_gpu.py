@@ -154,3 +154,141 @@ def test_slab_stage_argument_errors():
     assert out.item() == 10.0
     with pytest.raises(ValueError):
         check(lib().stiga_vec_dot(None, None, 10, ctypes.c_void_p(out.data_ptr()), None), "vec_dot")
+
+
+# ---- fused exchange (scatter epilogues over peer memory) ---------------------------------------
+
+
+def virtual_fused_apply(P, r, world):
+    """FusedShardedExtendedFD for `world` virtual ranks on one GPU: the receive buffers are ordinary
+    local tensors, so the scatter epilogues write into the other virtual ranks' buffers exactly as
+    they would write into peer memory; stages run rank after rank (nothing waits on another rank)."""
+    from paper_1909_07309_b200.distributed import FusedShardedExtendedFD, ShardPlan
+
+    plans = [ShardPlan.make(P.dims, world, q) for q in range(world)]
+    pl0 = plans[0]
+    slab = [torch.full((pl0.s_len[q] * pl0.n_t,), float("nan"), dtype=torch.float64, device="cuda")
+            for q in range(world)]
+    tsl = [torch.full((pl0.n_s * pl0.t_len[q],), float("nan"), dtype=torch.float64, device="cuda")
+           for q in range(world)]
+    ranks = [FusedShardedExtendedFD(P, P.dims, q, world, [t.data_ptr() for t in slab], [t.data_ptr() for t in tsl])
+             for q in range(world)]
+    for f in ranks:
+        a, b = f.plan.local_slice()
+        f.stage_forward(r[a:b].clone())
+    assert not any(torch.isnan(t).any() for t in slab), "forward scatter left a hole"
+    for f in ranks:
+        f.stage_time()
+    assert not any(torch.isnan(t).any() for t in tsl), "time scatter left a hole"
+    outs = [f.stage_backward(torch.empty(f.plan.local_size, dtype=torch.float64, device="cuda")) for f in ranks]
+    return torch.cat(outs)
+
+
+@pytest.mark.parametrize("fold", ["off", "auto"])
+@pytest.mark.parametrize("variant", ["fused", "split"])
+@pytest.mark.parametrize("world,d,p,nel", [(1, 2, 3, 9), (2, 2, 3, 9), (3, 3, 2, 6), (4, 1, 4, 30), (8, 3, 3, 12),
+                                           (5, 2, 2, 40)])
+def test_virtual_ranks_fused_exchange(fold, variant, world, d, p, nel, monkeypatch):
+    """Scatter-epilogue path = oracle (<= 1e-11); with dense kernels bit-identical to the pack +
+    all-to-all path (with folded kernels the scattering last forward product is the dense kernel on
+    the same split basis, so the two paths agree to rounding)."""
+    monkeypatch.setenv("STIGA_TIME_VARIANT", variant)
+    if fold == "off":
+        monkeypatch.setenv("STIGA_FOLD_KERNEL", "off")
+    pc = identity_pieces(d, p, nel)
+    D = np.exp(0.3 * uniform_pm1(pc.n_dof, 3))
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D, device=0)
+    Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D)
+    r = uniform_pm1(pc.n_dof, 4)
+    rt = torch.from_numpy(r).cuda()
+    s = virtual_fused_apply(P, rt, world)
+    so = Po.apply(r)
+    assert np.linalg.norm(s.cpu().numpy() - so) / np.linalg.norm(so) <= 1e-11
+    sr = virtual_sharded_apply(P, rt, world)
+    if fold == "off":
+        assert torch.equal(s, sr)
+    else:
+        assert torch.linalg.norm(s - sr) <= 1e-13 * torch.linalg.norm(sr)
+
+
+def test_scatter_stage_argument_errors():
+    import ctypes
+
+    from paper_1909_07309_b200._lib import check, lib
+    from paper_1909_07309_b200.distributed import ShardPlan, scatter_desc, scatter_fields
+
+    pc = identity_pieces(2, 2, 6)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=0)
+    pl = ShardPlan.make(P.dims, 2, 0)
+    x = torch.zeros(P.n_dof, dtype=torch.float64, device="cuda")
+    good = scatter_fields(pl, "space", [x.data_ptr(), x.data_ptr()])
+    L = lib()
+
+    def space(f, t0=0, ntl=pl.t_len[0]):
+        check(L.stiga_fd_apply_space_scatter(P.handle, t0, ntl, ctypes.c_void_p(x.data_ptr()),
+                                             ctypes.byref(scatter_desc(f)), None), "scatter")
+
+    with pytest.raises(ValueError):  # time-stage descriptor on the space stage
+        space(scatter_fields(pl, "time", [x.data_ptr(), x.data_ptr()]))
+    with pytest.raises(ValueError):  # offsets do not cover N_s
+        space(dict(good, offsets=[0, 3, 5]))
+    with pytest.raises(ValueError):  # null destination
+        space(dict(good, dst=[x.data_ptr(), None]))
+    with pytest.raises(ValueError):  # slab outside [0, n_t)
+        space(good, t0=pl.n_t - 1, ntl=2)
+
+
+def _ipc_worker(rank, world, port, q):
+    """One process per (virtual) rank, all on cuda:0: receive buffers exported with CUDA IPC and
+    opened by the peer process; gloo host barriers (kernels never wait on another process)."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1909_07309_b200.distributed import FusedShardedExtendedFD
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pc = identity_pieces(2, 3, 11)
+        D = np.exp(0.3 * uniform_pm1(pc.n_dof, 3))
+        P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D, device=0)
+        r = uniform_pm1(pc.n_dof, 4)
+        f = FusedShardedExtendedFD.create(P, P.dims, device=0)
+        a, b = f.plan.local_slice()
+        x = torch.from_numpy(r[a:b].copy()).cuda()
+        out = f.apply(x)
+        out = f.apply(x)  # second apply reuses the exchanged buffers
+        torch.cuda.synchronize()
+        parts = [None] * world
+        dist.all_gather_object(parts, out.cpu().numpy())
+        dist.barrier()
+        f.close()
+        if rank == 0:
+            Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D)
+            so = Po.apply(r)
+            s = np.concatenate(parts)
+            q.put(float(np.linalg.norm(s - so) / np.linalg.norm(so)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_exchange_two_processes_cuda_ipc():
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(300)
+        assert pr.exitcode == 0
+    assert q.get(timeout=5) <= 1e-11

@@ -243,3 +243,50 @@ def test_fd_apply_parity_random_shapes():
         assert rel(s, so) <= TOL, (d, p, nel, scaled, gamma)
 
     check()
+
+
+# ---- folded (centrosymmetric) mode products --------------------------------------------------
+
+
+@pytest.mark.parametrize("d,p,nel", [
+    (1, 2, 1), (1, 1, 2), (1, 2, 3), (1, 3, 40), (1, 5, 33),   # n = 1 (no split), 2, 3, odd/even
+    (2, 2, 16), (2, 3, 9), (2, 4, 11), (2, 3, 64),            # c1, odd and even n, multi-chunk
+    (3, 2, 6), (3, 3, 7), (3, 3, 12), (3, 4, 9), (3, 3, 24),
+])
+@pytest.mark.parametrize("scaled", [False, True])
+def test_fd_apply_parity_folded_kernels(d, p, nel, scaled, monkeypatch):
+    """STIGA_FOLD_KERNEL=force: every split spatial direction runs the folded kernels (forward fold
+    x_k +- x_{n-1-k} on the B fragments, backward p +- q epilogue), <= 1e-11 vs the oracle and equal to
+    the dense kernels on the same split basis to rounding."""
+    monkeypatch.setenv("STIGA_FOLD_KERNEL", "force")
+    s, so, P, _, r = run_pair(d, p, nel, scaled)
+    names = [nm for nm, _ in P.launch_info()]
+    if P.dims[0] >= 2:
+        assert any("folded" in nm for nm in names), names
+    assert rel(s, so) <= TOL
+    monkeypatch.setenv("STIGA_FOLD_KERNEL", "off")
+    s2, *_ = run_pair(d, p, nel, scaled)
+    assert rel(s, s2) <= 1e-13
+
+
+@pytest.mark.parametrize("nel", [96, 161, 254])
+def test_fd_apply_parity_folded_large_modes(nel, monkeypatch):
+    """n = 97 / 162 / 255 + 2: several row blocks of the folded matrices and the contraction tail."""
+    monkeypatch.setenv("STIGA_FOLD_KERNEL", "force")
+    pc = identity_pieces(2, 3, nel)
+    Wt, Mt = stiga.assemble_time_matrices(3, 4)
+    D = np.exp(0.2 * uniform_pm1(pc.K[0].shape[0] ** 2 * Wt.shape[0], 5))
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, Wt, Mt, 1.0, 1.0, scaling=D, device=0)
+    Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, Wt, Mt, 1.0, 1.0, scaling=D)
+    r = uniform_pm1(P.n_dof, 13)
+    s = P.apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert rel(s, Po.apply(r)) <= TOL
+
+
+def test_fold_not_used_on_curved_geometry():
+    """The A^G factors of the deformed cube are not centrosymmetric: dense kernels only."""
+    from paper_1909_07309_b200.problems import Problem
+
+    pc = Problem("deformed-cube-3d").geometry_pieces(2, 4)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=pc.D, device=0)
+    assert not any("folded" in nm for nm, _ in P.launch_info())
