@@ -81,6 +81,37 @@ void split_eig(const DenseMatrix& K, const DenseMatrix& M, FoldBasis& fb, DenseM
     lam_fold.insert(lam_fold.end(), lo.begin(), lo.end());
 }
 
+// Rayleigh-quotient refinement of the spatial eigenvalues: lambda_k = u_k^T K u_k / u_k^T M u_k with
+// long-double accumulation.  A backward-stable eigensolver returns lambda_k to an absolute error of
+// ~eps * lambda_max, i.e. a relative error of eps * lambda_max / lambda_min for the smallest (smoothest)
+// modes -- 1e-11 at n ~ 257 -- and those modes dominate the FD output.  The quotient of an
+// eigenvector accurate to delta is accurate to ~delta^2 * lambda_max, so the refined eigenvalues are
+// accurate to rounding and independent of the eigensolver.
+void refine_eigenvalues(const DenseMatrix& K, const DenseMatrix& M, const DenseMatrix& U, Vector& lam) {
+    const Index n = K.rows;
+    std::vector<long double> ku(n), mu(n);
+    for (Index k = 0; k < U.cols; ++k) {
+        const double* u = U.col(k);
+        for (Index i = 0; i < n; ++i) ku[i] = mu[i] = 0.0L;
+        for (Index j = 0; j < n; ++j) {
+            const long double uj = u[j];
+            if (uj == 0.0L) continue;
+            const double* kc = K.col(j);
+            const double* mc = M.col(j);
+            for (Index i = 0; i < n; ++i) {
+                ku[i] += static_cast<long double>(kc[i]) * uj;
+                mu[i] += static_cast<long double>(mc[i]) * uj;
+            }
+        }
+        long double num = 0.0L, den = 0.0L;
+        for (Index i = 0; i < n; ++i) {
+            num += static_cast<long double>(u[i]) * ku[i];
+            den += static_cast<long double>(u[i]) * mu[i];
+        }
+        if (den > 0.0L) lam[k] = static_cast<double>(num / den);
+    }
+}
+
 }  // namespace
 
 std::vector<double> fold_matrices(const FoldBasis& fb, bool forward, int Mp, int Kp) {
@@ -178,6 +209,7 @@ FDFactors fd_setup(const std::vector<DenseMatrix>& space_K, const std::vector<De
         } else {
             spd_generalized_eig(space_K[l], space_M[l], U, lam);
         }
+        refine_eigenvalues(space_K[l], space_M[l], U, lam);  // lambda_dev() reads these through dev_order
         F.n.push_back(static_cast<int>(lam.size()));
         F.U.push_back(std::move(U));
         F.lambda.push_back(std::move(lam));

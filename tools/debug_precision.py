@@ -161,3 +161,38 @@ print("worst spatial indices (device order):", top, "lambda_s:", lu.lambda_s[top
 per_t = E.max(axis=1) / Tn.max()
 print("worst time rows:", np.argsort(per_t)[::-1][:8], per_t[np.argsort(per_t)[::-1][:8]])
 print("output magnitude by time row (max):", Tn.max(axis=1)[:4], Tn.max(axis=1)[-4:])
+if os.environ.get("STIGA_DEBUG_ARROW") == "1":   # fused time kernel without the arrowhead: X U_t U_t^T
+    Xv = vin.astype(LD).reshape(nt, ns).T
+    Ut = Pb.time.U.astype(LD)
+    g_ld = ((Xv @ Ut) @ Ut.T).T.reshape(-1)
+    print("time GEMMs only (U_t U_t^T):", rel(t_gpu, g_ld))
+    Zg = (Xv @ Ut)
+    print("  |U_t^T x| column-0 magnitude:", float(np.abs(Zg[0].astype(np.float64)).max()), "max:",
+          float(np.abs(Zg.astype(np.float64)).max()))
+# arrowhead output of the device for the worst column, recovered by undoing the final U_t product
+c0 = int(np.argmin(lu.lambda_s))
+Ut64 = Pb.time.U
+Tg = t_gpu.reshape(nt, ns)[:, c0]            # = U_t @ xo  (time mode, J = U_t)
+Tl = t_ld.reshape(nt, ns)[:, c0].astype(np.float64)
+xo_g = np.linalg.solve(Ut64, Tg)
+xo_l = np.linalg.solve(Ut64, Tl)
+d = np.abs(xo_g - xo_l)
+print("arrowhead rows of the worst column: x_last gpu/ld", xo_g[-1], xo_l[-1], "rel", abs(xo_g[-1] - xo_l[-1]) / abs(xo_l[-1]))
+print("  zero row", xo_g[-2], xo_l[-2], " worst rows", np.argsort(d)[::-1][:6], (d / np.abs(xo_l).max())[np.argsort(d)[::-1][:6]])
+# device Z = (I (x) U_t^T) x through stiga_kron_matvec (same DMMA mode kernel) vs long double
+Zd = stiga.kron_matvec([np.eye(ns), Ut64.T], dev(vin)).cpu().numpy().reshape(nt, ns)
+Zl = (vin.astype(LD).reshape(nt, ns).T @ Ut64.astype(LD)).T       # (nt, ns)
+dz = np.abs((Zd.astype(LD) - Zl).astype(np.float64))
+print("Z via kron_matvec: worst column-0 rows", np.argsort(dz[:, c0])[::-1][:4],
+      (dz[:, c0] / np.abs(Zl[:, c0].astype(np.float64)))[np.argsort(dz[:, c0])[::-1][:4]],
+      "global rel", float(np.linalg.norm(dz) / np.linalg.norm(Zl.astype(np.float64))))
+print("x_last gpu / ld:", xo_g[-1], xo_l[-1])
+# same long-double reference, but with the product's own eigenvalues Lambda_s (ascending export)
+lam_p = P.export(1, 0)
+print("lambda_min product / oracle:", lam_p[0], Pb.lu.lambda_s[0], "rel", abs(lam_p[0] - Pb.lu.lambda_s[0]) / lam_p[0])
+Pc = copy.deepcopy(Pb)
+Pc.lu.lambda_s = lam_p.copy()
+Pc.lu.lambda_s_inv = 1.0 / lam_p
+s_ldp = ld_apply(Pc, r)
+print("gpu vs long double on the product's Lambda_s:",
+      float(np.linalg.norm((s_gpu.astype(LD) - s_ldp).astype(np.float64)) / np.linalg.norm(s_ldp.astype(np.float64))))
