@@ -69,19 +69,19 @@ struct FArgs {
     long long A2;  // offset (doubles) of the second folded matrix after the first (Mp * Kp)
 };
 
-template <int MI_, int WN_>
+template <int MI_, int WN_, int NI_>
 struct FShape {
-    static constexpr int MI = MI_, WN = WN_, NI = 2;
+    static constexpr int MI = MI_, WN = WN_, NI = NI_;
     static constexpr int NTHR = 32 * WN;
-    static constexpr int BN = 16 * WN;
-    static constexpr int LDX = BN + 4;
+    static constexpr int BN = 8 * NI * WN;
+    static constexpr int LDX = BN + 4;            // == 4 mod 16 doubles: conflict-free B fragments
     static constexpr int MPB = 8 * MI;
-    static constexpr int XCNT = kBK * BN / NTHR;  // fiber-chunk elements per thread and chunk (= 8)
+    static constexpr int XCNT = kBK * BN / NTHR;  // fiber-chunk elements per thread and buffer (4 NI)
     static constexpr int JPIECES = MPB * (kBK / 2);
     static constexpr int JROWSTEP = NTHR / 8;
     static constexpr int JCNT = (JPIECES + NTHR - 1) / NTHR;
-    static constexpr int XROWSTEP = NTHR / BN;  // L > 1: chunk rows between a thread's elements
-    static constexpr int XCOLSTEP = NTHR / 16;  // L == 1: fibers between a thread's elements
+    static constexpr int XROWSTEP = NTHR / BN;    // L > 1: chunk rows between a thread's elements
+    static constexpr int XCOLSTEP = NTHR / 16;    // L == 1: fibers between a thread's elements
     // stage: Xa (16 x LDX), Xb (16 x LDX), J1 (MPB x LDJ), J2 (MPB x LDJ)
     static constexpr int XB = kBK * LDX;
     static constexpr int J1 = 2 * kBK * LDX;
@@ -95,39 +95,52 @@ __device__ __forceinline__ long long fbase(long long cc, long long L, int n) {
     return (cc - r * L) + L * static_cast<long long>(n) * r;
 }
 
-// Per-thread loader state: element u of a chunk is fiber fc[u] (global base fb[u]), chunk row jr[u].
-template <class SH>
+// Per-thread loader state, computed once per tile (mirrors Prod in fd_common.cuh).  Element u of a
+// fiber chunk: L == 1: fiber tid/16 + u*XCOLSTEP, chunk row tid%16; L > 1: fiber tid%BN, chunk row
+// tid/BN + u*XROWSTEP.  Global address of (element u, fiber row r) = xg + u*xstep + L*r.
 struct FProd {
-    long long fb[SH::XCNT];  // global offset of element 0 of the element's fiber (valid fibers)
-    unsigned xs[SH::XCNT];   // smem byte offset within a stage (Xa; Xb adds XB)
-    int jr[SH::XCNT];        // chunk row 0..15
-    unsigned fmask;          // fiber inside the tensor
-    const double* jg;        // J1 row piece for chunk 0
+    const double* xg;  // element u = 0, fiber row 0
+    long long xstep;   // between elements u
+    long long L;       // between fiber rows
+    unsigned xs;       // smem byte offset of element u = 0 (Xa; Xb adds XB)
+    unsigned xsstep;   // smem bytes between elements u
+    int jr0, jrstep;   // chunk row of element u = jr0 + u*jrstep
+    unsigned colmask;  // element u's fiber inside the tensor
+    bool full_tile;
+    const double* jg;  // J1 row piece for chunk 0
     unsigned js;
     int jp2;
 };
 
 template <class SH>
-__device__ __forceinline__ FProd<SH> make_fprod(const FArgs& a, long long c0, const double* Jg) {
-    FProd<SH> p;
+__device__ __forceinline__ FProd make_fprod(const FArgs& a, long long c0, const double* X, const double* Jg) {
+    FProd p;
     const int tid = threadIdx.x;
-    p.fmask = 0;
+    p.L = a.geo.L;
+    p.full_tile = c0 + SH::BN <= a.geo.ncols;
+    p.colmask = 0;
+    if (a.geo.L == 1) {
+        const int j = tid & (kBK - 1), cf = tid >> 4;
+        p.jr0 = j;
+        p.jrstep = 0;
+        p.xs = 8u * (j * SH::LDX + cf);
+        p.xsstep = 8u * SH::XCOLSTEP;
+        p.xg = X + (c0 + cf) * a.geo.n;
+        p.xstep = static_cast<long long>(SH::XCOLSTEP) * a.geo.n;
 #pragma unroll
-    for (int u = 0; u < SH::XCNT; ++u) {
-        int c, j;
-        if (a.geo.L == 1) {
-            j = tid & (kBK - 1);
-            c = (tid >> 4) + u * SH::XCOLSTEP;
-        } else {
-            c = tid & (SH::BN - 1);
-            j = tid / SH::BN + u * SH::XROWSTEP;
-        }
+        for (int u = 0; u < SH::XCNT; ++u)
+            if (c0 + cf + u * SH::XCOLSTEP < a.geo.ncols) p.colmask |= 1u << u;
+    } else {
+        const int c = tid % SH::BN, j0 = tid / SH::BN;
         const long long cc = c0 + c;
-        const bool v = cc < a.geo.ncols;
-        if (v) p.fmask |= 1u << u;
-        p.fb[u] = fbase(v ? cc : 0, a.geo.L, a.geo.n);
-        p.jr[u] = j;
-        p.xs[u] = 8u * (j * SH::LDX + c);
+        const bool cv = cc < a.geo.ncols;
+        p.jr0 = j0;
+        p.jrstep = SH::XROWSTEP;
+        p.xs = 8u * (j0 * SH::LDX + c);
+        p.xsstep = 8u * SH::XROWSTEP * SH::LDX;
+        p.xg = X + fbase(cv ? cc : 0, a.geo.L, a.geo.n);
+        p.xstep = 0;  // the element's chunk row carries the stride
+        p.colmask = cv ? 0xffffffffu : 0u;
     }
     p.jp2 = 2 * (tid & 7);
     p.js = 8u * ((tid >> 3) * kLDJ + p.jp2);
@@ -136,10 +149,10 @@ __device__ __forceinline__ FProd<SH> make_fprod(const FArgs& a, long long c0, co
 }
 
 // Chunk q: matrix columns [16q, 16q+16) of both folded matrices; fiber rows ra0 + r (Xa) and
-// rb0 + r (Xb), r = 0..15, zero-filled outside [0, n).
+// rb0 + r (Xb), r = 0..15, zero-filled outside [0, n).  Interior chunks of full tiles take the
+// unpredicated path.
 template <class SH, bool FWD>
-__device__ __forceinline__ void fissue(const FArgs& a, const FProd<SH>& p, unsigned st, int q, const double* X,
-                                       const double* J) {
+__device__ __forceinline__ void fissue(const FArgs& a, const FProd& p, unsigned st, int q, const double* X) {
     const int k0 = q * kBK;
     const int kw = min(kBK, a.Kp - k0);
     if (p.jp2 < kw) {
@@ -154,68 +167,90 @@ __device__ __forceinline__ void fissue(const FArgs& a, const FProd<SH>& p, unsig
         }
     }
     const int n = a.geo.n;
-    const long long L = a.geo.L;
     const int ra0 = k0, rb0 = FWD ? n - k0 - kBK : a.F + k0;
+    const double* xa = p.xg + p.L * ra0;
+    const double* xb = p.xg + p.L * rb0;
+    const unsigned sa = st + p.xs, sb = st + 8u * SH::XB + p.xs;
+    if (p.full_tile && ra0 + kBK <= n && rb0 >= 0 && rb0 + kBK <= n) {
 #pragma unroll
-    for (int u = 0; u < SH::XCNT; ++u) {
-        const bool fv = (p.fmask >> u) & 1u;
-        const int ra = ra0 + p.jr[u], rb = rb0 + p.jr[u];
-        const bool va = fv && ra < n, vb = fv && rb >= 0 && rb < n;
-        cp8z(st + p.xs[u], va ? X + p.fb[u] + L * ra : X, va);
-        cp8z(st + 8u * SH::XB + p.xs[u], vb ? X + p.fb[u] + L * rb : X, vb);
+        for (int u = 0; u < SH::XCNT; ++u) {
+            const long long o = u * p.xstep + p.L * (p.jr0 + u * p.jrstep);
+            cp8z(sa + u * p.xsstep, xa + o, true);
+            cp8z(sb + u * p.xsstep, xb + o, true);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < SH::XCNT; ++u) {
+            const int jr = p.jr0 + u * p.jrstep;
+            const bool fv = (p.colmask >> u) & 1u;
+            const bool va = fv && ra0 + jr < n, vb = fv && rb0 + jr >= 0 && rb0 + jr < n;
+            const long long o = u * p.xstep + p.L * jr;
+            cp8z(sa + u * p.xsstep, va ? xa + o : X, va);
+            cp8z(sb + u * p.xsstep, vb ? xb + o : X, vb);
+        }
     }
 }
 
+template <class SH, bool FWD>
+__device__ __forceinline__ void fload(const double* ja, const double* xa, const double* xb, int kk, int mact,
+                                      double (&a1)[SH::MI], double (&a2)[SH::MI], double (&b1)[SH::NI],
+                                      double (&b2)[SH::NI]) {
+#pragma unroll
+    for (int mi = 0; mi < SH::MI; ++mi) {
+        a1[mi] = mi < mact ? ja[mi * 8 * kLDJ + kk * 4] : 0.0;
+        a2[mi] = mi < mact ? ja[(SH::J2 - SH::J1) + mi * 8 * kLDJ + kk * 4] : 0.0;
+    }
+#pragma unroll
+    for (int ni = 0; ni < SH::NI; ++ni) {
+        const double u = xa[kk * 4 * SH::LDX + ni * 8];
+        if (FWD) {  // xb points at mirrored row 15 - t; rows run backwards
+            const double w = xb[-kk * 4 * SH::LDX + ni * 8];
+            b1[ni] = u + w;
+            b2[ni] = u - w;
+        } else {
+            b1[ni] = u;
+            b2[ni] = xb[kk * 4 * SH::LDX + ni * 8];
+        }
+    }
+}
+
+// Both folded products over KS k-steps of 4, fragments double-buffered in registers.
 template <class SH, bool FWD, int KS>
 __device__ __forceinline__ void fmma(const double* ja, const double* xa, const double* xb, int mact,
                                      double (&c1)[SH::MI][SH::NI][2], double (&c2)[SH::MI][SH::NI][2]) {
     constexpr int MI = SH::MI, NI = SH::NI;
+    double a1[2][MI], a2[2][MI], b1[2][NI], b2[2][NI];
+    fload<SH, FWD>(ja, xa, xb, 0, mact, a1[0], a2[0], b1[0], b2[0]);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
-        double a1[MI], a2[MI], b1[NI], b2[NI];
-#pragma unroll
-        for (int mi = 0; mi < MI; ++mi) {
-            a1[mi] = mi < mact ? ja[mi * 8 * kLDJ + kk * 4] : 0.0;
-            a2[mi] = mi < mact ? ja[(SH::J2 - SH::J1) + mi * 8 * kLDJ + kk * 4] : 0.0;
-        }
-#pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-            const double u = xa[kk * 4 * SH::LDX + ni * 8];
-            if (FWD) {  // xb points at mirrored row 15 - t; rows run backwards
-                const double w = xb[-kk * 4 * SH::LDX + ni * 8];
-                b1[ni] = u + w;
-                b2[ni] = u - w;
-            } else {
-                b1[ni] = u;
-                b2[ni] = xb[kk * 4 * SH::LDX + ni * 8];
-            }
-        }
+        const int cur = kk & 1, nxt = cur ^ 1;
+        if (kk + 1 < KS) fload<SH, FWD>(ja, xa, xb, kk + 1, mact, a1[nxt], a2[nxt], b1[nxt], b2[nxt]);
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni)
                 if (mi < mact) {
-                    dmma(c1[mi][ni][0], c1[mi][ni][1], a1[mi], b1[ni]);
-                    dmma(c2[mi][ni][0], c2[mi][ni][1], a2[mi], b2[ni]);
+                    dmma(c1[mi][ni][0], c1[mi][ni][1], a1[cur][mi], b1[cur][ni]);
+                    dmma(c2[mi][ni][0], c2[mi][ni][1], a2[cur][mi], b2[cur][ni]);
                 }
     }
 }
 
-template <int MI, int WN, bool FWD>
+template <int MI, int WN, int NI, bool FWD>
 __global__ void __launch_bounds__(32 * WN)
     fold_mode_kernel(FArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
                      const double* __restrict__ post) {
-    using SH = FShape<MI, WN>;
+    using SH = FShape<MI, WN, NI>;
     extern __shared__ __align__(16) double smem[];
     const int rb = blockIdx.x % a.RB;
     const long long c0 = static_cast<long long>(blockIdx.x / a.RB) * SH::BN;
     const int strip0 = rb * MI;
-    const FProd<SH> p = make_fprod<SH>(a, c0, J + static_cast<size_t>(rb) * SH::MPB * a.Kp);
-    double c1[MI][SH::NI][2], c2[MI][SH::NI][2];
+    const FProd p = make_fprod<SH>(a, c0, X, J + static_cast<size_t>(rb) * SH::MPB * a.Kp);
+    double c1[MI][NI][2], c2[MI][NI][2];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < SH::NI; ++ni) c1[mi][ni][0] = c1[mi][ni][1] = c2[mi][ni][0] = c2[mi][ni][1] = 0.0;
+        for (int ni = 0; ni < NI; ++ni) c1[mi][ni][0] = c1[mi][ni][1] = c2[mi][ni][0] = c2[mi][ni][1] = 0.0;
 
     const int nchunks = (a.Kp + kBK - 1) / kBK;
     const int ns = a.nstage;
@@ -224,12 +259,12 @@ __global__ void __launch_bounds__(32 * WN)
     const int mact = min(MI, max(0, a.S - strip0));
     const unsigned st0 = smem_u32(smem);
     for (int s = 0; s < ns - 1; ++s) {
-        if (s < nchunks) fissue<SH, FWD>(a, p, st0 + 8u * s * SH::STAGE, s, X, J);
+        if (s < nchunks) fissue<SH, FWD>(a, p, st0 + 8u * s * SH::STAGE, s, X);
         commit();
     }
     const int ja_off = SH::J1 + g * kLDJ + t;
-    const int xa_off = t * SH::LDX + wn * SH::NI * 8 + g;
-    const int xb_off = SH::XB + (FWD ? (kBK - 1 - t) : t) * SH::LDX + wn * SH::NI * 8 + g;
+    const int xa_off = t * SH::LDX + wn * NI * 8 + g;
+    const int xb_off = SH::XB + (FWD ? (kBK - 1 - t) : t) * SH::LDX + wn * NI * 8 + g;
     int stage = 0;
     for (int q = 0; q < nchunks; ++q) {
         if (ns >= 3) wait_n<1>();
@@ -239,7 +274,7 @@ __global__ void __launch_bounds__(32 * WN)
         if (nq < nchunks) {
             int nst = stage + ns - 1;
             if (nst >= ns) nst -= ns;
-            fissue<SH, FWD>(a, p, st0 + 8u * nst * SH::STAGE, nq, X, J);
+            fissue<SH, FWD>(a, p, st0 + 8u * nst * SH::STAGE, nq, X);
         }
         commit();
         const double* sb = smem + stage * SH::STAGE;
@@ -254,13 +289,13 @@ __global__ void __launch_bounds__(32 * WN)
     // register epilogue
     const int n = a.geo.n;
     const long long L = a.geo.L;
-    long long ob[SH::NI][2];
-    bool cv[SH::NI][2];
+    long long ob[NI][2];
+    bool cv[NI][2];
 #pragma unroll
-    for (int ni = 0; ni < SH::NI; ++ni)
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-            const long long cc = c0 + (wn * SH::NI + ni) * 8 + 2 * t + v;
+            const long long cc = c0 + (wn * NI + ni) * 8 + 2 * t + v;
             cv[ni][v] = cc < a.geo.ncols;
             ob[ni][v] = fbase(cv[ni][v] ? cc : 0, L, n);
         }
@@ -268,7 +303,7 @@ __global__ void __launch_bounds__(32 * WN)
     for (int mi = 0; mi < MI; ++mi) {
         const int i = (strip0 + mi) * 8 + g;
 #pragma unroll
-        for (int ni = 0; ni < SH::NI; ++ni)
+        for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
                 if (!cv[ni][v]) continue;
@@ -314,10 +349,10 @@ FArgs make_fargs(const Tiling& t, const ModeGeom& g) {
     return a;
 }
 
-template <int MI, int WN>
+template <int MI, int WN, int NI>
 cudaError_t fold_launch_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
                           const double* post, bool fwd, cudaStream_t st, int* occ) {
-    auto k = fwd ? fold_mode_kernel<MI, WN, true> : fold_mode_kernel<MI, WN, false>;
+    auto k = fwd ? fold_mode_kernel<MI, WN, NI, true> : fold_mode_kernel<MI, WN, NI, false>;
     if (occ) {
         *occ = occ_of(k, 32 * WN, t.smem);
         return cudaSuccess;
@@ -329,25 +364,36 @@ cudaError_t fold_launch_t(const Tiling& t, const ModeGeom& g, const double* X, d
     return cudaGetLastError();
 }
 
-template <int WN>
+template <int WN, int NI>
 cudaError_t fold_dispatch_wn(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
                              const double* post, bool fwd, cudaStream_t st, int* occ) {
-    switch (t.MI) {
-        case 1: return fold_launch_t<1, WN>(t, g, X, Y, J, post, fwd, st, occ);
-        case 2: return fold_launch_t<2, WN>(t, g, X, Y, J, post, fwd, st, occ);
-        case 3: return fold_launch_t<3, WN>(t, g, X, Y, J, post, fwd, st, occ);
-        case 4: return fold_launch_t<4, WN>(t, g, X, Y, J, post, fwd, st, occ);
-        case 5: return fold_launch_t<5, WN>(t, g, X, Y, J, post, fwd, st, occ);
-        case 6: return fold_launch_t<6, WN>(t, g, X, Y, J, post, fwd, st, occ);
-        case 7: return fold_launch_t<7, WN>(t, g, X, Y, J, post, fwd, st, occ);
-        default: return cudaErrorInvalidValue;
+    if constexpr (NI == 4) {  // 16 MI accumulators: spills beyond MI = 3
+        switch (t.MI) {
+            case 1: return fold_launch_t<1, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 2: return fold_launch_t<2, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 3: return fold_launch_t<3, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            default: return cudaErrorInvalidValue;
+        }
+    } else {
+        switch (t.MI) {
+            case 1: return fold_launch_t<1, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 2: return fold_launch_t<2, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 3: return fold_launch_t<3, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 4: return fold_launch_t<4, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 5: return fold_launch_t<5, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 6: return fold_launch_t<6, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 7: return fold_launch_t<7, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            default: return cudaErrorInvalidValue;
+        }
     }
 }
 
 cudaError_t fold_dispatch(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
                           const double* post, bool fwd, cudaStream_t st, int* occ) {
-    if (t.WN == 4) return fold_dispatch_wn<4>(t, g, X, Y, J, post, fwd, st, occ);
-    if (t.WN == 2) return fold_dispatch_wn<2>(t, g, X, Y, J, post, fwd, st, occ);
+    if (t.NI == 2 && t.WN == 4) return fold_dispatch_wn<4, 2>(t, g, X, Y, J, post, fwd, st, occ);
+    if (t.NI == 2 && t.WN == 2) return fold_dispatch_wn<2, 2>(t, g, X, Y, J, post, fwd, st, occ);
+    if (t.NI == 4 && t.WN == 2) return fold_dispatch_wn<2, 4>(t, g, X, Y, J, post, fwd, st, occ);
+    if (t.NI == 4 && t.WN == 4) return fold_dispatch_wn<4, 4>(t, g, X, Y, J, post, fwd, st, occ);
     return cudaErrorInvalidValue;
 }
 
@@ -362,20 +408,22 @@ std::vector<Tiling> fold_tiling_candidates(int n) {
     for (int MI = 1; MI <= 7; ++MI) {
         const int RB = (S + MI - 1) / MI;
         if ((S + RB - 1) / RB != MI) continue;  // a smaller MI covers the strips with as many row blocks
-        for (int WN : {4, 2}) {
+        for (int WN : {4, 2})
+        for (int NI : {2, 4}) {
+            if (NI == 4 && MI > 3) continue;  // 16 MI accumulators
             for (int ns : {3, 2}) {
                 Tiling t;
                 t.fold = 1;
                 t.MI = MI;
                 t.WM = 1;
-                t.NI = 2;
+                t.NI = NI;
                 t.WN = WN;
                 t.S = S;
                 t.RB = RB;
                 t.MpB = 8 * MI;
                 t.Mp = RB * t.MpB;
                 t.Kp = Kp;
-                t.BN = 16 * WN;
+                t.BN = 8 * NI * WN;
                 t.LDX = t.BN + 4;
                 t.nstage = ns;
                 t.smem = sizeof(double) * static_cast<size_t>(ns) * (2 * kBK * t.LDX + 2 * t.MpB * kLDJ);
@@ -385,7 +433,7 @@ std::vector<Tiling> fold_tiling_candidates(int n) {
                 t.ctas_per_sm = occ;
                 if (occ < 1) continue;
                 const double eff = 0.85 + 0.15 * static_cast<double>(S) / (RB * MI);
-                c.emplace_back(std::min(occ * WN, 16) * eff - 0.05 * RB + 0.02 * WN + 0.01 * ns, t);
+                c.emplace_back(std::min(occ * WN, 16) * eff - 0.05 * RB + 0.02 * WN + 0.01 * ns + 0.03 * NI, t);
             }
         }
     }
