@@ -236,7 +236,7 @@ __device__ __forceinline__ void fmma(const double* ja, const double* xa, const d
     }
 }
 
-template <int MI, int WN, int NI, bool FWD>
+template <int MI, int WN, int NI, bool FWD, bool POST>
 __global__ void __launch_bounds__(32 * WN)
     fold_mode_kernel(FArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
                      const double* __restrict__ post) {
@@ -299,6 +299,39 @@ __global__ void __launch_bounds__(32 * WN)
             cv[ni][v] = cc < a.geo.ncols;
             ob[ni][v] = fbase(cv[ni][v] ? cc : 0, L, n);
         }
+    if constexpr (!FWD && POST) {  // D^-1/2 post-scale: every scale load issued before the first store
+        double plo[MI][NI][2], phi[MI][NI][2];
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+            const int i = (strip0 + mi) * 8 + g;
+            const int ilo = i < a.F ? i : 0, ihi = i < a.h ? n - 1 - i : 0;
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    plo[mi][ni][v] = cv[ni][v] ? __ldg(post + ob[ni][v] + L * ilo) : 0.0;
+                    phi[mi][ni][v] = cv[ni][v] ? __ldg(post + ob[ni][v] + L * ihi) : 0.0;
+                }
+        }
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+            const int i = (strip0 + mi) * 8 + g;
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    if (!cv[ni][v]) continue;
+                    double* y = Y + ob[ni][v];
+                    if (i < a.h) {
+                        y[L * i] = plo[mi][ni][v] * (c1[mi][ni][v] + c2[mi][ni][v]);
+                        y[L * (n - 1 - i)] = phi[mi][ni][v] * (c1[mi][ni][v] - c2[mi][ni][v]);
+                    } else if (i < a.F) {  // middle row (odd n)
+                        y[L * i] = plo[mi][ni][v] * c1[mi][ni][v];
+                    }
+                }
+        }
+        return;
+    }
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
         const int i = (strip0 + mi) * 8 + g;
@@ -308,18 +341,14 @@ __global__ void __launch_bounds__(32 * WN)
             for (int v = 0; v < 2; ++v) {
                 if (!cv[ni][v]) continue;
                 double* y = Y + ob[ni][v];
-                const double* ps = post ? post + ob[ni][v] : nullptr;
                 if (FWD) {
                     if (i < a.F) y[L * i] = c1[mi][ni][v];
                     if (i < a.h) y[L * (a.F + i)] = c2[mi][ni][v];
                 } else if (i < a.h) {
-                    const long long lo = L * i, hi = L * (n - 1 - i);
-                    const double s1 = c1[mi][ni][v] + c2[mi][ni][v], s2 = c1[mi][ni][v] - c2[mi][ni][v];
-                    y[lo] = ps ? __ldg(ps + lo) * s1 : s1;
-                    y[hi] = ps ? __ldg(ps + hi) * s2 : s2;
+                    y[L * i] = c1[mi][ni][v] + c2[mi][ni][v];
+                    y[L * (n - 1 - i)] = c1[mi][ni][v] - c2[mi][ni][v];
                 } else if (i < a.F) {  // middle row (odd n)
-                    const long long mid = L * i;
-                    y[mid] = ps ? __ldg(ps + mid) * c1[mi][ni][v] : c1[mi][ni][v];
+                    y[L * i] = c1[mi][ni][v];
                 }
             }
     }
@@ -352,7 +381,8 @@ FArgs make_fargs(const Tiling& t, const ModeGeom& g) {
 template <int MI, int WN, int NI>
 cudaError_t fold_launch_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
                           const double* post, bool fwd, cudaStream_t st, int* occ) {
-    auto k = fwd ? fold_mode_kernel<MI, WN, NI, true> : fold_mode_kernel<MI, WN, NI, false>;
+    auto k = fwd ? fold_mode_kernel<MI, WN, NI, true, false>
+                 : (post ? fold_mode_kernel<MI, WN, NI, false, true> : fold_mode_kernel<MI, WN, NI, false, false>);
     if (occ) {
         *occ = occ_of(k, 32 * WN, t.smem);
         return cudaSuccess;
