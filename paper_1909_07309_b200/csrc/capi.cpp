@@ -173,8 +173,8 @@ struct stiga_fd_s {
     void mprod(const gpu::Tiling& t, int l, bool backward, const gpu::ModeGeom& g, const double* src, double* dst,
                const double* post, cudaStream_t st, const double* pre = nullptr, const gpu::Scatter* sc = nullptr) {
         if (t.fold) {
-            if (pre || sc) throw std::runtime_error("internal: folded product with pre-scale / scatter");
-            ck(gpu::launch_fold_product(t, g, src, dst, backward ? Jfb[l]->p : Jft[l]->p, !backward, post, st),
+            if (sc) throw std::runtime_error("internal: folded product with a scatter epilogue");
+            ck(gpu::launch_fold_product(t, g, src, dst, backward ? Jfb[l]->p : Jft[l]->p, !backward, post, st, pre),
                "fd folded mode product");
         } else {
             ck(gpu::launch_mode_product(t, g, src, dst, backward ? J[l]->p : Jt[l]->p, post, st, pre, sc),
@@ -373,19 +373,18 @@ struct stiga_fd_s {
                 mprod(tl[0], 0, false, geom(0), scratch2.p, scratch.p, nullptr, nullptr);
             });
             float best_fus = 1e30f;
-            for (size_t c = 0; c < std::min(kMaxCand, cand_space[0].size()); ++c) {
+            size_t n_fold = 0, n_dense = 0;
+            for (size_t c = 0; c < cand_space[0].size(); ++c) {
                 const gpu::Tiling& t = cand_space[0][c];
                 if (!gpu::prescale_fits(t)) continue;
-                const float ms = time_once([&] {
-                    ck(gpu::launch_mode_product(t, geom(0), scratch.p, scratch2.p, Jt[0]->p, nullptr, nullptr, dinv.p),
-                       "tune");
-                });
+                if ((t.fold ? n_fold : n_dense)++ >= kMaxCand) continue;
+                const float ms = time_once([&] { mprod(t, 0, false, geom(0), scratch.p, scratch2.p, nullptr, nullptr, dinv.p); });
                 if (ms < best_fus) { best_fus = ms; tl_pre = t; pick_pre = static_cast<int>(c); }
             }
             use_fused_pre = pick_pre >= 0 && best_fus < sep;
             if (debug_tune)
-                std::fprintf(stderr, "[stiga tune] pre-scale separate %.4f ms, fused %.4f ms (MI=%d RB=%d)\n", sep,
-                             best_fus, tl_pre.MI, tl_pre.RB);
+                std::fprintf(stderr, "[stiga tune] pre-scale separate %.4f ms, fused %.4f ms (%s MI=%d RB=%d)\n", sep,
+                             best_fus, tl_pre.fold ? "folded" : "dense", tl_pre.MI, tl_pre.RB);
         }
         const bool fused_ok = !cand_time.empty();
         tl_t = fused_ok ? cand_time.front() : gpu::Tiling{};

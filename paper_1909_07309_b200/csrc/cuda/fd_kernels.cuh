@@ -108,9 +108,12 @@ bool prescale_fits(const Tiling& t);
 /// dense product.  Jfold holds the two folded matrices, each row-major zero-padded t.Mp x t.Kp,
 /// the second at offset t.Mp*t.Kp: forward (U^T) [A_e; A_o], backward (U) [A_p; A_q].
 /// post_scale (backward only) multiplies the outputs elementwise.
+/// pre_scale (forward only) multiplies both staged fiber chunks by D^-1/2 as the fold is formed.
 std::vector<Tiling> fold_tiling_candidates(int n);
 cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
-                                bool forward, const double* post_scale, cudaStream_t stream);
+                                bool forward, const double* post_scale, cudaStream_t stream,
+                                const double* pre_scale = nullptr);
+size_t fold_prescale_smem(const Tiling& t);
 
 /// Standalone block-arrowhead solve X = (gamma Delta_t (x) I + nu I (x) Lambda_s)^-1 Z on the
 /// time-eigen-coordinate tensor (N_s x n_t, time slowest); used when the time direction runs as

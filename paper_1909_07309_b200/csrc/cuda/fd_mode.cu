@@ -89,7 +89,10 @@ size_t prescale_smem(const Tiling& t) {
     return t.smem + sizeof(double) * static_cast<size_t>(t.nstage) * kBK * t.LDX;
 }
 
-bool prescale_fits(const Tiling& t) { return !t.fold && t.WM == 1 && prescale_smem(t) <= kSmemPerCTA; }
+bool prescale_fits(const Tiling& t) {
+    if (t.fold) return fold_prescale_smem(t) <= kSmemPerCTA;
+    return t.WM == 1 && prescale_smem(t) <= kSmemPerCTA;
+}
 
 cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jpad,
                                 const double* post_scale, cudaStream_t st, const double* pre_scale, const Scatter* sc) {

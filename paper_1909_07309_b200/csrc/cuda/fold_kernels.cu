@@ -69,9 +69,10 @@ struct FArgs {
     long long A2;  // offset (doubles) of the second folded matrix after the first (Mp * Kp)
 };
 
-template <int MI_, int WN_, int NI_>
+template <int MI_, int WN_, int NI_, bool PS_ = false>
 struct FShape {
     static constexpr int MI = MI_, WN = WN_, NI = NI_;
+    static constexpr bool PS = PS_;  // forward only: D^-1/2 pre-scale chunks staged beside both fiber chunks
     static constexpr int NTHR = 32 * WN;
     static constexpr int BN = 8 * NI * WN;
     static constexpr int LDX = BN + 4;            // == 4 mod 16 doubles: conflict-free B fragments
@@ -86,7 +87,8 @@ struct FShape {
     static constexpr int XB = kBK * LDX;
     static constexpr int J1 = 2 * kBK * LDX;
     static constexpr int J2 = J1 + MPB * kLDJ;
-    static constexpr int STAGE = J2 + MPB * kLDJ;
+    static constexpr int DA = J2 + MPB * kLDJ;       // PS: D chunk of Xa's rows (then Xb's at DA + XB)
+    static constexpr int STAGE = DA + (PS ? 2 * kBK * LDX : 0);
 };
 
 __device__ __forceinline__ long long fbase(long long cc, long long L, int n) {
@@ -152,7 +154,8 @@ __device__ __forceinline__ FProd make_fprod(const FArgs& a, long long c0, const 
 // rb0 + r (Xb), r = 0..15, zero-filled outside [0, n).  Interior chunks of full tiles take the
 // unpredicated path.
 template <class SH, bool FWD>
-__device__ __forceinline__ void fissue(const FArgs& a, const FProd& p, unsigned st, int q, const double* X) {
+__device__ __forceinline__ void fissue(const FArgs& a, const FProd& p, unsigned st, int q, const double* X,
+                                       const double* Dp = nullptr) {
     const int k0 = q * kBK;
     const int kw = min(kBK, a.Kp - k0);
     if (p.jp2 < kw) {
@@ -171,12 +174,18 @@ __device__ __forceinline__ void fissue(const FArgs& a, const FProd& p, unsigned 
     const double* xa = p.xg + p.L * ra0;
     const double* xb = p.xg + p.L * rb0;
     const unsigned sa = st + p.xs, sb = st + 8u * SH::XB + p.xs;
+    const long long dofs = SH::PS ? Dp - X : 0;  // D^-1/2 element = X element + dofs
+    const unsigned dsa = 8u * (SH::DA - 0), dsb = 8u * SH::DA;  // D chunks: Xa's at DA, Xb's at DA + XB
     if (p.full_tile && ra0 + kBK <= n && rb0 >= 0 && rb0 + kBK <= n) {
 #pragma unroll
         for (int u = 0; u < SH::XCNT; ++u) {
             const long long o = u * p.xstep + p.L * (p.jr0 + u * p.jrstep);
             cp8z(sa + u * p.xsstep, xa + o, true);
             cp8z(sb + u * p.xsstep, xb + o, true);
+            if constexpr (SH::PS) {
+                cp8z(sa + dsa + u * p.xsstep, xa + o + dofs, true);
+                cp8z(sb + dsb + u * p.xsstep, xb + o + dofs, true);
+            }
         }
     } else {
 #pragma unroll
@@ -187,6 +196,10 @@ __device__ __forceinline__ void fissue(const FArgs& a, const FProd& p, unsigned 
             const long long o = u * p.xstep + p.L * jr;
             cp8z(sa + u * p.xsstep, va ? xa + o : X, va);
             cp8z(sb + u * p.xsstep, vb ? xb + o : X, vb);
+            if constexpr (SH::PS) {
+                cp8z(sa + dsa + u * p.xsstep, va ? xa + o + dofs : Dp, va);
+                cp8z(sb + dsb + u * p.xsstep, vb ? xb + o + dofs : Dp, vb);
+            }
         }
     }
 }
@@ -202,9 +215,11 @@ __device__ __forceinline__ void fload(const double* ja, const double* xa, const 
     }
 #pragma unroll
     for (int ni = 0; ni < SH::NI; ++ni) {
-        const double u = xa[kk * 4 * SH::LDX + ni * 8];
+        double u = xa[kk * 4 * SH::LDX + ni * 8];
+        if (SH::PS) u *= xa[SH::DA + kk * 4 * SH::LDX + ni * 8];
         if (FWD) {  // xb points at mirrored row 15 - t; rows run backwards
-            const double w = xb[-kk * 4 * SH::LDX + ni * 8];
+            double w = xb[-kk * 4 * SH::LDX + ni * 8];
+            if (SH::PS) w *= xb[SH::DA - kk * 4 * SH::LDX + ni * 8];
             b1[ni] = u + w;
             b2[ni] = u - w;
         } else {
@@ -236,11 +251,11 @@ __device__ __forceinline__ void fmma(const double* ja, const double* xa, const d
     }
 }
 
-template <int MI, int WN, int NI, bool FWD, bool POST>
+template <int MI, int WN, int NI, bool FWD, bool POST, bool PS>
 __global__ void __launch_bounds__(32 * WN)
     fold_mode_kernel(FArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
-                     const double* __restrict__ post) {
-    using SH = FShape<MI, WN, NI>;
+                     const double* __restrict__ post, const double* __restrict__ pre) {
+    using SH = FShape<MI, WN, NI, PS>;
     extern __shared__ __align__(16) double smem[];
     const int rb = blockIdx.x % a.RB;
     const long long c0 = static_cast<long long>(blockIdx.x / a.RB) * SH::BN;
@@ -259,7 +274,7 @@ __global__ void __launch_bounds__(32 * WN)
     const int mact = min(MI, max(0, a.S - strip0));
     const unsigned st0 = smem_u32(smem);
     for (int s = 0; s < ns - 1; ++s) {
-        if (s < nchunks) fissue<SH, FWD>(a, p, st0 + 8u * s * SH::STAGE, s, X);
+        if (s < nchunks) fissue<SH, FWD>(a, p, st0 + 8u * s * SH::STAGE, s, X, pre);
         commit();
     }
     const int ja_off = SH::J1 + g * kLDJ + t;
@@ -274,7 +289,7 @@ __global__ void __launch_bounds__(32 * WN)
         if (nq < nchunks) {
             int nst = stage + ns - 1;
             if (nst >= ns) nst -= ns;
-            fissue<SH, FWD>(a, p, st0 + 8u * nst * SH::STAGE, nq, X);
+            fissue<SH, FWD>(a, p, st0 + 8u * nst * SH::STAGE, nq, X, pre);
         }
         commit();
         const double* sb = smem + stage * SH::STAGE;
@@ -380,50 +395,53 @@ FArgs make_fargs(const Tiling& t, const ModeGeom& g) {
 
 template <int MI, int WN, int NI>
 cudaError_t fold_launch_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                          const double* post, bool fwd, cudaStream_t st, int* occ) {
-    auto k = fwd ? fold_mode_kernel<MI, WN, NI, true, false>
-                 : (post ? fold_mode_kernel<MI, WN, NI, false, true> : fold_mode_kernel<MI, WN, NI, false, false>);
+                          const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
+    auto k = fwd ? (pre ? fold_mode_kernel<MI, WN, NI, true, false, true>
+                        : fold_mode_kernel<MI, WN, NI, true, false, false>)
+                 : (post ? fold_mode_kernel<MI, WN, NI, false, true, false>
+                         : fold_mode_kernel<MI, WN, NI, false, false, false>);
+    const size_t smem = pre ? fold_prescale_smem(t) : t.smem;
     if (occ) {
-        *occ = occ_of(k, 32 * WN, t.smem);
+        *occ = occ_of(k, 32 * WN, smem);
         return cudaSuccess;
     }
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(t.smem));
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const long long blocks = (g.ncols + t.BN - 1) / t.BN * t.RB;
-    k<<<static_cast<unsigned>(blocks), 32 * WN, t.smem, st>>>(make_fargs(t, g), X, Y, J, post);
+    k<<<static_cast<unsigned>(blocks), 32 * WN, smem, st>>>(make_fargs(t, g), X, Y, J, post, pre);
     return cudaGetLastError();
 }
 
 template <int WN, int NI>
 cudaError_t fold_dispatch_wn(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                             const double* post, bool fwd, cudaStream_t st, int* occ) {
+                             const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
     if constexpr (NI == 4) {  // 16 MI accumulators: spills beyond MI = 3
         switch (t.MI) {
-            case 1: return fold_launch_t<1, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
-            case 2: return fold_launch_t<2, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
-            case 3: return fold_launch_t<3, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 1: return fold_launch_t<1, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
+            case 2: return fold_launch_t<2, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
+            case 3: return fold_launch_t<3, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
             default: return cudaErrorInvalidValue;
         }
     } else {
         switch (t.MI) {
-            case 1: return fold_launch_t<1, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
-            case 2: return fold_launch_t<2, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
-            case 3: return fold_launch_t<3, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
-            case 4: return fold_launch_t<4, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
-            case 5: return fold_launch_t<5, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
-            case 6: return fold_launch_t<6, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
-            case 7: return fold_launch_t<7, WN, NI>(t, g, X, Y, J, post, fwd, st, occ);
+            case 1: return fold_launch_t<1, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
+            case 2: return fold_launch_t<2, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
+            case 3: return fold_launch_t<3, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
+            case 4: return fold_launch_t<4, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
+            case 5: return fold_launch_t<5, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
+            case 6: return fold_launch_t<6, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
+            case 7: return fold_launch_t<7, WN, NI>(t, g, X, Y, J, post, pre, fwd, st, occ);
             default: return cudaErrorInvalidValue;
         }
     }
 }
 
 cudaError_t fold_dispatch(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                          const double* post, bool fwd, cudaStream_t st, int* occ) {
-    if (t.NI == 2 && t.WN == 4) return fold_dispatch_wn<4, 2>(t, g, X, Y, J, post, fwd, st, occ);
-    if (t.NI == 2 && t.WN == 2) return fold_dispatch_wn<2, 2>(t, g, X, Y, J, post, fwd, st, occ);
-    if (t.NI == 4 && t.WN == 2) return fold_dispatch_wn<2, 4>(t, g, X, Y, J, post, fwd, st, occ);
-    if (t.NI == 4 && t.WN == 4) return fold_dispatch_wn<4, 4>(t, g, X, Y, J, post, fwd, st, occ);
+                          const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
+    if (t.NI == 2 && t.WN == 4) return fold_dispatch_wn<4, 2>(t, g, X, Y, J, post, pre, fwd, st, occ);
+    if (t.NI == 2 && t.WN == 2) return fold_dispatch_wn<2, 2>(t, g, X, Y, J, post, pre, fwd, st, occ);
+    if (t.NI == 4 && t.WN == 2) return fold_dispatch_wn<2, 4>(t, g, X, Y, J, post, pre, fwd, st, occ);
+    if (t.NI == 4 && t.WN == 4) return fold_dispatch_wn<4, 4>(t, g, X, Y, J, post, pre, fwd, st, occ);
     return cudaErrorInvalidValue;
 }
 
@@ -459,7 +477,7 @@ std::vector<Tiling> fold_tiling_candidates(int n) {
                 t.smem = sizeof(double) * static_cast<size_t>(ns) * (2 * kBK * t.LDX + 2 * t.MpB * kLDJ);
                 if (t.smem > kSmemPerCTA) continue;
                 int occ = 0;
-                fold_dispatch(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, true, nullptr, &occ);
+                fold_dispatch(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, nullptr, true, nullptr, &occ);
                 t.ctas_per_sm = occ;
                 if (occ < 1) continue;
                 const double eff = 0.85 + 0.15 * static_cast<double>(S) / (RB * MI);
@@ -474,10 +492,16 @@ std::vector<Tiling> fold_tiling_candidates(int n) {
 }
 
 cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
-                                bool forward, const double* post_scale, cudaStream_t st) {
+                                bool forward, const double* post_scale, cudaStream_t st, const double* pre_scale) {
     if (g.ncols <= 0) return cudaSuccess;
-    if (!t.fold || g.m != g.n || g.n < 2 || (forward && post_scale)) return cudaErrorInvalidValue;
-    return fold_dispatch(t, g, X, Y, Jfold, post_scale, forward, st, nullptr);
+    if (!t.fold || g.m != g.n || g.n < 2 || (forward && post_scale) || (!forward && pre_scale))
+        return cudaErrorInvalidValue;
+    if (pre_scale && fold_prescale_smem(t) > kSmemPerCTA) return cudaErrorInvalidValue;
+    return fold_dispatch(t, g, X, Y, Jfold, post_scale, pre_scale, forward, st, nullptr);
+}
+
+size_t fold_prescale_smem(const Tiling& t) {
+    return t.smem + sizeof(double) * static_cast<size_t>(t.nstage) * 2 * kBK * t.LDX;
 }
 
 }  // namespace gpu
