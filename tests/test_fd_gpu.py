@@ -195,10 +195,11 @@ def _oracle_with_product_basis(Po, P, d, gamma=1.0, nu=1.0):
     return Po
 
 
-@pytest.mark.parametrize("cfg_name", ["c2", "c4"])
+@pytest.mark.parametrize("cfg_name", ["c2", "c3", "c4", "c5p2"])
 def test_fd_apply_parity_full_baseline_configs(cfg_name):
     """Full-size BASELINE configs against the oracle apply (oracle/fdsolve.py, fdsolve.cpp:155-164)
-    built from the same host pieces: c2 (17.0M DoF, identity geometry, split time path) and c4
+    built from the same host pieces: c2 (17.0M DoF, identity geometry, split time path, folded
+    spatial products), c3 (89.4M DoF, d = 3, fused time kernel), c5p2 (17.0M DoF, p = 2) and c4
     (19.3M DoF, fitted deformed cube with kappa(x), c(x) and the D^-1/2 geometry scaling).  The
     pieces themselves are pinned against the oracle at small sizes (test_geometry.py).
 
