@@ -303,6 +303,8 @@ class FusedShardedExtendedFD:
         return self
 
     def close(self):
+        """Releases the peer mappings and this rank's receive buffers.  Call it on every rank after a
+        group barrier that follows the last apply (a peer may still be storing into these buffers)."""
         L = lib()
         for p, kind in self._owned:
             if kind == "ipc":
