@@ -60,6 +60,8 @@ __device__ __forceinline__ void wait_n() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
 struct FArgs {
     ModeGeom geo;
     int F, h;      // folded length F = h + (n mod 2), h = n / 2
@@ -69,11 +71,14 @@ struct FArgs {
     long long A2;  // offset (doubles) of the second folded matrix after the first (Mp * Kp)
 };
 
-template <int MI_, int WN_, int NI_, bool PS_ = false>
+template <int MI_, int WN_, int NI_, bool PS_ = false, int WM_ = 1>
 struct FShape {
     static constexpr int MI = MI_, WN = WN_, NI = NI_;
     static constexpr bool PS = PS_;  // forward only: D^-1/2 pre-scale chunks staged beside both fiber chunks
-    static constexpr int NTHR = 32 * WN;
+    // WM = 1: every warp accumulates both folded products; WM = 2: warp row 0 the first, warp row 1
+    // the second (half the accumulators per thread: larger row blocks at the same occupancy)
+    static constexpr int WM = WM_;
+    static constexpr int NTHR = 32 * WM * WN;
     static constexpr int BN = 8 * NI * WN;
     static constexpr int LDX = BN + 4;            // == 4 mod 16 doubles: conflict-free B fragments
     static constexpr int MPB = 8 * MI;
@@ -229,6 +234,47 @@ __device__ __forceinline__ void fload(const double* ja, const double* xa, const 
     }
 }
 
+// WM = 2: one folded product per warp (matrix m = warp row): A fragments from J1 or J2, B fragments
+// x_k + x_{n-1-k} (m = 0) / x_k - x_{n-1-k} (m = 1) forward, the first / second half backward.
+template <class SH, bool FWD>
+__device__ __forceinline__ void fload1(const double* ja, const double* xa, const double* xb, int kk, int mact,
+                                       double sgn, double (&a)[SH::MI], double (&b)[SH::NI]) {
+#pragma unroll
+    for (int mi = 0; mi < SH::MI; ++mi) a[mi] = mi < mact ? ja[mi * 8 * kLDJ + kk * 4] : 0.0;
+#pragma unroll
+    for (int ni = 0; ni < SH::NI; ++ni) {
+        if (FWD) {
+            double u = xa[kk * 4 * SH::LDX + ni * 8];
+            double w = xb[-kk * 4 * SH::LDX + ni * 8];
+            if (SH::PS) {
+                u *= xa[SH::DA + kk * 4 * SH::LDX + ni * 8];
+                w *= xb[SH::DA - kk * 4 * SH::LDX + ni * 8];
+            }
+            b[ni] = fma(sgn, w, u);  // exact: sgn = +-1
+        } else {
+            b[ni] = xa[kk * 4 * SH::LDX + ni * 8];  // xa already points at this warp's half
+        }
+    }
+}
+
+template <class SH, bool FWD, int KS>
+__device__ __forceinline__ void fmma1(const double* ja, const double* xa, const double* xb, int mact, double sgn,
+                                      double (&c)[SH::MI][SH::NI][2]) {
+    constexpr int MI = SH::MI, NI = SH::NI;
+    double a[2][MI], b[2][NI];
+    fload1<SH, FWD>(ja, xa, xb, 0, mact, sgn, a[0], b[0]);
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+        const int cur = kk & 1, nxt = cur ^ 1;
+        if (kk + 1 < KS) fload1<SH, FWD>(ja, xa, xb, kk + 1, mact, sgn, a[nxt], b[nxt]);
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+                if (mi < mact) dmma(c[mi][ni][0], c[mi][ni][1], a[cur][mi], b[cur][ni]);
+    }
+}
+
 // Both folded products over KS k-steps of 4, fragments double-buffered in registers.
 template <class SH, bool FWD, int KS>
 __device__ __forceinline__ void fmma(const double* ja, const double* xa, const double* xb, int mact,
@@ -369,6 +415,140 @@ __global__ void __launch_bounds__(32 * WN)
     }
 }
 
+
+// WM = 2 variant: warp row 0 accumulates the first folded product, warp row 1 the second; each thread
+// holds MI x NI accumulator tiles of ONE matrix, so a CTA covers twice the rows per register budget.
+// Backward, the q half goes through shared memory to the warp that holds p (x = p +- q).
+template <int MI, int WN, int NI, bool FWD, bool POST, bool PS>
+__global__ void __launch_bounds__(64 * WN)
+    fold_ms_kernel(FArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
+                   const double* __restrict__ post, const double* __restrict__ pre) {
+    using SH = FShape<MI, WN, NI, PS, 2>;
+    extern __shared__ __align__(16) double smem[];
+    const int rb = blockIdx.x % a.RB;
+    const long long c0 = static_cast<long long>(blockIdx.x / a.RB) * SH::BN;
+    const int strip0 = rb * MI;
+    const FProd p = make_fprod<SH>(a, c0, X, J + static_cast<size_t>(rb) * SH::MPB * a.Kp);
+    double c[MI][NI][2];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) c[mi][ni][0] = c[mi][ni][1] = 0.0;
+
+    const int nchunks = (a.Kp + kBK - 1) / kBK;
+    const int ns = a.nstage;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wn = warp % WN, wm = warp / WN;
+    const int g = lane >> 2, t = lane & 3;
+    const int mact = min(MI, max(0, a.S - strip0));
+    const unsigned st0 = smem_u32(smem);
+    for (int s = 0; s < ns - 1; ++s) {
+        if (s < nchunks) fissue<SH, FWD>(a, p, st0 + 8u * s * SH::STAGE, s, X, pre);
+        commit();
+    }
+    const int ja_off = SH::J1 + wm * (SH::J2 - SH::J1) + g * kLDJ + t;
+    const int xa_off = (FWD ? 0 : wm * SH::XB) + t * SH::LDX + wn * NI * 8 + g;
+    const int xb_off = SH::XB + (kBK - 1 - t) * SH::LDX + wn * NI * 8 + g;
+    const double sgn = wm ? -1.0 : 1.0;
+    int stage = 0;
+    for (int q = 0; q < nchunks; ++q) {
+        if (ns >= 3) wait_n<1>();
+        else wait_n<0>();
+        __syncthreads();
+        const int nq = q + ns - 1;
+        if (nq < nchunks) {
+            int nst = stage + ns - 1;
+            if (nst >= ns) nst -= ns;
+            fissue<SH, FWD>(a, p, st0 + 8u * nst * SH::STAGE, nq, X, pre);
+        }
+        commit();
+        const double* sb = smem + stage * SH::STAGE;
+        const int ks = min(kBK, a.Kp - q * kBK) >> 2;
+        if (ks == 4) fmma1<SH, FWD, 4>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
+        else if (ks == 3) fmma1<SH, FWD, 3>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
+        else if (ks == 2) fmma1<SH, FWD, 2>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
+        else fmma1<SH, FWD, 1>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
+        if (++stage == ns) stage = 0;
+    }
+
+    const int n = a.geo.n;
+    const long long L = a.geo.L;
+    long long ob[NI][2];
+    bool cv[NI][2];
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const long long cc = c0 + (wn * NI + ni) * 8 + 2 * t + v;
+            cv[ni][v] = cc < a.geo.ncols;
+            ob[ni][v] = fbase(cv[ni][v] ? cc : 0, L, n);
+        }
+    if constexpr (FWD) {
+        const int row0 = wm ? a.F : 0, rows = wm ? a.h : a.F;
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+            const int i = (strip0 + mi) * 8 + g;
+            if (i >= rows) continue;
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                for (int v = 0; v < 2; ++v)
+                    if (cv[ni][v]) Y[ob[ni][v] + L * (row0 + i)] = c[mi][ni][v];
+        }
+    } else {
+        cp_wait_all();
+        __syncthreads();  // every warp is done with the pipeline stages: reuse them for q
+        double* Qs = smem;  // MPB x LDX
+        if (wm == 1) {
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) Qs[(mi * 8 + g) * SH::LDX + (wn * NI + ni) * 8 + 2 * t + v] = c[mi][ni][v];
+        }
+        __syncthreads();
+        if (wm == 1) return;
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+            const int i = (strip0 + mi) * 8 + g;
+            double plo[NI][2], phi[NI][2];
+            if constexpr (POST) {  // this strip's scale loads issued before its stores
+                const int ilo = i < a.F ? i : 0, ihi = i < a.h ? n - 1 - i : 0;
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        plo[ni][v] = cv[ni][v] ? __ldg(post + ob[ni][v] + L * ilo) : 0.0;
+                        phi[ni][v] = cv[ni][v] ? __ldg(post + ob[ni][v] + L * ihi) : 0.0;
+                    }
+            }
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    if (!cv[ni][v]) continue;
+                    const double pv = c[mi][ni][v];
+                    const double qv = Qs[(mi * 8 + g) * SH::LDX + (wn * NI + ni) * 8 + 2 * t + v];
+                    double* y = Y + ob[ni][v];
+                    if (i < a.h) {
+                        double lo = pv + qv, hi = pv - qv;
+                        if constexpr (POST) {
+                            lo *= plo[ni][v];
+                            hi *= phi[ni][v];
+                        }
+                        y[L * i] = lo;
+                        y[L * (n - 1 - i)] = hi;
+                    } else if (i < a.F) {  // middle row (odd n)
+                        double m = pv;
+                        if constexpr (POST) m *= plo[ni][v];
+                        y[L * i] = m;
+                    }
+                }
+        }
+    }
+}
+
 template <typename K>
 int occ_of(K kernel, int threads, size_t smem) {
     int n = 0;
@@ -412,6 +592,41 @@ cudaError_t fold_launch_t(const Tiling& t, const ModeGeom& g, const double* X, d
     return cudaGetLastError();
 }
 
+template <int MI, int WN>
+cudaError_t fold_ms_launch_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
+                             const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
+    auto k = fwd ? (pre ? fold_ms_kernel<MI, WN, 2, true, false, true> : fold_ms_kernel<MI, WN, 2, true, false, false>)
+                 : (post ? fold_ms_kernel<MI, WN, 2, false, true, false>
+                         : fold_ms_kernel<MI, WN, 2, false, false, false>);
+    const size_t smem = pre ? fold_prescale_smem(t) : t.smem;
+    if (occ) {
+        *occ = occ_of(k, 64 * WN, smem);
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const long long blocks = (g.ncols + t.BN - 1) / t.BN * t.RB;
+    k<<<static_cast<unsigned>(blocks), 64 * WN, smem, st>>>(make_fargs(t, g), X, Y, J, post, pre);
+    return cudaGetLastError();
+}
+
+template <int WN>
+cudaError_t fold_ms_dispatch_wn(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
+                                const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
+    switch (t.MI) {
+        case 1: return fold_ms_launch_t<1, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        case 2: return fold_ms_launch_t<2, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        case 3: return fold_ms_launch_t<3, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        case 4: return fold_ms_launch_t<4, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        case 5: return fold_ms_launch_t<5, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        case 6: return fold_ms_launch_t<6, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        case 7: return fold_ms_launch_t<7, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        case 8: return fold_ms_launch_t<8, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        case 9: return fold_ms_launch_t<9, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <int WN, int NI>
 cudaError_t fold_dispatch_wn(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
                              const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
@@ -438,6 +653,12 @@ cudaError_t fold_dispatch_wn(const Tiling& t, const ModeGeom& g, const double* X
 
 cudaError_t fold_dispatch(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
                           const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
+    if (t.WM == 2) {
+        if (t.NI != 2) return cudaErrorInvalidValue;
+        if (t.WN == 4) return fold_ms_dispatch_wn<4>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        if (t.WN == 2) return fold_ms_dispatch_wn<2>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        return cudaErrorInvalidValue;
+    }
     if (t.NI == 2 && t.WN == 4) return fold_dispatch_wn<4, 2>(t, g, X, Y, J, post, pre, fwd, st, occ);
     if (t.NI == 2 && t.WN == 2) return fold_dispatch_wn<2, 2>(t, g, X, Y, J, post, pre, fwd, st, occ);
     if (t.NI == 4 && t.WN == 2) return fold_dispatch_wn<2, 4>(t, g, X, Y, J, post, pre, fwd, st, occ);
@@ -453,17 +674,18 @@ std::vector<Tiling> fold_tiling_candidates(int n) {
     if (h < 1) return {};
     const int S = (F + 7) / 8;
     const int Kp = (F + 3) / 4 * 4;
-    for (int MI = 1; MI <= 7; ++MI) {
+    for (int WM : {1, 2})
+    for (int MI = 1; MI <= (WM == 2 ? 9 : 7); ++MI) {
         const int RB = (S + MI - 1) / MI;
         if ((S + RB - 1) / RB != MI) continue;  // a smaller MI covers the strips with as many row blocks
         for (int WN : {4, 2})
         for (int NI : {2, 4}) {
-            if (NI == 4 && MI > 3) continue;  // 16 MI accumulators
+            if (NI == 4 && (MI > 3 || WM == 2)) continue;  // 16 MI accumulators
             for (int ns : {3, 2}) {
                 Tiling t;
                 t.fold = 1;
                 t.MI = MI;
-                t.WM = 1;
+                t.WM = WM;
                 t.NI = NI;
                 t.WN = WN;
                 t.S = S;
@@ -481,7 +703,9 @@ std::vector<Tiling> fold_tiling_candidates(int n) {
                 t.ctas_per_sm = occ;
                 if (occ < 1) continue;
                 const double eff = 0.85 + 0.15 * static_cast<double>(S) / (RB * MI);
-                c.emplace_back(std::min(occ * WN, 16) * eff - 0.05 * RB + 0.02 * WN + 0.01 * ns + 0.03 * NI, t);
+                c.emplace_back(std::min(occ * WM * WN, 16) * eff - 0.05 * RB + 0.02 * WN + 0.01 * ns + 0.03 * NI -
+                                   0.04 * WM,
+                               t);
             }
         }
     }
