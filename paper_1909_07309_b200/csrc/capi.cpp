@@ -184,7 +184,7 @@ struct stiga_fd_s {
     }
     // best dense (unfolded) candidate of direction l (for stages the folded kernel cannot do)
     std::vector<gpu::Tiling> tl_dense;  // heuristic dense tiling per direction (J / Jt are padded for it)
-    const gpu::Tiling& dense_tiling(int l) const { return tl[l].fold ? tl_dense[l] : tl[l]; }
+    const gpu::Tiling& dense_tiling(int l) const { return (tl[l].fold || tl[l].WM != 1) ? tl_dense[l] : tl[l]; }
 
     // Distributed building blocks.
     void apply_space(bool backward, long long t0, long long nt_local, const double* in, double* out, cudaStream_t st) {
@@ -258,7 +258,14 @@ struct stiga_fd_s {
         if (time_split) {
             ck(gpu::launch_mode_product(tl_ts, g, in, scratch.p, Jt_t.p, nullptr, st), "slab time U_t^T");
             ck(gpu::launch_arrowhead(scratch.p, scratch2.p, ns_local, a2, st), "slab arrowhead");
-            ck(gpu::launch_mode_product(tl_ts, g, scratch2.p, nullptr, J_t.p, nullptr, st, nullptr, &sc),
+            gpu::Tiling tsc = tl_ts;
+            if (tsc.WM != 1)
+                for (const auto& t : cand_ts)
+                    if (t.WM == 1) {
+                        tsc = t;
+                        break;
+                    }
+            ck(gpu::launch_mode_product(tsc, g, scratch2.p, nullptr, J_t.p, nullptr, st, nullptr, &sc),
                "slab time U_t (scatter)");
         } else {
             ck(gpu::launch_time_fused(tl_t, g, in, nullptr, Jt_t.p, J_t.p, a2, st, &sc), "slab time fused (scatter)");
@@ -370,7 +377,7 @@ struct stiga_fd_s {
             size_t n_fold = 0, n_dense = 0;
             for (size_t c = 0; c < cand_space[l].size(); ++c) {
                 const gpu::Tiling& t = cand_space[l][c];
-                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : kMaxCand)) continue;
+                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : 2 * kMaxCand)) continue;
                 const float ms = time_once([&] {
                     mprod(t, l, false, geom(l), scratch.p, scratch2.p, nullptr, nullptr);
                 });
@@ -393,7 +400,7 @@ struct stiga_fd_s {
             size_t n_fold = 0, n_dense = 0;
             for (size_t c = 0; c < cand_space[l].size(); ++c) {
                 const gpu::Tiling& t = cand_space[l][c];
-                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : kMaxCand)) continue;
+                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : 2 * kMaxCand)) continue;
                 const float ms = time_once([&] { mprod(t, l, true, geom(l), scratch.p, scratch2.p, post, nullptr); });
                 if (ms < 0.985f * best) { best = ms; tl_b[l] = t; pick_b[l] = static_cast<int>(c); }
                 if (debug_tune)
@@ -853,7 +860,14 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
             }
             if (!(fold_only && !cands.empty())) cands.insert(cands.end(), dense.begin(), dense.end());
             h->cand_space.push_back(cands);
-            h->tl_dense.push_back(dense.front());
+            // WM = 1 dense tiling: the only kind with the scatter epilogue (and the pre-scale)
+            gpu::Tiling tdense = dense.front();
+            for (const auto& t : dense)
+                if (t.WM == 1) {
+                    tdense = t;
+                    break;
+                }
+            h->tl_dense.push_back(tdense);
             h->tl_b.push_back(cands.front());
             h->tl.push_back(cands.front());
             h->lam.emplace_back(new DBuf);

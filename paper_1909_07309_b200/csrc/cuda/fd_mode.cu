@@ -67,6 +67,37 @@ std::vector<Tiling> mode_tiling_candidates(int m, int n) {
             c.emplace_back(std::min(occ * t.WN, 16) * eff + 0.02 * WN - 0.05 * RB, t);
         }
     }
+    // two warp rows per CTA (WM = 2): twice the rows of one fiber tile per CTA at the same registers
+    // per thread -- fewer row blocks re-staging the fiber tile
+    const int rb2 = (S + 15) / 16;
+    for (int RB = rb2; RB <= std::min(S, rb2 + 2); ++RB) {
+        const int MI = (S + 2 * RB - 1) / (2 * RB);
+        if (MI > 8 || MI < 1) continue;
+        if (RB > rb2 && (S + 2 * rb2 - 1) / (2 * rb2) == MI) continue;
+        for (int WN : {4, 2}) {
+            Tiling t;
+            t.MI = MI;
+            t.WM = 2;
+            t.NI = 2;
+            t.WN = WN;
+            t.S = S;
+            t.RB = RB;
+            t.MpB = 16 * MI;
+            t.Mp = RB * t.MpB;
+            t.Kp = Kp;
+            t.BN = 16 * WN;
+            t.LDX = t.BN + 4;
+            t.nstage = 3;
+            t.smem = sizeof(double) * static_cast<size_t>(t.nstage) * (kBK * t.LDX + t.MpB * kLDJ);
+            if (t.smem > kSmemPerCTA) continue;
+            int occ = 0;
+            dispatch_mode(t, ModeGeom{}, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &occ);
+            t.ctas_per_sm = occ;
+            if (occ < 1) continue;
+            const double eff = 0.85 + 0.15 * static_cast<double>(S) / (RB * 2 * MI);
+            c.emplace_back(std::min(occ * 2 * t.WN, 16) * eff + 0.02 * WN - 0.05 * RB - 0.06, t);
+        }
+    }
     std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
     std::vector<Tiling> out;
     for (auto& e : c) out.push_back(e.second);
