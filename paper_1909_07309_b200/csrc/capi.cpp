@@ -436,7 +436,7 @@ struct stiga_fd_s {
         float best_fused = 1e30f, best_split = 1e30f;
         if (!no_tune) {
             if (fused_ok && !(force && std::string(force) == "split")) {
-                for (size_t c = 0; c < std::min(kMaxCand, cand_time.size()); ++c) {
+                for (size_t c = 0; c < std::min(3 * kMaxCand, cand_time.size()); ++c) {
                     const gpu::Tiling& t = cand_time[c];
                     const float ms = time_once([&] {
                         ck(gpu::launch_time_fused(t, geom(d), scratch.p, scratch2.p, Jt_t.p, J_t.p, ap, nullptr), "tune");
@@ -449,7 +449,7 @@ struct stiga_fd_s {
             }
             if (!(force && std::string(force) == "fused")) {
                 float best_gemm = 1e30f;
-                for (size_t c = 0; c < std::min(kMaxCand, cand_ts.size()); ++c) {
+                for (size_t c = 0; c < std::min(2 * kMaxCand, cand_ts.size()); ++c) {
                     const gpu::Tiling& t = cand_ts[c];
                     const float ms = time_once([&] {
                         ck(gpu::launch_mode_product(t, geom(d), scratch.p, scratch2.p, Jt_t.p, nullptr, nullptr), "tune");
