@@ -107,9 +107,21 @@ class Problem:
                     "fields")
         return nu.value, gam.value
 
-    def geometry_pieces(self, p, n_el, want_D=True):
+    def geometry_pieces(self, p, n_el, want_D=True, device=None):
         """make_geometry_preconditioner inputs (solver.cpp:127-144): SpaceTimePieces with the
-        separated-coefficient factors K~, M~, W_t, weighted M_t, plus D and phi/Phi."""
+        separated-coefficient factors K~, M~, W_t, weighted M_t, plus D and phi/Phi.
+
+        device=None: D = diag(A)/diag(A~) with diag(A) from the host quadrature of the physical
+        diagonal.  device=k: diag(A) from the physical K_s, M_s assembled on GPU k (the operator the
+        GMRES solve applies; `pc.A` keeps it) -- the same quadrature sums in another order, seconds
+        instead of the host's per-element loop at c4 sizes."""
+        if want_D and device is not None:
+            pc = self.geometry_pieces(p, n_el, want_D=False)
+            A = stiga.KronSumOperator.physical(self, p, n_el, device=device)
+            den = kron_sum_diagonal(stiga.kron_sum_terms(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0))
+            pc.D = A.diagonal() / den
+            pc.A = A
+            return pc
         ns = stiga.space_dim(p, n_el)
         nt = stiga.space_dim(p, n_el, temporal=True)
         d = self.d

@@ -100,3 +100,15 @@ def test_gmres_full_c2_one_iteration():
     assert rep.converged and rep.iterations == 1
     res = torch.linalg.norm(A.apply(x) - b) / torch.linalg.norm(b)
     assert res.item() <= 1e-8
+
+
+@pytest.mark.parametrize("pid,p,nel", [("deformed-cube-3d", 2, 4), ("quarter-annulus-2d", 3, 6), ("separable-nu-2d", 2, 5)])
+def test_geometry_scaling_from_device_assembly(pid, p, nel):
+    """D = diag(A)/diag(A~) with diag(A) from the device-assembled physical operator equals the host
+    quadrature of the physical diagonal (solver.cpp:138-142) to rounding."""
+    from paper_1909_07309_b200.problems import Problem
+
+    prob = Problem(pid)
+    Dh = prob.geometry_pieces(p, nel, want_D=True).D
+    Dd = prob.geometry_pieces(p, nel, want_D=True, device=0).D
+    assert np.abs(Dd - Dh).max() <= 1e-13 * np.abs(Dh).max()
