@@ -212,6 +212,11 @@ int stiga_kronsum_apply_time(stiga_kronsum_t A, long long t0, long long nt_local
    deterministic dot into *d_result (device scalar), y += alpha x, y = alpha x. */
 int stiga_vec_dot(const double* d_x, const double* d_y, long long n, double* d_result, void* stream);
 int stiga_vec_axpy(double alpha, const double* d_x, double* d_y, long long n, void* stream);
+/* Batched Krylov operations for classical Gram-Schmidt with reorthogonalisation (CGS2) in the
+   sharded GMRES: d_out[j] = V_j . w for j < k (d_V: host array of k <= 64 device pointers, d_out: k
+   device doubles, deterministic reduction) and w += sum_j coefs[j] V_j (coefs: k host doubles). */
+int stiga_vec_multidot(const double* const* d_V, int k, const double* d_w, long long n, double* d_out, void* stream);
+int stiga_vec_multiaxpy(const double* coefs, const double* const* d_V, int k, double* d_w, long long n, void* stream);
 int stiga_vec_scal(double alpha, const double* d_x, double* d_y, long long n, void* stream);
 
 /* ---- GMRES (gmres.hpp:12-35) ---------------------------------------------------------- */

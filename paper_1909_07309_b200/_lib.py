@@ -92,6 +92,8 @@ SIGNATURES = {
     "stiga_kronsum_apply_time": (_c_int, [_vp, _c_ll, _c_ll, _c_int, _c_int, _vp, _vp, _vp, _vp]),
     "stiga_vec_dot": (_c_int, [_vp, _vp, _c_ll, _vp, _vp]),
     "stiga_vec_axpy": (_c_int, [_c_dbl, _vp, _vp, _c_ll, _vp]),
+    "stiga_vec_multidot": (_c_int, [ctypes.POINTER(_vp), _c_int, _vp, _c_ll, _vp, _vp]),
+    "stiga_vec_multiaxpy": (_c_int, [_pd, ctypes.POINTER(_vp), _c_int, _vp, _c_ll, _vp]),
     "stiga_vec_scal": (_c_int, [_c_dbl, _vp, _vp, _c_ll, _vp]),
 }
 

@@ -1551,6 +1551,30 @@ int stiga_vec_dot(const double* d_x, const double* d_y, long long n, double* d_r
     });
 }
 
+int stiga_vec_multidot(const double* const* d_V, int k, const double* d_w, long long n, double* d_out, void* stream) {
+    return guarded([&] {
+        require(d_V && d_w && d_out && k >= 1 && k <= 64 && n >= 1, "stiga_vec_multidot: invalid argument");
+        for (int j = 0; j < k; ++j) require(d_V[j] != nullptr, "stiga_vec_multidot: null basis vector");
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        thread_local std::vector<std::unique_ptr<DBuf>> partials;  // per device of this host thread
+        if (static_cast<int>(partials.size()) <= dev) partials.resize(dev + 1);
+        if (!partials[dev]) {
+            partials[dev] = std::make_unique<DBuf>();
+            partials[dev]->alloc(static_cast<size_t>(gpu::multidot_partials_size()));
+        }
+        ck(gpu::launch_multidot(d_V, k, d_w, n, partials[dev]->p, d_out, as_stream(stream)), "multidot");
+    });
+}
+
+int stiga_vec_multiaxpy(const double* coefs, const double* const* d_V, int k, double* d_w, long long n, void* stream) {
+    return guarded([&] {
+        require(coefs && d_V && d_w && k >= 1 && k <= 64 && n >= 0, "stiga_vec_multiaxpy: invalid argument");
+        for (int j = 0; j < k; ++j) require(d_V[j] != nullptr, "stiga_vec_multiaxpy: null basis vector");
+        ck(gpu::launch_multiaxpy(coefs, d_V, k, d_w, n, as_stream(stream)), "multiaxpy");
+    });
+}
+
 int stiga_vec_axpy(double alpha, const double* d_x, double* d_y, long long n, void* stream) {
     return guarded([&] {
         require(n >= 0 && (n == 0 || (d_x && d_y)), "stiga_vec_axpy: invalid argument");

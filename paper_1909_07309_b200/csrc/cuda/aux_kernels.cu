@@ -16,6 +16,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kDotBlocks = 148 * 4;
+constexpr int kMaxMulti = 64;  // basis vectors per batched Gram-Schmidt call
 
 inline unsigned grid_for(long long n) {
     const long long b = (n + kThreads - 1) / kThreads;
@@ -329,6 +330,69 @@ __global__ void axpy_dot_partial_kernel(const double* __restrict__ h, const doub
     }
 }
 
+// Batched Krylov dots / updates for classical Gram-Schmidt (CGS2) in the sharded GMRES: one pass
+// over w serves KB basis vectors, so an Arnoldi column needs two all-reduces instead of k + 1.
+struct VecPtrs {
+    const double* v[kMaxMulti];
+};
+struct MultiCoefs {
+    double c[kMaxMulti];
+};
+
+template <int KB>
+__global__ void multidot_partial_kernel(VecPtrs V, int j0, int k, const double* __restrict__ w, long long n,
+                                        double* __restrict__ partials) {
+    __shared__ double ws[KB][32];
+    double s[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) s[j] = 0.0;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double wi = w[i];
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+            if (j0 + j < k) s[j] = fma(V.v[j0 + j][i], wi, s[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+        const double r = warp_sum(s[j]);
+        if ((threadIdx.x & 31) == 0) ws[j][threadIdx.x >> 5] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+            double u = threadIdx.x < (blockDim.x >> 5) ? ws[j][threadIdx.x] : 0.0;
+            u = warp_sum(u);
+            if (threadIdx.x == 0 && j0 + j < k) partials[static_cast<long long>(j0 + j) * gridDim.x + blockIdx.x] = u;
+        }
+    }
+}
+
+__global__ void multidot_finish_kernel(const double* __restrict__ partials, int np, double* __restrict__ out) {
+    __shared__ double ws[32];
+    const double* pj = partials + static_cast<long long>(blockIdx.x) * np;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) s += pj[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) out[blockIdx.x] = v;
+    }
+}
+
+__global__ void multiaxpy_kernel(VecPtrs V, MultiCoefs c, int k, double* __restrict__ w, long long n) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < k; ++j) acc = fma(c.c[j], V.v[j][i], acc);
+        w[i] += acc;
+    }
+}
+
 __global__ void scal_kernel(double alpha, const double* __restrict__ x, double* __restrict__ y, long long n) {
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -482,6 +546,33 @@ cudaError_t launch_axpy_dot(const double* d_h, const double* v, double* w, const
                             double* d_partials, double* d_result, cudaStream_t st) {
     axpy_dot_partial_kernel<<<kDotBlocks, kThreads, 0, st>>>(d_h, v, w, vn, n, d_partials);
     dot_finish_kernel<<<1, 1024, 0, st>>>(d_partials, kDotBlocks, d_result);
+    return cudaGetLastError();
+}
+
+int multidot_partials_size() { return kMaxMulti * kDotBlocks; }
+
+cudaError_t launch_multidot(const double* const* V, int k, const double* w, long long n, double* d_partials,
+                            double* d_out, cudaStream_t st) {
+    if (k < 1 || k > kMaxMulti) return cudaErrorInvalidValue;
+    VecPtrs vp{};
+    for (int j = 0; j < k; ++j) vp.v[j] = V[j];
+    constexpr int KB = 8;
+    for (int j0 = 0; j0 < k; j0 += KB) multidot_partial_kernel<KB><<<kDotBlocks, kThreads, 0, st>>>(vp, j0, k, w, n, d_partials);
+    multidot_finish_kernel<<<k, 1024, 0, st>>>(d_partials, kDotBlocks, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_multiaxpy(const double* coefs, const double* const* V, int k, double* w, long long n,
+                             cudaStream_t st) {
+    if (k < 1 || k > kMaxMulti) return cudaErrorInvalidValue;
+    if (n <= 0) return cudaSuccess;
+    VecPtrs vp{};
+    MultiCoefs mc{};
+    for (int j = 0; j < k; ++j) {
+        vp.v[j] = V[j];
+        mc.c[j] = coefs[j];
+    }
+    multiaxpy_kernel<<<grid_for(n), kThreads, 0, st>>>(vp, mc, k, w, n);
     return cudaGetLastError();
 }
 

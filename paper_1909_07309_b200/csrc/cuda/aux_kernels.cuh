@@ -30,6 +30,13 @@ cudaError_t launch_time_band_slab(long long Ns, int nt, long long t0, long long 
 cudaError_t launch_dot(const double* x, const double* y, long long n, double* d_partials, double* d_result,
                        cudaStream_t st);
 int dot_partials_size();
+/// Batched dots d_out[j] = V[j] . w (j < k <= 64; deterministic two-level reduction; d_partials of
+/// multidot_partials_size() doubles) and the batched update w += sum_j coefs[j] V[j] (host coefs).
+int multidot_partials_size();
+cudaError_t launch_multidot(const double* const* V, int k, const double* w, long long n, double* d_partials,
+                            double* d_out, cudaStream_t st);
+cudaError_t launch_multiaxpy(const double* coefs, const double* const* V, int k, double* w, long long n,
+                             cudaStream_t st);
 /// MGS step: w -= (*d_h) * v, then *d_result = dot(vn, w) (vn == nullptr: dot(w, w)); bit-identical
 /// to launch_axpy(-h) followed by launch_dot.
 cudaError_t launch_axpy_dot(const double* d_h, const double* v, double* w, const double* vn, long long n,

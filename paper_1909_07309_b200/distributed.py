@@ -500,6 +500,27 @@ class DeviceVec:
         check(lib().stiga_vec_scal(float(alpha), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
                                    x.numel(), self._st()), "vec_scal")
 
+    def multidot(self, Vs, w):
+        """[V_j . w for j], all-reduced over the group in ONE collective (CGS2)."""
+        import torch
+
+        k = len(Vs)
+        out = torch.empty(k, dtype=torch.float64, device=w.device)
+        ptrs = (ctypes.c_void_p * k)(*[v.data_ptr() for v in Vs])
+        check(lib().stiga_vec_multidot(ptrs, k, ctypes.c_void_p(w.data_ptr()), w.numel(),
+                                       ctypes.c_void_p(out.data_ptr()), self._st()), "vec_multidot")
+        if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
+            self.dist.all_reduce(out, group=self.group)
+        return out.cpu().numpy()
+
+    def multiaxpy(self, coefs, Vs, w):
+        """w += sum_j coefs[j] V_j."""
+        k = len(Vs)
+        c = np.ascontiguousarray(coefs, dtype=np.float64)
+        ptrs = (ctypes.c_void_p * k)(*[v.data_ptr() for v in Vs])
+        check(lib().stiga_vec_multiaxpy(c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ptrs, k,
+                                        ctypes.c_void_p(w.data_ptr()), w.numel(), self._st()), "vec_multiaxpy")
+
 
 class SolveReport:
     """gmres.hpp:15-21 (replicated on every rank)."""
@@ -512,7 +533,21 @@ class SolveReport:
         self.precond_time_fraction = 0.0
 
 
-def sharded_gmres(A, P, b, vec, tol=1e-8, max_krylov=100, restart=None):
+def _multidot(vec, Vs, w):
+    if hasattr(vec, "multidot"):
+        return np.asarray(vec.multidot(Vs, w), dtype=np.float64)
+    return np.array([vec.dot(v, w) for v in Vs])
+
+
+def _multiaxpy(vec, coefs, Vs, w):
+    if hasattr(vec, "multiaxpy"):
+        vec.multiaxpy(coefs, Vs, w)
+        return
+    for c, v in zip(coefs, Vs):
+        vec.axpy(float(c), v, w)
+
+
+def sharded_gmres(A, P, b, vec, tol=1e-8, max_krylov=100, restart=None, ortho="mgs"):
     """Left-preconditioned GMRES (gmres.cpp:19-132) on time-sharded vectors.
 
     A and P expose apply(x_local, out) (ShardedSystem / ShardedExtendedFD, or any rank-local
@@ -520,12 +555,19 @@ def sharded_gmres(A, P, b, vec, tol=1e-8, max_krylov=100, restart=None):
     Same control flow as the reference: x0 = 0, beta0 = ||P b||, MGS Arnoldi (k+1 sequential
     all-reduced dots per iteration), Givens on the replicated host Hessenberg, breakdown
     H(k+1,k) <= 1e-14 beta0 -> converged, true preconditioned residual at each restart, and
-    `max_krylov` capping the TOTAL iteration count across restarts (gmres.cpp:52-56, 65)."""
+    `max_krylov` capping the TOTAL iteration count across restarts (gmres.cpp:52-56, 65).
+
+    ortho="cgs2": classical Gram-Schmidt with one reorthogonalisation pass instead of the reference's
+    MGS: h = V^T w, w -= V h, twice, with batched dots (vec.multidot) -- two all-reduces per Arnoldi
+    column instead of k + 1 sequential ones.  Equal to MGS in exact arithmetic and as stable in
+    practice (tested: iteration counts within one of the oracle's MGS)."""
     import math
     import time
 
     import torch
 
+    if ortho not in ("mgs", "cgs2"):
+        raise ValueError(f"gmres: unknown orthogonalisation {ortho!r}")
     if tol <= 0.0:
         raise ValueError("gmres: tolerance must be positive")
     if max_krylov < 1:
@@ -585,9 +627,15 @@ def sharded_gmres(A, P, b, vec, tol=1e-8, max_krylov=100, restart=None):
         while k < m:
             A.apply(V[k], tmp)
             apply_P(tmp, w)
-            for i in range(k + 1):
-                H[i, k] = vec.dot(V[i], w)
-                vec.axpy(-H[i, k], V[i], w)
+            if ortho == "mgs":
+                for i in range(k + 1):
+                    H[i, k] = vec.dot(V[i], w)
+                    vec.axpy(-H[i, k], V[i], w)
+            else:
+                for _ in range(2):
+                    h = _multidot(vec, V[:k + 1], w)
+                    _multiaxpy(vec, -h, V[:k + 1], w)
+                    H[:k + 1, k] += h
             H[k + 1, k] = norm(w)
             tiny = H[k + 1, k] <= 1e-14 * beta0
             if not tiny:

@@ -74,6 +74,16 @@ class CpuVec:
     def scal(self, alpha, x, y):
         torch.mul(x, alpha, out=y)
 
+    def multidot(self, Vs, w):
+        s = torch.tensor([float(torch.dot(v, w)) for v in Vs], dtype=torch.float64)
+        if dist.is_initialized() and dist.get_world_size() > 1:
+            dist.all_reduce(s)  # one collective for the whole column
+        return s.numpy()
+
+    def multiaxpy(self, coefs, Vs, w):
+        for c, v in zip(coefs, Vs):
+            w.add_(v, alpha=float(c))
+
 
 def _setup(d, p, nel, gamma, nu, scaled):
     W, Mt = oasm.assemble_time_matrices(p, nel, 1.0)
@@ -86,7 +96,7 @@ def _setup(d, p, nel, gamma, nu, scaled):
     return K, M, W, Mt, dims, Po, Ao
 
 
-def _worker(rank, world, port, d, p, nel, gamma, nu, scaled, restart, q):
+def _worker(rank, world, port, d, p, nel, gamma, nu, scaled, restart, q, ortho="mgs"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -105,7 +115,7 @@ def _worker(rank, world, port, d, p, nel, gamma, nu, scaled, restart, q):
             yo = Ao.apply(rhs)
             yerr = float(np.linalg.norm(np.concatenate(parts) - yo) / np.linalg.norm(yo))
         # GMRES parity
-        x, rep = sharded_gmres(Ash, Psh, torch.from_numpy(rhs[a:b].copy()), CpuVec(), 1e-8, 200, restart)
+        x, rep = sharded_gmres(Ash, Psh, torch.from_numpy(rhs[a:b].copy()), CpuVec(), 1e-8, 200, restart, ortho=ortho)
         xs = [None] * world
         dist.all_gather_object(xs, x.numpy())
         if rank == 0:
@@ -117,17 +127,19 @@ def _worker(rank, world, port, d, p, nel, gamma, nu, scaled, restart, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,d,p,nel,gamma,nu,scaled,restart", [
-    (2, 2, 2, 6, 1.0, 1.0, True, None),
-    (3, 2, 3, 8, 1.3, 0.7, True, 5),
-    (2, 1, 3, 12, 1.0, 1.0, True, 4),
-    (3, 3, 2, 5, 1.0, 1.0, False, None),
+@pytest.mark.parametrize("world,d,p,nel,gamma,nu,scaled,restart,ortho", [
+    (2, 2, 2, 6, 1.0, 1.0, True, None, "mgs"),
+    (3, 2, 3, 8, 1.3, 0.7, True, 5, "mgs"),
+    (2, 1, 3, 12, 1.0, 1.0, True, 4, "mgs"),
+    (3, 3, 2, 5, 1.0, 1.0, False, None, "mgs"),
+    (2, 2, 2, 6, 1.0, 1.0, True, None, "cgs2"),
+    (3, 2, 3, 8, 1.3, 0.7, True, 5, "cgs2"),
 ])
-def test_sharded_system_and_gmres_match_oracle(world, d, p, nel, gamma, nu, scaled, restart):
+def test_sharded_system_and_gmres_match_oracle(world, d, p, nel, gamma, nu, scaled, restart, ortho):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, d, p, nel, gamma, nu, scaled, restart, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, d, p, nel, gamma, nu, scaled, restart, q, ortho))
              for r in range(world)]
     for pr in procs:
         pr.start()
