@@ -201,9 +201,16 @@ def run_ours(args):
     from paper_1909_07309_b200.configs import CONFIGS
     from paper_1909_07309_b200.inputs import uniform_pm1
     ws, rank, local = dist_env()
+    if os.environ.get("STIGA_BENCH_BACKEND") == "gloo":
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # STIGA_BENCH_BACKEND=gloo: plumbing check of the N > 1 path with several ranks on one GPU
+        # (no NCCL); the fused exchange then uses host barriers
+        if os.environ.get("STIGA_BENCH_BACKEND") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
     cfg = CONFIGS[args.config]
     K_steps, W_steps = args.steps, max(args.warmup, 3)
@@ -252,7 +259,8 @@ def run_ours(args):
     def max_over_ranks(x):
         if ws == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        on_cpu = os.environ.get("STIGA_BENCH_BACKEND") == "gloo"
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if on_cpu else f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 

@@ -23,6 +23,12 @@ import numpy as np
 from ._lib import check, lib
 
 
+def torch_empty_like_host(t):
+    import torch
+
+    return torch.empty(t.shape, dtype=t.dtype, device="cpu")
+
+
 def partition(n, parts):
     """Balanced contiguous partition of range(n): (offsets, sizes); the first n % parts get +1."""
     base, extra = divmod(n, parts)
@@ -455,13 +461,41 @@ class ShardedSystem:
             if v["recv_hi"] is not None:
                 ops.append(dist.P2POp(dist.irecv, v["recv_hi"], r + 1, self.group))
                 ops.append(dist.P2POp(dist.isend, v["send_hi"], r + 1, self.group))
+        if dist.get_backend(self.group) == "gloo" and ops and ops[0].tensor.is_cuda:
+            ops, staged = self._host_staged(ops)
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            for dev_t, host_t in staged:
+                dev_t.copy_(host_t)
+            return
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+
+    def _host_staged(self, ops):
+        """gloo moves host memory only: send copies / receive into host buffers, copied back after."""
+        dist = self.dist
+        out, staged = [], []
+        for op in ops:
+            h = op.tensor.cpu() if op.op is dist.isend else torch_empty_like_host(op.tensor)
+            if op.op is not dist.isend:
+                staged.append((op.tensor, h))
+            out.append(dist.P2POp(op.op, h, op.peer, op.group))
+        return out, staged
 
     def apply(self, x_local, out=None):
         self.stage_space(x_local)
         self.exchange_halos()
         return self.stage_time(out if out is not None else x_local.new_empty(x_local.shape))
+
+
+def _all_reduce_sum(dist, t, group):
+    """Sum over the group; a gloo group reduces a host copy (gloo's TCP transport reads host memory)."""
+    if dist.get_backend(group) == "gloo" and t.is_cuda:
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
 
 
 class DeviceVec:
@@ -489,7 +523,7 @@ class DeviceVec:
         check(lib().stiga_vec_dot(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), x.numel(),
                                   ctypes.c_void_p(self._scalar.data_ptr()), self._st()), "vec_dot")
         if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
-            self.dist.all_reduce(self._scalar, group=self.group)
+            _all_reduce_sum(self.dist, self._scalar, self.group)
         return float(self._scalar.item())
 
     def axpy(self, alpha, x, y):
@@ -510,7 +544,7 @@ class DeviceVec:
         check(lib().stiga_vec_multidot(ptrs, k, ctypes.c_void_p(w.data_ptr()), w.numel(),
                                        ctypes.c_void_p(out.data_ptr()), self._st()), "vec_multidot")
         if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
-            self.dist.all_reduce(out, group=self.group)
+            _all_reduce_sum(self.dist, out, self.group)
         return out.cpu().numpy()
 
     def multiaxpy(self, coefs, Vs, w):

@@ -331,3 +331,30 @@ def test_sharded_gmres_cgs2_on_device_matches_native():
     assert rep.converged and repn.converged and rep.iterations > 3
     assert abs(rep.iterations - repn.iterations) <= 1
     assert torch.linalg.norm(x - xn) <= 1e-8 * torch.linalg.norm(xn)
+
+
+def test_bench_two_ranks_share_one_gpu_gloo():
+    """bench.py's N > 1 path end to end with two ranks on this one GPU (STIGA_BENCH_BACKEND=gloo):
+    receive buffers exchanged with CUDA IPC, the time-sharded apply with the fused scatter exchange,
+    the halo-exchanged system mat-vec and the CGS2 sharded GMRES; one JSON line, converged solve."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, STIGA_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"), "--gpus", "2", "--config", "c1",
+           "--steps", "5", "--warmup", "3"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and "p2p" in d["config"]["parallelism"]
+    assert d["gmres"]["converged"] and d["gmres"]["true_rel_residual"] < 1e-8
