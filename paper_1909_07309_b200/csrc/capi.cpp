@@ -174,8 +174,8 @@ struct stiga_fd_s {
     void mprod(const gpu::Tiling& t, int l, bool backward, const gpu::ModeGeom& g, const double* src, double* dst,
                const double* post, cudaStream_t st, const double* pre = nullptr, const gpu::Scatter* sc = nullptr) {
         if (t.fold) {
-            if (sc) throw std::runtime_error("internal: folded product with a scatter epilogue");
-            ck(gpu::launch_fold_product(t, g, src, dst, backward ? Jfb[l]->p : Jft[l]->p, !backward, post, st, pre),
+            if (sc && (backward || t.WM != 2)) throw std::runtime_error("internal: folded scatter needs a WM = 2 tiling");
+            ck(gpu::launch_fold_product(t, g, src, dst, backward ? Jfb[l]->p : Jft[l]->p, !backward, post, st, pre, sc),
                "fd folded mode product");
         } else {
             ck(gpu::launch_mode_product(t, g, src, dst, backward ? J[l]->p : Jt[l]->p, post, st, pre, sc),
@@ -242,8 +242,11 @@ struct stiga_fd_s {
         for (int l = 0; l < d; ++l) {
             const bool last = l == d - 1;
             double* dst = last ? nullptr : bufs[k++ % 2];
-            const gpu::Tiling& t = last ? (l == 0 && fused_pre ? first_tiling() : dense_tiling(l))
-                                        : (l == 0 ? first_tiling() : tl[l]);
+            // the scattering product: the tuned tiling when it has a scatter epilogue (dense WM = 1 or
+            // folded WM = 2), else the dense fallback
+            const gpu::Tiling& tt = (l == 0 && fused_pre) ? first_tiling() : tl[l];
+            const bool scatter_ok = !(fused_pre && l == 0) && (tt.fold ? tt.WM == 2 : tt.WM == 1);
+            const gpu::Tiling& t = last ? (scatter_ok ? tt : dense_tiling(l)) : (l == 0 ? first_tiling() : tl[l]);
             mprod(t, l, false, slab_geom(l, nt_local), src, dst, nullptr, st, (fused_pre && l == 0) ? dsl : nullptr,
                   last ? &sc : nullptr);
             src = dst;

@@ -110,9 +110,10 @@ bool prescale_fits(const Tiling& t);
 /// post_scale (backward only) multiplies the outputs elementwise.
 /// pre_scale (forward only) multiplies both staged fiber chunks by D^-1/2 as the fold is formed.
 std::vector<Tiling> fold_tiling_candidates(int n);
+/// sc (forward, WM = 2 tilings only): scatter epilogue of the fused all-to-all (Scatter above).
 cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
                                 bool forward, const double* post_scale, cudaStream_t stream,
-                                const double* pre_scale = nullptr);
+                                const double* pre_scale = nullptr, const Scatter* sc = nullptr);
 size_t fold_prescale_smem(const Tiling& t);
 
 /// Standalone block-arrowhead solve X = (gamma Delta_t (x) I + nu I (x) Lambda_s)^-1 Z on the

@@ -419,10 +419,11 @@ __global__ void __launch_bounds__(32 * WN)
 // WM = 2 variant: warp row 0 accumulates the first folded product, warp row 1 the second; each thread
 // holds MI x NI accumulator tiles of ONE matrix, so a CTA covers twice the rows per register budget.
 // Backward, the q half goes through shared memory to the warp that holds p (x = p +- q).
-template <int MI, int WN, int NI, bool FWD, bool POST, bool PS>
+template <int MI, int WN, int NI, bool FWD, bool POST, bool PS, bool SC = false>
 __global__ void __launch_bounds__(64 * WN)
     fold_ms_kernel(FArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
-                   const double* __restrict__ post, const double* __restrict__ pre) {
+                   const double* __restrict__ post, const double* __restrict__ pre,
+                   const __grid_constant__ Scatter sc) {
     using SH = FShape<MI, WN, NI, PS, 2>;
     extern __shared__ __align__(16) double smem[];
     const int rb = blockIdx.x % a.RB;
@@ -483,7 +484,43 @@ __global__ void __launch_bounds__(64 * WN)
             cv[ni][v] = cc < a.geo.ncols;
             ob[ni][v] = fbase(cv[ni][v] ? cc : 0, L, n);
         }
-    if constexpr (FWD) {
+    if constexpr (FWD && SC) {
+        // scatter epilogue (fd_kernels.cuh Scatter, forward): output element (fiber l + L r, row) of
+        // the time slab is spatial index a = l + L row at local time b = r; it goes to the rank that
+        // owns a, at (a - off[q]) + ld[q] (b + b_shift) -- the fused all-to-all of the sharded apply
+        const int row0 = wm ? a.F : 0, rows = wm ? a.h : a.F;
+        long long fl[NI][2], fr[NI][2];
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const long long cc = c0 + (wn * NI + ni) * 8 + 2 * t + v;
+                fr[ni][v] = cc / L;
+                fl[ni][v] = cc - fr[ni][v] * L;
+            }
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+            const int i = (strip0 + mi) * 8 + g;
+            if (i >= rows) continue;
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    if (!cv[ni][v]) continue;
+                    const long long ca = fl[ni][v] + L * (row0 + i);
+                    double* base = sc.ptr[0];
+                    long long o = 0, ld = sc.ld[0];
+#pragma unroll
+                    for (int k = 1; k < kMaxRanks; ++k)
+                        if (k < sc.G && ca >= sc.off[k]) {
+                            base = sc.ptr[k];
+                            o = sc.off[k];
+                            ld = sc.ld[k];
+                        }
+                    base[ca - o + sc.a_shift + ld * (fr[ni][v] + sc.b_shift)] = c[mi][ni][v];
+                }
+        }
+    } else if constexpr (FWD) {
         const int row0 = wm ? a.F : 0, rows = wm ? a.h : a.F;
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
@@ -594,8 +631,11 @@ cudaError_t fold_launch_t(const Tiling& t, const ModeGeom& g, const double* X, d
 
 template <int MI, int WN>
 cudaError_t fold_ms_launch_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                             const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
-    auto k = fwd ? (pre ? fold_ms_kernel<MI, WN, 2, true, false, true> : fold_ms_kernel<MI, WN, 2, true, false, false>)
+                             const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ,
+                             const Scatter* sc = nullptr) {
+    auto k = fwd ? (sc ? fold_ms_kernel<MI, WN, 2, true, false, false, true>
+                       : (pre ? fold_ms_kernel<MI, WN, 2, true, false, true>
+                              : fold_ms_kernel<MI, WN, 2, true, false, false>))
                  : (post ? fold_ms_kernel<MI, WN, 2, false, true, false>
                          : fold_ms_kernel<MI, WN, 2, false, false, false>);
     const size_t smem = pre ? fold_prescale_smem(t) : t.smem;
@@ -606,23 +646,25 @@ cudaError_t fold_ms_launch_t(const Tiling& t, const ModeGeom& g, const double* X
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const long long blocks = (g.ncols + t.BN - 1) / t.BN * t.RB;
-    k<<<static_cast<unsigned>(blocks), 64 * WN, smem, st>>>(make_fargs(t, g), X, Y, J, post, pre);
+    k<<<static_cast<unsigned>(blocks), 64 * WN, smem, st>>>(make_fargs(t, g), X, Y, J, post, pre,
+                                                              sc ? *sc : Scatter{});
     return cudaGetLastError();
 }
 
 template <int WN>
 cudaError_t fold_ms_dispatch_wn(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                                const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
+                                const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ,
+                                const Scatter* sc = nullptr) {
     switch (t.MI) {
-        case 1: return fold_ms_launch_t<1, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
-        case 2: return fold_ms_launch_t<2, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
-        case 3: return fold_ms_launch_t<3, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
-        case 4: return fold_ms_launch_t<4, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
-        case 5: return fold_ms_launch_t<5, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
-        case 6: return fold_ms_launch_t<6, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
-        case 7: return fold_ms_launch_t<7, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
-        case 8: return fold_ms_launch_t<8, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
-        case 9: return fold_ms_launch_t<9, WN>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        case 1: return fold_ms_launch_t<1, WN>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
+        case 2: return fold_ms_launch_t<2, WN>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
+        case 3: return fold_ms_launch_t<3, WN>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
+        case 4: return fold_ms_launch_t<4, WN>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
+        case 5: return fold_ms_launch_t<5, WN>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
+        case 6: return fold_ms_launch_t<6, WN>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
+        case 7: return fold_ms_launch_t<7, WN>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
+        case 8: return fold_ms_launch_t<8, WN>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
+        case 9: return fold_ms_launch_t<9, WN>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -652,13 +694,15 @@ cudaError_t fold_dispatch_wn(const Tiling& t, const ModeGeom& g, const double* X
 }
 
 cudaError_t fold_dispatch(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
-                          const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ) {
+                          const double* post, const double* pre, bool fwd, cudaStream_t st, int* occ,
+                          const Scatter* sc = nullptr) {
     if (t.WM == 2) {
         if (t.NI != 2) return cudaErrorInvalidValue;
-        if (t.WN == 4) return fold_ms_dispatch_wn<4>(t, g, X, Y, J, post, pre, fwd, st, occ);
-        if (t.WN == 2) return fold_ms_dispatch_wn<2>(t, g, X, Y, J, post, pre, fwd, st, occ);
+        if (t.WN == 4) return fold_ms_dispatch_wn<4>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
+        if (t.WN == 2) return fold_ms_dispatch_wn<2>(t, g, X, Y, J, post, pre, fwd, st, occ, sc);
         return cudaErrorInvalidValue;
     }
+    if (sc) return cudaErrorInvalidValue;  // scatter epilogue: WM = 2 layout only
     if (t.NI == 2 && t.WN == 4) return fold_dispatch_wn<4, 2>(t, g, X, Y, J, post, pre, fwd, st, occ);
     if (t.NI == 2 && t.WN == 2) return fold_dispatch_wn<2, 2>(t, g, X, Y, J, post, pre, fwd, st, occ);
     if (t.NI == 4 && t.WN == 2) return fold_dispatch_wn<2, 4>(t, g, X, Y, J, post, pre, fwd, st, occ);
@@ -716,12 +760,14 @@ std::vector<Tiling> fold_tiling_candidates(int n) {
 }
 
 cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
-                                bool forward, const double* post_scale, cudaStream_t st, const double* pre_scale) {
+                                bool forward, const double* post_scale, cudaStream_t st, const double* pre_scale,
+                                const Scatter* sc) {
     if (g.ncols <= 0) return cudaSuccess;
     if (!t.fold || g.m != g.n || g.n < 2 || (forward && post_scale) || (!forward && pre_scale))
         return cudaErrorInvalidValue;
+    if (sc && (!forward || pre_scale || t.WM != 2 || sc->G < 1 || sc->G > kMaxRanks)) return cudaErrorInvalidValue;
     if (pre_scale && fold_prescale_smem(t) > kSmemPerCTA) return cudaErrorInvalidValue;
-    return fold_dispatch(t, g, X, Y, Jfold, post_scale, pre_scale, forward, st, nullptr);
+    return fold_dispatch(t, g, X, Y, Jfold, post_scale, pre_scale, forward, st, nullptr, sc);
 }
 
 size_t fold_prescale_smem(const Tiling& t) {
