@@ -22,15 +22,15 @@ class SkewPencilEig:
         self.U, self.lam, self.zero_count = U, lam, zero_count
 
 
-def skew_pencil_eig(W, M):
-    """pencil.cpp:23-95: Cholesky reduction, eig of S^T S, pair walk, zero columns last."""
+def _reduce_skew(W, M):
+    """pencil.cpp:30-44: shape / skewness checks, Cholesky of M, S = L^-1 W L^-T skew-symmetrized."""
     W = np.asarray(W, dtype=np.float64)
     M = np.asarray(M, dtype=np.float64)
     n = W.shape[0]
     if W.shape != (n, n) or M.shape != (n, n):
         raise ValueError("skew_pencil_eig: shape mismatch")
     if n == 0:
-        return SkewPencilEig(np.zeros((0, 0)), [], 0)
+        return None, None, None
     wmax = np.abs(W).max()
     if np.abs(W + W.T).max() > 1e-13 * max(wmax, 1.0):
         raise RuntimeError("skew_pencil_eig: matrix is not skew-symmetric (assembly bug)")
@@ -41,6 +41,50 @@ def skew_pencil_eig(W, M):
     S = sla.solve_triangular(L, W, lower=True)
     S = sla.solve_triangular(L, S.T, lower=True).T
     S = 0.5 * (S - S.T)
+    return n, L, S
+
+
+def skew_pencil_eig(W, M):
+    """Real-block eigendecomposition of the skew pencil (W, M) with the contract of
+    pencil.cpp:23-95: U^T M U = I, U^T W U = blockdiag([[0, lam_j], [-lam_j, 0]], 0..), pair columns
+    (v, q) in ascending lam, zero columns last.
+
+    Deliberate deviation: the pairs come from the Hermitian eigenproblem of iS through
+    its real symmetric embedding (`_embedding_pairs`), not from the eigenvectors of S^T S.  The
+    reference's S^T S walk (restated in `skew_pencil_eig_walk`) squares the conditioning: at p = 4,
+    n_el = 64 (config 4) its U^T M U - I is 1e-8, the embedding's 5e-15; at p = 3, n_el = 256
+    (config 2) the walk fails outright ("eigenvalue pairing failed")."""
+    n, L, S = _reduce_skew(W, M)
+    if n is None:
+        return SkewPencilEig(np.zeros((0, 0)), [], 0)
+    mu, Q = np.linalg.eigh(S.T @ S)  # only to count / seed the zero columns (pencil.cpp:50-52, 72-76)
+    mu = np.maximum(mu, 0.0)
+    zero_tol = 1e-12 * max(mu[n - 1], 1.0)
+    lam_out, pair_cols = _embedding_pairs(S, zero_tol)
+    nz = n - 2 * len(lam_out)
+    if nz < 0 or nz > int(np.sum(mu <= zero_tol)) + 1:
+        raise RuntimeError("skew_pencil_eig: eigenvalue pairing failed")
+    B = np.column_stack(pair_cols) if pair_cols else np.zeros((n, 0))
+    zero_cols = []
+    for k in range(nz):  # null vectors of S, orthogonal to every pair column (two passes)
+        q = Q[:, k].copy()
+        for _ in range(2):
+            q -= B @ (B.T @ q)
+            for c in zero_cols:
+                q -= c.dot(q) * c
+        zero_cols.append(q / np.linalg.norm(q))
+    Ublk = np.column_stack(pair_cols + zero_cols)
+    U = sla.solve_triangular(L.T, Ublk, lower=False)  # pencil.cpp:93
+    return SkewPencilEig(U, lam_out, nz)
+
+
+def skew_pencil_eig_walk(W, M):
+    """pencil.cpp:23-95 as written: Cholesky reduction, eig of S^T S, pair walk, zero columns last.
+    Kept as the restatement of the reference algorithm (tests pin where it fails or loses accuracy);
+    `skew_pencil_eig` is the one the oracle uses."""
+    n, L, S = _reduce_skew(W, M)
+    if n is None:
+        return SkewPencilEig(np.zeros((0, 0)), [], 0)
     C = S.T @ S
     mu, Q = np.linalg.eigh(C)
     mu = np.maximum(mu, 0.0)
@@ -69,24 +113,20 @@ def skew_pencil_eig(W, M):
         pair_cols += [v, q]
         cluster += [q, v]
     if len(pair_cols) + len(zero_cols) != n:
-        # The reference throws here (pencil.cpp:86-87).  This happens for real inputs: at p = 3,
-        # n_el = 256 (config 2) the two largest pairs of S^T S are within 4e-11 relative, the
-        # eigenvectors mix at the 1e-5 level and the 1e-6 projection threshold accepts a spurious
-        # pair.  Deliberate deviation: extract the pairs from the
-        # Hermitian eigenproblem of iS instead; same contract, basis-invariant FD output at nu = 1.
-        lam_out, pair_cols = _robust_pairs(S, zero_tol)
-        if 2 * len(lam_out) + len(zero_cols) != n:
-            raise RuntimeError("skew_pencil_eig: eigenvalue pairing failed")
+        raise RuntimeError("skew_pencil_eig: eigenvalue pairing failed")  # pencil.cpp:86-87
     Ublk = np.column_stack(pair_cols + zero_cols)
     U = sla.solve_triangular(L.T, Ublk, lower=False)
     return SkewPencilEig(U, lam_out, len(zero_cols))
 
 
-def _robust_pairs(S, zero_tol_mu):
+def _embedding_pairs(S, zero_tol_mu):
     """Real pairs (v, q) with S q = lam v, S v = -lam q from the real symmetric embedding
     E = [[0, -S], [S, 0]] of the Hermitian iS: E [x; y] = lam [x; y]  <=>  S x = lam y, -S y = lam x,
-    so q = sqrt(2) x, v = sqrt(2) y.  Near-degenerate clusters are resolved by pivoted Gram-Schmidt
-    over the J-invariant eigenspace (J [x; y] = [-y; x])."""
+    so q = sqrt(2) x, v = sqrt(2) y.  Every positive eigenvalue of E is double (z and Jz,
+    J [x; y] = [-y; x]); the pairs are built by pivoted Gram-Schmidt over each cluster's J-invariant
+    eigenspace, orthogonalising every new z and Jz against ALL accepted vectors (two passes), so
+    distinct pairs whose eigenvalues are closer than the eigensolver can separate stay exactly
+    orthonormal (their mixing only perturbs U^T W U by gap x mixing ~ eps)."""
     n = S.shape[0]
     E = np.zeros((2 * n, 2 * n))
     E[:n, n:] = -S
@@ -103,37 +143,41 @@ def _robust_pairs(S, zero_tol_mu):
         cur.append(k)
     if cur:
         clusters.append(cur)
+    basis = []
+
+    def project(r):
+        for _ in range(2):
+            for b in basis:
+                r -= b.dot(r) * b
+        return r
+
     pairs = []
     for cl in clusters:
-        basis = []
         cand = [V[:, k].copy() for k in cl]
         for _ in range(len(cl) // 2):
             best, bnorm = None, -1.0
             for c in cand:
-                r = c.copy()
-                for b in basis:
-                    r -= b.dot(r) * b
+                r = project(c.copy())
                 nr = np.linalg.norm(r)
                 if nr > bnorm:
                     best, bnorm = r, nr
-            z = best / bnorm
-            for b in basis:
-                z -= b.dot(z) * b
+            z = project(best / bnorm)
             z /= np.linalg.norm(z)
-            jz = np.concatenate([-z[n:], z[:n]])
-            for b in basis + [z]:
-                jz -= b.dot(jz) * b
+            basis.append(z)
+            jz = project(np.concatenate([-z[n:], z[:n]]))
             jz /= np.linalg.norm(jz)
-            basis += [z, jz]
+            basis.append(jz)
             lam = z.dot(E @ z)
-            q, v = np.sqrt(2.0) * z[:n], np.sqrt(2.0) * z[n:]
-            pairs.append((lam, v, q))
+            pairs.append((lam, np.sqrt(2.0) * z[n:], np.sqrt(2.0) * z[:n]))
     pairs.sort(key=lambda t: t[0])
     lam_out = [t[0] for t in pairs]
     cols = []
     for _, v, q in pairs:
         cols += [v, q]
     return lam_out, cols
+
+
+_robust_pairs = _embedding_pairs  # name used by round-1 tests
 
 
 class TimeFactorization:

@@ -849,9 +849,12 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
             // unset: both kinds are candidates of the setup-time autotuner
             const char* fk = std::getenv("STIGA_FOLD_KERNEL");
             const bool dense_only = fk && std::string(fk) == "off";
-            const bool fold_only = fk && std::string(fk) == "force";
+            const bool fold_only = fk && (std::string(fk) == "force" || std::string(fk) == "force_wm2");
+            const bool fold_wm2 = fk && std::string(fk) == "force_wm2";  // tests: folded WM = 2 tilings only
             if (F.fold[l].on && !dense_only) {  // folded candidates first (half the FLOPs)
                 std::vector<gpu::Tiling> fc = gpu::fold_tiling_candidates(F.n[l]);
+                if (fold_wm2) fc.erase(std::remove_if(fc.begin(), fc.end(), [](const gpu::Tiling& t) { return t.WM != 2; }),
+                                       fc.end());
                 int frows = 0;
                 for (const auto& t : fc) frows = std::max(frows, t.Mp);
                 for (auto& t : fc) t.Mp = frows;  // both matrices padded to the largest row-block cover
@@ -863,7 +866,8 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
             }
             if (!(fold_only && !cands.empty())) cands.insert(cands.end(), dense.begin(), dense.end());
             h->cand_space.push_back(cands);
-            // WM = 1 dense tiling: the only kind with the scatter epilogue (and the pre-scale)
+            // WM = 1 dense tiling: the fallback for the scatter / pre-scale stages when the chosen tiling
+            // has no such epilogue (folded WM = 2 tilings carry their own scatter epilogue)
             gpu::Tiling tdense = dense.front();
             for (const auto& t : dense)
                 if (t.WM == 1) {

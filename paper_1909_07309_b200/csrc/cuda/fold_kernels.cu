@@ -765,7 +765,9 @@ cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double
     if (g.ncols <= 0) return cudaSuccess;
     if (!t.fold || g.m != g.n || g.n < 2 || (forward && post_scale) || (!forward && pre_scale))
         return cudaErrorInvalidValue;
-    if (sc && (!forward || pre_scale || t.WM != 2 || sc->G < 1 || sc->G > kMaxRanks)) return cudaErrorInvalidValue;
+    // the folded epilogue picks the owner from the spatial index: only by_time = 0 descriptors
+    if (sc && (!forward || pre_scale || t.WM != 2 || sc->G < 1 || sc->G > kMaxRanks || sc->by_time != 0))
+        return cudaErrorInvalidValue;
     if (pre_scale && fold_prescale_smem(t) > kSmemPerCTA) return cudaErrorInvalidValue;
     return fold_dispatch(t, g, X, Y, Jfold, post_scale, pre_scale, forward, st, nullptr, sc);
 }

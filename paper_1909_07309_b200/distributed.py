@@ -297,10 +297,12 @@ class FusedShardedExtendedFD:
             flag = torch.zeros(1, dtype=torch.float64, device=f"cuda:{dev}")
 
             def barrier():  # stream-ordered: the next stage's kernels wait for every rank's scatter
-                dist.all_reduce(flag, group=group)
+                st = stream if stream is not None else torch.cuda.current_stream()
+                with torch.cuda.stream(st):  # order the all-reduce on the stage stream
+                    dist.all_reduce(flag, group=group)
         elif world > 1:
             def barrier():
-                torch.cuda.current_stream().synchronize()
+                (stream if stream is not None else torch.cuda.current_stream()).synchronize()
                 dist.barrier(group=group)
         else:
             barrier = None
@@ -534,26 +536,34 @@ class DeviceVec:
         check(lib().stiga_vec_scal(float(alpha), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
                                    x.numel(), self._st()), "vec_scal")
 
+    MULTI_MAX = 64  # stiga_vec_multidot / stiga_vec_multiaxpy accept k <= 64 vectors per call
+
     def multidot(self, Vs, w):
-        """[V_j . w for j], all-reduced over the group in ONE collective (CGS2)."""
+        """[V_j . w for j], all-reduced over the group in ONE collective (CGS2).  Cycles longer than 64
+        columns are reduced in chunks of 64 into one output vector before the single all-reduce."""
         import torch
 
         k = len(Vs)
         out = torch.empty(k, dtype=torch.float64, device=w.device)
-        ptrs = (ctypes.c_void_p * k)(*[v.data_ptr() for v in Vs])
-        check(lib().stiga_vec_multidot(ptrs, k, ctypes.c_void_p(w.data_ptr()), w.numel(),
-                                       ctypes.c_void_p(out.data_ptr()), self._st()), "vec_multidot")
+        for c0 in range(0, k, self.MULTI_MAX):
+            c1 = min(k, c0 + self.MULTI_MAX)
+            ptrs = (ctypes.c_void_p * (c1 - c0))(*[v.data_ptr() for v in Vs[c0:c1]])
+            check(lib().stiga_vec_multidot(ptrs, c1 - c0, ctypes.c_void_p(w.data_ptr()), w.numel(),
+                                           ctypes.c_void_p(out[c0:c1].data_ptr()), self._st()), "vec_multidot")
         if self.dist.is_initialized() and self.dist.get_world_size(self.group) > 1:
             _all_reduce_sum(self.dist, out, self.group)
         return out.cpu().numpy()
 
     def multiaxpy(self, coefs, Vs, w):
-        """w += sum_j coefs[j] V_j."""
+        """w += sum_j coefs[j] V_j (chunks of <= 64 vectors)."""
         k = len(Vs)
         c = np.ascontiguousarray(coefs, dtype=np.float64)
-        ptrs = (ctypes.c_void_p * k)(*[v.data_ptr() for v in Vs])
-        check(lib().stiga_vec_multiaxpy(c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ptrs, k,
-                                        ctypes.c_void_p(w.data_ptr()), w.numel(), self._st()), "vec_multiaxpy")
+        for c0 in range(0, k, self.MULTI_MAX):
+            c1 = min(k, c0 + self.MULTI_MAX)
+            ptrs = (ctypes.c_void_p * (c1 - c0))(*[v.data_ptr() for v in Vs[c0:c1]])
+            cc = np.ascontiguousarray(c[c0:c1])
+            check(lib().stiga_vec_multiaxpy(cc.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ptrs, c1 - c0,
+                                            ctypes.c_void_p(w.data_ptr()), w.numel(), self._st()), "vec_multiaxpy")
 
 
 class SolveReport:

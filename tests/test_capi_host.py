@@ -117,3 +117,22 @@ def test_host_setup_errors():
     P = stiga.ExtendedFDPreconditioner.setup(K, M, W, Mt, 1.0, 1.0, device=-1)
     with pytest.raises(ValueError):  # host-only handle cannot apply
         P.apply(np.zeros(P.n_dof))
+
+
+@pytest.mark.parametrize("p,nel", [(2, 16), (3, 256), (3, 96), (4, 64), (2, 64), (4, 128), (5, 160)])
+def test_host_time_factorization_accuracy_baseline_pencils(p, nel):
+    """The product's own eigensolver (Householder + QL on the Hermitian embedding, host/pencil.cpp)
+    reaches the oracle's accuracy on every BASELINE time pencil: U_t^T M_t U_t = I and
+    U_t^T W_t U_t = Delta_t to ~1e-14 (p = 4 at config 4 was 2.5e-8 with the S^T S walk)."""
+    K, M = stiga.assemble_spatial_parametric(p, 4, 1)
+    W, Mt = stiga.assemble_time_matrices(p, nel)
+    P = stiga.ExtendedFDPreconditioner.setup(K, M, W, Mt, 1.0, 1.0, device=-1)
+    ti = P.time_info()
+    Ut = P.export(2)
+    n = Ut.shape[0]
+    Dt = open_.TimeFactorization(Ut, list(P.export(3)), ti["zero_count"], P.export(4), ti["sigma"], None,
+                                 ti["rho"]).delta()
+    assert np.abs(Ut.T @ Mt @ Ut - np.eye(n)).max() <= 1e-13
+    assert np.abs(Ut.T @ W @ Ut - Dt).max() <= 1e-13 * np.abs(Dt).max()
+    tf = open_.time_factorization(W, Mt)
+    assert np.abs(P.export(3) - np.array(tf.lam)).max() <= 1e-12 * max(tf.lam)

@@ -184,23 +184,27 @@ def virtual_fused_apply(P, r, world):
     return torch.cat(outs)
 
 
-@pytest.mark.parametrize("fold", ["off", "auto"])
+@pytest.mark.parametrize("fold", ["off", "auto", "force_wm2"])
 @pytest.mark.parametrize("variant", ["fused", "split"])
 @pytest.mark.parametrize("world,d,p,nel", [(1, 2, 3, 9), (2, 2, 3, 9), (3, 3, 2, 6), (4, 1, 4, 30), (8, 3, 3, 12),
                                            (5, 2, 2, 40)])
 def test_virtual_ranks_fused_exchange(fold, variant, world, d, p, nel, monkeypatch):
     """Scatter-epilogue path = oracle (<= 1e-11); with dense kernels bit-identical to the pack +
-    all-to-all path (with folded kernels the scattering last forward product is the dense kernel on
-    the same split basis, so the two paths agree to rounding)."""
+    all-to-all path.  fold = force_wm2 restricts every split direction to folded WM = 2 tilings, so
+    the last forward product runs the folded kernel's own scatter epilogue (fold_kernels.cu); with
+    folded kernels the two paths agree to rounding."""
     monkeypatch.setenv("STIGA_TIME_VARIANT", variant)
-    if fold == "off":
-        monkeypatch.setenv("STIGA_FOLD_KERNEL", "off")
+    if fold != "auto":
+        monkeypatch.setenv("STIGA_FOLD_KERNEL", fold)
     pc = identity_pieces(d, p, nel)
     D = np.exp(0.3 * uniform_pm1(pc.n_dof, 3))
     P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D, device=0)
     Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D)
     r = uniform_pm1(pc.n_dof, 4)
     rt = torch.from_numpy(r).cuda()
+    if fold == "force_wm2" and P.dims[0] >= 2:
+        names = [nm for nm, _ in P.launch_info()]
+        assert f"fwd_mode{d - 1}(folded)" in names, names  # the scattering product is the folded kernel
     s = virtual_fused_apply(P, rt, world)
     so = Po.apply(r)
     assert np.linalg.norm(s.cpu().numpy() - so) / np.linalg.norm(so) <= 1e-11

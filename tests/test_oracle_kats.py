@@ -310,3 +310,39 @@ def test_reference_pairing_walk_fails_on_config2():
     for j, l_ in enumerate(lam):
         v, q = cols[2 * j], cols[2 * j + 1]
         assert np.linalg.norm(S @ q - l_ * v) <= 1e-12 * l_ and np.linalg.norm(S @ v + l_ * q) <= 1e-12 * l_
+
+
+# BASELINE time pencils: c1 (p2 n16), c2 (p3 n256), c3 / c5p3 (p3 n96), c4 (p4 n64), c5p2 (p2 n64),
+# c5p4 (p4 n128), c5p5 (p5 n160)
+BASELINE_TIME = [(2, 16), (3, 256), (3, 96), (4, 64), (2, 64), (4, 128), (5, 160)]
+
+
+def _time_residuals(tf, W, M):
+    n = W.shape[0]
+    e_m = np.abs(tf.U.T @ M @ tf.U - np.eye(n)).max()
+    Dt = tf.delta()
+    e_w = np.abs(tf.U.T @ W @ tf.U - Dt).max() / np.abs(Dt).max()
+    return e_m, e_w
+
+
+@pytest.mark.parametrize("p,nel", BASELINE_TIME)
+def test_time_factorization_accuracy_baseline_pencils(p, nel):
+    """The Hermitian-embedding pairs give U_t^T M_t U_t = I and U_t^T W_t U_t =
+    Delta_t to ~1e-14 on every BASELINE time pencil, p = 4 / 5 included."""
+    W, M = assembly.assemble_time_matrices(p, nel, 1.0)
+    e_m, e_w = _time_residuals(pencil.time_factorization(W, M), W, M)
+    assert e_m <= 1e-13 and e_w <= 1e-13, (e_m, e_w)
+
+
+def test_reference_walk_loses_accuracy_at_config4():
+    """Why the deviation: the reference's S^T S walk (pencil.cpp:54-87) squares the conditioning.  On
+    the config-4 time pencil (p = 4, n_el = 64) its U_t^T M_t U_t - I is ~1e-8, so two correct
+    implementations of the walk disagree by ~1e-8 on the FD output -- above the 1e-11 parity bar."""
+    W, M = assembly.assemble_time_matrices(4, 64, 1.0)
+    n = W.shape[0] - 1
+    walk = pencil.skew_pencil_eig_walk(W[:n, :n], M[:n, :n])
+    e_walk = np.abs(walk.U.T @ M[:n, :n] @ walk.U - np.eye(n)).max()
+    emb = pencil.skew_pencil_eig(W[:n, :n], M[:n, :n])
+    e_emb = np.abs(emb.U.T @ M[:n, :n] @ emb.U - np.eye(n)).max()
+    assert e_walk > 1e-10 and e_emb <= 1e-13
+    assert np.allclose(walk.lam, emb.lam, rtol=1e-10, atol=0)  # same spectrum, better vectors

@@ -112,3 +112,31 @@ def test_geometry_scaling_from_device_assembly(pid, p, nel):
     Dh = prob.geometry_pieces(p, nel, want_D=True).D
     Dd = prob.geometry_pieces(p, nel, want_D=True, device=0).D
     assert np.abs(Dd - Dh).max() <= 1e-13 * np.abs(Dh).max()
+
+
+def test_gmres_full_c4_iterations_match_oracle():
+    """BASELINE config 4 at full size (19.3M DoF, fitted deformed cube, kappa(x), c(x), A^G with the
+    D^-1/2 geometry scaling): the device GMRES (csrc/gmres.cpp) and the oracle's GMRES
+    (oracle/gmres.py = gmres.cpp:19-132) with the ORACLE's preconditioner (its own, independent
+    factorization) converge to 1e-8 within +-1 iteration of each other (13 here).  The oracle cannot
+    assemble the physical A of c4 on the host (64^3 elements x 125^2 local entries), so both solves
+    use the device-assembled physical operator for A (pinned against the oracle's
+    assemble_spatial_physical at small sizes, tests/test_geometry.py)."""
+    from paper_1909_07309_b200.problems import Problem
+
+    cfg = CONFIGS["c4"]
+    prob = Problem(cfg.problem)
+    pc = prob.geometry_pieces(cfg.p, cfg.n_el, want_D=True, device=0)
+    A = stiga.KronSumOperator.physical(prob, cfg.p, cfg.n_el)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=pc.D, device=0)
+    b = uniform_pm1(P.n_dof, cfg.seed)
+    x, rep = stiga.gmres(A, P, torch.from_numpy(b).cuda(), stiga.GmresOptions(1e-8, 500, 50))
+    Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=pc.D)
+
+    def A_host(v):
+        return A.apply(torch.from_numpy(v).cuda()).cpu().numpy()
+
+    xo, repo = ogm.gmres(A_host, Po.apply, b, 1e-8, 500, 50)
+    assert rep.converged and repo.converged
+    assert rep.iterations > 5 and abs(rep.iterations - repo.iterations) <= 1, (rep.iterations, repo.iterations)
+    assert rel(x.cpu().numpy(), xo) <= 1e-6
