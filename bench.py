@@ -1,14 +1,17 @@
 """Benchmark of the extended-FD preconditioner apply (+ GMRES time-to-1e-8) on B200.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5p5] [--impl ours|reference]
 
 One step = one ExtendedFDPreconditioner::apply (fdsolve.cpp:155-164) of the A^G preconditioner
-over one seeded uniform[-1,1] vector of the configuration (BASELINE.json configs[1] = c2 by
-default: d=2, p=3, n_el=256, 17,040,642 DoF).  Inputs are resident in HBM and larger than L2
-(136 MB > 126 MB), so no L2 flush is needed between steps.  Prints ONE JSON line (rank 0).
+over one seeded uniform[-1,1] vector of the configuration.  Default: the largest single-GPU BASELINE
+configuration, c5p5 (configs[4]: d = 3, p = 5, n_el = 160, 710,242,508 DoF, 5.7 GB per vector).
+Inputs are resident in HBM and larger than L2 (126 MB), so no L2 flush is needed between steps.
+Prints ONE JSON line (rank 0).  --gpus N > 1 without a launcher starts N ranks itself
+(torch.distributed.run, 127.0.0.1) and runs the time-sharded apply (strong scaling, same config).
 
 --impl reference times the reference's CPU path for the same workload: the Eigen-free restatement
-in oracle/ (the reference itself needs Eigen and cannot be compiled here).
+in oracle/ (the reference itself needs Eigen and cannot be compiled here), each
+step a bounded sample of the full apply (oracle/sampled.py).
 """
 import argparse
 import json
@@ -29,11 +32,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5p5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--cpu-frac", type=float, default=None,
+                    help="fraction of every pass's units in one sampled CPU apply (default: sized to ~2 s)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1 time-sharded apply: p2p = all-to-all fused into the kernels' scatter epilogues "
                          "over NVLink peer memory (CUDA IPC); nccl = pack + NCCL all_to_all_single + unpack")
@@ -103,35 +107,57 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------
 # CPU path (oracle restatement of the reference) -- baseline and --impl reference
 # ------------------------------------------------------------------------------------------
-def cpu_fd_timing(cfg, steps, warmup, budget_s=None):
-    import numpy as np
+def cpu_sampler(cfg, frac=None, target_s=2.0):
+    """oracle.sampled.SampledFD for cfg (host pieces of the same workload; c4's geometry pieces come
+    from the product's host setup, the timed apply is the oracle's).  frac=None sizes the sample so
+    one sampled apply takes ~target_s on all host cores."""
+    from oracle.sampled import SampledFD
 
-    from oracle.assembly import assemble_spatial_parametric, assemble_time_matrices
-    from oracle.fdsolve import ExtendedFDPreconditioner as OracleFD
-    from paper_1909_07309_b200.inputs import uniform_pm1
+    pieces = None
+    if cfg.problem != "identity":
+        pc, _ = problem_pieces(cfg)
+        pieces = (pc.K, pc.M, pc.Wt, pc.Mt)
+    f = frac if frac is not None else min(1.0, 0.05 * 17.0e6 / cfg.n_dof)
+    S = SampledFD(cfg, f, pieces)
+    if frac is None:  # rescale from one timed sample
+        est, wall, _ = S.run()
+        f2 = min(1.0, max(1e-4, f * target_s / max(wall, 1e-3)))
+        if abs(f2 - f) / f > 0.3:
+            S = SampledFD(cfg, f2, pieces)
+    return S
 
+
+def cpu_baseline(cfg, frac=None):
+    """cpu_baseline of the JSON line: the oracle port on a bounded sample, all host cores (OpenBLAS
+    threads) and 1 core, plus the CPU GMRES estimate (n_P P + n_A A applies of the identity-geometry
+    solve, one iteration: gmres.cpp:42, 76)."""
+    from oracle.sampled import SampledMatvec, blas_threads, threads_limit
+
+    S = cpu_sampler(cfg, frac)
+    S.run()  # warm-up (study.cpp:210-213 excludes one warm-up apply)
+    ests = [S.run()[0] for _ in range(3)]
+    t_all = statistics.median(ests)
+    cores = blas_threads()
+    with threads_limit(1):
+        S1 = S if S.frac <= 0.02 else type(S)(cfg, max(1e-4, S.frac / 4), (S.K, S.M, S.Wt, S.Mt))
+        S1.run()
+        t_one = statistics.median([S1.run()[0] for _ in range(2)])
+    out = {"value": 1.0 / t_all, "unit": "applies/s", "cores": cores, "kind": "port",
+           "sample": f"oracle/fdsolve.py apply of {cfg.name} (fdsolve.cpp:155-164), every pass on "
+                     f"{100 * S.frac:.2f}% of its independent units (slabs / columns / spatial indices) and "
+                     f"extrapolated; median of 3 after 1 warm-up; numpy/OpenBLAS on {cores} threads",
+           "single_core": {"value": 1.0 / t_one, "unit": "applies/s", "cores": 1,
+                           "sample": f"same, {100 * S1.frac:.2f}% of the units, BLAS limited to 1 thread "
+                                     f"(the reference is single-threaded, PAPER.md:1120)"},
+           "apply_s_all_cores": t_all, "apply_s_single_core": t_one}
     if cfg.problem == "identity":
-        W, Mt = assemble_time_matrices(cfg.p, cfg.n_el, 1.0)
-        K, M = assemble_spatial_parametric(cfg.p, cfg.n_el, cfg.d)
-        D = np.ones(cfg.n_dof)  # diag(A)/diag(A~) on the identity map (see problems.geometry_scaling)
-    else:  # host pieces (geometry fit, separation, D) from the product's setup code; the apply is timed
-        pc, D = problem_pieces(cfg)
-        K, M, W, Mt = pc.K, pc.M, pc.Wt, pc.Mt
-    t0 = time.perf_counter()
-    P = OracleFD.setup(K, M, W, Mt, 1.0, 1.0, scaling=D)
-    setup_s = time.perf_counter() - t0
-    r = uniform_pm1(cfg.n_dof, cfg.seed)
-    for _ in range(warmup):
-        P.apply(r)
-    times = []
-    t_start = time.perf_counter()
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        P.apply(r)
-        times.append(time.perf_counter() - t0)
-        if budget_s is not None and time.perf_counter() - t_start > budget_s:
-            break
-    return times, setup_s
+        A = SampledMatvec(S, S.frac)
+        t_a = statistics.median([A.run() for _ in range(2)])
+        out["gmres_cpu_est"] = {"time_s": 2 * t_all + t_a, "n_P": 2, "n_A": 1, "matvec_s": t_a,
+                                "note": "one-iteration solve (identity geometry): P b, A v_0, P(A v_0); "
+                                        "mat-vec = sparse banded Kronecker factors (kronop.cpp:7-41) on the "
+                                        "same sampling; Krylov vector updates excluded"}
+    return out
 
 
 def problem_pieces(cfg, device=None):
@@ -149,40 +175,43 @@ def problem_pieces(cfg, device=None):
     return pc, pc.D
 
 
-def cores_used():
-    try:
-        from threadpoolctl import threadpool_info
-
-        info = threadpool_info()
-        n = max((i.get("num_threads", 1) for i in info if i.get("user_api") == "blas"), default=1)
-        return int(n)
-    except Exception:
-        return os.cpu_count() or 1
-
-
 def run_reference(args):
+    """The reference arm: the oracle port of the reference's CPU path on the box's host cores (all
+    BLAS threads), on our arm's config / metric / unit; each step one bounded sample of the full apply
+    (oracle/sampled.py), extrapolated to applies/s.  Rank 0 only under a launcher."""
+    from oracle.sampled import blas_threads
     from paper_1909_07309_b200.configs import CONFIGS
 
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
-    warm = max(1, min(args.warmup, 3))
-    steps = max(1, min(args.steps, 20))
-    times, setup_s = cpu_fd_timing(cfg, steps, warm, budget_s=150.0)
-    total = sum(times)
-    v = len(times) / total
-    cores = cores_used()
+    warm, steps = max(args.warmup, 3), max(1, args.steps)
+    t0 = time.perf_counter()
+    S = cpu_sampler(cfg, args.cpu_frac, target_s=min(2.0, 150.0 / (warm + steps)))
+    setup_s = time.perf_counter() - t0
+    for _ in range(warm):
+        S.run()
+    ests, walls = [], []
+    for _ in range(steps):
+        e, w, _ = S.run()
+        ests.append(e)
+        walls.append(w)
+    t = sum(ests) / len(ests)
+    v = 1.0 / t
+    cores = blas_threads()
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "applies/s", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": warm, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * t, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1])",
         "dof_per_s": v * cfg.n_dof, "setup_s": setup_s,
-        "config": {"workload": f"{cfg.name}: {cfg.note}; A^G FD apply", "d": cfg.d, "p": cfg.p, "n_el": cfg.n_el,
-                   "n_dof": cfg.n_dof, "parallelism": "cpu"},
+        "config": {"workload": f"{cfg.name}: {cfg.note}; A^G FD apply (D^-1/2 scaled), {cfg.problem} geometry",
+                   "d": cfg.d, "p": cfg.p, "n_el": cfg.n_el, "n_dof": cfg.n_dof, "parallelism": "cpu"},
         "cpu_baseline": {"value": v, "unit": "applies/s", "cores": cores, "kind": "port",
-                         "sample": f"{len(times)} full {cfg.name} applies of the numpy/OpenBLAS restatement "
-                                   f"(oracle/fdsolve.py, reference fdsolve.cpp:155-164)"},
+                         "sample": f"each step: every pass of the oracle apply (oracle/fdsolve.py = fdsolve.cpp:155-164) "
+                                   f"on {100 * S.frac:.2f}% of its independent units, extrapolated "
+                                   f"(sample wall {1e3 * sum(walls) / len(walls):.0f} ms per step; ms_per_step is "
+                                   f"the extrapolated full apply)"},
         "e2e": {"value": v, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -430,10 +459,7 @@ def run_ours(args):
     # ---- CPU baseline (rank 0, N = 1 only) ------------------------------------------------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        times, _ = cpu_fd_timing(cfg, 100, 1, budget_s=args.cpu_budget_s)
-        cpu = {"value": len(times) / sum(times), "unit": "applies/s", "cores": cores_used(), "kind": "port",
-               "sample": f"{len(times)} full {cfg.name} applies (after 1 warm-up) of the numpy/OpenBLAS restatement "
-                         f"oracle/fdsolve.py of fdsolve.cpp:155-164"}
+        cpu = cpu_baseline(cfg, args.cpu_frac)
 
     f_alg = cfg.flops_fd()
     t_roof_flop = f_alg / (peak_dmma * 1e12)
@@ -480,8 +506,24 @@ def run_ours(args):
     return 0
 
 
+def spawn_ranks(n):
+    """--gpus N > 1 without a launcher: start N ranks (one process per GPU) with torch.distributed.run on
+    127.0.0.1 and relay rank 0's line; the exit code is the launcher's."""
+    import socket
+    import subprocess
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -202,9 +202,9 @@ def test_virtual_ranks_fused_exchange(fold, variant, world, d, p, nel, monkeypat
     Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D)
     r = uniform_pm1(pc.n_dof, 4)
     rt = torch.from_numpy(r).cuda()
-    if fold == "force_wm2" and P.dims[0] >= 2:
+    if fold == "force_wm2" and P.dims[0] >= 2 and d > 1:  # (d = 1: the scatter product cannot also pre-scale)
         names = [nm for nm, _ in P.launch_info()]
-        assert f"fwd_mode{d - 1}(folded)" in names, names  # the scattering product is the folded kernel
+        assert any(nm.startswith(f"fwd_mode{d - 1}(folded)") for nm in names), names  # folded scatter epilogue
     s = virtual_fused_apply(P, rt, world)
     so = Po.apply(r)
     assert np.linalg.norm(s.cpu().numpy() - so) / np.linalg.norm(so) <= 1e-11
