@@ -161,6 +161,54 @@ int stiga_ipc_close(void* d_ptr);
 int stiga_copy_blocks(const double* d_src, long long src_ld, double* d_dst, long long dst_ld, long long rows,
                       long long cols, void* stream);
 
+/* ---- multi-GPU: communicator and time-sharded handles ------------------------
+   One process per GPU.  Rank r owns the time slices T_r = [t_off[r], t_off[r] + t_len[r]) of every
+   N_dof vector (a contiguous piece of the colex vector; balanced contiguous partition of n_t, the
+   first n_t % world ranks get one slice more -- stiga_shard_partition).  A sharded handle's apply,
+   mat-vec and GMRES take and return only the local slab; every rank calls them collectively.
+   The reference is serial; this is new work, not a replacement of a reference API. */
+typedef struct stiga_comm_s* stiga_comm_t;
+#define STIGA_COMM_ID_BYTES 128
+/* NCCL unique id (ncclGetUniqueId) for rank 0 to broadcast out of band. */
+int stiga_comm_unique_id(void* id_out);
+/* NCCL communicator of this rank over `world` ranks (ncclCommInitRank; NCCL is loaded at run time).
+   Collectives and barriers are stream-ordered on the caller's stream. */
+int stiga_comm_init_nccl(int world, int rank, const void* id, int device, stiga_comm_t* out);
+/* Host-callback communicator: the caller supplies the collectives (e.g. over an existing process
+   group); the library synchronizes the stream before calling them.  allreduce reduces n host doubles
+   in place (op 0 = sum, 1 = max); allgather gathers `bytes` from every rank into recv (world x bytes,
+   rank order).  Each returns 0 on success. */
+typedef struct {
+    void* ctx;
+    int (*allreduce)(void* ctx, double* buf, int n, int op);
+    int (*allgather)(void* ctx, const void* send, int bytes, void* recv);
+    int (*barrier)(void* ctx);
+} stiga_comm_callbacks;
+int stiga_comm_init_host(int world, int rank, const stiga_comm_callbacks* cb, int device, stiga_comm_t* out);
+int stiga_comm_destroy(stiga_comm_t C);
+/* world, rank, device, kind (0 = NCCL, 1 = host callbacks); any output may be NULL. */
+int stiga_comm_info(stiga_comm_t C, int* world, int* rank, int* device, int* kind);
+/* Sum-all-reduce of n doubles of device memory (stream-ordered for NCCL). */
+int stiga_comm_allreduce(stiga_comm_t C, double* d_buf, long long n, void* stream);
+/* Balanced contiguous partition of range(n) over world parts: offset and length of part `rank`. */
+int stiga_shard_partition(long long n, int world, int rank, long long* off, long long* len);
+
+/* Time-sharded ExtendedFDPreconditioner (collective): the same host setup on every rank, then the
+   rank's stage kernels are tuned on its slab geometry.  scaling_local: D for the local time slab only
+   (N_s x t_len[rank] entries, colex), or NULL.  Device memory per rank ~ 4-5 N_dof / world doubles
+   (two scratch slabs, two receive buffers, the D^-1/2 slab) plus the factors.  stiga_fd_apply on
+   the handle then runs the sharded apply on local slabs: forward spatial products with the last one
+   scattering into the owners' spatial-slab buffers (the all-to-all fused into the epilogue, NVLink P2P
+   stores through CUDA IPC pointers), a stream-ordered barrier, the time stage (U_t^T, arrowhead, U_t)
+   on the rank's spatial slab scattering back into the owners' time-slab buffers, a barrier, and the
+   backward spatial products with the D^-1/2 post-scale. */
+int stiga_fd_setup_sharded(int d, const int* n, const double* const* K, const double* const* M, int n_t,
+                           const double* Wt, const double* Mt, double gamma, double nu, const double* scaling_local,
+                           long long scaling_len, stiga_comm_t comm, stiga_fd_t* out);
+/* Local slab of a handle: time slices [*t0, *t0 + *nt_local), i.e. vector entries [*offset, *offset + *len)
+   of the global colex vector (t0 = 0, nt_local = n_t for a single-device handle). */
+int stiga_fd_local(stiga_fd_t P, long long* t0, long long* nt_local, long long* offset, long long* len);
+
 /* ---- Kronecker operators (kronop.hpp:47-79) ------------------------------------------- */
 
 /* kron_matvec(factors, x) (kronop.cpp:75-89) on device buffers: D factors, factor l is
@@ -208,6 +256,17 @@ int stiga_kronsum_apply_space(stiga_kronsum_t A, long long nt_local, const doubl
 int stiga_kronsum_apply_time(stiga_kronsum_t A, long long t0, long long nt_local, int halo_lo, int halo_hi,
                              const double* d_a, const double* d_b, double* d_y, void* stream);
 
+/* Time-sharded system operators (collective; same meaning as the single-device constructors below /
+   above).  stiga_kronsum_apply then maps the local slab of x to the local slab of y: the spatial halves
+   of the slab, a push of the p edge slices into the time neighbours' halos (peer copies through CUDA
+   IPC), a stream-ordered barrier, and the banded time pass.  Needs t_len[r] >= p on every rank. */
+int stiga_kronsum_create_spacetime_sharded(int d, const int* n, const double* const* K, const double* const* M,
+                                           int n_t, const double* Wt, const double* Mt, double gamma, double nu,
+                                           stiga_comm_t comm, stiga_kronsum_t* out);
+int stiga_kronsum_create_physical_sharded(stiga_problem_t prob, int p, int n_el, stiga_comm_t comm,
+                                          stiga_kronsum_t* out);
+int stiga_kronsum_local(stiga_kronsum_t A, long long* t0, long long* nt_local, long long* offset, long long* len);
+
 /* GMRES BLAS-1 on the device (gmres.cpp:76-85, 121), for the distributed solver above the ABI:
    deterministic dot into *d_result (device scalar), y += alpha x, y = alpha x. */
 int stiga_vec_dot(const double* d_x, const double* d_y, long long n, double* d_result, void* stream);
@@ -241,9 +300,22 @@ typedef struct {
 } stiga_gmres_report;
 
 /* gmres(A, P, b, opts) (gmres.cpp:19-132): left-preconditioned GMRES from x0 = 0 with A a
-   KronSumOperator handle and P an FD handle (P may be NULL).  d_b, d_x are device buffers. */
+   KronSumOperator handle and P an FD handle (P may be NULL).  d_b, d_x are device buffers.  With
+   time-sharded handles (same communicator) d_b, d_x are the local slabs and the solve is collective
+   (the CGS2 variant of stiga_gmres_op). */
 int stiga_gmres(stiga_kronsum_t A, stiga_fd_t P, const double* d_b, double* d_x,
                 const stiga_gmres_options* opts, stiga_gmres_report* report, void* stream);
+
+/* gmres(A, P, b, opts) over caller-supplied operators (gmres.hpp:12 LinOp, gmres.cpp:19-132): A and P
+   (P may be NULL) map a device vector of n entries to another on `stream` and return 0 on success.
+   With comm != NULL the vectors are this rank's slabs (n local entries) and every Krylov dot is
+   all-reduced over the communicator; the Arnoldi column is then orthogonalised by classical
+   Gram-Schmidt with one reorthogonalisation (CGS2, two batched reductions per column) instead of the
+   reference's MGS (k + 1 sequential reductions).  Without comm the control flow is the reference's MGS. */
+typedef int (*stiga_linop_fn)(void* ctx, const double* d_in, double* d_out, void* stream);
+int stiga_gmres_op(long long n, stiga_linop_fn A, void* A_ctx, stiga_linop_fn P, void* P_ctx, stiga_comm_t comm,
+                   const double* d_b, double* d_x, const stiga_gmres_options* opts, stiga_gmres_report* report,
+                   void* stream);
 
 /* ---- measurement helpers ---------------------------------------------------------------- */
 

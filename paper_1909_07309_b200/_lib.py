@@ -38,6 +38,21 @@ class ScatterDesc(ctypes.Structure):
                 ("dst", ctypes.c_void_p * MAX_RANKS)]
 
 
+COMM_ID_BYTES = 128
+# int (*)(void* ctx, double* buf, int n, int op) / (ctx, send, bytes, recv) / (ctx)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                                ctypes.c_int)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p)
+BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+# int (*)(void* ctx, const double* d_in, double* d_out, void* stream)
+LINOP_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class CommCallbacks(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("allreduce", ALLREDUCE_FN), ("allgather", ALLGATHER_FN),
+                ("barrier", BARRIER_FN)]
+
+
 # name -> (restype, argtypes); every symbol of include/stiga_gpu.h
 SIGNATURES = {
     "stiga_last_error": (ctypes.c_char_p, []),
@@ -95,6 +110,24 @@ SIGNATURES = {
     "stiga_vec_multidot": (_c_int, [ctypes.POINTER(_vp), _c_int, _vp, _c_ll, _vp, _vp]),
     "stiga_vec_multiaxpy": (_c_int, [_pd, ctypes.POINTER(_vp), _c_int, _vp, _c_ll, _vp]),
     "stiga_vec_scal": (_c_int, [_c_dbl, _vp, _vp, _c_ll, _vp]),
+    "stiga_comm_unique_id": (_c_int, [ctypes.c_char_p]),
+    "stiga_comm_init_nccl": (_c_int, [_c_int, _c_int, ctypes.c_char_p, _c_int, ctypes.POINTER(_vp)]),
+    "stiga_comm_init_host": (_c_int, [_c_int, _c_int, ctypes.POINTER(CommCallbacks), _c_int, ctypes.POINTER(_vp)]),
+    "stiga_comm_destroy": (_c_int, [_vp]),
+    "stiga_comm_info": (_c_int, [_vp, _pi, _pi, _pi, _pi]),
+    "stiga_comm_allreduce": (_c_int, [_vp, _vp, _c_ll, _vp]),
+    "stiga_shard_partition": (_c_int, [_c_ll, _c_int, _c_int, ctypes.POINTER(_c_ll), ctypes.POINTER(_c_ll)]),
+    "stiga_fd_setup_sharded": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl, _pd, _c_ll, _vp,
+                                        ctypes.POINTER(_vp)]),
+    "stiga_fd_local": (_c_int, [_vp, ctypes.POINTER(_c_ll), ctypes.POINTER(_c_ll), ctypes.POINTER(_c_ll),
+                                ctypes.POINTER(_c_ll)]),
+    "stiga_kronsum_create_spacetime_sharded": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl,
+                                                        _vp, ctypes.POINTER(_vp)]),
+    "stiga_kronsum_create_physical_sharded": (_c_int, [_vp, _c_int, _c_int, _vp, ctypes.POINTER(_vp)]),
+    "stiga_kronsum_local": (_c_int, [_vp, ctypes.POINTER(_c_ll), ctypes.POINTER(_c_ll), ctypes.POINTER(_c_ll),
+                                     ctypes.POINTER(_c_ll)]),
+    "stiga_gmres_op": (_c_int, [_c_ll, LINOP_FN, _vp, LINOP_FN, _vp, _vp, _vp, _vp, ctypes.POINTER(GmresOptions),
+                                ctypes.POINTER(GmresReport), _vp]),
 }
 
 _lib = None

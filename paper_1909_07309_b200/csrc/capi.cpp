@@ -30,630 +30,19 @@
 
 using namespace stiga;
 
+#include "common.hpp"
+#include "handles.hpp"
+
+using namespace stiga;
+using namespace stiga::capi;
+
 namespace {
-
 thread_local std::string g_last_error;
-
-struct CudaFailure : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-template <typename F>
-int guarded(F&& f) {
-    try {
-        f();
-        g_last_error.clear();
-        return STIGA_OK;
-    } catch (const std::invalid_argument& e) {
-        g_last_error = e.what();
-        return STIGA_INVALID_ARGUMENT;
-    } catch (const CudaFailure& e) {
-        g_last_error = e.what();
-        return STIGA_CUDA;
-    } catch (const std::bad_alloc&) {
-        g_last_error = "host allocation failed";
-        return STIGA_NUMERICAL;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return STIGA_NUMERICAL;
-    }
-}
-
-void require(bool ok, const char* msg) {
-    if (!ok) throw std::invalid_argument(msg);
-}
-
-// Scoped device selection (restores the caller's current device).
-struct DeviceGuard {
-    int prev = 0;
-    explicit DeviceGuard(int dev) {
-        ck(cudaGetDevice(&prev), "cudaGetDevice");
-        if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
-    }
-    ~DeviceGuard() { cudaSetDevice(prev); }
-};
-
-struct DBuf {
-    double* p = nullptr;
-    size_t n = 0;
-    DBuf() = default;
-    DBuf(const DBuf&) = delete;
-    DBuf& operator=(const DBuf&) = delete;
-    ~DBuf() {
-        if (p) cudaFree(p);
-    }
-    void alloc(size_t count) {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = count;
-        if (count) ck(cudaMalloc(&p, count * sizeof(double)), "cudaMalloc");
-    }
-    void upload(const std::vector<double>& h) {
-        alloc(h.size());
-        if (!h.empty()) ck(cudaMemcpy(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice), "upload");
-    }
-};
-
-DenseMatrix from_colmajor(const double* a, int n) {
-    DenseMatrix m(n, n);
-    std::memcpy(m.a.data(), a, sizeof(double) * n * static_cast<size_t>(n));
-    return m;
-}
-
-// Row-major, zero-padded (Mp x Kp) copy of J, with J(i,j) = transpose ? U(j,i) : U(i,j).
-std::vector<double> pad_factor(const DenseMatrix& U, bool transpose, int Mp, int Kp) {
-    std::vector<double> out(static_cast<size_t>(Mp) * Kp, 0.0);
-    const Index rows = transpose ? U.cols : U.rows;
-    const Index cols = transpose ? U.rows : U.cols;
-    if (rows > Mp || cols > Kp || Mp < 1)
-        throw std::runtime_error("internal: no kernel tiling for a factor of size " + std::to_string(rows));
-    for (Index i = 0; i < rows; ++i)
-        for (Index j = 0; j < cols; ++j) out[i * Kp + j] = transpose ? U(j, i) : U(i, j);
-    return out;
-}
-
-cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-
 }  // namespace
 
 namespace stiga {
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 }  // namespace stiga
-
-// ------------------------------------------------------------------------------------------
-// FD preconditioner handle
-// ------------------------------------------------------------------------------------------
-struct stiga_fd_s {
-    int device = 0;
-    FDFactors F;
-    int d = 0;
-    std::vector<int> dims;  // n_1..n_d, n_t
-    long long n_dof = 0, n_s = 0;
-    std::vector<gpu::Tiling> tl;        // per spatial direction (forward products U_l^T)
-    std::vector<gpu::Tiling> tl_b;      // backward products U_l (the last one tuned with the D^-1/2 post-scale)
-    gpu::Tiling tl_t;
-    gpu::Tiling tl_ts;                  // mode-kernel tiling of the split time products
-    std::vector<std::unique_ptr<DBuf>> Jt, J;  // padded U_l^T, U_l (device eigen-order)
-    std::vector<std::unique_ptr<DBuf>> Jft, Jfb;  // folded [A_e; A_o] / [A_p; A_q] (split directions)
-    DBuf Jt_t, J_t;
-    std::vector<std::unique_ptr<DBuf>> lam;
-    DBuf S_inv, pair_c, pair_c1, pair_c1sq, pair_gg, g, dinv;
-    DBuf scratch, scratch2;
-    gpu::ArrowParams ap;
-
-    gpu::ModeGeom geom(int mode) const {
-        gpu::ModeGeom g;
-        long long L = 1;
-        for (int l = 0; l < mode; ++l) L *= dims[l];
-        g.L = L;
-        g.n = g.m = dims[mode];
-        g.ncols = n_dof / dims[mode];
-        return g;
-    }
-    // spatial mode m of a time slab with nt_local slices
-    gpu::ModeGeom slab_geom(int mode, long long nt_local) const {
-        gpu::ModeGeom g = geom(mode);
-        g.ncols = n_s / dims[mode] * nt_local;
-        return g;
-    }
-    // time mode of a spatial slab with ns_local spatial indices (ns_local x n_t, colex)
-    gpu::ModeGeom time_geom(long long ns_local) const {
-        gpu::ModeGeom g;
-        g.L = ns_local;
-        g.n = g.m = dims[d];
-        g.ncols = ns_local;
-        return g;
-    }
-
-    // One spatial mode product with tiling t: the folded kernel for a folded tiling (split
-    // direction), the dense DMMA kernel otherwise.
-    void mprod(const gpu::Tiling& t, int l, bool backward, const gpu::ModeGeom& g, const double* src, double* dst,
-               const double* post, cudaStream_t st, const double* pre = nullptr, const gpu::Scatter* sc = nullptr) {
-        if (t.fold) {
-            if (sc && (backward || t.WM != 2)) throw std::runtime_error("internal: folded scatter needs a WM = 2 tiling");
-            ck(gpu::launch_fold_product(t, g, src, dst, backward ? Jfb[l]->p : Jft[l]->p, !backward, post, st, pre, sc),
-               "fd folded mode product");
-        } else {
-            ck(gpu::launch_mode_product(t, g, src, dst, backward ? J[l]->p : Jt[l]->p, post, st, pre, sc),
-               "fd mode product");
-        }
-    }
-    // best dense (unfolded) candidate of direction l (for stages the folded kernel cannot do)
-    std::vector<gpu::Tiling> tl_dense;  // heuristic dense tiling per direction (J / Jt are padded for it)
-    const gpu::Tiling& dense_tiling(int l) const { return (tl[l].fold || tl[l].WM != 1) ? tl_dense[l] : tl[l]; }
-
-    // Distributed building blocks.
-    void apply_space(bool backward, long long t0, long long nt_local, const double* in, double* out, cudaStream_t st) {
-        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
-        double* bufs[2] = {scratch.p, scratch2.p};
-        const double* dsl = dinv.p ? dinv.p + n_s * t0 : nullptr;
-        const long long nloc = n_s * nt_local;
-        const bool fused_pre = !backward && dsl && fused_prescale();
-        const int nops = d + ((!backward && dsl && !fused_pre) ? 1 : 0);
-        int k = 0;
-        const double* src = in;
-        auto next = [&]() -> double* { double* r = (k == nops - 1) ? out : bufs[k % 2]; ++k; return r; };
-        if (!backward && dsl && !fused_pre) {
-            double* dst = next();
-            ck(gpu::launch_scale(dsl, src, dst, nloc, st), "slab pre-scale");
-            src = dst;
-        }
-        for (int l = 0; l < d; ++l) {
-            double* dst = next();
-            mprod(backward ? tl_b[l] : (l == 0 ? first_tiling() : tl[l]), l, backward, slab_geom(l, nt_local), src, dst,
-                  (backward && l == d - 1) ? dsl : nullptr, st, (fused_pre && l == 0) ? dsl : nullptr);
-            src = dst;
-        }
-    }
-    void apply_time(long long s0, long long ns_local, const double* in, double* out, cudaStream_t st) {
-        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
-        gpu::ArrowParams a2 = ap;
-        a2.s_off = s0;
-        const gpu::ModeGeom g = time_geom(ns_local);
-        if (time_split) {
-            ck(gpu::launch_mode_product(tl_ts, g, in, scratch.p, Jt_t.p, nullptr, st), "slab time U_t^T");
-            ck(gpu::launch_arrowhead(scratch.p, scratch2.p, ns_local, a2, st), "slab arrowhead");
-            ck(gpu::launch_mode_product(tl_ts, g, scratch2.p, out, J_t.p, nullptr, st), "slab time U_t");
-        } else {
-            ck(gpu::launch_time_fused(tl_t, g, in, out, Jt_t.p, J_t.p, a2, st), "slab time fused");
-        }
-    }
-
-    // Fused-exchange variants: the last product of the stage stores straight into the
-    // owner ranks' receive buffers through the scatter epilogue, so no pack / all-to-all / unpack.
-    void apply_space_scatter(long long t0, long long nt_local, const double* in, const gpu::Scatter& sc,
-                             cudaStream_t st) {
-        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
-        double* bufs[2] = {scratch.p, scratch2.p};
-        const double* dsl = dinv.p ? dinv.p + n_s * t0 : nullptr;
-        const long long nloc = n_s * nt_local;
-        // the scattering product cannot also pre-scale: with d = 1 the pre-scale runs as its own pass
-        const bool fused_pre = dsl && fused_prescale() && d > 1;
-        const double* src = in;
-        int k = 0;
-        if (dsl && !fused_pre) {
-            ck(gpu::launch_scale(dsl, src, bufs[k % 2], nloc, st), "slab pre-scale");
-            src = bufs[k++ % 2];
-        }
-        for (int l = 0; l < d; ++l) {
-            const bool last = l == d - 1;
-            double* dst = last ? nullptr : bufs[k++ % 2];
-            // the scattering product: the tuned tiling when it has a scatter epilogue (dense WM = 1 or
-            // folded WM = 2), else the dense fallback
-            const gpu::Tiling& tt = (l == 0 && fused_pre) ? first_tiling() : tl[l];
-            const bool scatter_ok = !(fused_pre && l == 0) && (tt.fold ? tt.WM == 2 : tt.WM == 1);
-            const gpu::Tiling& t = last ? (scatter_ok ? tt : dense_tiling(l)) : (l == 0 ? first_tiling() : tl[l]);
-            mprod(t, l, false, slab_geom(l, nt_local), src, dst, nullptr, st, (fused_pre && l == 0) ? dsl : nullptr,
-                  last ? &sc : nullptr);
-            src = dst;
-        }
-    }
-    void apply_time_scatter(long long s0, long long ns_local, const double* in, const gpu::Scatter& sc,
-                            cudaStream_t st) {
-        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
-        gpu::ArrowParams a2 = ap;
-        a2.s_off = s0;
-        const gpu::ModeGeom g = time_geom(ns_local);
-        if (time_split) {
-            ck(gpu::launch_mode_product(tl_ts, g, in, scratch.p, Jt_t.p, nullptr, st), "slab time U_t^T");
-            ck(gpu::launch_arrowhead(scratch.p, scratch2.p, ns_local, a2, st), "slab arrowhead");
-            gpu::Tiling tsc = tl_ts;
-            if (tsc.WM != 1)
-                for (const auto& t : cand_ts)
-                    if (t.WM == 1) {
-                        tsc = t;
-                        break;
-                    }
-            ck(gpu::launch_mode_product(tsc, g, scratch2.p, nullptr, J_t.p, nullptr, st, nullptr, &sc),
-               "slab time U_t (scatter)");
-        } else {
-            ck(gpu::launch_time_fused(tl_t, g, in, nullptr, Jt_t.p, J_t.p, a2, st, &sc), "slab time fused (scatter)");
-        }
-    }
-
-    bool time_split = false;            // time direction as U_t^T GEMM + arrowhead + U_t GEMM
-
-    // Setup-time autotuning: every candidate tiling of every mode (and both time-direction
-    // variants) is timed once on the scratch vectors at the real tensor geometry and the fastest is
-    // kept.  STIGA_TIME_VARIANT=fused|split forces the time path; STIGA_NO_AUTOTUNE=1 keeps the
-    // heuristic first choices.
-    std::vector<std::vector<gpu::Tiling>> cand_space;
-    std::vector<gpu::Tiling> cand_time, cand_ts;
-
-    float time_once(const std::function<void()>& f) {
-        cudaEvent_t e0, e1;
-        ck(cudaEventCreate(&e0), "event");
-        ck(cudaEventCreate(&e1), "event");
-        f();  // warm (sets the smem attribute, loads the module)
-        f();
-        // short launches (< 0.25 ms) are timed in groups of 4 so launch gaps and event resolution do
-        // not decide between candidates that differ by a few percent
-        int inner = 1;
-        float best = 1e30f;
-        for (int rep = 0; rep < 4; ++rep) {
-            ck(cudaEventRecord(e0, nullptr), "event");
-            for (int k = 0; k < inner; ++k) f();
-            ck(cudaEventRecord(e1, nullptr), "event");
-            ck(cudaEventSynchronize(e1), "event");
-            float ms = 0.f;
-            ck(cudaEventElapsedTime(&ms, e0, e1), "event");
-            ms /= inner;
-            if (rep == 0 && ms < 0.25f) {
-                inner = 4;
-                continue;
-            }
-            best = std::min(best, ms);
-        }
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        return best;
-    }
-
-    // STIGA_TUNE_CACHE=<file>: tuned choices (candidate indices) keyed by device + tensor shape, so a
-    // profiled run (where ncu serialisation would distort the timings) replays the plain run's picks.
-    std::string tune_key() const {
-        cudaDeviceProp prop{};
-        cudaGetDeviceProperties(&prop, device);
-        std::string k = std::string(prop.name) + " d" + std::to_string(d);
-        for (int l = 0; l < d; ++l) k += " " + std::to_string(dims[l]);
-        return k + " t" + std::to_string(dims[d]) + (dinv.p ? " D" : "");
-    }
-    bool load_tuned(const char* path) {
-        std::FILE* f = std::fopen(path, "r");
-        if (!f) return false;
-        const std::string key = tune_key() + " |";
-        char line[1024];
-        bool found = false;
-        while (std::fgets(line, sizeof line, f)) {
-            std::string ln(line);
-            if (ln.compare(0, key.size(), key) != 0) continue;
-            std::vector<int> v;
-            const char* p = ln.c_str() + key.size();
-            char* end = nullptr;
-            for (long x = std::strtol(p, &end, 10); end != p; x = std::strtol(p, &end, 10)) {
-                v.push_back(static_cast<int>(x));
-                p = end;
-            }
-            if (static_cast<int>(v.size()) != d + 4 && static_cast<int>(v.size()) != 2 * d + 4) continue;
-            bool ok = true;
-            for (int l = 0; l < d; ++l) ok = ok && v[l] >= 0 && v[l] < static_cast<int>(cand_space[l].size());
-            ok = ok && v[d] >= -1 && v[d] < static_cast<int>(cand_time.size()) && v[d + 1] >= 0 &&
-                 v[d + 1] < static_cast<int>(cand_ts.size()) && (v[d + 2] == 1 || v[d] >= 0);
-            if (!ok) continue;
-            const bool has_b = static_cast<int>(v.size()) == 2 * d + 4;
-            for (int l = 0; l < d && has_b; ++l)
-                ok = ok && v[d + 4 + l] >= 0 && v[d + 4 + l] < static_cast<int>(cand_space[l].size());
-            if (!ok) continue;
-            for (int l = 0; l < d; ++l) {
-                tl[l] = cand_space[l][v[l]];
-                tl_b[l] = cand_space[l][has_b ? v[d + 4 + l] : v[l]];
-            }
-            tl_t = v[d] >= 0 ? cand_time[v[d]] : gpu::Tiling{};
-            tl_ts = cand_ts[v[d + 1]];
-            time_split = v[d + 2] == 1;
-            use_fused_pre = v[d + 3] >= 0 && v[d + 3] < static_cast<int>(cand_space[0].size());
-            tl_pre = use_fused_pre ? cand_space[0][v[d + 3]] : tl[0];
-            found = true;
-        }
-        std::fclose(f);
-        return found;
-    }
-
-    void autotune() {
-        const char* force = std::getenv("STIGA_TIME_VARIANT");
-        const bool no_tune = std::getenv("STIGA_NO_AUTOTUNE") != nullptr;
-        const bool debug_tune = std::getenv("STIGA_DEBUG_TUNE") != nullptr;
-        const char* cache = std::getenv("STIGA_TUNE_CACHE");
-        if (cache && !no_tune && !force && load_tuned(cache)) return;
-        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
-        ck(cudaMemset(scratch.p, 0, sizeof(double) * n_dof), "memset");
-        const size_t kMaxCand = 8;
-        std::vector<int> pick(d + 2, 0);
-        for (int l = 0; l < d; ++l) {
-            tl[l] = cand_space[l].front();
-            if (no_tune) continue;
-            float best = 1e30f;
-            size_t n_fold = 0, n_dense = 0;
-            for (size_t c = 0; c < cand_space[l].size(); ++c) {
-                const gpu::Tiling& t = cand_space[l][c];
-                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : 2 * kMaxCand)) continue;
-                const float ms = time_once([&] {
-                    mprod(t, l, false, geom(l), scratch.p, scratch2.p, nullptr, nullptr);
-                });
-                if (ms < 0.985f * best) { best = ms; tl[l] = t; pick[l] = static_cast<int>(c); }  // 1.5%: above timing noise
-                if (debug_tune)
-                    std::fprintf(stderr, "[stiga tune] mode %d %s MI=%d WM=%d WN=%d NI=%d RB=%d ns=%d occ=%d: %.4f ms\n",
-                                 l, t.fold ? "folded" : "dense", t.MI, t.WM, t.WN, t.NI, t.RB, t.nstage, t.ctas_per_sm,
-                                 ms);
-            }
-        }
-        // backward products U_l: tuned on their own (the folded backward kernel differs from the forward
-        // one), the last direction with the D^-1/2 post-scale it carries in the apply
-        std::vector<int> pick_b(d, 0);
-        for (int l = 0; l < d; ++l) {
-            tl_b[l] = tl[l];
-            pick_b[l] = pick[l];
-            if (no_tune) continue;
-            const double* post = (l == d - 1) ? dinv.p : nullptr;
-            float best = 1e30f;
-            size_t n_fold = 0, n_dense = 0;
-            for (size_t c = 0; c < cand_space[l].size(); ++c) {
-                const gpu::Tiling& t = cand_space[l][c];
-                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : 2 * kMaxCand)) continue;
-                const float ms = time_once([&] { mprod(t, l, true, geom(l), scratch.p, scratch2.p, post, nullptr); });
-                if (ms < 0.985f * best) { best = ms; tl_b[l] = t; pick_b[l] = static_cast<int>(c); }
-                if (debug_tune)
-                    std::fprintf(stderr, "[stiga tune] bwd mode %d%s %s MI=%d WM=%d WN=%d RB=%d ns=%d: %.4f ms\n", l,
-                                 post ? "+post" : "", t.fold ? "folded" : "dense", t.MI, t.WM, t.WN, t.RB, t.nstage, ms);
-            }
-        }
-        use_fused_pre = false;
-        tl_pre = tl[0];
-        int pick_pre = -1;
-        if (!no_tune && dinv.p) {
-            const float sep = time_once([&] {
-                ck(gpu::launch_scale(dinv.p, scratch.p, scratch2.p, n_dof, nullptr), "tune");
-                mprod(tl[0], 0, false, geom(0), scratch2.p, scratch.p, nullptr, nullptr);
-            });
-            float best_fus = 1e30f;
-            size_t n_fold = 0, n_dense = 0;
-            for (size_t c = 0; c < cand_space[0].size(); ++c) {
-                const gpu::Tiling& t = cand_space[0][c];
-                if (!gpu::prescale_fits(t)) continue;
-                if ((t.fold ? n_fold : n_dense)++ >= kMaxCand) continue;
-                const float ms = time_once([&] { mprod(t, 0, false, geom(0), scratch.p, scratch2.p, nullptr, nullptr, dinv.p); });
-                if (ms < best_fus) { best_fus = ms; tl_pre = t; pick_pre = static_cast<int>(c); }
-            }
-            use_fused_pre = pick_pre >= 0 && best_fus < sep;
-            if (debug_tune)
-                std::fprintf(stderr, "[stiga tune] pre-scale separate %.4f ms, fused %.4f ms (%s MI=%d RB=%d)\n", sep,
-                             best_fus, tl_pre.fold ? "folded" : "dense", tl_pre.MI, tl_pre.RB);
-        }
-        const bool fused_ok = !cand_time.empty();
-        tl_t = fused_ok ? cand_time.front() : gpu::Tiling{};
-        tl_ts = cand_ts.front();
-        float best_fused = 1e30f, best_split = 1e30f;
-        if (!no_tune) {
-            if (fused_ok && !(force && std::string(force) == "split")) {
-                for (size_t c = 0; c < std::min(3 * kMaxCand, cand_time.size()); ++c) {
-                    const gpu::Tiling& t = cand_time[c];
-                    const float ms = time_once([&] {
-                        ck(gpu::launch_time_fused(t, geom(d), scratch.p, scratch2.p, Jt_t.p, J_t.p, ap, nullptr), "tune");
-                    });
-                    if (ms < best_fused) { best_fused = ms; tl_t = t; pick[d] = static_cast<int>(c); }
-                    if (debug_tune)
-                        std::fprintf(stderr, "[stiga tune] time fused MI=%d WM=%d WN=%d ns=%d occ=%d: %.4f ms\n", t.MI,
-                                     t.WM, t.WN, t.nstage, t.ctas_per_sm, ms);
-                }
-            }
-            if (!(force && std::string(force) == "fused")) {
-                float best_gemm = 1e30f;
-                for (size_t c = 0; c < std::min(2 * kMaxCand, cand_ts.size()); ++c) {
-                    const gpu::Tiling& t = cand_ts[c];
-                    const float ms = time_once([&] {
-                        ck(gpu::launch_mode_product(t, geom(d), scratch.p, scratch2.p, Jt_t.p, nullptr, nullptr), "tune");
-                    });
-                    if (ms < best_gemm) { best_gemm = ms; tl_ts = t; pick[d + 1] = static_cast<int>(c); }
-                    if (debug_tune)
-                        std::fprintf(stderr, "[stiga tune] time gemm MI=%d WN=%d RB=%d occ=%d: %.4f ms\n", t.MI, t.WN,
-                                     t.RB, t.ctas_per_sm, ms);
-                }
-                const float arrow = time_once([&] {
-                    ck(gpu::launch_arrowhead(scratch2.p, scratch.p, n_s, ap, nullptr), "tune");
-                });
-                best_split = 2.f * best_gemm + arrow;
-                if (debug_tune) std::fprintf(stderr, "[stiga tune] arrowhead: %.4f ms\n", arrow);
-            }
-        }
-        if (force && std::string(force) == "split") time_split = true;
-        else if (force && std::string(force) == "fused" && fused_ok) time_split = false;
-        else if (!fused_ok) time_split = true;
-        else time_split = !no_tune && best_split < best_fused;
-        if (cache && !no_tune && !force) {
-            if (std::FILE* f = std::fopen(cache, "a")) {
-                std::string ln = tune_key() + " |";
-                for (int l = 0; l < d; ++l) ln += " " + std::to_string(pick[l]);
-                ln += " " + std::to_string(fused_ok ? pick[d] : -1) + " " + std::to_string(pick[d + 1]) + " " +
-                      std::to_string(time_split ? 1 : 0) + " " + std::to_string(use_fused_pre ? pick_pre : -1);
-                for (int l = 0; l < d; ++l) ln += " " + std::to_string(pick_b[l]);
-                ln += "\n";
-                std::fputs(ln.c_str(), f);
-                std::fclose(f);
-            }
-        }
-    }
-
-    // D^-1/2 pre-scale fused into the first forward mode product when its smem allows (the
-    // separate scale pass otherwise); STIGA_NO_FUSED_PRESCALE=1 forces the separate pass.
-    bool use_fused_pre = false;  // decided by the autotuner (fused vs separate, timed)
-    gpu::Tiling tl_pre;          // tiling of the pre-scaled first forward pass (tuned separately: every
-                                 // row block re-stages the D chunk, so it prefers fewer row blocks)
-    bool fused_prescale() const {
-        static const bool off = std::getenv("STIGA_NO_FUSED_PRESCALE") != nullptr;
-        return dinv.p != nullptr && use_fused_pre && !off && gpu::prescale_fits(tl_pre);
-    }
-    const gpu::Tiling& first_tiling() const { return fused_prescale() ? tl_pre : tl[0]; }
-    int launches() const { return 2 * d + (time_split ? 3 : 1) + (dinv.p && !fused_prescale() ? 1 : 0); }
-
-    // Launch sequence (fdsolve.cpp:158-163): [D^-1/2 pre-scale], forward spatial modes U_l^T, the
-    // time direction (fused U_t^T / arrowhead / U_t kernel, or the three as separate passes),
-    // backward spatial modes U_l with the D^-1/2 post-scale fused into the last epilogue.  The
-    // reference back transform applies U_1..U_d, U_t; Kronecker factors on distinct modes commute,
-    // so applying U_t first is equal in exact arithmetic.  Intermediates ping-pong between two
-    // handle-owned scratch vectors, so d_r may equal d_s.
-    void apply(const double* in, double* out, cudaStream_t st, std::vector<cudaEvent_t>* ev) {
-        if (!scratch2.p) scratch2.alloc(static_cast<size_t>(n_dof));
-        double* bufs[2] = {scratch.p, scratch2.p};
-        const bool scaled = dinv.p != nullptr;
-        const int nops = launches();
-        const double* src = in;
-        int e = 0, k = 0;
-        auto next = [&]() -> double* {
-            double* dst = (k == nops - 1) ? out : bufs[k % 2];
-            if (ev) ck(cudaEventRecord((*ev)[e++], st), "event");
-            ++k;
-            return dst;
-        };
-        const bool fused_pre = fused_prescale();
-        if (scaled && !fused_pre) {
-            double* dst = next();
-            ck(gpu::launch_scale(dinv.p, src, dst, n_dof, st), "fd D^-1/2 pre-scale");
-            src = dst;
-        }
-        for (int l = 0; l < d; ++l) {
-            double* dst = next();
-            mprod(l == 0 ? first_tiling() : tl[l], l, false, geom(l), src, dst, nullptr, st,
-                  (l == 0 && fused_pre) ? dinv.p : nullptr);
-            src = dst;
-        }
-        if (time_split) {
-            double* dst = next();
-            ck(gpu::launch_mode_product(tl_ts, geom(d), src, dst, Jt_t.p, nullptr, st), "fd time U_t^T product");
-            src = dst;
-            dst = next();
-            ck(gpu::launch_arrowhead(src, dst, n_s, ap, st), "fd arrowhead solve");
-            src = dst;
-            dst = next();
-            ck(gpu::launch_mode_product(tl_ts, geom(d), src, dst, J_t.p, nullptr, st), "fd time U_t product");
-            src = dst;
-        } else {
-            double* dst = next();
-            ck(gpu::launch_time_fused(tl_t, geom(d), src, dst, Jt_t.p, J_t.p, ap, st), "fd time-fused kernel");
-            src = dst;
-        }
-        for (int l = 0; l < d; ++l) {
-            double* dst = next();
-            mprod(tl_b[l], l, true, geom(l), src, dst, (l == d - 1 && scaled) ? dinv.p : nullptr, st);
-            src = dst;
-        }
-        if (ev) ck(cudaEventRecord((*ev)[e], st), "event");
-    }
-};
-
-// ------------------------------------------------------------------------------------------
-// KronSum handle
-// ------------------------------------------------------------------------------------------
-struct stiga_kronsum_s {
-    int device = 0;
-    int D = 0;
-    std::vector<int> dims;
-    long long n_dof = 0;
-    bool spacetime = false;
-    // generic: terms x D bands
-    std::vector<double> coeffs;
-    std::vector<std::vector<DenseMatrix>> factors;  // host copies (for diagonal)
-    std::vector<std::unique_ptr<DBuf>> bands;       // term*D + l
-    std::vector<int> hbw;
-    // spacetime: per direction M_l, K_l bands, time gamma*W_t and nu*M_t bands
-    DBuf t0, t1, t2, t3;  // scratch N_dof each
-    // physical (geometry-mapped) system: stencil K_s, M_s on the device + time bands
-    bool physical = false;
-    gpu::PhysicalDesc pdesc;
-    DBuf Kst, Mst, cp, qnode, qweight, bval, bder;
-    int* bfirst = nullptr;
-    std::vector<double> time_W, time_M;  // host copies for diagonal()
-    ~stiga_kronsum_s() {
-        if (bfirst) cudaFree(bfirst);
-    }
-
-    gpu::ModeGeom geom(int mode) const {
-        gpu::ModeGeom g;
-        long long L = 1;
-        for (int l = 0; l < mode; ++l) L *= dims[l];
-        g.L = L;
-        g.n = g.m = dims[mode];
-        g.ncols = n_dof / dims[mode];
-        return g;
-    }
-    gpu::Band band(int idx) const { return gpu::Band{bands[idx]->p, hbw[idx]}; }
-
-    void ensure_scratch(int count) {
-        DBuf* s[4] = {&t0, &t1, &t2, &t3};
-        for (int i = 0; i < count; ++i)
-            if (!s[i]->p) s[i]->alloc(static_cast<size_t>(n_dof));
-    }
-
-    void apply(const double* x, double* y, cudaStream_t st) {
-        const gpu::Band none{};
-        if (physical) {  // y = M_s X W_t^T + K_s X M_t^T  (solver.cpp:67-70)
-            // spatial stencils first, as the reference's mode order (kronop.cpp:75-89): MX = M_s X,
-            // KX = K_s X on the tensor cores, then y = MX W_t^T + KX M_t^T in one banded time pass
-            ensure_scratch(2);
-            const int d = D - 1;
-            ck(gpu::launch_stencil_apply2(pdesc, Mst.p, Kst.p, x, t0.p, t1.p, dims[d], st), "stencil apply");
-            ck(gpu::launch_banded_pass(geom(d), t0.p, t1.p, y, nullptr, band(0), band(1), none, none, 0.0, st),
-               "time bands");
-            return;
-        }
-        if (spacetime) {
-            // bands: [M_1, K_1, ..., M_d, K_d, gamma W_t, nu M_t]
-            const int d = D - 1;
-            ensure_scratch(4);
-            double* a = t0.p;  // t_m  (M-chain)
-            double* b = t1.p;  // k_m  (stiffness-sum chain)
-            double* a2 = t2.p;
-            double* b2 = t3.p;
-            // mode 0: a = M_1 x, b = K_1 x
-            ck(gpu::launch_banded_pass(geom(0), x, nullptr, a, b, band(0), none, band(1), none, 0.0, st), "banded");
-            for (int m = 1; m < d; ++m) {
-                // a2 = M_m a ; b2 = K_m a + M_m b
-                ck(gpu::launch_banded_pass(geom(m), a, b, a2, b2, band(2 * m), none, band(2 * m + 1), band(2 * m), 0.0,
-                                           st),
-                   "banded");
-                std::swap(a, a2);
-                std::swap(b, b2);
-            }
-            // time: y = gamma W_t a + nu M_t b
-            ck(gpu::launch_banded_pass(geom(d), a, b, y, nullptr, band(2 * d), band(2 * d + 1), none, none, 0.0, st),
-               "banded");
-            return;
-        }
-        // generic: per term D banded passes, the last accumulating into y
-        ensure_scratch(2);
-        const int nterms = static_cast<int>(coeffs.size());
-        if (nterms == 0) {
-            ck(cudaMemsetAsync(y, 0, sizeof(double) * n_dof, st), "memset");
-            return;
-        }
-        for (int t = 0; t < nterms; ++t) {
-            const double* src = x;
-            double* ping[2] = {t0.p, t1.p};
-            for (int l = 0; l < D; ++l) {
-                const bool last = l == D - 1;
-                double* dst = last ? y : ping[l % 2];
-                gpu::Band Bd = band(t * D + l);
-                ck(gpu::launch_banded_pass(geom(l), src, nullptr, dst, nullptr, Bd, none, none, none,
-                                           last && t > 0 ? 1.0 : 0.0, st),
-                   "banded");
-                src = dst;
-            }
-        }
-    }
-};
 
 namespace {
 
@@ -798,12 +187,15 @@ int stiga_geometry_preconditioner_pieces(stiga_problem_t P, int p, int n_el, dou
     });
 }
 
-int stiga_fd_setup(int d, const int* n, const double* const* K, const double* const* M, int n_t, const double* Wt,
-                   const double* Mt, double gamma, double nu, const double* scaling, long long scaling_len, int device,
-                   stiga_fd_t* out) {
-    return guarded([&] {
-        require(out != nullptr, "stiga_fd_setup: null handle output");
-        *out = nullptr;
+}  // extern "C"
+
+namespace stiga {
+// Host setup (fdsolve.cpp:67-153) + device upload + autotune of an FD handle.  `prepare` (sharded
+// handles, dist.cpp) runs after the host setup and before the uploads: it sets the stage spans, the
+// shard state and the D^-1/2 slab.
+stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* const* M, int n_t, const double* Wt,
+                     const double* Mt, double gamma, double nu, const double* scaling, long long scaling_len,
+                     int device, const std::function<void(stiga_fd_s&)>& prepare) {
         require(d >= 1 && d <= gpu::kMaxDim, "ExtendedFDPreconditioner: per-direction matrices mismatch");
         require(n && K && M && Wt && Mt, "stiga_fd_setup: null input");
         require(n_t >= 1, "time_factorization: shape mismatch");
@@ -826,12 +218,13 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         h->dims.push_back(F.n_t);
         h->n_dof = F.n_dof;
         h->n_s = F.n_s_total;
-        if (device < 0) {  // host-only handle: setup + export, no device resources
-            *out = h.release();
-            return;
-        }
+        h->nt_span = F.n_t;
+        h->ns_span = F.n_s_total;
+        h->scratch_len = F.n_dof;
+        if (device < 0) return h.release();  // host-only handle: setup + export, no device resources
 
         DeviceGuard dg(device);
+        if (prepare) prepare(*h);
         for (int l = 0; l < d; ++l) {
             std::vector<gpu::Tiling> dense = gpu::mode_tiling_candidates(F.n[l], F.n[l]);
             if (dense.empty()) throw std::runtime_error("internal: no mode-product tiling");
@@ -914,7 +307,7 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         if (gg.empty()) gg.push_back(0.0);
         h->g.upload(gg);
         if (!F.d_inv_sqrt.empty()) h->dinv.upload(F.d_inv_sqrt);
-        h->scratch.alloc(static_cast<size_t>(h->n_dof));
+        h->scratch.alloc(static_cast<size_t>(h->scratch_len));
 
         gpu::ArrowParams& ap = h->ap;
         ap.d = d;
@@ -936,7 +329,19 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
         ap.inv_nu = 1.0 / nu;
         if (const char* dbg = std::getenv("STIGA_DEBUG_ARROW")) ap.debug = std::atoi(dbg);
         h->autotune();
-        *out = h.release();
+        return h.release();
+}
+}  // namespace stiga
+
+extern "C" {
+
+int stiga_fd_setup(int d, const int* n, const double* const* K, const double* const* M, int n_t, const double* Wt,
+                   const double* Mt, double gamma, double nu, const double* scaling, long long scaling_len, int device,
+                   stiga_fd_t* out) {
+    return guarded([&] {
+        require(out != nullptr, "stiga_fd_setup: null handle output");
+        *out = nullptr;
+        *out = fd_build(d, n, K, M, n_t, Wt, Mt, gamma, nu, scaling, scaling_len, device, nullptr);
     });
 }
 
@@ -1003,7 +408,20 @@ int stiga_fd_apply(stiga_fd_t P, const double* d_r, double* d_s, void* stream) {
         require(P && d_r && d_s, "ExtendedFDPreconditioner::apply: null argument");
         require(P->device >= 0, "ExtendedFDPreconditioner::apply: host-only handle (setup with device < 0)");
         DeviceGuard dg(P->device);
-        P->apply(d_r, d_s, as_stream(stream), nullptr);
+        if (P->shard) fd_apply_sharded(*P, d_r, d_s, as_stream(stream), nullptr);
+        else P->apply(d_r, d_s, as_stream(stream), nullptr);
+    });
+}
+
+int stiga_fd_local(stiga_fd_t P, long long* t0, long long* nt_local, long long* offset, long long* len) {
+    return guarded([&] {
+        require(P != nullptr, "stiga_fd_local: null handle");
+        const long long a = P->shard ? P->shard->t_off[P->shard->rank] : 0;
+        const long long b = P->shard ? P->shard->t_len[P->shard->rank] : P->dims[P->d];
+        if (t0) *t0 = a;
+        if (nt_local) *nt_local = b;
+        if (offset) *offset = P->n_s * a;
+        if (len) *len = P->n_s * b;
     });
 }
 
@@ -1015,7 +433,8 @@ int stiga_fd_apply_profiled(stiga_fd_t P, const double* d_r, double* d_s, void* 
         const int passes = P->launches();
         std::vector<cudaEvent_t> ev(passes + 1);
         for (auto& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
-        P->apply(d_r, d_s, as_stream(stream), &ev);
+        if (P->shard) fd_apply_sharded(*P, d_r, d_s, as_stream(stream), &ev);
+        else P->apply(d_r, d_s, as_stream(stream), &ev);
         ck(cudaEventSynchronize(ev[passes]), "cudaEventSynchronize");
         for (int k = 0; k < passes; ++k) ck(cudaEventElapsedTime(&pass_ms[k], ev[k], ev[k + 1]), "elapsed");
         for (auto& e : ev) cudaEventDestroy(e);
@@ -1027,6 +446,7 @@ int stiga_fd_apply_space(stiga_fd_t P, int backward, long long t0, long long nt_
     return guarded([&] {
         require(P && d_in && d_out, "stiga_fd_apply_space: null argument");
         require(P->device >= 0, "stiga_fd_apply_space: host-only handle");
+        require(!P->shard, "stiga_fd_apply_space: stage building blocks need a single-device handle");
         require(t0 >= 0 && nt_local >= 1 && t0 + nt_local <= P->dims[P->d], "stiga_fd_apply_space: time slab out of range");
         require(d_in != d_out, "stiga_fd_apply_space: input and output must not alias");
         DeviceGuard dg(P->device);
@@ -1039,6 +459,7 @@ int stiga_fd_apply_time(stiga_fd_t P, long long s0, long long ns_local, const do
     return guarded([&] {
         require(P && d_in && d_out, "stiga_fd_apply_time: null argument");
         require(P->device >= 0, "stiga_fd_apply_time: host-only handle");
+        require(!P->shard, "stiga_fd_apply_time: stage building blocks need a single-device handle");
         require(s0 >= 0 && ns_local >= 1 && s0 + ns_local <= P->n_s, "stiga_fd_apply_time: spatial slab out of range");
         require(d_in != d_out, "stiga_fd_apply_time: input and output must not alias");
         DeviceGuard dg(P->device);
@@ -1078,6 +499,7 @@ int stiga_fd_apply_space_scatter(stiga_fd_t P, long long t0, long long nt_local,
     return guarded([&] {
         require(P && d_in, "stiga_fd_apply_space_scatter: null argument");
         require(P->device >= 0, "stiga_fd_apply_space_scatter: host-only handle");
+        require(!P->shard, "stiga_fd_apply_space_scatter: stage building blocks need a single-device handle");
         require(t0 >= 0 && nt_local >= 1 && t0 + nt_local <= P->dims[P->d],
                 "stiga_fd_apply_space_scatter: time slab out of range");
         const gpu::Scatter s = to_scatter(sc, false, P->n_s, nt_local, "stiga_fd_apply_space_scatter");
@@ -1091,6 +513,7 @@ int stiga_fd_apply_time_scatter(stiga_fd_t P, long long s0, long long ns_local, 
     return guarded([&] {
         require(P && d_in, "stiga_fd_apply_time_scatter: null argument");
         require(P->device >= 0, "stiga_fd_apply_time_scatter: host-only handle");
+        require(!P->shard, "stiga_fd_apply_time_scatter: stage building blocks need a single-device handle");
         require(s0 >= 0 && ns_local >= 1 && s0 + ns_local <= P->n_s,
                 "stiga_fd_apply_time_scatter: spatial slab out of range");
         const gpu::Scatter s = to_scatter(sc, true, ns_local, P->dims[P->d], "stiga_fd_apply_time_scatter");
@@ -1153,33 +576,8 @@ int stiga_copy_blocks(const double* d_src, long long src_ld, double* d_dst, long
 int stiga_fd_launch_info(stiga_fd_t P, int i, char* name, int name_len, double* flops) {
     return guarded([&] {
         require(P && name && name_len > 0 && flops, "stiga_fd_launch_info: null argument");
-        require(i >= 0 && i < P->launches(), "stiga_fd_launch_info: launch index out of range");
-        std::vector<std::pair<std::string, double>> L;
-        const double N = static_cast<double>(P->n_dof);
-        if (P->dinv.p && !P->fused_prescale()) L.emplace_back("pre_scale", 0.0);
-        // executed FP64 work: 2 n N per dense product, 4 F^2 N / n per folded one (F = ceil(n/2))
-        auto prod_flops = [&](const gpu::Tiling& t, int l) {
-            const double n = P->dims[l], Fh = n - std::floor(n / 2);
-            return t.fold ? 4.0 * Fh * Fh * N / n : 2.0 * n * N;
-        };
-        auto tag = [](const gpu::Tiling& t) { return t.fold ? std::string("(folded)") : std::string(); };
-        for (int l = 0; l < P->d; ++l) {
-            const gpu::Tiling& t = l == 0 ? P->first_tiling() : P->tl[l];
-            L.emplace_back("fwd_mode" + std::to_string(l) + tag(t) + (l == 0 && P->fused_prescale() ? "+pre_scale" : ""),
-                           prod_flops(t, l));
-        }
-        const double nt = P->dims[P->d];
-        if (P->time_split) {
-            L.emplace_back("time_UtT", 2.0 * nt * N);
-            L.emplace_back("arrowhead", 0.0);
-            L.emplace_back("time_Ut", 2.0 * nt * N);
-        } else {
-            L.emplace_back("time_fused", 4.0 * nt * N);
-        }
-        for (int l = 0; l < P->d; ++l)
-            L.emplace_back("bwd_mode" + std::to_string(l) + tag(P->tl_b[l]) +
-                               (l == P->d - 1 && P->dinv.p ? "+post_scale" : ""),
-                           prod_flops(P->tl_b[l], l));
+        const std::vector<std::pair<std::string, double>> L = P->launch_list();
+        require(i >= 0 && i < static_cast<int>(L.size()), "stiga_fd_launch_info: launch index out of range");
         std::snprintf(name, static_cast<size_t>(name_len), "%s", L[i].first.c_str());
         *flops = L[i].second;
     });
@@ -1197,12 +595,15 @@ int stiga_fd_apply_host(stiga_fd_t P, const double* h_r, double* h_s) {
         require(P && h_r && h_s, "ExtendedFDPreconditioner::apply: null argument");
         require(P->device >= 0, "ExtendedFDPreconditioner::apply: host-only handle (setup with device < 0)");
         DeviceGuard dg(P->device);
+        // local slab for a sharded handle (collective), the whole vector otherwise
+        const long long n = P->shard ? P->n_s * P->shard->t_len[P->shard->rank] : P->n_dof;
         DBuf in, out;
-        in.alloc(static_cast<size_t>(P->n_dof));
-        out.alloc(static_cast<size_t>(P->n_dof));
-        ck(cudaMemcpy(in.p, h_r, sizeof(double) * P->n_dof, cudaMemcpyHostToDevice), "H2D");
-        P->apply(in.p, out.p, nullptr, nullptr);
-        ck(cudaMemcpy(h_s, out.p, sizeof(double) * P->n_dof, cudaMemcpyDeviceToHost), "D2H");
+        in.alloc(static_cast<size_t>(n));
+        out.alloc(static_cast<size_t>(n));
+        ck(cudaMemcpy(in.p, h_r, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+        if (P->shard) fd_apply_sharded(*P, in.p, out.p, nullptr, nullptr);
+        else P->apply(in.p, out.p, nullptr, nullptr);
+        ck(cudaMemcpy(h_s, out.p, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
     });
 }
 
@@ -1284,12 +685,11 @@ int stiga_kronsum_create(int D, const int* dims, int nterms, const double* coeff
     });
 }
 
-int stiga_kronsum_create_spacetime(int d, const int* n, const double* const* K, const double* const* M, int n_t,
-                                   const double* Wt, const double* Mt, double gamma, double nu, int device,
-                                   stiga_kronsum_t* out) {
-    return guarded([&] {
-        require(out != nullptr, "stiga_kronsum_create_spacetime: null handle output");
-        *out = nullptr;
+}  // extern "C"
+
+namespace stiga {
+stiga_kronsum_s* ks_build_spacetime(int d, const int* n, const double* const* K, const double* const* M, int n_t,
+                                    const double* Wt, const double* Mt, double gamma, double nu, int device) {
         require(d >= 1 && n && K && M && Wt && Mt && n_t >= 1, "KronSumOperator: dimensions must be positive");
         auto h = std::make_unique<stiga_kronsum_s>();
         h->device = device;
@@ -1334,14 +734,26 @@ int stiga_kronsum_create_spacetime(int d, const int* n, const double* const* K, 
         }
         push(Wd, gamma);
         push(Mtd, nu);
-        *out = h.release();
+        return h.release();
+}
+}  // namespace stiga
+
+extern "C" {
+
+int stiga_kronsum_create_spacetime(int d, const int* n, const double* const* K, const double* const* M, int n_t,
+                                   const double* Wt, const double* Mt, double gamma, double nu, int device,
+                                   stiga_kronsum_t* out) {
+    return guarded([&] {
+        require(out != nullptr, "stiga_kronsum_create_spacetime: null handle output");
+        *out = nullptr;
+        *out = ks_build_spacetime(d, n, K, M, n_t, Wt, Mt, gamma, nu, device);
     });
 }
 
-int stiga_kronsum_create_physical(stiga_problem_t prob, int p, int n_el, int device, stiga_kronsum_t* out) {
-    return guarded([&] {
-        require(prob && out, "stiga_kronsum_create_physical: null argument");
-        *out = nullptr;
+}  // extern "C"
+
+namespace stiga {
+stiga_kronsum_s* ks_build_physical(stiga_problem_s* prob, int p, int n_el, int device) {
         const ProblemSpec& spec = prob->spec;
         const int d = spec.d;
         const SplineSpace1D space = SplineSpace1D::spatial(p, n_el);
@@ -1426,7 +838,17 @@ int stiga_kronsum_create_physical(stiga_problem_t prob, int p, int n_el, int dev
         ck(cudaMemset(h->Mst.p, 0, sizeof(double) * Ns * S), "memset");
         ck(gpu::launch_physical_assembly(g, h->Kst.p, h->Mst.p, nullptr), "physical assembly");
         ck(cudaDeviceSynchronize(), "physical assembly");
-        *out = h.release();
+        return h.release();
+}
+}  // namespace stiga
+
+extern "C" {
+
+int stiga_kronsum_create_physical(stiga_problem_t prob, int p, int n_el, int device, stiga_kronsum_t* out) {
+    return guarded([&] {
+        require(prob && out, "stiga_kronsum_create_physical: null argument");
+        *out = nullptr;
+        *out = ks_build_physical(prob, p, n_el, device);
     });
 }
 
@@ -1459,7 +881,22 @@ int stiga_kronsum_apply(stiga_kronsum_t A, const double* d_x, double* d_y, void*
         require(A && d_x && d_y, "KronSumOperator::apply: vector length mismatch");
         require(d_x != d_y, "KronSumOperator::apply: input and output must not alias");
         DeviceGuard dg(A->device);
-        A->apply(d_x, d_y, as_stream(stream));
+        if (A->kshard) kronsum_apply_sharded(*A, d_x, d_y, as_stream(stream));
+        else A->apply(d_x, d_y, as_stream(stream));
+    });
+}
+
+int stiga_kronsum_local(stiga_kronsum_t A, long long* t0, long long* nt_local, long long* offset, long long* len) {
+    return guarded([&] {
+        require(A != nullptr, "stiga_kronsum_local: null handle");
+        const int nt = A->dims[A->D - 1];
+        const long long Ns = A->n_dof / nt;
+        const long long a = A->kshard ? A->kshard->t_off[A->kshard->rank] : 0;
+        const long long b = A->kshard ? A->kshard->t_len[A->kshard->rank] : nt;
+        if (t0) *t0 = a;
+        if (nt_local) *nt_local = b;
+        if (offset) *offset = Ns * a;
+        if (len) *len = Ns * b;
     });
 }
 
@@ -1482,37 +919,7 @@ int stiga_kronsum_apply_space(stiga_kronsum_t A, long long nt_local, const doubl
         require(d_x != d_a && d_x != d_b && d_a != d_b, "stiga_kronsum_apply_space: buffers must not alias");
         if (nt_local == 0) return;
         DeviceGuard dg(A->device);
-        cudaStream_t st = as_stream(stream);
-        if (A->physical) {
-            ck(gpu::launch_stencil_apply2(A->pdesc, A->Mst.p, A->Kst.p, d_x, d_a, d_b, nt_local, st), "stencil apply");
-            return;
-        }
-        // spatial chain of the spacetime form over dims [n_1 .. n_d, nt_local]
-        const long long Ns = A->n_dof / A->dims[d];
-        auto geo = [&](int m) {
-            gpu::ModeGeom g;
-            long long L = 1;
-            for (int l = 0; l < m; ++l) L *= A->dims[l];
-            g.L = L;
-            g.n = g.m = A->dims[m];
-            g.ncols = Ns * nt_local / A->dims[m];
-            return g;
-        };
-        const gpu::Band none{};
-        A->ensure_scratch(4);
-        double* bufs[2][2] = {{A->t0.p, A->t1.p}, {A->t2.p, A->t3.p}};
-        double* a = d == 1 ? d_a : bufs[0][0];
-        double* b = d == 1 ? d_b : bufs[0][1];
-        ck(gpu::launch_banded_pass(geo(0), d_x, nullptr, a, b, A->band(0), none, A->band(1), none, 0.0, st), "banded");
-        for (int m = 1; m < d; ++m) {
-            double* a2 = m == d - 1 ? d_a : bufs[m % 2][0];
-            double* b2 = m == d - 1 ? d_b : bufs[m % 2][1];
-            ck(gpu::launch_banded_pass(geo(m), a, b, a2, b2, A->band(2 * m), none, A->band(2 * m + 1), A->band(2 * m), 0.0,
-                                       st),
-               "banded");
-            a = a2;
-            b = b2;
-        }
+        A->apply_space_slab(nt_local, d_x, d_a, d_b, as_stream(stream));
     });
 }
 

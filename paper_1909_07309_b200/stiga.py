@@ -17,6 +17,7 @@ from typing import List, Optional
 
 import numpy as np
 
+from ._lib import ALLGATHER_FN, ALLREDUCE_FN, BARRIER_FN, COMM_ID_BYTES, LINOP_FN, CommCallbacks
 from ._lib import GmresOptions as _GOpts
 from ._lib import GmresReport as _GRep
 from ._lib import check, lib
@@ -119,14 +120,127 @@ def kron_sum_terms(K, M, Wt, Mt, gamma, nu):
 
 
 # ----------------------------------------------------------------------------------------
+# Communicator (multi-GPU)
+# ----------------------------------------------------------------------------------------
+def shard_partition(n, world, rank):
+    """Balanced contiguous partition (stiga_shard_partition): (offset, length) of part `rank`."""
+    o, l_ = ctypes.c_longlong(), ctypes.c_longlong()
+    check(lib().stiga_shard_partition(int(n), int(world), int(rank), ctypes.byref(o), ctypes.byref(l_)),
+          "shard_partition")
+    return o.value, l_.value
+
+
+class Comm:
+    """stiga_comm_t: one rank of a communicator.  Comm.nccl(...) wraps NCCL (collectives stream-ordered
+    on the device); Comm.from_process_group() builds NCCL for an nccl torch.distributed group and a
+    host-callback communicator over the group's collectives otherwise (gloo: the CPU / one-GPU tests)."""
+
+    def __init__(self, handle, world, rank, device, keep=None):
+        self._h = ctypes.c_void_p(handle)
+        self.world, self.rank, self.device = world, rank, device
+        self._keep = keep  # ctypes callbacks must outlive the handle
+
+    @staticmethod
+    def unique_id():
+        buf = ctypes.create_string_buffer(COMM_ID_BYTES)
+        check(lib().stiga_comm_unique_id(buf), "comm_unique_id")
+        return buf.raw
+
+    @staticmethod
+    def nccl(world, rank, uid, device=0):
+        h = ctypes.c_void_p()
+        check(lib().stiga_comm_init_nccl(int(world), int(rank), uid, int(device), ctypes.byref(h)), "comm_init_nccl")
+        return Comm(h.value, world, rank, device)
+
+    @staticmethod
+    def host(world, rank, allreduce, allgather, barrier, device=0):
+        """Host-callback communicator: allreduce(np.ndarray (in place), op: 0 sum / 1 max),
+        allgather(bytes) -> list of bytes (rank order), barrier()."""
+
+        def _ar(ctx, buf, n, op):
+            try:
+                a = np.ctypeslib.as_array(buf, shape=(n,))
+                allreduce(a, op)
+                return 0
+            except Exception:
+                return 1
+
+        def _ag(ctx, send, nbytes, recv):
+            try:
+                parts = allgather(ctypes.string_at(send, nbytes))
+                ctypes.memmove(recv, b"".join(parts), nbytes * world)
+                return 0
+            except Exception:
+                return 1
+
+        def _br(ctx):
+            try:
+                barrier()
+                return 0
+            except Exception:
+                return 1
+
+        cb = CommCallbacks(None, ALLREDUCE_FN(_ar), ALLGATHER_FN(_ag), BARRIER_FN(_br))
+        h = ctypes.c_void_p()
+        check(lib().stiga_comm_init_host(int(world), int(rank), ctypes.byref(cb), int(device), ctypes.byref(h)),
+              "comm_init_host")
+        return Comm(h.value, world, rank, device, keep=cb)
+
+    @staticmethod
+    def from_process_group(group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        dev = torch.cuda.current_device() if device is None else device
+        if dist.get_backend(group) == "nccl":
+            box = [Comm.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            return Comm.nccl(world, rank, box[0], dev)
+
+        def allreduce(a, op):
+            t = torch.from_numpy(a)  # shares memory with the C buffer
+            dist.all_reduce(t, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
+
+        def allgather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b, group=group)
+            return out
+
+        return Comm.host(world, rank, allreduce, allgather, lambda: dist.barrier(group=group), dev)
+
+    def allreduce(self, t, stream=None):
+        """Sum-all-reduce of a float64 CUDA tensor in place."""
+        check(lib().stiga_comm_allreduce(self._h, ctypes.c_void_p(t.data_ptr()), t.numel(), _stream_handle(stream)),
+              "comm_allreduce")
+        return t
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().stiga_comm_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+
+# ----------------------------------------------------------------------------------------
 # ExtendedFDPreconditioner
 # ----------------------------------------------------------------------------------------
 class ExtendedFDPreconditioner:
     """fdsolve.hpp:41-70.  Build with ExtendedFDPreconditioner.setup(...)."""
 
-    def __init__(self, handle, device):
+    def __init__(self, handle, device, comm=None):
         self._h = ctypes.c_void_p(handle)
         self.device = device
+        self.comm = comm  # keeps the communicator alive for a sharded handle
         n = ctypes.c_longlong()
         check(lib().stiga_fd_size(self._h, ctypes.byref(n)), "fd_size")
         self.n_dof = n.value
@@ -135,10 +249,18 @@ class ExtendedFDPreconditioner:
         check(lib().stiga_fd_dims(self._h, ctypes.byref(d), dims), "fd_dims")
         self.d = d.value
         self.dims = [dims[i] for i in range(self.d + 1)]
+        v = [ctypes.c_longlong() for _ in range(4)]
+        check(lib().stiga_fd_local(self._h, *[ctypes.byref(x) for x in v]), "fd_local")
+        self.t0, self.nt_local, self.offset, self.n_local = [x.value for x in v]
+
+    def local_slice(self):
+        """Range of the global colex vector this handle's apply maps (the whole vector unsharded)."""
+        return self.offset, self.offset + self.n_local
 
     @staticmethod
-    def setup(space_K, space_M, Wt, Mt, gamma, nu, scaling=None, device=0):
-        """fdsolve.cpp:67-153 (host factorizations, one upload of the factors)."""
+    def setup(space_K, space_M, Wt, Mt, gamma, nu, scaling=None, device=0, comm=None):
+        """fdsolve.cpp:67-153 (host factorizations, one upload of the factors).  With comm (a Comm):
+        the time-sharded handle of this rank (collective); `scaling` is then D on the local time slab."""
         if len(space_K) != len(space_M) or len(space_K) == 0:
             raise ValueError("ExtendedFDPreconditioner: per-direction matrices mismatch")
         Ks = [_colmajor(k) for k in space_K]
@@ -154,6 +276,12 @@ class ExtendedFDPreconditioner:
         n_t = int(np.asarray(Wt).shape[0])
         sc = None if scaling is None else _f64(scaling)
         h = ctypes.c_void_p()
+        if comm is not None:
+            check(lib().stiga_fd_setup_sharded(len(Ks), n, _ptr_array(Ks), _ptr_array(Ms), n_t, _ptr(W), _ptr(Mm),
+                                               float(gamma), float(nu), _ptr(sc) if sc is not None else None,
+                                               len(sc) if sc is not None else 0, comm.handle, ctypes.byref(h)),
+                  "fd_setup_sharded")
+            return ExtendedFDPreconditioner(h.value, comm.device, comm)
         check(lib().stiga_fd_setup(len(Ks), n, _ptr_array(Ks), _ptr_array(Ms), n_t, _ptr(W), _ptr(Mm),
                                    float(gamma), float(nu), _ptr(sc) if sc is not None else None,
                                    len(sc) if sc is not None else 0, int(device), ctypes.byref(h)), "fd_setup")
@@ -221,7 +349,7 @@ class ExtendedFDPreconditioner:
 
             if r.dtype != torch.float64 or not r.is_cuda or not r.is_contiguous():
                 raise ValueError("ExtendedFDPreconditioner::apply: expected a contiguous float64 CUDA tensor")
-            if r.numel() != self.n_dof:
+            if r.numel() != self.n_local:
                 raise ValueError("ExtendedFDPreconditioner::apply: vector length mismatch")
             if out is None:
                 out = torch.empty_like(r)
@@ -229,7 +357,7 @@ class ExtendedFDPreconditioner:
                                        _stream_handle(stream)), "fd_apply")
             return out
         r = _f64(r)
-        if r.size != self.n_dof:
+        if r.size != self.n_local:
             raise ValueError("ExtendedFDPreconditioner::apply: vector length mismatch")
         s = np.empty_like(r) if out is None else out
         check(lib().stiga_fd_apply_host(self._h, _ptr(r), _ptr(s)), "fd_apply_host")
@@ -289,15 +417,18 @@ class KronSumOperator:
         n = ctypes.c_longlong()
         check(lib().stiga_kronsum_size(self._h, ctypes.byref(n)), "kronsum_size")
         self.n_dof = n.value
+        v = [ctypes.c_longlong() for _ in range(4)]
+        check(lib().stiga_kronsum_local(self._h, *[ctypes.byref(x) for x in v]), "kronsum_local")
+        self.t0, self.nt_local, self.offset, self.n_local = [x.value for x in v]
         nd = ctypes.c_int()
         dims_buf = (ctypes.c_int * 8)()
         check(lib().stiga_kronsum_dims(self._h, ctypes.byref(nd), dims_buf, 8), "kronsum_dims")
         self.dims = [dims_buf[i] for i in range(nd.value)]
 
     @staticmethod
-    def spacetime(K, M, Wt, Mt, gamma, nu, device=0):
+    def spacetime(K, M, Wt, Mt, gamma, nu, device=0, comm=None):
         """KronSumOperator(dims, kron_sum_terms(K, M, Wt, Mt, gamma, nu)) with the sum-factorized
-        banded apply (solver.cpp:10-30, 67-70)."""
+        banded apply (solver.cpp:10-30, 67-70).  comm: the time-sharded operator of this rank."""
         d = len(K)
         Ks = [_colmajor(k) for k in K]
         Ms = [_colmajor(m) for m in M]
@@ -305,16 +436,30 @@ class KronSumOperator:
         W = _colmajor(Wt)
         Mm = _colmajor(Mt)
         h = ctypes.c_void_p()
+        if comm is not None:
+            check(lib().stiga_kronsum_create_spacetime_sharded(d, n, _ptr_array(Ks), _ptr_array(Ms), W.shape[0],
+                                                               _ptr(W), _ptr(Mm), float(gamma), float(nu),
+                                                               comm.handle, ctypes.byref(h)),
+                  "kronsum_create_spacetime_sharded")
+            op = KronSumOperator(None, None, comm.device, _handle=h.value)
+            op.comm = comm
+            return op
         check(lib().stiga_kronsum_create_spacetime(d, n, _ptr_array(Ks), _ptr_array(Ms), W.shape[0], _ptr(W),
                                                    _ptr(Mm), float(gamma), float(nu), int(device), ctypes.byref(h)),
               "kronsum_create_spacetime")
         return KronSumOperator(None, None, device, _handle=h.value)
 
     @staticmethod
-    def physical(problem, p, n_el, device=0):
+    def physical(problem, p, n_el, device=0, comm=None):
         """SpaceTimeSystem's A_ = M_s (x) W_t + K_s (x) M_t (solver.cpp:58-70) with the physical
-        spatial matrices of `problem` (problems.Problem) assembled on the device."""
+        spatial matrices of `problem` (problems.Problem) assembled on the device.  comm: sharded."""
         h = ctypes.c_void_p()
+        if comm is not None:
+            check(lib().stiga_kronsum_create_physical_sharded(problem._h, int(p), int(n_el), comm.handle,
+                                                              ctypes.byref(h)), "kronsum_create_physical_sharded")
+            op = KronSumOperator(None, None, comm.device, _handle=h.value)
+            op.comm = comm
+            return op
         check(lib().stiga_kronsum_create_physical(problem._h, int(p), int(n_el), int(device), ctypes.byref(h)),
               "kronsum_create_physical")
         return KronSumOperator(None, None, device, _handle=h.value)
@@ -338,7 +483,7 @@ class KronSumOperator:
     def apply(self, x, out=None, stream=None):
         import torch
 
-        if x.numel() != self.n_dof:
+        if x.numel() != self.n_local:
             raise ValueError("KronSumOperator::apply: vector length mismatch")
         if out is None:
             out = torch.empty_like(x)
@@ -394,6 +539,60 @@ def gmres(A, P, b, opts=None, stream=None):
                             _stream_handle(stream)), "gmres")
     return x, SolveReport(rep.iterations, list(hist[: min(cap, rep.history_len)]), bool(rep.converged),
                           rep.wall_time_s, rep.precond_time_fraction)
+
+
+def gmres_op(n, A, P, b, opts=None, comm=None, stream=None):
+    """gmres(A, P, b, opts) over Python-callable operators (gmres.hpp:12 LinOp): A(x, y) and P(x, y)
+    (P may be None) write the image of the CUDA tensor x into y (both n float64 entries, on the current
+    stream).  comm: Krylov dots all-reduced over the communicator (local slabs, CGS2).  Through
+    stiga_gmres_op; the solver itself is the native one."""
+    import torch
+
+    opts = opts or GmresOptions()
+    if opts.restart is not None and opts.restart < 1:
+        raise ValueError("gmres: restart cycle must be >= 1")
+    dev = b.device
+    nb = int(n)
+    errors = []
+
+    def wrap(f):
+        def cb(ctx, d_in, d_out, stream_):
+            try:
+                x = _device_view(d_in, nb, dev)
+                y = _device_view(d_out, nb, dev)
+                f(x, y)
+                return 0
+            except Exception as e:  # reported by the solver as a callback failure
+                errors.append(e)
+                return 1
+        return LINOP_FN(cb)
+
+    fa = wrap(A)
+    fp = wrap(P) if P is not None else LINOP_FN()
+    x = torch.empty_like(b)
+    cap = opts.max_krylov + 2
+    hist = np.zeros(cap)
+    rep = _GRep(0, 0, 0.0, 0.0, _ptr(hist), cap, 0)
+    o = _GOpts(float(opts.tol), int(opts.max_krylov), int(opts.restart or 0))
+    st = check_status = lib().stiga_gmres_op(nb, fa, None, fp, None, comm.handle if comm is not None else None,
+                                             ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(x.data_ptr()),
+                                             ctypes.byref(o), ctypes.byref(rep), _stream_handle(stream))
+    if st != 0 and errors:
+        raise errors[0]
+    check(check_status, "gmres_op")
+    return x, SolveReport(rep.iterations, list(hist[: min(cap, rep.history_len)]), bool(rep.converged),
+                          rep.wall_time_s, rep.precond_time_fraction)
+
+
+def _device_view(ptr, n, device):
+    """A float64 CUDA tensor viewing n doubles at device address ptr (no copy)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+
+    return torch.as_tensor(_Arr(), device=device)
 
 
 def fp64_peak(device=0, ms=200.0):
