@@ -175,6 +175,24 @@ def problem_pieces(cfg, device=None):
     return pc, pc.D
 
 
+def problem_pieces_slab(cfg, world, rank, device=None):
+    """problem_pieces for one rank of the time-sharded run: the 1D factors and D on the rank's time slab
+    only (per-rank host and device memory ~ N_dof / world)."""
+    from paper_1909_07309_b200 import stiga
+    from paper_1909_07309_b200.problems import Problem, geometry_scaling, identity_pieces
+
+    n_t = cfg.n_t
+    t0, ntl = stiga.shard_partition(n_t, world, rank)
+    if cfg.problem == "identity":
+        pc = identity_pieces(cfg.d, cfg.p, cfg.n_el)
+        return pc, geometry_scaling(pc, t_range=(t0, t0 + ntl)), (t0, ntl)
+    pc = Problem(cfg.problem).geometry_pieces(cfg.p, cfg.n_el, want_D=True, device=device)
+    if hasattr(pc, "A"):
+        del pc.A
+    n_s = pc.n_dof // n_t
+    return pc, pc.D[n_s * t0:n_s * (t0 + ntl)].copy(), (t0, ntl)
+
+
 def run_reference(args):
     """The reference arm: the oracle port of the reference's CPU path on the box's host cores (all
     BLAS threads), on our arm's config / metric / unit; each step one bounded sample of the full apply
@@ -243,31 +261,39 @@ def run_ours(args):
     dev = local
     cfg = CONFIGS[args.config]
     K_steps, W_steps = args.steps, max(args.warmup, 3)
+    sharded = ws > 1 and not args.replicas
+    exchange = None
 
     t0 = time.perf_counter()
-    pc, D = problem_pieces(cfg, device=local)
+    if sharded:  # this rank's time slab only: the pieces are 1D factors, D is built for the slab
+        comm = stiga.Comm.from_process_group(device=dev)
+        pc, D, (t_lo, t_len) = problem_pieces_slab(cfg, ws, rank, device=local)
+    else:
+        pc, D = problem_pieces(cfg, device=local)
     pieces_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D, device=dev)
+    if sharded and args.exchange == "p2p":
+        # native time-sharded handle (C ABI): all-to-all fused into the scatter epilogues over CUDA-IPC
+        # peer buffers, stream-ordered NCCL barriers between the stages
+        P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=D, comm=comm)
+        exchange = "native C ABI: scatter epilogues into peer buffers (CUDA IPC / NVLink), " + \
+                   ("NCCL stream-ordered barriers" if dist.get_backend() == "nccl" else "host barriers (gloo)")
+    else:
+        P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0,
+                                                 scaling=D if not sharded else None, device=dev)
     setup_s = time.perf_counter() - t0
     n = P.n_dof
     launches = P.launches()
 
-    sharded = ws > 1 and not args.replicas
-    exchange = None
-    if sharded:  # time-sharded apply: rank owns a time slab, two all-to-all transposes per apply
-        from paper_1909_07309_b200.distributed import DeviceBackend, FusedShardedExtendedFD, ShardedExtendedFD
+    if sharded and args.exchange == "p2p":
+        a0, a1 = P.local_slice()
+        r_host = torch.from_numpy(uniform_pm1(a1 - a0, cfg.seed, start=a0)).pin_memory()
+        apply_fn = lambda x, y: P.apply(x, out=y)  # noqa: E731
+    elif sharded:  # --exchange nccl: pack + NCCL all_to_all_single + unpack (the Python baseline path)
+        from paper_1909_07309_b200.distributed import DeviceBackend, ShardedExtendedFD
 
-        sh = None
-        if args.exchange == "p2p":
-            try:
-                sh = FusedShardedExtendedFD.create(P, P.dims, device=dev)
-                exchange = "p2p scatter epilogues (CUDA IPC peer memory)"
-            except Exception as e:  # e.g. no peer access between these GPUs: keep the NCCL exchange
-                exchange = f"nccl (p2p unavailable: {type(e).__name__}: {str(e)[:120]})"
-        if sh is None:
-            sh = ShardedExtendedFD(DeviceBackend(P), P.dims)
-            exchange = exchange or "nccl all_to_all_single (pack / unpack)"
+        sh = ShardedExtendedFD(DeviceBackend(P), P.dims)
+        exchange = "nccl all_to_all_single (pack / unpack), unscaled"
         a0, a1 = sh.plan.local_slice()
         r_host = torch.from_numpy(uniform_pm1(a1 - a0, cfg.seed, start=a0)).pin_memory()
         apply_fn = lambda x, y: sh.apply(x, out=y)  # noqa: E731
@@ -320,8 +346,8 @@ def run_ours(args):
     # ---- per-launch durations (separate profiled pass over K steps, events on the same stream) --
     pass_ms = np.zeros(launches)
     kp = min(K_steps, 50)
-    rp, sp = (r, s) if not sharded else (torch.zeros(n, dtype=torch.float64, device=f"cuda:{dev}"),
-                                         torch.empty(n, dtype=torch.float64, device=f"cuda:{dev}"))
+    rp, sp = (r, s) if (not sharded or args.exchange == "p2p") else (
+        torch.zeros(n, dtype=torch.float64, device=f"cuda:{dev}"), torch.empty(n, dtype=torch.float64, device=f"cuda:{dev}"))
     for _ in range(kp):
         pass_ms += np.array(P.apply_profiled(rp, sp))
     pass_ms /= kp
@@ -425,34 +451,39 @@ def run_ours(args):
               "final_rel_precond_residual": rep.residual_history[-1], "true_rel_residual": res,
               "precond_time_fraction": rep.precond_time_fraction, "restart": 50, "tol": 1e-8}
         del A
-    elif not args.no_gmres and sharded:  # time-sharded GMRES: halo-exchanged A, all-reduced dots
+    elif not args.no_gmres and sharded:  # collective GMRES on the native time-sharded handles (CGS2)
         try:
-            from paper_1909_07309_b200.distributed import (DeviceSystemBackend, DeviceVec, ShardedSystem,
-                                                           sharded_gmres)
-
             t_a = time.perf_counter()
+            if args.exchange != "p2p":
+                raise RuntimeError("the GMRES section needs the native sharded handles (--exchange p2p)")
             if cfg.problem == "identity":
-                A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=dev)
+                A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, comm=comm)
             else:
                 from paper_1909_07309_b200.problems import Problem
 
-                A = stiga.KronSumOperator.physical(Problem(cfg.problem), cfg.p, cfg.n_el, device=dev)
+                A = stiga.KronSumOperator.physical(Problem(cfg.problem), cfg.p, cfg.n_el, comm=comm)
             torch.cuda.synchronize()
             a_setup_s = time.perf_counter() - t_a
-            Ash = ShardedSystem(DeviceSystemBackend(A), A.dims)
-            vec = DeviceVec()
-            x, rep = sharded_gmres(Ash, sh, r, vec, 1e-8, 500, 50, ortho="cgs2")
+            opts = stiga.GmresOptions(tol=1e-8, max_krylov=500, restart=50)
+            x, rep = stiga.gmres(A, P, r, opts)
             barrier()
-            x, rep = sharded_gmres(Ash, sh, r, vec, 1e-8, 500, 50, ortho="cgs2")
-            res_v = Ash.apply(x)
-            vec.axpy(-1.0, r, res_v)
-            res = (vec.dot(res_v, res_v) / vec.dot(r, r)) ** 0.5
+            x, rep = stiga.gmres(A, P, r, opts)
+            res_v = A.apply(x) - r
+            nums = torch.stack([torch.dot(res_v, res_v), torch.dot(r, r)])
+            comm.allreduce(nums)
+            res = (nums[0] / nums[1]).sqrt().item()
+            ev0.record(stream)
+            for _ in range(5):
+                A.apply(r, out=s)
+            ev1.record(stream)
+            torch.cuda.synchronize()
             gm = {"time_s": max_over_ranks(rep.wall_time_s), "iterations": rep.iterations,
                   "converged": rep.converged, "operator_setup_s": a_setup_s,
+                  "matvec_ms": max_over_ranks(ev0.elapsed_time(ev1) / 5),
                   "final_rel_precond_residual": rep.residual_history[-1], "true_rel_residual": res,
-                  "restart": 50, "tol": 1e-8, "sharded": f"time x{ws}",
+                  "restart": 50, "tol": 1e-8, "sharded": f"time x{ws} (native C ABI, halo push over CUDA IPC)",
                   "ortho": "CGS2, batched dots (two all-reduces per Arnoldi column)"}
-            del A, Ash
+            del A
         except Exception as e:  # report, do not lose the apply numbers
             gm = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
 
@@ -462,8 +493,9 @@ def run_ours(args):
         cpu = cpu_baseline(cfg, args.cpu_frac)
 
     f_alg = cfg.flops_fd()
-    t_roof_flop = f_alg / (peak_dmma * 1e12)
-    t_roof_hbm = 32.0 * n / 6538.9e9
+    g_eff = ws if sharded else 1  # the sharded job's roofline is the N-GPU one
+    t_roof_flop = f_alg / (g_eff * peak_dmma * 1e12)
+    t_roof_hbm = 32.0 * n / (g_eff * 6538.9e9)
     out = {
         "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": ws, "steps": K_steps, "warmup": W_steps,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
@@ -479,7 +511,7 @@ def run_ours(args):
                            "frac": max(t_roof_flop, t_roof_hbm) / (ms * 1e-3), "peak_tflops": peak_dmma,
                            "bound": "fp64 (DMMA)",
                            "F_exec_flop": float(sum(flops)),
-                           "frac_exec": float(sum(flops)) / (peak_dmma * 1e12) / (ms * 1e-3),
+                           "frac_exec": float(sum(flops)) / (peak_dmma * 1e12) / (ms * 1e-3),  # per rank
                            "note": "F_alg = 4 N (sum n_l + n_t) (PAPER.md:1061-1064, dense mode products); "
                                    "F_exec = FP64 work the launches execute (a folded centrosymmetric product "
                                    "does ~half of a dense one, DESIGN.md §5)"},
@@ -493,7 +525,8 @@ def run_ours(args):
                 "h2d_bytes_per_step": 8 * r.numel(), "d2h_bytes_per_step": 8 * r.numel(), "ms_per_step": e2e_ms,
                 "pipelining": "H2D / apply / D2H on three streams, two buffer pairs",
                 "serial_value": (1 if sharded else ws) / (e2e_serial_ms * 1e-3)},
-        "gpu_launches": K_steps * (launches + (2 * ws if sharded and exchange.startswith("nccl") else 0)),
+        "gpu_launches": K_steps * (len([nm for nm in names if not nm.startswith("exchange_barrier")]) +
+                                   (2 * ws if sharded and exchange.startswith("nccl") else 0)),
         "setup_s": setup_s, "pieces_s": pieces_s,
         "gmres": gm,
         "cpu_baseline": cpu,

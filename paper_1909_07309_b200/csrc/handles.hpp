@@ -452,7 +452,7 @@ struct stiga_fd_s {
                                      t.RB, t.ctas_per_sm, ms);
                 }
                 const float arrow = time_once([&] {
-                    ck(gpu::launch_arrowhead(scratch2.p, scratch.p, n_s, ap, nullptr), "tune");
+                    ck(gpu::launch_arrowhead(scratch2.p, scratch.p, ns_span, ap, nullptr), "tune");
                 });
                 best_split = 2.f * best_gemm + arrow;
                 if (debug_tune) std::fprintf(stderr, "[stiga tune] arrowhead: %.4f ms\n", arrow);

@@ -43,24 +43,28 @@ def identity_pieces(d, p, n_el, T=1.0):
     return SpaceTimePieces(d, p, n_el, K, M, Wt, Mt)
 
 
-def kron_sum_diagonal(terms):
-    """KronSumOperator::diagonal (kronop.cpp:117-131): sum_t c_t kron(diag F_D, ..., diag F_1)."""
+def kron_sum_diagonal(terms, t_range=None):
+    """KronSumOperator::diagonal (kronop.cpp:117-131): sum_t c_t kron(diag F_D, ..., diag F_1).
+    t_range = (t0, t1): only the slices t0 <= t < t1 of the last (slowest) mode -- a rank's time slab."""
     out = None
     for c, fs in terms:
         acc = np.ones(1)
-        for f in fs:
-            acc = np.kron(np.diag(f), acc)
+        for k, f in enumerate(fs):
+            dg = np.diag(f)
+            if t_range is not None and k == len(fs) - 1:
+                dg = dg[t_range[0]:t_range[1]]
+            acc = np.kron(dg, acc)
         out = c * acc if out is None else out + c * acc
     return out
 
 
-def geometry_scaling(pc, K_tilde=None, M_tilde=None, Mt_tilde=None):
+def geometry_scaling(pc, K_tilde=None, M_tilde=None, Mt_tilde=None, t_range=None):
     """D = diag(A) / diag(A~) with A~ in (d+1)-factor form (solver.cpp:138-142).  On the identity
-    map with constant coefficients K~ = K, M~ = M and D == 1."""
+    map with constant coefficients K~ = K, M~ = M and D == 1.  t_range: a time slab of it."""
     A = stiga.kron_sum_terms(pc.K, pc.M, pc.Wt, pc.Mt, pc.gamma, pc.nu)
     At = stiga.kron_sum_terms(K_tilde or pc.K, M_tilde or pc.M, pc.Wt,
                               pc.Mt if Mt_tilde is None else Mt_tilde, 1.0, 1.0)
-    return kron_sum_diagonal(A) / kron_sum_diagonal(At)
+    return kron_sum_diagonal(A, t_range) / kron_sum_diagonal(At, t_range)
 
 
 class Problem:

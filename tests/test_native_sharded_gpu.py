@@ -23,7 +23,8 @@ def run_ranks(world, case):
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "_native_sharded_worker.py"), case]
     out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
-    assert out.returncode == 0, (out.stdout[-2000:], out.stderr[-3000:])
+    errs = [ln for ln in out.stderr.splitlines() if "Error" in ln or "error" in ln][:20]
+    assert out.returncode == 0, ("\n".join(errs), out.stdout[-2000:], out.stderr[-3000:])
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     return json.loads(lines[0])
