@@ -734,6 +734,39 @@ stiga_kronsum_s* ks_build_spacetime(int d, const int* n, const double* const* K,
         }
         push(Wd, gamma);
         push(Mtd, nu);
+        // fused mat-vec: widened spatial bands and the time band columns (cuda/matvec_fused.cu)
+        int fp = 0;
+        for (int hb : h->hbw) fp = std::max(fp, hb);
+        fp = std::max(fp, 1);
+        if (fp <= gpu::kMaxFusedP && d <= 3 && (d < 2 || gpu::plane2_smem_bytes(n[0], fp, 1) <= 227 * 1024)) {
+            h->fp = fp;
+            const int W = 2 * fp + 1;
+            auto widened = [&](const DenseMatrix& F) {
+                const int m = static_cast<int>(F.rows);
+                std::vector<double> b(static_cast<size_t>(m) * W, 0.0);
+                for (int i = 0; i < m; ++i)
+                    for (int k = 0; k < W; ++k) {
+                        const int j = i + k - fp;
+                        if (j >= 0 && j < m) b[static_cast<size_t>(i) * W + k] = F(i, j);
+                    }
+                return b;
+            };
+            for (int l = 0; l < d; ++l) {
+                h->wband.emplace_back(new DBuf);
+                h->wband.back()->upload(widened(Md[l]));
+                h->wband.emplace_back(new DBuf);
+                h->wband.back()->upload(widened(Kd[l]));
+            }
+            auto columns = [&](const DenseMatrix& F, double c) {  // col[t' * W + (dd + fp)] = c F(t' + dd, t')
+                std::vector<double> col(static_cast<size_t>(n_t) * W, 0.0);
+                for (int tp = 0; tp < n_t; ++tp)
+                    for (int dd = -fp; dd <= fp; ++dd)
+                        if (tp + dd >= 0 && tp + dd < n_t) col[static_cast<size_t>(tp) * W + dd + fp] = c * F(tp + dd, tp);
+                return col;
+            };
+            h->tcol_w.upload(columns(Wd, gamma));
+            h->tcol_m.upload(columns(Mtd, nu));
+        }
         return h.release();
 }
 }  // namespace stiga

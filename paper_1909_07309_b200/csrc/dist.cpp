@@ -222,8 +222,11 @@ void kronsum_apply_sharded(stiga_kronsum_s& A, const double* x, double* y, cudaS
     const long long ntl = K.t_len[r];
     // 1. every neighbour finished reading the halos it got from the previous apply
     K.comm->barrier(st);
-    // 2. spatial halves of the local slab into the interior of the halo-extended buffers
-    A.apply_space_slab(ntl, x, K.ext_a.p + Ns * K.halo_lo, K.ext_b.p + Ns * K.halo_lo, st);
+    // 2. spatial halves of the local slab into the interior of the halo-extended buffers (fused path:
+    //    for d = 3 the mode-(0,1) halves; mode 2 then runs inside the time stage, halos included)
+    const bool fused = A.use_fused();
+    if (fused) A.fused_space(ntl, x, K.ext_a.p + Ns * K.halo_lo, K.ext_b.p + Ns * K.halo_lo, st);
+    else A.apply_space_slab(ntl, x, K.ext_a.p + Ns * K.halo_lo, K.ext_b.p + Ns * K.halo_lo, st);
     // 3. push the edge slices into the neighbours' halos (peer copies over NVLink)
     const size_t slab_bytes = sizeof(double) * static_cast<size_t>(Ns);
     if (K.prev_a) {  // my first slices -> previous rank's upper halo
@@ -242,6 +245,12 @@ void kronsum_apply_sharded(stiga_kronsum_s& A, const double* x, double* y, cudaS
     }
     // 4. the halos of this rank are complete once every rank passed the barrier
     K.comm->barrier(st);
+    if (fused) {
+        const int ti0 = static_cast<int>(K.t_off[r]) - K.halo_lo;
+        A.fused_time(ti0, K.halo_lo + static_cast<int>(ntl) + K.halo_hi, static_cast<int>(K.t_off[r]), static_cast<int>(ntl),
+                     K.ext_a.p, K.ext_b.p, y, st);
+        return;
+    }
     const int ia = A.physical ? 0 : 2 * d, ib = ia + 1;
     ck(gpu::launch_time_band_slab(Ns, nt, K.t_off[r], ntl, K.halo_lo, K.ext_a.p, K.ext_b.p, y, A.band(ia), A.band(ib),
                                   st),

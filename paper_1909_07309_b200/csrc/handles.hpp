@@ -17,6 +17,7 @@
 #include "common.hpp"
 #include "cuda/aux_kernels.cuh"
 #include "cuda/fd_kernels.cuh"
+#include "cuda/matvec_fused.cuh"
 #include "cuda/physical.cuh"
 #include "host/fdsetup.hpp"
 
@@ -600,6 +601,46 @@ struct stiga_kronsum_s {
     std::vector<int> hbw;
     // spacetime: per direction M_l, K_l bands, time gamma*W_t and nu*M_t bands
     DBuf t0, t1, t2, t3;  // scratch N_dof each
+    // fused mat-vec (cuda/matvec_fused.cu): bands widened to 2 fp + 1 taps per spatial direction
+    // (M_l, K_l rows) and the COLUMNS of gamma W_t, nu M_t; fp = max half-bandwidth (0 = not available)
+    int fp = 0;
+    std::vector<std::unique_ptr<DBuf>> wband;  // [M_1, K_1, ..., M_d, K_d]
+    DBuf tcol_w, tcol_m;
+    bool use_fused() const {
+        static const bool off = std::getenv("STIGA_MATVEC_PASSES") != nullptr;
+        return spacetime && fp > 0 && !off;
+    }
+    // fields the fused time stage consumes for a slab of nt_local slices: d <= 2 the spatial halves
+    // (a, b); d = 3 the mode-(0,1) halves a2, b2 (mode 2 runs inside the time stage)
+    void fused_space(long long nt_local, const double* x, double* a, double* b, cudaStream_t st) {
+        const int d = D - 1;
+        const gpu::Band none{};
+        if (d == 1) {
+            gpu::ModeGeom g;
+            g.L = 1;
+            g.n = g.m = dims[0];
+            g.ncols = nt_local;
+            ck(gpu::launch_banded_pass(g, x, nullptr, a, b, band(0), none, band(1), none, 0.0, st), "banded");
+            return;
+        }
+        const long long R = (d == 3 ? dims[2] : 1) * nt_local;
+        ck(gpu::launch_plane2(dims[0], dims[1], R, fp, x, a, b, wband[0]->p, wband[1]->p, wband[2]->p, wband[3]->p, st),
+           "fused mat-vec modes 0+1");
+    }
+    // y (slices [to0, to0+nto)) from the fields of the input slices [ti0, ti0+nti)
+    void fused_time(int ti0, int nti, int to0, int nto, const double* a, const double* b, double* y, cudaStream_t st) {
+        const int d = D - 1;
+        long long Ns = 1;
+        for (int l = 0; l < d; ++l) Ns *= dims[l];
+        if (d == 3) {
+            ck(gpu::launch_stream(true, static_cast<long long>(dims[0]) * dims[1], dims[2], ti0, nti, to0, nto, fp, a, b, y,
+                                  wband[4]->p, wband[5]->p, tcol_w.p, tcol_m.p, st),
+               "fused mat-vec mode 2 + time");
+        } else {
+            ck(gpu::launch_stream(false, Ns, 1, ti0, nti, to0, nto, fp, a, b, y, nullptr, nullptr, tcol_w.p, tcol_m.p, st),
+               "fused mat-vec time");
+        }
+    }
     // physical (geometry-mapped) system: stencil K_s, M_s on the device + time bands
     bool physical = false;
     gpu::PhysicalDesc pdesc;
@@ -672,6 +713,13 @@ struct stiga_kronsum_s {
             ck(gpu::launch_stencil_apply2(pdesc, Mst.p, Kst.p, x, t0.p, t1.p, dims[d], st), "stencil apply");
             ck(gpu::launch_banded_pass(geom(d), t0.p, t1.p, y, nullptr, band(0), band(1), none, none, 0.0, st),
                "time bands");
+            return;
+        }
+        if (use_fused()) {  // two kernels: modes 0+1 (plane tiles), [mode 2 +] time (streamed ring)
+            const int d = D - 1, nt = dims[d];
+            ensure_scratch(2);
+            fused_space(nt, x, t0.p, t1.p, st);
+            fused_time(0, nt, 0, nt, t0.p, t1.p, y, st);
             return;
         }
         if (spacetime) {
