@@ -738,7 +738,8 @@ stiga_kronsum_s* ks_build_spacetime(int d, const int* n, const double* const* K,
         int fp = 0;
         for (int hb : h->hbw) fp = std::max(fp, hb);
         fp = std::max(fp, 1);
-        if (fp <= gpu::kMaxFusedP && d <= 3 && (d < 2 || gpu::plane2_smem_bytes(n[0], fp, 1) <= 227 * 1024)) {
+        const bool plane_ok = d < 2 || (gpu::plane2_smem_bytes(n[0], fp) <= 227 * 1024 && (n[0] + 1) / 2 <= 256);
+        if (fp <= gpu::kMaxFusedP && d <= 3 && plane_ok) {
             h->fp = fp;
             const int W = 2 * fp + 1;
             auto widened = [&](const DenseMatrix& F) {

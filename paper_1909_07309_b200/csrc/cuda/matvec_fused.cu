@@ -43,206 +43,247 @@ __device__ __forceinline__ void cpa_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-constexpr int kTR = 32;  // tile rows of plane2_kernel (interior rows = kTR - 2P)
-constexpr int kR0 = 4;   // mode-0 outputs per thread (register window along i0)
+constexpr int kTR = 32;             // x rows per plane2 tile (outputs: the kTR - 2P interior rows)
+constexpr int kPlaneThreads = 256;  // 8 warps, two CTAs per SM where the tiles fit (n0 <= ~170)
+constexpr int kR1 = 6;              // mode-1 output rows per warp task (register window of kR1 + 2P rows)
 
-// smem pitch (in doubles) >= w, odd: 8-byte accesses of lanes at consecutive rows are conflict free
-__host__ __device__ inline int odd_pitch(int w) { return w | 1; }
+__host__ __device__ inline int even_up(int w) { return (w + 1) & ~1; }
 
-template <int P>
+// smem layout of plane2_kernel (doubles): x tile [kTR][xp], the mode-1 results a1 = M1 x, b1 = K1 x of the
+// B interior rows [B][ap] each (P zero columns on the left, >= P + 1 on the right, so mode 0 reads
+// padded windows), the tile's mode-1 coefficient rows [B][wp] for M1 and K1.
 struct Plane2Smem {
-    int xp, ap;  // pitches of the x tile (n0 + 2P zero-padded columns) and of the a, b tiles
-    int nbuf;    // x buffers (2 = next tile prefetched with cp.async)
+    int B, xp, ap, wp;
+    __host__ __device__ Plane2Smem(int n0, int P)
+        : B(kTR - 2 * P), xp(n0), ap(even_up(n0 + 2 * P + 1)), wp(even_up(2 * P + 1)) {}
     __host__ __device__ size_t x_elems() const { return static_cast<size_t>(kTR) * xp; }
-    __host__ __device__ size_t a_elems() const { return static_cast<size_t>(kTR) * ap; }
-    __host__ __device__ size_t bytes() const { return sizeof(double) * (nbuf * x_elems() + 2 * a_elems()); }
+    __host__ __device__ size_t a_elems() const { return static_cast<size_t>(B) * ap; }
+    __host__ __device__ size_t c_elems() const { return static_cast<size_t>(B) * wp; }
+    __host__ __device__ size_t bytes() const { return sizeof(double) * (x_elems() + 2 * a_elems() + 2 * c_elems()); }
 };
 
+// Modes 0 and 1 of the colex tensor (n0, n1, R): x -> a2 = (M1 (x) M0) x, b2 = (K1 (x) M0 + M1 (x) K0) x,
+// evaluated as mode 1 first (a1 = M1 x, b1 = K1 x on the interior rows: no halo recomputation), then
+// mode 0 (a2 = M0 a1, b2 = K0 a1 + M0 b1); Kronecker factors on distinct modes commute.
+//  stage 1 (mode 1): lane = column, warp task = kR1 consecutive output rows of a 32-column block with a
+//    register window of kR1 + 2P x rows; the coefficient rows (uniform per warp) are staged in smem.
+//  stage 2 (mode 0): thread = a fixed pair of columns i0 = 2 pi, 2 pi + 1 (their four coefficient rows stay
+//    in registers for the whole kernel) and rows g, g + G, ...; 16-byte window loads.
 template <int P>
-__host__ __device__ inline Plane2Smem<P> plane2_smem(int n0, int nbuf) {
-    Plane2Smem<P> s;
-    s.xp = odd_pitch(n0 + 2 * P);
-    s.ap = odd_pitch(n0);
-    s.nbuf = nbuf;
-    return s;
-}
-
-// Modes 0 and 1 of the colex tensor (n0, n1, R): x -> a2 = (M1 (x) M0) x, b2 = (K1 (x) M0 + M1 (x) K0) x.
-// Bands (widened to 2P+1): m0/k0 rows of mode 0 (n0 rows), m1/k1 rows of mode 1 (n1 rows).
-template <int P>
-__global__ void __launch_bounds__(256) plane2_kernel(int n0, int n1, long long R, const double* __restrict__ x,
-                                                     double* __restrict__ a2, double* __restrict__ b2,
-                                                     const double* __restrict__ m0, const double* __restrict__ k0,
-                                                     const double* __restrict__ m1, const double* __restrict__ k1,
-                                                     int nbuf) {
+__global__ void __launch_bounds__(kPlaneThreads, 2) plane2_kernel(int n0, int n1, long long R,
+                                                                  const double* __restrict__ x, double* __restrict__ a2,
+                                                                  double* __restrict__ b2,
+                                                                  const double* __restrict__ m0,
+                                                                  const double* __restrict__ k0,
+                                                                  const double* __restrict__ m1,
+                                                                  const double* __restrict__ k1) {
     constexpr int W = 2 * P + 1;
-    constexpr int B = kTR - 2 * P;      // interior (output) rows per tile
-    constexpr int R1 = (B + 1) / 2;     // mode-1 output rows per warp task
-    extern __shared__ double sm[];
-    const Plane2Smem<P> L = plane2_smem<P>(n0, nbuf);
-    double* xs[2] = {sm, sm + (nbuf > 1 ? L.x_elems() : 0)};
-    double* as = sm + nbuf * L.x_elems();
+    constexpr int B = kTR - 2 * P;
+    constexpr int WP = (W + 1) & ~1;
+    extern __shared__ __align__(16) double sm[];
+    const Plane2Smem L(n0, P);
+    double* xs = sm;
+    double* as = xs + L.x_elems();
     double* bs = as + L.a_elems();
+    double* cm = bs + L.a_elems();
+    double* ck = cm + L.c_elems();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const long long tiles_j = (n1 + B - 1) / B;
     const long long ntiles = tiles_j * R;
-
-    // zero the P pad columns of the x buffers once (the copies never touch them)
-    for (int e = threadIdx.x; e < nbuf * kTR * 2 * P; e += blockDim.x) {
-        const int bb = e / (kTR * 2 * P), rem = e - bb * kTR * 2 * P;
-        const int row = rem / (2 * P), c = rem - row * 2 * P;
-        xs[bb][row * L.xp + (c < P ? c : n0 + c)] = 0.0;
+    // stage-2 role and its coefficient rows (constant for the whole kernel)
+    const int NP = (n0 + 1) / 2, G = max(1, static_cast<int>(blockDim.x) / NP);
+    const int pi = threadIdx.x % NP, grp = threadIdx.x / NP;
+    const bool s2 = grp < G;
+    double cma[W], cmb[W], cka[W], ckb[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const int i0 = 2 * pi, i1 = 2 * pi + 1;
+        cma[k] = s2 ? __ldg(m0 + static_cast<long long>(i0) * W + k) : 0.0;
+        cka[k] = s2 ? __ldg(k0 + static_cast<long long>(i0) * W + k) : 0.0;
+        cmb[k] = (s2 && i1 < n0) ? __ldg(m0 + static_cast<long long>(i1) * W + k) : 0.0;
+        ckb[k] = (s2 && i1 < n0) ? __ldg(k0 + static_cast<long long>(i1) * W + k) : 0.0;
     }
-    // stage the x rows j0 - P .. j0 + B + P - 1 of tile `t` (zero rows outside [0, n1)) into buffer dst
-    auto issue = [&](long long t, double* dst) {
+    // zero the pad columns of the a1 / b1 tiles once (stage 1 writes only columns P .. P + n0 - 1)
+    const int padw = L.ap - n0;
+    for (int e = threadIdx.x; e < 2 * B * padw; e += blockDim.x) {
+        const int f = e / (B * padw), rem = e - f * B * padw;
+        const int row = rem / padw, c = rem - row * padw;
+        (f ? bs : as)[row * L.ap + (c < P ? c : n0 + c)] = 0.0;
+    }
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const long long r = t / tiles_j;
         const int j0 = static_cast<int>(t - r * tiles_j) * B;
-        const double* src = x + static_cast<long long>(n0) * n1 * r;
-        for (int e = threadIdx.x; e < kTR * n0; e += blockDim.x) {
-            const int row = e / n0, i0 = e - row * n0;
-            const int j = j0 - P + row;
-            double* d = dst + row * L.xp + P + i0;
-            if (j >= 0 && j < n1) cpa8(d, src + static_cast<long long>(n0) * j + i0);
-            else *d = 0.0;
-        }
-        cpa_commit();
-    };
-    long long t = blockIdx.x;
-    int cur = 0;
-    if (t < ntiles) issue(t, xs[0]);
-    for (; t < ntiles; t += gridDim.x) {
-        const long long tn = t + gridDim.x;
-        if (nbuf > 1 && tn < ntiles) {
-            issue(tn, xs[cur ^ 1]);
-            cpa_wait<1>();
-        } else {
-            cpa_wait<0>();
-        }
-        __syncthreads();
-        const double* X = xs[cur];
-        // ---- stage 1: mode 0 on all kTR rows; lane = row, warp = segments of kR0 consecutive i0 ----
+        // x rows j0 - P .. j0 + B + P - 1 (zero rows outside [0, n1)) and the tile's mode-1 coefficient rows
+        // (the tile's x rows are one contiguous chunk of the colex vector; smem pitch = n0)
         {
-            const int row = lane;
-            const int nseg = (n0 + kR0 - 1) / kR0;
-            for (int sg = warp; sg < nseg; sg += nwarp) {
-                const int i0s = sg * kR0;
-                double xw[kR0 + 2 * P];
-#pragma unroll
-                for (int k = 0; k < kR0 + 2 * P; ++k) {
-                    const int c = i0s + k;  // padded column (P pad on the left)
-                    xw[k] = c < n0 + 2 * P ? X[row * L.xp + c] : 0.0;
-                }
-#pragma unroll
-                for (int q = 0; q < kR0; ++q) {
-                    const int i0 = i0s + q;
-                    if (i0 >= n0) break;
-                    const double* mr = m0 + static_cast<long long>(i0) * W;
-                    const double* kr = k0 + static_cast<long long>(i0) * W;
-                    double sa = 0.0, sb = 0.0;
-#pragma unroll
-                    for (int k = 0; k < W; ++k) {
-                        sa = fma(__ldg(mr + k), xw[q + k], sa);
-                        sb = fma(__ldg(kr + k), xw[q + k], sb);
-                    }
-                    as[row * L.ap + i0] = sa;
-                    bs[row * L.ap + i0] = sb;
-                }
+            const int jlo = max(j0 - P, 0), jhi = min(j0 + B + P, n1);  // rows that exist
+            const int e0 = (jlo - (j0 - P)) * n0, e1 = (jhi - (j0 - P)) * n0;
+            const double* src = x + static_cast<long long>(n0) * (n1 * r + jlo) - e0;
+            for (int e = threadIdx.x; e < kTR * n0; e += blockDim.x) {
+                if (e >= e0 && e < e1) cpa8(xs + e, src + e);
+                else xs[e] = 0.0;
             }
+            cpa_commit();
         }
+        for (int e = threadIdx.x; e < B * WP; e += blockDim.x) {
+            const int q = e / WP, k = e - q * WP;
+            const int j = j0 + q;
+            const bool ok = k < W && j < n1;
+            cm[q * WP + k] = ok ? __ldg(m1 + static_cast<long long>(j) * W + k) : 0.0;
+            ck[q * WP + k] = ok ? __ldg(k1 + static_cast<long long>(j) * W + k) : 0.0;
+        }
+        cpa_wait<0>();
         __syncthreads();
-        // ---- stage 2: mode 1 on the B interior rows; lane = column, task = (32-column block, row group) --
+        // ---- stage 1: mode 1 on the B interior rows ----
         {
-            const long long r = t / tiles_j;
-            const int j0 = static_cast<int>(t - r * tiles_j) * B;
             const int ncb = (n0 + 31) / 32;
-            const int ngroups = (B + R1 - 1) / R1;
+            constexpr int ngroups = (B + kR1 - 1) / kR1;
             for (int task = warp; task < ncb * ngroups; task += nwarp) {
                 const int cb = task / ngroups, g = task - cb * ngroups;
-                const int col = cb * 32 + lane;
-                const int rs = g * R1;  // first interior row of the group (tile row P + rs)
-                if (col < n0) {
-                    double aw[R1 + 2 * P], bw[R1 + 2 * P];
+                const int col = min(cb * 32 + lane, n0 - 1);  // lanes past n0 recompute the last column
+                const int rs = g * kR1;                       // first output row of the group (tile row P + rs)
+                double xw[kR1 + 2 * P];
 #pragma unroll
-                    for (int k = 0; k < R1 + 2 * P; ++k) {
-                        const int row = rs + k;  // tile row of output rs - P + k ... (halo included)
-                        aw[k] = row < kTR ? as[row * L.ap + col] : 0.0;
-                        bw[k] = row < kTR ? bs[row * L.ap + col] : 0.0;
-                    }
-                    double* ya = a2 + static_cast<long long>(n0) * n1 * r;
-                    double* yb = b2 + static_cast<long long>(n0) * n1 * r;
+                for (int k = 0; k < kR1 + 2 * P; ++k) xw[k] = xs[min(rs + k, kTR - 1) * L.xp + col];
 #pragma unroll
-                    for (int q = 0; q < R1; ++q) {
-                        const int j = j0 + rs + q;
-                        if (rs + q >= B || j >= n1) break;
-                        const double* mr = m1 + static_cast<long long>(j) * W;
-                        const double* kr = k1 + static_cast<long long>(j) * W;
-                        double sa = 0.0, sb = 0.0;
+                for (int q = 0; q < kR1; ++q) {
+                    if (rs + q >= B) break;
+                    const double2* mr = reinterpret_cast<const double2*>(cm + (rs + q) * WP);
+                    const double2* kr = reinterpret_cast<const double2*>(ck + (rs + q) * WP);
+                    double sa = 0.0, sb = 0.0;
 #pragma unroll
-                        for (int k = 0; k < W; ++k) {
-                            const double mk = __ldg(mr + k), kk = __ldg(kr + k);
-                            sa = fma(mk, aw[q + k], sa);
-                            sb = fma(kk, aw[q + k], sb);
-                            sb = fma(mk, bw[q + k], sb);
+                    for (int k2 = 0; k2 < WP / 2; ++k2) {
+                        const double2 mk = mr[k2], kk = kr[k2];
+                        sa = fma(mk.x, xw[q + 2 * k2], sa);
+                        sb = fma(kk.x, xw[q + 2 * k2], sb);
+                        if (2 * k2 + 1 < W) {
+                            sa = fma(mk.y, xw[q + 2 * k2 + 1], sa);
+                            sb = fma(kk.y, xw[q + 2 * k2 + 1], sb);
                         }
-                        ya[static_cast<long long>(n0) * j + col] = sa;
-                        yb[static_cast<long long>(n0) * j + col] = sb;
                     }
+                    as[(rs + q) * L.ap + P + col] = sa;
+                    bs[(rs + q) * L.ap + P + col] = sb;
                 }
             }
         }
-        __syncthreads();  // a/b tiles and x buffer `cur` are rewritten by the next tile
-        if (nbuf == 1 && tn < ntiles) issue(tn, xs[0]);
-        cur ^= (nbuf > 1 ? 1 : 0);
+        __syncthreads();
+        // ---- stage 2: mode 0 on the B interior rows -> HBM ----
+        if (s2) {
+            double* ya = a2 + static_cast<long long>(n0) * n1 * r;
+            double* yb = b2 + static_cast<long long>(n0) * n1 * r;
+            for (int row = grp; row < B; row += G) {
+                const int j = j0 + row;
+                if (j >= n1) break;
+                const double2* ar = reinterpret_cast<const double2*>(as + row * L.ap + 2 * pi);
+                const double2* br = reinterpret_cast<const double2*>(bs + row * L.ap + 2 * pi);
+                double aw[W + 1], bw[W + 1];
+#pragma unroll
+                for (int k = 0; k < (W + 1) / 2; ++k) {
+                    const double2 va = ar[k], vb = br[k];
+                    aw[2 * k] = va.x;
+                    aw[2 * k + 1] = va.y;
+                    bw[2 * k] = vb.x;
+                    bw[2 * k + 1] = vb.y;
+                }
+                double sa0 = 0.0, sb0 = 0.0, sa1 = 0.0, sb1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    sa0 = fma(cma[k], aw[k], sa0);
+                    sb0 = fma(cka[k], aw[k], sb0);
+                    sb0 = fma(cma[k], bw[k], sb0);
+                    sa1 = fma(cmb[k], aw[k + 1], sa1);
+                    sb1 = fma(ckb[k], aw[k + 1], sb1);
+                    sb1 = fma(cmb[k], bw[k + 1], sb1);
+                }
+                const long long o = static_cast<long long>(n0) * j + 2 * pi;
+                ya[o] = sa0;
+                yb[o] = sb0;
+                if (2 * pi + 1 < n0) {
+                    ya[o + 1] = sa1;
+                    yb[o + 1] = sb1;
+                }
+            }
+        }
+        __syncthreads();  // x, a1/b1 tiles and coefficient rows are rewritten by the next tile
     }
 }
 
 // ---- stream kernel ----------------------------------------------------------------------------
-constexpr int kSQ = 4;    // output rows (mode 2) or columns (time only) per thread
+// Threads and outputs per thread: mode 2 + time: 8 warps x 2 rows (a 16-row tile; the 2 P + 1 accumulators,
+// the mode-2 coefficient rows and the row window live in registers, up to 255 of them); time only: 256
+// columns per tile (one per thread), several CTAs per SM.
+__host__ __device__ constexpr int st_threads(bool mode2) { return 256; }
+__host__ __device__ constexpr int st_sq(bool mode2) { return mode2 ? 2 : 1; }
 constexpr int kNS = 3;    // cp.async ring depth over time slices
 
+struct StreamSmem {
+    int rows_in, cols, cp, wp, nt;
+    __host__ __device__ StreamSmem(bool mode2, int P, int nt_)
+        : rows_in(mode2 ? (st_threads(true) / 32) * st_sq(true) + 2 * P : 1),
+          cols(mode2 ? 32 : st_threads(false) * st_sq(false)), cp(mode2 ? 33 : st_threads(false) * st_sq(false)),
+          wp(even_up(2 * P + 1)), nt(nt_) {}
+    __host__ __device__ size_t stage() const { return 2 * static_cast<size_t>(rows_in) * cp; }
+    __host__ __device__ size_t ring() const { return kNS * stage(); }
+    __host__ __device__ size_t tcoef() const { return 2 * static_cast<size_t>(nt) * wp; }   // time columns
+    __host__ __device__ size_t bytes() const { return sizeof(double) * (ring() + tcoef()); }
+};
+
 // MODE2 = true: fields (L, n2, T) colex, tile = 32 consecutive l x 32 rows i2 (8 warps x kSQ rows).
-// MODE2 = false: fields (L, T) (n2 = 1), tile = 256 * kSQ consecutive l (thread = kSQ columns, stride 256).
+// MODE2 = false: fields (L, T) (n2 = 1), tile = kST * kSQ consecutive l (thread = kSQ columns, stride kST).
 // Inputs a, b hold the time slices [ti0, ti0 + nti) (global indices), outputs y the slices
-// [to0, to0 + nto) ⊂ [ti0, ti0 + nti) ... (the caller passes base pointers of those slices).
-// cw / cm: band COLUMNS of gamma W_t and nu M_t: cw[t' * W + (d + P)] = gamma W_t(t' + d, t') (0 outside).
+// [to0, to0 + nto) inside them (the caller passes base pointers of those slices).
+// cw / cm: band COLUMNS of gamma W_t and nu M_t, cw[t' * W + (d + P)] = gamma W_t(t' + d, t') (0 outside);
+// nt = rows of the time factors.
 template <int P, bool MODE2>
-__global__ void __launch_bounds__(256) stream_kernel(long long Lc, int n2, int ti0, int nti, int to0, int nto,
+__global__ void __launch_bounds__(st_threads(MODE2), 1) stream_kernel(long long Lc, int n2, int nt, int ti0, int nti, int to0, int nto,
                                                      const double* __restrict__ a, const double* __restrict__ b,
                                                      double* __restrict__ y, const double* __restrict__ m2,
                                                      const double* __restrict__ k2, const double* __restrict__ cw,
                                                      const double* __restrict__ cm) {
     constexpr int W = 2 * P + 1;
-    constexpr int ROWS_IN = MODE2 ? (8 * kSQ + 2 * P) : 1;   // staged rows per slice
-    constexpr int COLS = MODE2 ? 32 : 256 * kSQ;             // staged columns per row
-    constexpr int CP = MODE2 ? 33 : COLS;                    // column pitch
-    constexpr int STAGE = 2 * ROWS_IN * CP;                  // a then b
-    extern __shared__ double sm[];
+    constexpr int kST = st_threads(MODE2), kSQ = st_sq(MODE2);
+    constexpr int RPT = (kST / 32) * kSQ;  // mode-2 output rows per tile
+    extern __shared__ __align__(16) double sm[];
+    const StreamSmem S(MODE2, P, nt);
+    const int ROWS_IN = S.rows_in, COLS = S.cols, CP = S.cp, WP = S.wp;
+    const size_t STAGE = S.stage();
+    double* tcw = sm + S.ring();
+    double* tcm = tcw + static_cast<size_t>(nt) * WP;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long slice = Lc * n2;  // entries per time slice
     const long long ncolb = (Lc + COLS - 1) / COLS;
-    const int nrowb = MODE2 ? (n2 + 8 * kSQ - 1) / (8 * kSQ) : 1;
+    const int nrowb = MODE2 ? (n2 + RPT - 1) / RPT : 1;
     const long long ntiles = ncolb * nrowb;
     const int te = ti0 + nti + P;  // streaming end (virtual zero slices finalize the last outputs)
+    // time band columns -> smem (padded to WP), once
+    for (int e = threadIdx.x; e < nt * WP; e += blockDim.x) {
+        const int tp = e / WP, k = e - tp * WP;
+        tcw[e] = k < W ? __ldg(cw + static_cast<long long>(tp) * W + k) : 0.0;
+        tcm[e] = k < W ? __ldg(cm + static_cast<long long>(tp) * W + k) : 0.0;
+    }
 
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long cb = tile % ncolb;
         const int rb = static_cast<int>(tile / ncolb);
         const long long l0 = cb * COLS;
-        const int r0 = rb * 8 * kSQ;  // first output row (MODE2)
-        auto issue = [&](int tp) {   // stage slice tp (global index) of a and b
+        const int r0 = rb * RPT;  // first output row (MODE2)
+        // staged elements of this thread: e = tid + kST k (row = e / COLS with COLS a power of two)
+        constexpr int kLogCols = MODE2 ? 5 : 8;  // COLS = 32 (mode 2) or kST * kSQ = 256 (time only)
+        static_assert((1 << kLogCols) == (MODE2 ? 32 : kST * kSQ), "COLS must be a power of two");
+        auto issue = [&](int tp) {  // stage slice tp (global index) of a and b
             if (tp < ti0 + nti) {
-                double* st = sm + (tp - ti0) % kNS * STAGE;
-                const long long sbase = static_cast<long long>(tp - ti0) * slice;
-                for (int e = threadIdx.x; e < ROWS_IN * COLS; e += blockDim.x) {
-                    const int row = e / COLS, c = e - row * COLS;
-                    const long long l = l0 + c;
+                double* st = sm + static_cast<size_t>((tp - ti0) % kNS) * STAGE;
+                const double* as_ = a + static_cast<long long>(tp - ti0) * slice + l0;
+                const double* bs_ = b + static_cast<long long>(tp - ti0) * slice + l0;
+                for (int e = threadIdx.x; e < ROWS_IN * COLS; e += kST) {
+                    const int row = e >> kLogCols, c = e & (COLS - 1);
                     const int i2 = MODE2 ? r0 - P + row : 0;
                     double* da = st + row * CP + c;
                     double* db = da + ROWS_IN * CP;
-                    if (l < Lc && i2 >= 0 && i2 < n2) {
-                        const long long off = sbase + l + Lc * i2;
-                        cpa8(da, a + off);
-                        cpa8(db, b + off);
+                    if (l0 + c < Lc && i2 >= 0 && i2 < n2) {
+                        const long long off = c + Lc * i2;
+                        cpa8(da, as_ + off);
+                        cpa8(db, bs_ + off);
                     } else {
                         *da = 0.0;
                         *db = 0.0;
@@ -251,24 +292,37 @@ __global__ void __launch_bounds__(256) stream_kernel(long long Lc, int n2, int t
             }
             cpa_commit();
         };
+        __syncthreads();  // previous tile done with the ring
+        // mode-2 coefficient rows of this thread's output rows (fixed for the tile) in registers
+        double c2m[MODE2 ? kSQ : 1][W], c2k[MODE2 ? kSQ : 1][W];
+        if (MODE2) {
+#pragma unroll
+            for (int q = 0; q < kSQ; ++q) {
+                const int i2 = min(r0 + warp * kSQ + q, n2 - 1);  // rows past n2 are computed, not stored
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    c2m[q][k] = __ldg(m2 + static_cast<long long>(i2) * W + k);
+                    c2k[q][k] = __ldg(k2 + static_cast<long long>(i2) * W + k);
+                }
+            }
+        }
         double acc[kSQ][W];
 #pragma unroll
         for (int q = 0; q < kSQ; ++q)
 #pragma unroll
             for (int s = 0; s < W; ++s) acc[q][s] = 0.0;
-        __syncthreads();  // previous tile done with the ring
         for (int k = 0; k < kNS - 1; ++k) issue(ti0 + k);
-        for (int base = ti0; base < te; base += W) {
-#pragma unroll
-            for (int u = 0; u < W; ++u) {
-                const int tp = base + u;
-                if (tp >= te) break;
+        // acc[q][k] accumulates output t = tp - P + k; after step tp, acc[q][0] (t = tp - P) is complete
+        // and the ring shifts by one (register moves, no dynamic indexing)
+        {
+#pragma unroll 1
+            for (int tp = ti0; tp < te; ++tp) {
                 issue(tp + kNS - 1);
                 cpa_wait<kNS - 1>();
                 __syncthreads();
-                double v3a[kSQ], v3b[kSQ];
                 if (tp < ti0 + nti) {
-                    const double* st = sm + (tp - ti0) % kNS * STAGE;
+                    double v3a[kSQ], v3b[kSQ];
+                    const double* st = sm + static_cast<size_t>((tp - ti0) % kNS) * STAGE;
                     if (MODE2) {  // mode 2 on rows r0 + warp*kSQ + q, column lane
                         const int rw = warp * kSQ;
                         double aw[kSQ + 2 * P], bw[kSQ + 2 * P];
@@ -279,16 +333,12 @@ __global__ void __launch_bounds__(256) stream_kernel(long long Lc, int n2, int t
                         }
 #pragma unroll
                         for (int q = 0; q < kSQ; ++q) {
-                            const int i2 = min(r0 + rw + q, n2 - 1);  // rows past n2 are computed, not stored
-                            const double* mr = m2 + static_cast<long long>(i2) * W;
-                            const double* kr = k2 + static_cast<long long>(i2) * W;
                             double sa = 0.0, sb = 0.0;
 #pragma unroll
                             for (int k = 0; k < W; ++k) {
-                                const double mk = __ldg(mr + k), kk = __ldg(kr + k);
-                                sa = fma(mk, aw[q + k], sa);
-                                sb = fma(kk, aw[q + k], sb);
-                                sb = fma(mk, bw[q + k], sb);
+                                sa = fma(c2m[q][k], aw[q + k], sa);
+                                sb = fma(c2k[q][k], aw[q + k], sb);
+                                sb = fma(c2m[q][k], bw[q + k], sb);
                             }
                             v3a[q] = sa;
                             v3b[q] = sb;
@@ -296,27 +346,32 @@ __global__ void __launch_bounds__(256) stream_kernel(long long Lc, int n2, int t
                     } else {
 #pragma unroll
                         for (int q = 0; q < kSQ; ++q) {
-                            v3a[q] = st[threadIdx.x + 256 * q];
-                            v3b[q] = st[CP + threadIdx.x + 256 * q];
+                            v3a[q] = st[threadIdx.x + kST * q];
+                            v3b[q] = st[CP + threadIdx.x + kST * q];
                         }
                     }
                     // time: output t = tp + dd receives cw(tp)[dd + P] a3 + cm(tp)[dd + P] b3
-                    const double* cwr = cw + static_cast<long long>(tp) * W;
-                    const double* cmr = cm + static_cast<long long>(tp) * W;
+                    const double2* cwr = reinterpret_cast<const double2*>(tcw + static_cast<size_t>(tp) * WP);
+                    const double2* cmr = reinterpret_cast<const double2*>(tcm + static_cast<size_t>(tp) * WP);
 #pragma unroll
-                    for (int dd = -P; dd <= P; ++dd) {
-                        const double w = __ldg(cwr + dd + P), m = __ldg(cmr + dd + P);
-                        constexpr int dummy = 0;
-                        (void)dummy;
-                        const int s = ((u + dd) % W + W) % W;
+                    for (int k2 = 0; k2 < (W + 1) / 2; ++k2) {
+                        const double2 w2 = cwr[k2], m2v = cmr[k2];
 #pragma unroll
-                        for (int q = 0; q < kSQ; ++q) acc[q][s] = fma(m, v3b[q], fma(w, v3a[q], acc[q][s]));
+                        for (int h = 0; h < 2; ++h) {
+                            const int kk = 2 * k2 + h;  // dd = kk - P
+                            if (kk < W) {
+                                const double w = h ? w2.y : w2.x, m = h ? m2v.y : m2v.x;
+                                // output t = tp + kk - P sits in acc[.][kk]
+#pragma unroll
+                                for (int q = 0; q < kSQ; ++q) acc[q][kk] = fma(m, v3b[q], fma(w, v3a[q], acc[q][kk]));
+                            }
+                        }
                     }
                 }
                 // output t = tp - P is complete
                 {
                     const int tdone = tp - P;
-                    const int s = ((u - P) % W + W) % W;
+                    constexpr int s = 0;
                     if (tdone >= to0 && tdone < to0 + nto) {
                         double* yt = y + static_cast<long long>(tdone - to0) * slice;
 #pragma unroll
@@ -326,13 +381,17 @@ __global__ void __launch_bounds__(256) stream_kernel(long long Lc, int n2, int t
                                 const long long l = l0 + lane;
                                 if (i2 < n2 && l < Lc) yt[l + Lc * i2] = acc[q][s];
                             } else {
-                                const long long l = l0 + threadIdx.x + 256 * q;
+                                const long long l = l0 + threadIdx.x + kST * q;
                                 if (l < Lc) yt[l] = acc[q][s];
                             }
                         }
                     }
 #pragma unroll
-                    for (int q = 0; q < kSQ; ++q) acc[q][s] = 0.0;
+                    for (int q = 0; q < kSQ; ++q) {
+#pragma unroll
+                        for (int k = 0; k + 1 < W; ++k) acc[q][k] = acc[q][k + 1];
+                        acc[q][W - 1] = 0.0;
+                    }
                 }
                 __syncthreads();  // stage (tp - ti0) % kNS is refilled by the next iteration's issue
             }
@@ -345,30 +404,22 @@ __global__ void __launch_bounds__(256) stream_kernel(long long Lc, int n2, int t
 
 // ---- host launchers ---------------------------------------------------------------------------
 
-size_t plane2_smem_bytes(int n0, int P, int nbuf) {
-    const size_t xp = odd_pitch(n0 + 2 * P), ap = odd_pitch(n0);
-    return sizeof(double) * (nbuf * kTR * xp + 2 * kTR * ap);
-}
+size_t plane2_smem_bytes(int n0, int P) { return Plane2Smem(n0, P).bytes(); }
 
 cudaError_t launch_plane2(int n0, int n1, long long R, int P, const double* x, double* a2, double* b2,
                           const double* m0, const double* k0, const double* m1, const double* k1, cudaStream_t st) {
     if (R <= 0 || n0 <= 0 || n1 <= 0) return cudaSuccess;
-    if (P < 1 || P > kMaxFusedP || kTR - 2 * P < 2) return cudaErrorInvalidValue;
-    int nbuf = 2;
-    size_t sm = plane2_smem_bytes(n0, P, nbuf);
-    if (sm > 227 * 1024) {
-        nbuf = 1;
-        sm = plane2_smem_bytes(n0, P, nbuf);
-    }
+    if (P < 1 || P > kMaxFusedP || kTR - 2 * P < 2 || (n0 + 1) / 2 > kPlaneThreads) return cudaErrorInvalidValue;
+    const size_t sm = plane2_smem_bytes(n0, P);
     if (sm > 227 * 1024) return cudaErrorInvalidValue;
     const int B = kTR - 2 * P;
     const long long ntiles = (n1 + B - 1) / B * R;
     const int per_sm = std::max(1, static_cast<int>((227 * 1024) / (sm + 1024)));
-    const unsigned grid = static_cast<unsigned>(std::min<long long>(ntiles, 148LL * std::min(per_sm, 4)));
+    const unsigned grid = static_cast<unsigned>(std::min<long long>(ntiles, 148LL * std::min(per_sm, 2)));
 #define STIGA_P2(PP)                                                                                                 \
     case PP:                                                                                                         \
         cudaFuncSetAttribute(plane2_kernel<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)); \
-        plane2_kernel<PP><<<grid, 256, sm, st>>>(n0, n1, R, x, a2, b2, m0, k0, m1, k1, nbuf);                        \
+        plane2_kernel<PP><<<grid, kPlaneThreads, sm, st>>>(n0, n1, R, x, a2, b2, m0, k0, m1, k1);                    \
         break;
     switch (P) {
         STIGA_P2(1)
@@ -383,27 +434,29 @@ cudaError_t launch_plane2(int n0, int n1, long long R, int P, const double* x, d
     return cudaGetLastError();
 }
 
-cudaError_t launch_stream(bool mode2, long long Lc, int n2, int ti0, int nti, int to0, int nto, int P, const double* a,
-                          const double* b, double* y, const double* m2, const double* k2, const double* cw,
-                          const double* cm, cudaStream_t st) {
+cudaError_t launch_stream(bool mode2, long long Lc, int n2, int nt, int ti0, int nti, int to0, int nto, int P,
+                          const double* a, const double* b, double* y, const double* m2, const double* k2,
+                          const double* cw, const double* cm, cudaStream_t st) {
     if (Lc <= 0 || nti <= 0 || nto <= 0) return cudaSuccess;
-    if (P < 1 || P > kMaxFusedP || to0 < ti0 || to0 + nto > ti0 + nti) return cudaErrorInvalidValue;
-    const int rows_in = mode2 ? 8 * kSQ + 2 * P : 1;
-    const int cp = mode2 ? 33 : 256 * kSQ;
-    const size_t sm = sizeof(double) * kNS * 2 * static_cast<size_t>(rows_in) * cp;
-    const long long cols = mode2 ? 32 : 256 * kSQ;
-    const long long ntiles = (Lc + cols - 1) / cols * (mode2 ? (n2 + 8 * kSQ - 1) / (8 * kSQ) : 1);
-    const unsigned grid = static_cast<unsigned>(std::min<long long>(ntiles, 148LL * 4));
+    if (P < 1 || P > kMaxFusedP || to0 < ti0 || to0 + nto > ti0 + nti || ti0 < 0 || ti0 + nti > nt)
+        return cudaErrorInvalidValue;
+    const StreamSmem S(mode2, P, nt);
+    const size_t sm = S.bytes();
+    if (sm > 227 * 1024) return cudaErrorInvalidValue;
+    const int rpt = (st_threads(true) / 32) * st_sq(true);
+    const long long ntiles = (Lc + S.cols - 1) / S.cols * (mode2 ? (n2 + rpt - 1) / rpt : 1);
+    const int per_sm = std::max(1, std::min(4, static_cast<int>((227 * 1024) / (sm + 1024))));
+    const unsigned grid = static_cast<unsigned>(std::min<long long>(ntiles, 148LL * per_sm));
 #define STIGA_ST(PP)                                                                                                  \
     case PP:                                                                                                          \
         if (mode2) {                                                                                                  \
             cudaFuncSetAttribute(stream_kernel<PP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                  static_cast<int>(sm));                                                              \
-            stream_kernel<PP, true><<<grid, 256, sm, st>>>(Lc, n2, ti0, nti, to0, nto, a, b, y, m2, k2, cw, cm);     \
+            stream_kernel<PP, true><<<grid, st_threads(true), sm, st>>>(Lc, n2, nt, ti0, nti, to0, nto, a, b, y, m2, k2, cw, cm);  \
         } else {                                                                                                      \
             cudaFuncSetAttribute(stream_kernel<PP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
                                  static_cast<int>(sm));                                                              \
-            stream_kernel<PP, false><<<grid, 256, sm, st>>>(Lc, 1, ti0, nti, to0, nto, a, b, y, m2, k2, cw, cm);     \
+            stream_kernel<PP, false><<<grid, st_threads(false), sm, st>>>(Lc, 1, nt, ti0, nti, to0, nto, a, b, y, m2, k2, cw, cm);  \
         }                                                                                                             \
         break;
     switch (P) {

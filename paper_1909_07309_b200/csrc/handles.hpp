@@ -633,11 +633,11 @@ struct stiga_kronsum_s {
         long long Ns = 1;
         for (int l = 0; l < d; ++l) Ns *= dims[l];
         if (d == 3) {
-            ck(gpu::launch_stream(true, static_cast<long long>(dims[0]) * dims[1], dims[2], ti0, nti, to0, nto, fp, a, b, y,
+            ck(gpu::launch_stream(true, static_cast<long long>(dims[0]) * dims[1], dims[2], dims[d], ti0, nti, to0, nto, fp, a, b, y,
                                   wband[4]->p, wband[5]->p, tcol_w.p, tcol_m.p, st),
                "fused mat-vec mode 2 + time");
         } else {
-            ck(gpu::launch_stream(false, Ns, 1, ti0, nti, to0, nto, fp, a, b, y, nullptr, nullptr, tcol_w.p, tcol_m.p, st),
+            ck(gpu::launch_stream(false, Ns, 1, dims[d], ti0, nti, to0, nto, fp, a, b, y, nullptr, nullptr, tcol_w.p, tcol_m.p, st),
                "fused mat-vec time");
         }
     }
