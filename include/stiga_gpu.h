@@ -317,6 +317,28 @@ int stiga_gmres_op(long long n, stiga_linop_fn A, void* A_ctx, stiga_linop_fn P,
                    const double* d_b, double* d_x, const stiga_gmres_options* opts, stiga_gmres_report* report,
                    void* stream);
 
+/* ---- space-time system glue (solver.cpp:34-155, assembly.cpp:413-504, problems.cpp:305-402) ---- */
+
+/* ProblemSpec fields (problems.hpp:25-37): d, T, whether the problem carries an analytic source term
+   and exact solution (the identity-*, quarter-annulus-2d and separable-nu-2d manufactured problems;
+   deformed-cube-3d has none), and the constants gamma0, nu0.  Any output may be NULL. */
+int stiga_problem_info(stiga_problem_t P, int* d, double* T, int* has_rhs, int* has_exact, double* gamma0,
+                       double* nu0);
+/* SpaceTimeSystem's gamma_mean_ / nu_mean_ (solver.cpp:82-112), the constants of
+   make_parametric_preconditioner (solver.cpp:122-125); host quadrature with p + 1 Gauss points. */
+int stiga_system_means(stiga_problem_t P, int p, int n_el, double* gamma_mean, double* nu_mean);
+/* b_ = assemble_rhs(f / gamma_t, T, spatial spaces, time space, geometry, points_per_element)
+   (solver.cpp:72-76 with points_per_element = p + 1; assembly.cpp:413-504) into the device vector
+   d_b (N_dof, colex, time slowest), sum-factorized on the device.  Returns STIGA_INVALID_ARGUMENT for
+   a problem without a source term and STIGA_NUMERICAL for a non-positive Jacobian. Synchronous. */
+int stiga_assemble_rhs(stiga_problem_t P, int p, int n_el, int points_per_element, int device, double* d_b,
+                       void* stream);
+/* compute_errors(u_h, problem, points_per_element) (problems.cpp:305-402) for the device coefficient
+   vector d_coeffs (N_dof) of the degree-p / n_el discretisation: relative L2(0,T;L2) error and the
+   relative X-norm upper bound.  STIGA_INVALID_ARGUMENT without an exact solution. Synchronous. */
+int stiga_compute_errors(stiga_problem_t P, int p, int n_el, const double* d_coeffs, int points_per_element,
+                         int device, double* l2l2, double* x_upper);
+
 /* ---- measurement helpers ---------------------------------------------------------------- */
 
 /* Sustained FP64 DMMA (m8n8k4) throughput of the device in TFLOP/s over ~`ms` milliseconds. */

@@ -68,6 +68,10 @@ SIGNATURES = {
     "stiga_problem_eval_geometry": (_c_int, [_vp, _pd, _pd, _pd]),
     "stiga_problem_eval_fields": (_c_int, [_vp, _pd, _pd, _pd]),
     "stiga_geometry_preconditioner_pieces": (_c_int, [_vp, _c_int, _c_int, _pd, _pd, _pd, _pd, _pd, _pd, _pd, _pd, _pi]),
+    "stiga_problem_info": (_c_int, [_vp, _pi, _pd, _pi, _pi, _pd, _pd]),
+    "stiga_system_means": (_c_int, [_vp, _c_int, _c_int, _pd, _pd]),
+    "stiga_assemble_rhs": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
+    "stiga_compute_errors": (_c_int, [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _pd, _pd]),
     "stiga_fd_setup": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl, _pd, _c_ll, _c_int,
                                 ctypes.POINTER(_vp)]),
     "stiga_fd_destroy": (_c_int, [_vp]),

@@ -122,10 +122,6 @@ int stiga_assemble_univariate(int p, int n_el, int kind, int q, int deriv_row, i
     });
 }
 
-struct stiga_problem_s {
-    ProblemSpec spec;
-};
-
 int stiga_problem_create(const char* id, stiga_problem_t* out) {
     return guarded([&] {
         require(id && out, "make_problem: null argument");

@@ -20,8 +20,14 @@
 #include "cuda/matvec_fused.cuh"
 #include "cuda/physical.cuh"
 #include "host/fdsetup.hpp"
+#include "host/geometry.hpp"
 
 struct stiga_comm_s;  // dist.cpp: NCCL or host-callback communicator of one rank
+
+// make_problem(id) result behind stiga_problem_t (capi.cpp, system.cpp).
+struct stiga_problem_s {
+    stiga::ProblemSpec spec;
+};
 
 namespace stiga {
 // Balanced contiguous partition of range(n) over `world` parts (the first n % world get +1).

@@ -533,6 +533,50 @@ void problem_field_kinds(const ProblemSpec& prob, int& nu_kind, int& gamma_kind)
     }
 }
 
+int problem_source_kind(const ProblemSpec& prob) {
+    if (prob.name.rfind("identity-", 0) == 0) return 1;
+    if (prob.name == "quarter-annulus-2d") return 2;
+    if (prob.name == "separable-nu-2d") return 3;
+    return 0;  // deformed-cube-3d: BASELINE config 4 runs on a seeded RHS
+}
+
+void system_means(const ProblemSpec& prob, int p, int n_el, double& gamma_mean, double& nu_mean) {
+    const int d = prob.d, q = p + 1;
+    const double T = prob.T;
+    std::vector<QuadratureRule> rules;
+    std::vector<int> npts(d);
+    for (int l = 0; l < d; ++l) {
+        rules.push_back(gauss_rule(SplineSpace1D::spatial(p, n_el).knot_vector(), q));
+        npts[l] = rules[l].num_points();
+    }
+    double vol = 0.0, g_int = 0.0, n_int = 0.0;
+    std::vector<int> idx(d, 0);
+    double eta[3], x[3], J[9];
+    do {
+        double w = 1.0;
+        for (int l = 0; l < d; ++l) {
+            eta[l] = rules[l].nodes[idx[l]];
+            w *= rules[l].weights[idx[l]];
+        }
+        prob.geometry.jacobian(eta, J);
+        const double det = det_small(J, d);
+        prob.geometry.value(eta, x);
+        vol += w * det;
+        g_int += w * det * (prob.gamma_s ? prob.gamma_s(x) : 1.0);
+        n_int += w * det * (prob.nu_s ? prob.nu_s(x) : 1.0);
+    } while (advance(idx, npts));
+    const QuadratureRule tquad = gauss_rule(SplineSpace1D::temporal(p, n_el).knot_vector(), q);
+    double t_mean = 0.0;
+    for (int qt = 0; qt < tquad.num_points(); ++qt) {
+        const double tau = tquad.nodes[qt];
+        const double nt = prob.nu_t ? prob.nu_t(T * tau) : 1.0;
+        const double gt = prob.gamma_t ? prob.gamma_t(T * tau) : 1.0;
+        t_mean += tquad.weights[qt] * (nt / gt);
+    }
+    gamma_mean = g_int / vol;
+    nu_mean = n_int / vol * t_mean;
+}
+
 GeometryPreconditionerPieces geometry_preconditioner_pieces(const ProblemSpec& prob, int p, int n_el, bool want_D) {
     const int d = prob.d, q = p + 1;
     const double T = prob.T;

@@ -98,4 +98,12 @@ void time_matrices(const ProblemSpec& prob, int p, int n_el, DenseMatrix& Wt, De
 /// Device field kinds of a catalog problem (nu_s, gamma_s) for the in-kernel physical assembly.
 void problem_field_kinds(const ProblemSpec& prob, int& nu_kind, int& gamma_kind);
 
+/// Device kind (gpu::SourceKind) of the problem's manufactured source term / exact solution
+/// (problems.cpp:131-241): 1 identity-*, 2 quarter-annulus-2d, 3 separable-nu-2d, 0 none.
+int problem_source_kind(const ProblemSpec& prob);
+
+/// The constants of A-hat (solver.cpp:82-112): gamma_mean = int gamma_s / |Omega| and
+/// nu_mean = int nu_s / |Omega| * int_0^1 nu_t/gamma_t, Gauss rule with p + 1 points per element.
+void system_means(const ProblemSpec& prob, int p, int n_el, double& gamma_mean, double& nu_mean);
+
 }  // namespace stiga

@@ -151,3 +151,154 @@ class Problem:
         pc.residuals = res
         pc.sweeps = sweeps.value
         return pc
+
+
+# ------------------------------------------------------------------------------------------------
+# SpaceTimeSystem (solver.hpp:13-58) on the device
+# ------------------------------------------------------------------------------------------------
+def _as_problem(problem):
+    return Problem(problem) if isinstance(problem, str) else problem
+
+
+def problem_info(problem):
+    """(d, T, has_rhs, has_exact, gamma0, nu0) of a catalog problem (problems.hpp:25-37)."""
+    import ctypes
+
+    from ._lib import check, lib
+
+    problem = _as_problem(problem)
+    d, hr, he = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    T, g0, n0 = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    check(lib().stiga_problem_info(problem._h, ctypes.byref(d), ctypes.byref(T), ctypes.byref(hr), ctypes.byref(he),
+                                   ctypes.byref(g0), ctypes.byref(n0)), "problem_info")
+    return d.value, T.value, bool(hr.value), bool(he.value), g0.value, n0.value
+
+
+def system_means(problem, p, n_el):
+    """SpaceTimeSystem::gamma_mean() / nu_mean() (solver.cpp:82-112)."""
+    import ctypes
+
+    from ._lib import check, lib
+
+    problem = _as_problem(problem)
+    g, n = ctypes.c_double(), ctypes.c_double()
+    check(lib().stiga_system_means(problem._h, int(p), int(n_el), ctypes.byref(g), ctypes.byref(n)), "system_means")
+    return g.value, n.value
+
+
+def assemble_rhs(problem, p, n_el, points_per_element=None, device=0, out=None):
+    """b_ of SpaceTimeSystem (solver.cpp:72-76 -> assemble_rhs, assembly.cpp:413-504), sum-factorized
+    on the device; returns a float64 CUDA tensor of N_dof (colex, time slowest)."""
+    import ctypes
+
+    import torch
+
+    from ._lib import check, lib
+
+    problem = _as_problem(problem)
+    ns = stiga.space_dim(p, n_el) ** problem.d
+    nt = stiga.space_dim(p, n_el, temporal=True)
+    if out is None:
+        out = torch.empty(ns * nt, dtype=torch.float64, device=f"cuda:{device}")
+    if out.numel() != ns * nt:
+        raise ValueError("assemble_rhs: output length mismatch")
+    ppe = p + 1 if points_per_element is None else int(points_per_element)
+    check(lib().stiga_assemble_rhs(problem._h, int(p), int(n_el), ppe, int(device), ctypes.c_void_p(out.data_ptr()),
+                                   None), "assemble_rhs")
+    return out
+
+
+class DiscreteSolution:
+    """problems.hpp:67-77: Galerkin coefficients (device tensor) + the discretisation they live on."""
+
+    def __init__(self, coefficients, problem, p, n_el):
+        self.coefficients, self.problem, self.p, self.n_el = coefficients, problem, p, n_el
+
+    @property
+    def n_dof(self):
+        return self.coefficients.numel()
+
+
+def compute_errors(uh, problem=None, points_per_element=None):
+    """compute_errors(u_h, problem, points_per_element) (problems.cpp:305-402) on the device:
+    (relative L2(0,T;L2) error, relative X-norm upper bound).  Default rule: p + 3 points per element
+    (study.cpp:164)."""
+    import ctypes
+
+    from ._lib import check, lib
+
+    problem = _as_problem(problem or uh.problem)
+    ppe = uh.p + 3 if points_per_element is None else int(points_per_element)
+    c = uh.coefficients.contiguous()
+    l2, xu = ctypes.c_double(), ctypes.c_double()
+    check(lib().stiga_compute_errors(problem._h, int(uh.p), int(uh.n_el), ctypes.c_void_p(c.data_ptr()), ppe,
+                                     int(c.device.index or 0), ctypes.byref(l2), ctypes.byref(xu)), "compute_errors")
+    return l2.value, xu.value
+
+
+class SpaceTimeSystem:
+    """SpaceTimeSystem(problem, p, n_el) (solver.hpp:13-58, solver.cpp:34-155) on one device.
+
+    A_ is the physical system M_s (x) W_t + K_s (x) M_t: on the identity map with constant coefficients
+    (identity-* problems) the sum-factorized Kronecker-sum form (equal in exact arithmetic), otherwise
+    the device-assembled physical operator.  b_ is assembled on the device (assemble_rhs above) when the
+    problem carries a source term.  Holds the problem by reference like the reference (solver.hpp:46)."""
+
+    def __init__(self, problem, p, n_el, device=0):
+        self.problem = _as_problem(problem)
+        self.p, self.n_el, self.device = int(p), int(n_el), int(device)
+        d, self.T, has_rhs, _, _, _ = problem_info(self.problem)
+        self.d = d
+        self.gamma_mean, self.nu_mean = system_means(self.problem, p, n_el)
+        self._pc = None
+        if self.problem.name.startswith("identity-"):
+            pc = identity_pieces(d, p, n_el, self.T)
+            self.Wt, self.Mt, self.Mt_plain = pc.Wt, pc.Mt, pc.Mt
+            self.A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=device)
+        else:
+            pc = self.problem.geometry_pieces(p, n_el, want_D=True, device=device)
+            self._pc = pc
+            self.Wt, self.Mt = pc.Wt, pc.Mt
+            _, self.Mt_plain = stiga.assemble_time_matrices(p, n_el, self.T)
+            self.A = pc.A
+        self.b = assemble_rhs(self.problem, p, n_el, device=device) if has_rhs else None
+
+    @property
+    def n_dof(self):
+        return self.A.n_dof
+
+    @property
+    def n_s(self):
+        return self.A.n_dof // self.A.dims[-1]
+
+    @property
+    def n_t(self):
+        return self.A.dims[-1]
+
+    def system_operator(self):
+        return self.A
+
+    def rhs(self):
+        return self.b
+
+    def make_parametric_preconditioner(self):
+        """A-hat (solver.cpp:122-125): parametric factors, plain M_t, mean coefficients, no scaling."""
+        K, M = stiga.assemble_spatial_parametric(self.p, self.n_el, self.d, q=self.p + 1)
+        return stiga.ExtendedFDPreconditioner.setup(K, M, self.Wt, self.Mt_plain, self.gamma_mean, self.nu_mean,
+                                                    device=self.device)
+
+    def make_geometry_preconditioner(self):
+        """A-hat-G (solver.cpp:127-144): separated factors, weighted M_t, D = diag(A)/diag(A~)."""
+        if self._pc is None:
+            self._pc = self.problem.geometry_pieces(self.p, self.n_el, want_D=True, device=self.device)
+        pc = self._pc
+        return stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=pc.D,
+                                                    device=self.device)
+
+    def solve(self, P=None, opts=None, b=None):
+        """solver.cpp:146-155: left-preconditioned GMRES from x0 = 0 -> (DiscreteSolution, SolveReport)."""
+        rhs = self.b if b is None else b
+        if rhs is None:
+            raise ValueError("SpaceTimeSystem::solve: the problem has no source term; pass b")
+        x, rep = stiga.gmres(self.A, P, rhs, opts or stiga.GmresOptions())
+        return DiscreteSolution(x, self.problem, self.p, self.n_el), rep
