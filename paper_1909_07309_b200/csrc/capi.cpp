@@ -238,12 +238,19 @@ stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* 
             // unset: both kinds are candidates of the setup-time autotuner
             const char* fk = std::getenv("STIGA_FOLD_KERNEL");
             const bool dense_only = fk && std::string(fk) == "off";
-            const bool fold_only = fk && (std::string(fk) == "force" || std::string(fk) == "force_wm2");
+            const bool fold_only = fk && (std::string(fk) == "force" || std::string(fk) == "force_wm2" ||
+                                          std::string(fk) == "res" || std::string(fk) == "stream");
             const bool fold_wm2 = fk && std::string(fk) == "force_wm2";  // tests: folded WM = 2 tilings only
+            const bool fold_res = fk && std::string(fk) == "res";        // tests: resident-factor kernel only
+            const bool fold_stream = fk && std::string(fk) == "stream";  // tests: streaming folded kernels only
             if (F.fold[l].on && !dense_only) {  // folded candidates first (half the FLOPs)
                 std::vector<gpu::Tiling> fc = gpu::fold_tiling_candidates(F.n[l]);
-                if (fold_wm2) fc.erase(std::remove_if(fc.begin(), fc.end(), [](const gpu::Tiling& t) { return t.WM != 2; }),
+                if (fold_wm2) fc.erase(std::remove_if(fc.begin(), fc.end(), [](const gpu::Tiling& t) { return t.WM != 2 || t.fold != 1; }),
                                        fc.end());
+                if (fold_res) fc.erase(std::remove_if(fc.begin(), fc.end(), [](const gpu::Tiling& t) { return t.fold != 2; }),
+                                       fc.end());
+                if (fold_stream) fc.erase(std::remove_if(fc.begin(), fc.end(), [](const gpu::Tiling& t) { return t.fold != 1; }),
+                                          fc.end());
                 int frows = 0;
                 for (const auto& t : fc) frows = std::max(frows, t.Mp);
                 for (auto& t : fc) t.Mp = frows;  // both matrices padded to the largest row-block cover

@@ -79,7 +79,8 @@ struct Tiling {
     int LDX = 68;     // smem row stride of a fiber chunk (== 4 mod 16 doubles)
     int Zrows = 0;    // time kernel: rows of the resident Z tile (= Kp)
     int nstage = 3;
-    int fold = 0;     // 1: folded (centrosymmetric) product, fold_kernels.cu; MI/RB/Mp/Kp refer to the folded matrices
+    int fold = 0;     // 1: folded (centrosymmetric) product, fold_kernels.cu; 2: the resident-factor persistent
+                      // folded kernel, fold_res.cu; MI/RB/Mp/Kp refer to the folded matrices
     size_t smem = 0;
     int ctas_per_sm = 1;
     int threads() const { return 32 * WM * WN; }
@@ -115,6 +116,12 @@ cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double
                                 bool forward, const double* post_scale, cudaStream_t stream,
                                 const double* pre_scale = nullptr, const Scatter* sc = nullptr);
 size_t fold_prescale_smem(const Tiling& t);
+/// Resident-factor persistent folded product (fold_res.cu, Tiling::fold == 2): both folded matrices in
+/// shared memory for the whole launch, one CTA per SM, warp-specialised cp.async/mbarrier pipeline.
+/// Candidates for n with 4 <= ceil(ceil(n/2)/8) <= 11; no pre-scale / scatter epilogue.
+std::vector<Tiling> fold_res_candidates(int n, int Mp_hint);
+cudaError_t launch_fold_res(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
+                            bool forward, const double* post_scale, cudaStream_t stream);
 
 /// Standalone block-arrowhead solve X = (gamma Delta_t (x) I + nu I (x) Lambda_s)^-1 Z on the
 /// time-eigen-coordinate tensor (N_s x n_t, time slowest); used when the time direction runs as

@@ -22,6 +22,7 @@
 #include "fd_kernels.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -755,6 +756,7 @@ std::vector<Tiling> fold_tiling_candidates(int n) {
     }
     std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
     std::vector<Tiling> out;
+    if (!std::getenv("STIGA_NO_FOLD_RES")) out = fold_res_candidates(n, 0);  // resident-factor kernels first
     for (auto& e : c) out.push_back(e.second);
     return out;
 }
@@ -763,6 +765,10 @@ cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double
                                 bool forward, const double* post_scale, cudaStream_t st, const double* pre_scale,
                                 const Scatter* sc) {
     if (g.ncols <= 0) return cudaSuccess;
+    if (t.fold == 2) {
+        if (pre_scale || sc) return cudaErrorInvalidValue;
+        return launch_fold_res(t, g, X, Y, Jfold, forward, post_scale, st);
+    }
     if (!t.fold || g.m != g.n || g.n < 2 || (forward && post_scale) || (!forward && pre_scale))
         return cudaErrorInvalidValue;
     // the folded epilogue picks the owner from the spatial index: only by_time = 0 descriptors
@@ -773,6 +779,7 @@ cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double
 }
 
 size_t fold_prescale_smem(const Tiling& t) {
+    if (t.fold == 2) return static_cast<size_t>(1) << 40;  // no pre-scale variant
     return t.smem + sizeof(double) * static_cast<size_t>(t.nstage) * 2 * kBK * t.LDX;
 }
 

@@ -1,0 +1,422 @@
+// Folded (centrosymmetric) mode product with the factor pair RESIDENT in shared memory, a persistent
+// CTA per SM and a warp-specialised cp.async -> mbarrier pipeline (Tiling::fold == 2).
+//
+// Same arithmetic as fold_kernels.cu (the split-basis fold of DESIGN.md §3.4 / §5; mode_product,
+// kronop.cpp:43-73, on half the FLOPs):
+//   forward  y[r] = sum_k A_e[r][k] (x[k] + x[n-1-k]),  y[F+r] = sum_k A_o[r][k] (x[k] - x[n-1-k])
+//   backward p = A_p y_e, q = A_q y_o,  x[i] = p[i] + q[i],  x[n-1-i] = p[i] - q[i],  x[h] = p[h]
+// but organised for the B200 instead of per-tile streaming of the factors:
+//  * the two folded F x F factors (<= 120 KB for n <= 170) are copied into shared memory ONCE per CTA;
+//    only the fiber data streams (16 B/DoF of HBM per pass, no factor traffic from L2);
+//  * one CTA per SM walks the fiber tiles of the whole tensor (static stride), and one producer warp
+//    keeps an NS-deep ring of 16-row fiber chunks (a chunk and its mirror / second half) in flight
+//    ACROSS tile boundaries, so the next tile's first chunks land while the current tile finishes --
+//    the per-tile prologue/epilogue that held the streaming kernel at 50-60 % of the DMMA pipe;
+//  * the stages are filled with 8-byte cp.async (the odd tensor strides of these configurations are
+//    not TMA-legal) whose completion is signalled to a full mbarrier by cp.async.mbarrier.arrive;
+//    consumers release a stage through an empty mbarrier -- no CTA-wide barrier in the main loop;
+//  * every consumer warp owns NI 8-fiber groups x all strips of BOTH folded matrices, so the fold
+//    (x_k +- x_{n-1-k}) is formed once per B fragment and the backward combination x = p +- q is done
+//    in registers;
+//  * DMMA.8x8x4 (FP64 tensor core) with A fragments from the resident factors (row stride == 4 mod 16
+//    doubles) and B fragments from the stage (row stride BN + 4): bank-conflict free.
+#include "fd_kernels.cuh"
+
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+namespace stiga {
+namespace gpu {
+
+namespace {
+
+constexpr int kBK = 16;
+constexpr size_t kSmemPerCTA = 227 * 1024;
+
+__device__ __forceinline__ void rdmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ unsigned ru32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void rcp8(unsigned dst, const double* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void rmb_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(ru32(bar)), "r"(count));
+}
+__device__ __forceinline__ void rmb_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(ru32(bar)) : "memory");
+}
+// arrive on `bar` when every cp.async issued so far by this thread has landed (counts against the
+// barrier's expected arrivals: .noinc)
+__device__ __forceinline__ void rmb_cp_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(ru32(bar)) : "memory");
+}
+__device__ __forceinline__ void rmb_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "RWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra RWAIT_%=;\n"
+        "}\n" ::"r"(ru32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ long long rbase(long long cc, long long L, int n) {
+    if (L == 1) return cc * n;
+    const long long r = cc / L;
+    return (cc - r * L) + L * static_cast<long long>(n) * r;
+}
+
+struct RArgs {
+    ModeGeom geo;
+    int F, h;       // folded lengths (F = h + n mod 2)
+    int Kp, LDA;    // contraction length of both folded matrices (round4(F)); smem row stride (== 4 mod 16)
+    int NQ;         // 16-column chunks per tile
+    int S1, S2;     // live 8-row strips of the first / second matrix
+    long long A2;   // offset of the second matrix in the global factor buffer (Mp * Kp)
+    long long ntiles;
+};
+
+template <int NI, int NW>  // NW = fiber-group warps (WF)
+struct RShape {
+    static constexpr int BN = 8 * NI * NW;   // fibers per tile
+    static constexpr int LDX = BN + 4;       // == 4 mod 16 doubles
+    static constexpr int XB = kBK * LDX;     // one 16-row chunk
+    static constexpr int STAGE = 2 * XB;     // chunk + mirror (forward) / + second half (backward)
+    static constexpr int FPL = (BN + 31) / 32;  // fibers per producer lane (L > 1)
+};
+
+// One 16-column chunk: KS k-steps of 4 over both matrices for this warp's NI fiber groups.
+template <int MS, int NI, int NW, bool FWD, int KS>
+__device__ __forceinline__ void rchunk(const double* __restrict__ a1, const double* __restrict__ a2,
+                                       const double* __restrict__ xa, const double* __restrict__ xb, int LDA,
+                                       int S1, int S2, double (&c1)[MS][NI][2], double (&c2)[MS][NI][2]) {
+    using SH = RShape<NI, NW>;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+        double b1[NI], b2[NI];
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+            const double u = xa[kk * 4 * SH::LDX + ni * 8];
+            if (FWD) {  // xb points at the mirrored row of k-step 0; rows run backwards
+                const double w = xb[-kk * 4 * SH::LDX + ni * 8];
+                b1[ni] = u + w;
+                b2[ni] = u - w;
+            } else {
+                b1[ni] = u;
+                b2[ni] = xb[kk * 4 * SH::LDX + ni * 8];
+            }
+        }
+#pragma unroll
+        for (int mi = 0; mi < MS; ++mi) {
+            if (mi < S1) {
+                const double av = a1[mi * 8 * LDA + kk * 4];
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) rdmma(c1[mi][ni][0], c1[mi][ni][1], av, b1[ni]);
+            }
+            if (mi < S2) {
+                const double av = a2[mi * 8 * LDA + kk * 4];
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) rdmma(c2[mi][ni][0], c2[mi][ni][1], av, b2[ni]);
+            }
+        }
+    }
+}
+
+// Consumer warps: WS strip groups x WF fiber groups; warp (ws, wf) owns strips [ws MSW, ws MSW + MSW) of
+// BOTH matrices and fiber groups [wf NI, wf NI + NI) of the tile.
+template <int MS, int MSW, int NI, int WS, int WF, int NS, bool FWD, bool POST>
+__global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
+    fold_res_kernel(RArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
+                    const double* __restrict__ post) {
+    constexpr int NW = WS * WF;
+    using SH = RShape<NI, WF>;
+    extern __shared__ __align__(16) double smem[];
+    __shared__ uint64_t full[NS], empty[NS];
+    const int LDA = a.LDA;
+    const int MR = 8 * MS;  // resident rows per matrix
+    double* sA = smem;                  // [2][MR][LDA]
+    double* sX = smem + 2 * MR * LDA;   // [NS][STAGE]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    // resident factors (both matrices), once per CTA
+    for (int i = tid; i < 2 * MR * a.Kp; i += blockDim.x) {
+        const int m = i / (MR * a.Kp), rem = i - m * MR * a.Kp;
+        const int row = rem / a.Kp, col = rem - row * a.Kp;
+        sA[(m * MR + row) * LDA + col] = J[m * a.A2 + static_cast<long long>(row) * a.Kp + col];
+    }
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            rmb_init(&full[s], 32);
+            rmb_init(&empty[s], NW);
+        }
+    }
+    __syncthreads();
+
+    const long long L = a.geo.L, ncols = a.geo.ncols;
+    const int n = a.geo.n;
+    if (warp == NW) {
+        // ---------------- producer warp ----------------
+        unsigned seq = 0;
+        for (long long tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+            const long long c0 = tile * SH::BN;
+            for (int q = 0; q < a.NQ; ++q, ++seq) {
+                const int s = seq % NS;
+                rmb_wait(&empty[s], ((seq / NS) & 1u) ^ 1u);
+                const unsigned sa = ru32(sX + s * SH::STAGE), sb = sa + 8u * SH::XB;
+                const int ra0 = q * kBK, rb0 = FWD ? n - q * kBK - kBK : a.F + q * kBK;
+                if (L == 1) {
+                    // fibers contiguous: lane = (row r = lane % 16, fiber parity lane / 16)
+                    const int r = lane & 15, fp = lane >> 4;
+                    const int rowa = ra0 + r, rowb = rb0 + r;
+                    const bool va = rowa < n, vb = rowb >= 0 && rowb < n;
+#pragma unroll 4
+                    for (int f = fp; f < SH::BN; f += 2) {
+                        const long long cc = c0 + f;
+                        const bool fv = cc < ncols;
+                        const double* base = X + (fv ? cc : 0) * n;
+                        rcp8(sa + 8u * (r * SH::LDX + f), (va && fv) ? base + rowa : X, va && fv);
+                        rcp8(sb + 8u * (r * SH::LDX + f), (vb && fv) ? base + rowb : X, vb && fv);
+                    }
+                } else {
+                    long long fb[SH::FPL];
+                    bool fv[SH::FPL];
+#pragma unroll
+                    for (int u = 0; u < SH::FPL; ++u) {
+                        const long long cc = c0 + lane + 32 * u;
+                        fv[u] = cc < ncols && lane + 32 * u < SH::BN;
+                        fb[u] = rbase(fv[u] ? cc : 0, L, n);
+                    }
+#pragma unroll 4
+                    for (int r = 0; r < kBK; ++r) {
+                        const int rowa = ra0 + r, rowb = rb0 + r;
+                        const bool va = rowa < n, vb = rowb >= 0 && rowb < n;
+#pragma unroll
+                        for (int u = 0; u < SH::FPL; ++u) {
+                            const int f = lane + 32 * u;
+                            if (SH::BN % 32 != 0 && f >= SH::BN) continue;
+                            rcp8(sa + 8u * (r * SH::LDX + f), (va && fv[u]) ? X + fb[u] + L * rowa : X, va && fv[u]);
+                            rcp8(sb + 8u * (r * SH::LDX + f), (vb && fv[u]) ? X + fb[u] + L * rowb : X, vb && fv[u]);
+                        }
+                    }
+                }
+                rmb_cp_arrive(&full[s]);
+            }
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const int g = lane >> 2, t = lane & 3;
+    const int ws = warp / WF, wf = warp - ws * WF;
+    const int so = ws * MSW;  // first strip of this warp
+    const double* a1 = sA + (so * 8 + g) * LDA + t;
+    const double* a2 = sA + MR * LDA + (so * 8 + g) * LDA + t;
+    const int S1w = min(MSW, a.S1 - so), S2w = min(MSW, a.S2 - so);
+    const int fcol = wf * NI * 8 + g;  // this lane's B-fragment fiber column within the tile
+    unsigned seq = 0;
+    for (long long tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        const long long c0 = tile * SH::BN;
+        double c1[MSW][NI][2], c2[MSW][NI][2];
+#pragma unroll
+        for (int mi = 0; mi < MSW; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) c1[mi][ni][0] = c1[mi][ni][1] = c2[mi][ni][0] = c2[mi][ni][1] = 0.0;
+        for (int q = 0; q < a.NQ; ++q, ++seq) {
+            const int s = seq % NS;
+            rmb_wait(&full[s], (seq / NS) & 1u);
+            const double* st = sX + s * SH::STAGE;
+            const double* xa = st + t * SH::LDX + fcol;
+            const double* xb = st + SH::XB + (FWD ? (kBK - 1 - t) : t) * SH::LDX + fcol;
+            const int k0 = q * kBK;
+            const int ks = min(kBK, a.Kp - k0) >> 2;
+            if (ks == 4) rchunk<MSW, NI, WF, FWD, 4>(a1 + k0, a2 + k0, xa, xb, LDA, S1w, S2w, c1, c2);
+            else if (ks == 3) rchunk<MSW, NI, WF, FWD, 3>(a1 + k0, a2 + k0, xa, xb, LDA, S1w, S2w, c1, c2);
+            else if (ks == 2) rchunk<MSW, NI, WF, FWD, 2>(a1 + k0, a2 + k0, xa, xb, LDA, S1w, S2w, c1, c2);
+            else rchunk<MSW, NI, WF, FWD, 1>(a1 + k0, a2 + k0, xa, xb, LDA, S1w, S2w, c1, c2);
+            __syncwarp();
+            if (lane == 0) rmb_arrive(&empty[s]);
+        }
+        // register epilogue (same output mapping as fold_mode_kernel)
+        long long ob[NI][2];
+        bool cv[NI][2];
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const long long cc = c0 + (wf * NI + ni) * 8 + 2 * t + v;
+                cv[ni][v] = cc < ncols;
+                ob[ni][v] = rbase(cv[ni][v] ? cc : 0, L, n);
+            }
+#pragma unroll
+        for (int mi = 0; mi < MSW; ++mi) {
+            const int i = (so + mi) * 8 + g;
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    if (!cv[ni][v]) continue;
+                    double* y = Y + ob[ni][v];
+                    if (FWD) {
+                        if (i < a.F) y[L * i] = c1[mi][ni][v];
+                        if (i < a.h) y[L * (a.F + i)] = c2[mi][ni][v];
+                    } else if (i < a.h) {
+                        double lo = c1[mi][ni][v] + c2[mi][ni][v], hi = c1[mi][ni][v] - c2[mi][ni][v];
+                        if (POST) {
+                            lo *= __ldg(post + ob[ni][v] + L * i);
+                            hi *= __ldg(post + ob[ni][v] + L * (n - 1 - i));
+                        }
+                        y[L * i] = lo;
+                        y[L * (n - 1 - i)] = hi;
+                    } else if (i < a.F) {  // middle row (odd n)
+                        double mid = c1[mi][ni][v];
+                        if (POST) mid *= __ldg(post + ob[ni][v] + L * i);
+                        y[L * i] = mid;
+                    }
+                }
+        }
+    }
+}
+
+int lda_of(int Kp) { return Kp + ((4 - Kp % 16) % 16 + 16) % 16; }
+
+size_t res_smem(int MS, int NI, int WF, int NS, int Kp) {
+    const int BN = 8 * NI * WF;
+    return sizeof(double) * (2 * 8 * static_cast<size_t>(MS) * lda_of(Kp) + static_cast<size_t>(NS) * 2 * kBK * (BN + 4));
+}
+
+RArgs make_rargs(const Tiling& t, const ModeGeom& g) {
+    RArgs a;
+    a.geo = g;
+    a.h = g.n / 2;
+    a.F = g.n - a.h;
+    a.Kp = t.Kp;
+    a.LDA = lda_of(t.Kp);
+    a.NQ = (t.Kp + kBK - 1) / kBK;
+    a.S1 = (a.F + 7) / 8;
+    a.S2 = (a.h + 7) / 8;
+    a.A2 = static_cast<long long>(t.Mp) * t.Kp;
+    a.ntiles = (g.ncols + t.BN - 1) / t.BN;
+    return a;
+}
+
+int g_sms = 0;
+
+template <int MS, int MSW, int NI, int WS, int WF, int NS>
+cudaError_t res_launch_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J, bool fwd,
+                         const double* post, cudaStream_t st, int* occ) {
+    constexpr int NW = WS * WF;
+    auto k = fwd ? fold_res_kernel<MS, MSW, NI, WS, WF, NS, true, false>
+                 : (post ? fold_res_kernel<MS, MSW, NI, WS, WF, NS, false, true>
+                         : fold_res_kernel<MS, MSW, NI, WS, WF, NS, false, false>);
+    const size_t smem = res_smem(MS, NI, WF, NS, t.Kp);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (occ) *occ = 0;
+        return occ ? cudaSuccess : e;
+    }
+    if (occ) {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 32 * (NW + 1), smem) != cudaSuccess) {
+            cudaGetLastError();
+            nb = 0;
+        }
+        *occ = nb;
+        return cudaSuccess;
+    }
+    if (g_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms <= 0) g_sms = 148;
+    }
+    const RArgs ra = make_rargs(t, g);
+    const long long grid = std::min<long long>(ra.ntiles, static_cast<long long>(g_sms) * std::max(1, t.ctas_per_sm));
+    k<<<static_cast<unsigned>(grid), 32 * (NW + 1), smem, st>>>(ra, X, Y, J, post);
+    return cudaGetLastError();
+}
+
+template <int MS>
+cudaError_t res_dispatch_ms(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J, bool fwd,
+                            const double* post, cudaStream_t st, int* occ) {
+    // (NI, NW, NS) variants
+    // Tiling fields: WM = strip groups (WS), WN = fiber groups (WF), NI, nstage.  Consumer warps + 1
+    // producer stay <= 8 warps (a 9-warp CTA caps the registers at 168).
+    constexpr int H = (MS + 1) / 2;  // strips per warp with two strip groups
+    if (t.WM == 1 && t.NI == 1 && t.WN == 7 && t.nstage == 4) return res_launch_t<MS, MS, 1, 1, 7, 4>(t, g, X, Y, J, fwd, post, st, occ);
+    if (t.WM == 2 && t.NI == 2 && t.WN == 3 && t.nstage == 4) return res_launch_t<MS, H, 2, 2, 3, 4>(t, g, X, Y, J, fwd, post, st, occ);
+    if (t.WM == 2 && t.NI == 1 && t.WN == 3 && t.nstage == 6) return res_launch_t<MS, H, 1, 2, 3, 6>(t, g, X, Y, J, fwd, post, st, occ);
+    if constexpr (MS <= 8) {
+        if (t.WM == 1 && t.NI == 2 && t.WN == 4 && t.nstage == 4) return res_launch_t<MS, MS, 2, 1, 4, 4>(t, g, X, Y, J, fwd, post, st, occ);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t res_dispatch(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J, bool fwd,
+                         const double* post, cudaStream_t st, int* occ) {
+    switch (t.MI) {
+        case 4: return res_dispatch_ms<4>(t, g, X, Y, J, fwd, post, st, occ);
+        case 5: return res_dispatch_ms<5>(t, g, X, Y, J, fwd, post, st, occ);
+        case 6: return res_dispatch_ms<6>(t, g, X, Y, J, fwd, post, st, occ);
+        case 7: return res_dispatch_ms<7>(t, g, X, Y, J, fwd, post, st, occ);
+        case 8: return res_dispatch_ms<8>(t, g, X, Y, J, fwd, post, st, occ);
+        case 9: return res_dispatch_ms<9>(t, g, X, Y, J, fwd, post, st, occ);
+        case 10: return res_dispatch_ms<10>(t, g, X, Y, J, fwd, post, st, occ);
+        case 11: return res_dispatch_ms<11>(t, g, X, Y, J, fwd, post, st, occ);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+std::vector<Tiling> fold_res_candidates(int n, int Mp_hint) {
+    std::vector<Tiling> out;
+    const int h = n / 2, F = n - h;
+    if (h < 1) return out;
+    const int S = (F + 7) / 8;
+    if (S < 4 || S > 11) return out;  // small factors: the streaming kernel; n > 176: factors exceed smem
+    const int Kp = (F + 3) / 4 * 4;
+    const int variants[4][4] = {{2, 2, 3, 4}, {1, 1, 7, 4}, {2, 1, 3, 6}, {1, 2, 4, 4}};  // WM(WS), NI, WN(WF), NS
+    for (const auto& v : variants) {
+        Tiling t;
+        t.fold = 2;
+        t.MI = S;
+        t.WM = v[0];
+        t.NI = v[1];
+        t.WN = v[2];
+        t.nstage = v[3];
+        t.S = S;
+        t.RB = 1;
+        t.MpB = 8 * S;
+        t.Mp = std::max(8 * S, Mp_hint);
+        t.Kp = Kp;
+        t.BN = 8 * t.NI * t.WN;
+        t.LDX = t.BN + 4;
+        t.smem = res_smem(S, t.NI, t.WN, t.nstage, Kp);
+        if (t.smem + 1024 > kSmemPerCTA) continue;
+        if (t.WM == 1 && t.NI == 2 && S > 8) continue;  // 4 S NI accumulator doubles: spills beyond S = 8
+        int occ = 0;
+        res_dispatch(t, ModeGeom{}, nullptr, nullptr, nullptr, true, nullptr, nullptr, &occ);
+        if (occ < 1) continue;
+        t.ctas_per_sm = 1;
+        out.push_back(t);
+    }
+    return out;
+}
+
+cudaError_t launch_fold_res(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
+                            bool forward, const double* post_scale, cudaStream_t st) {
+    if (g.ncols <= 0) return cudaSuccess;
+    if (t.fold != 2 || g.m != g.n || g.n < 2 || (forward && post_scale)) return cudaErrorInvalidValue;
+    return res_dispatch(t, g, X, Y, Jfold, forward, post_scale, st, nullptr);
+}
+
+}  // namespace gpu
+}  // namespace stiga

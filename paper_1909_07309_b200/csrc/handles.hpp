@@ -153,7 +153,7 @@ struct stiga_fd_s {
     void mprod(const gpu::Tiling& t, int l, bool backward, const gpu::ModeGeom& g, const double* src, double* dst,
                const double* post, cudaStream_t st, const double* pre = nullptr, const gpu::Scatter* sc = nullptr) {
         if (t.fold) {
-            if (sc && (backward || t.WM != 2)) throw std::runtime_error("internal: folded scatter needs a WM = 2 tiling");
+            if (sc && (backward || t.WM != 2 || t.fold != 1)) throw std::runtime_error("internal: folded scatter needs a WM = 2 tiling");
             ck(gpu::launch_fold_product(t, g, src, dst, backward ? Jfb[l]->p : Jft[l]->p, !backward, post, st, pre, sc),
                "fd folded mode product");
         } else {
@@ -235,7 +235,7 @@ struct stiga_fd_s {
             // the scattering product: the tuned tiling when it has a scatter epilogue (dense WM = 1 or
             // folded WM = 2), else the dense fallback
             const gpu::Tiling& tt = (l == 0 && fused_pre) ? first_tiling() : tl[l];
-            const bool scatter_ok = !(fused_pre && l == 0) && (tt.fold ? tt.WM == 2 : tt.WM == 1);
+            const bool scatter_ok = !(fused_pre && l == 0) && (tt.fold == 1 ? tt.WM == 2 : (tt.fold == 0 && tt.WM == 1));
             const gpu::Tiling& t = last ? (scatter_ok ? tt : dense_tiling(l)) : (l == 0 ? first_tiling() : tl[l]);
             mark(st);
             mprod(t, l, false, slab_geom(l, nt_local), src, dst, nullptr, st, (fused_pre && l == 0) ? dsl : nullptr,
@@ -510,7 +510,9 @@ struct stiga_fd_s {
             const double n = dims[l], Fh = n - std::floor(n / 2);
             return t.fold ? 4.0 * Fh * Fh * Nsp / n : 2.0 * n * Nsp;
         };
-        auto tag = [](const gpu::Tiling& t) { return t.fold ? std::string("(folded)") : std::string(); };
+        auto tag = [](const gpu::Tiling& t) {
+            return t.fold == 2 ? std::string("(folded,res)") : (t.fold ? std::string("(folded)") : std::string());
+        };
         for (int l = 0; l < d; ++l) {
             const gpu::Tiling& t = l == 0 ? (fused_pre ? tl_pre : tl[0]) : tl[l];
             L.emplace_back("fwd_mode" + std::to_string(l) + tag(t) + (l == 0 && fused_pre ? "+pre_scale" : "") +

@@ -282,6 +282,25 @@ def test_fd_apply_parity_folded_large_modes(nel, monkeypatch):
     assert rel(s, Po.apply(r)) <= TOL
 
 
+@pytest.mark.parametrize("d,p,nel", [
+    (1, 3, 150), (2, 3, 96), (2, 5, 160), (2, 4, 128), (3, 2, 64), (3, 3, 60), (3, 3, 50), (2, 2, 90),
+])
+@pytest.mark.parametrize("scaled", [False, True])
+def test_fd_apply_parity_resident_fold(d, p, nel, scaled, monkeypatch):
+    """STIGA_FOLD_KERNEL=res: every split direction on the resident-factor persistent folded kernel
+    (fold_res.cu: both folded factors in smem, producer warp + mbarrier ring across tiles), odd and even
+    n, 4..11 strips, mode 0 (contiguous fibers) and strided modes; <= 1e-11 vs the oracle and equal to
+    the streaming folded kernel to rounding."""
+    monkeypatch.setenv("STIGA_FOLD_KERNEL", "res")
+    s, so, P, _, r = run_pair(d, p, nel, scaled)
+    names = [nm for nm, _ in P.launch_info()]
+    assert sum("folded,res" in nm for nm in names) == 2 * d, names
+    assert rel(s, so) <= TOL
+    monkeypatch.setenv("STIGA_FOLD_KERNEL", "stream")
+    s2, *_ = run_pair(d, p, nel, scaled)
+    assert rel(s, s2) <= 1e-13
+
+
 def test_fold_not_used_on_curved_geometry():
     """The A^G factors of the deformed cube are not centrosymmetric: dense kernels only."""
     from paper_1909_07309_b200.problems import Problem
