@@ -162,14 +162,21 @@ def cpu_baseline(cfg, frac=None):
 
 def problem_pieces(cfg, device=None):
     """1D factors + D of the A^G preconditioner: identity geometry for c1/c2/c3/c5 (D = 1), the
-    fitted deformed cube with kappa(x), c(x) for c4 (BASELINE configs[3]).  With a device, diag(A)
-    of D comes from the device-assembled physical operator instead of the host quadrature."""
+    fitted deformed cube with kappa(x), c(x) for c4 (BASELINE configs[3]).  With a device, D =
+    diag(A)/diag(A~) is formed on the device (stiga_geometry_scaling_device; diag(A) of the
+    device-assembled physical operator for c4) and stays there as a CUDA tensor."""
+    from paper_1909_07309_b200 import stiga
     from paper_1909_07309_b200.problems import Problem, geometry_scaling, identity_pieces
 
     if cfg.problem == "identity":
         pc = identity_pieces(cfg.d, cfg.p, cfg.n_el)
-        return pc, geometry_scaling(pc)
-    pc = Problem(cfg.problem).geometry_pieces(cfg.p, cfg.n_el, want_D=True, device=device)
+        if device is None:
+            return pc, geometry_scaling(pc)
+        A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, pc.gamma, pc.nu, device=device)
+        At = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=device)
+        return pc, stiga.geometry_scaling_device(A, At)
+    pc = Problem(cfg.problem).geometry_pieces(cfg.p, cfg.n_el, want_D=True, device=device,
+                                              D_on_device=device is not None)
     if hasattr(pc, "A"):
         del pc.A  # the GMRES section builds (and times) its own operator
     return pc, pc.D
@@ -280,7 +287,8 @@ def run_ours(args):
                    ("NCCL stream-ordered barriers" if dist.get_backend() == "nccl" else "host barriers (gloo)")
     else:
         P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0,
-                                                 scaling=D if not sharded else None, device=dev)
+                                                 scaling=D if not sharded else None, device=dev,
+                                                 device_schur=True)
     setup_s = time.perf_counter() - t0
     n = P.n_dof
     launches = P.launches()

@@ -108,8 +108,47 @@ public:
     }
     stiga_fd_t handle() const { return h_; }
 
+    // Device-side setup (stiga_fd_setup_ex): D on the device (d_D, N_dof doubles, may be
+    // null), Lambda_s / S^-1 on the device, optionally cuSOLVER eigensolves.
+    static Preconditioner setup_device(const std::vector<Dense>& K, const std::vector<Dense>& M, const Dense& Wt,
+                                       const Dense& Mt, double gamma, double nu, const double* d_D, long long n_dof,
+                                       bool cusolver = false, int device = 0) {
+        std::vector<int> n;
+        std::vector<const double*> Kp, Mp;
+        for (size_t l = 0; l < K.size(); ++l) {
+            n.push_back(K[l].n);
+            Kp.push_back(K[l].a.data());
+            Mp.push_back(M[l].a.data());
+        }
+        stiga_fd_setup_options o{STIGA_SETUP_DEVICE_SCHUR | (cusolver ? STIGA_SETUP_CUSOLVER : 0), d_D};
+        Preconditioner P;
+        check(stiga_fd_setup_ex(static_cast<int>(K.size()), n.data(), Kp.data(), Mp.data(), Wt.n, Wt.a.data(),
+                                Mt.a.data(), gamma, nu, nullptr, d_D ? n_dof : 0, &o, device, &P.h_));
+        return P;
+    }
+
 private:
     stiga_fd_t h_ = nullptr;
+};
+
+// make_problem(id) (problems.cpp:244-261): geometry, coefficients, source term / exact solution.
+class Problem {
+public:
+    explicit Problem(const std::string& id) { check(stiga_problem_create(id.c_str(), &h_)); }
+    Problem(const Problem&) = delete;
+    Problem& operator=(const Problem&) = delete;
+    ~Problem() {
+        if (h_) stiga_problem_destroy(h_);
+    }
+    int dim() const {
+        int d = 0;
+        check(stiga_problem_dim(h_, &d));
+        return d;
+    }
+    stiga_problem_t handle() const { return h_; }
+
+private:
+    stiga_problem_t h_ = nullptr;
 };
 
 // KronSumOperator (kronop.hpp:61-79) in the kron_sum_terms form of SpaceTimeSystem (solver.cpp:10-30).
@@ -128,6 +167,16 @@ public:
         check(stiga_kronsum_create_spacetime(static_cast<int>(K.size()), n.data(), Kp.data(), Mp.data(), Wt.n,
                                              Wt.a.data(), Mt.a.data(), gamma, nu, device, &A.h_));
         return A;
+    }
+    // SpaceTimeSystem's A_ = M_s (x) W_t + K_s (x) M_t with the physical K_s, M_s of `prob`
+    // (solver.cpp:58-70), assembled on the device.
+    static KronSumOperator physical(const Problem& prob, int p, int n_el, int device = 0) {
+        KronSumOperator A;
+        check(stiga_kronsum_create_physical(prob.handle(), p, n_el, device, &A.h_));
+        return A;
+    }
+    void diagonal_device(double* d_diag, cudaStream_t st = nullptr) const {
+        check(stiga_kronsum_diagonal_device(h_, d_diag, st));
     }
     KronSumOperator() = default;
     KronSumOperator(KronSumOperator&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
@@ -205,6 +254,30 @@ inline SolveReport gmres(const KronSumOperator& A, const Preconditioner* P, cons
     stiga_gmres_report r{0, 0, 0.0, 0.0, hist.data(), static_cast<int>(hist.size()), 0};
     check(stiga_gmres(A.handle(), P ? P->handle() : nullptr, d_b, d_x, &o, &r, st));
     return detail::to_report(r, hist);
+}
+
+// SpaceTimeSystem pieces around the solve (solver.cpp:82-112, assembly.cpp:413-504, problems.cpp:305-402).
+inline std::pair<double, double> system_means(const Problem& prob, int p, int n_el) {
+    double g = 0.0, nu = 0.0;
+    check(stiga_system_means(prob.handle(), p, n_el, &g, &nu));
+    return {g, nu};
+}
+inline void assemble_rhs(const Problem& prob, int p, int n_el, double* d_b, int device = 0, cudaStream_t st = nullptr) {
+    check(stiga_assemble_rhs(prob.handle(), p, n_el, p + 1, device, d_b, st));
+}
+struct Errors {
+    double l2l2 = 0.0, x_upper = 0.0;
+};
+inline Errors compute_errors(const Problem& prob, int p, int n_el, const double* d_coeffs, int points_per_element,
+                             int device = 0) {
+    Errors e;
+    check(stiga_compute_errors(prob.handle(), p, n_el, d_coeffs, points_per_element, device, &e.l2l2, &e.x_upper));
+    return e;
+}
+// D = diag(A) / diag(A~) of make_geometry_preconditioner (solver.cpp:138-142), on the device.
+inline void geometry_scaling_device(const KronSumOperator& A, const KronSumOperator& Atilde, double* d_D,
+                                    cudaStream_t st = nullptr) {
+    check(stiga_geometry_scaling_device(A.handle(), Atilde.handle(), d_D, st));
 }
 
 }  // namespace b200

@@ -87,6 +87,22 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
                    const double* Wt, const double* Mt, double gamma, double nu, const double* scaling,
                    long long scaling_len, int device, stiga_fd_t* out);
 /* device < 0 creates a host-only handle (setup + stiga_fd_export, no device apply). */
+
+/* Device-side setup.  STIGA_SETUP_DEVICE_SCHUR: Lambda_s and the Schur diagonal S^-1
+   (fdsolve.cpp:91-136) computed on the device, bit-identical to the host loop (correctly rounded
+   arithmetic in the host's operation order); STIGA_SETUP_CUSOLVER: every symmetric eigenproblem of the
+   setup (spatial pencils after the Cholesky reduction, the split half-pencils, the Hermitian embedding of
+   the time pencil) solved by cuSOLVER syevd on `device`.  d_scaling: D (scaling_len == N_dof entries) in
+   DEVICE memory instead of the host `scaling`; D^-1/2 is then formed on the device (unsharded handles). */
+#define STIGA_SETUP_DEVICE_SCHUR 1
+#define STIGA_SETUP_CUSOLVER 2
+typedef struct {
+    int flags;
+    const double* d_scaling;
+} stiga_fd_setup_options;
+int stiga_fd_setup_ex(int d, const int* n, const double* const* K, const double* const* M, int n_t,
+                      const double* Wt, const double* Mt, double gamma, double nu, const double* scaling,
+                      long long scaling_len, const stiga_fd_setup_options* opts, int device, stiga_fd_t* out);
 int stiga_fd_destroy(stiga_fd_t P);
 /* ExtendedFDPreconditioner::size() and the tensor dims (d spatial sizes then n_t). */
 int stiga_fd_size(stiga_fd_t P, long long* n_dof);
@@ -241,6 +257,12 @@ int stiga_kronsum_dims(stiga_kronsum_t A, int* D, int* dims, int cap);
 int stiga_kronsum_apply(stiga_kronsum_t A, const double* d_x, double* d_y, void* stream);
 /* KronSumOperator::diagonal() (kronop.cpp:117-131) into a host buffer of N_dof. */
 int stiga_kronsum_diagonal(stiga_kronsum_t A, double* h_diag);
+/* The same diagonal into a DEVICE buffer of N_dof (bit-identical to stiga_kronsum_diagonal). */
+int stiga_kronsum_diagonal_device(stiga_kronsum_t A, double* d_diag, void* stream);
+/* make_geometry_preconditioner's D = diag(A) / diag(A~) (solver.cpp:138-142) on the device: A the
+   system operator (physical or Kronecker-sum), A~ a Kronecker-sum operator of the same size (the
+   separated factors K~, M~, W_t, M_t with gamma = nu = 1).  d_D: N_dof device doubles. */
+int stiga_geometry_scaling_device(stiga_kronsum_t A, stiga_kronsum_t Atilde, double* d_D, void* stream);
 
 /* Time-sharded mat-vec building blocks, for the space-time (identity geometry) and
    physical systems: A x = W~ (x) a(x) + M~ (x) b(x) with a, b the spatial halves.

@@ -18,6 +18,13 @@ _pi = ctypes.POINTER(ctypes.c_int)
 _ppd = ctypes.POINTER(_pd)
 
 
+class FdSetupOptions(ctypes.Structure):
+    _fields_ = [("flags", ctypes.c_int), ("d_scaling", ctypes.c_void_p)]
+
+
+SETUP_DEVICE_SCHUR, SETUP_CUSOLVER = 1, 2
+
+
 class GmresOptions(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_krylov", ctypes.c_int), ("restart", ctypes.c_int)]
 
@@ -74,6 +81,8 @@ SIGNATURES = {
     "stiga_compute_errors": (_c_int, [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _pd, _pd]),
     "stiga_fd_setup": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl, _pd, _c_ll, _c_int,
                                 ctypes.POINTER(_vp)]),
+    "stiga_fd_setup_ex": (_c_int, [_c_int, _pi, _ppd, _ppd, _c_int, _pd, _pd, _c_dbl, _c_dbl, _pd, _c_ll, _vp, _c_int,
+                                   ctypes.POINTER(_vp)]),
     "stiga_fd_destroy": (_c_int, [_vp]),
     "stiga_fd_size": (_c_int, [_vp, ctypes.POINTER(_c_ll)]),
     "stiga_fd_dims": (_c_int, [_vp, _pi, _pi]),
@@ -103,6 +112,8 @@ SIGNATURES = {
     "stiga_kronsum_size": (_c_int, [_vp, ctypes.POINTER(_c_ll)]),
     "stiga_kronsum_apply": (_c_int, [_vp, _vp, _vp, _vp]),
     "stiga_kronsum_diagonal": (_c_int, [_vp, _pd]),
+    "stiga_kronsum_diagonal_device": (_c_int, [_vp, _vp, _vp]),
+    "stiga_geometry_scaling_device": (_c_int, [_vp, _vp, _vp, _vp]),
     "stiga_gmres": (_c_int, [_vp, _vp, _vp, _vp, ctypes.POINTER(GmresOptions), ctypes.POINTER(GmresReport), _vp]),
     "stiga_fp64_peak": (_c_int, [_c_int, _c_dbl, _pd, _pd]),
     "stiga_kronsum_time_halfband": (_c_int, [_vp, _pi]),

@@ -24,6 +24,8 @@
 #include "cuda/aux_kernels.cuh"
 #include "cuda/fd_kernels.cuh"
 #include "cuda/physical.cuh"
+#include "cuda/setup_kernels.cuh"
+#include "host/eig_device.hpp"
 #include "host/assembly.hpp"
 #include "host/fdsetup.hpp"
 #include "host/geometry.hpp"
@@ -191,8 +193,15 @@ namespace stiga {
 // shard state and the D^-1/2 slab.
 stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* const* M, int n_t, const double* Wt,
                      const double* Mt, double gamma, double nu, const double* scaling, long long scaling_len,
-                     int device, const std::function<void(stiga_fd_s&)>& prepare) {
+                     int device, const std::function<void(stiga_fd_s&)>& prepare, int flags,
+                     const double* d_scaling) {
         require(d >= 1 && d <= gpu::kMaxDim, "ExtendedFDPreconditioner: per-direction matrices mismatch");
+        require((flags & ~(STIGA_SETUP_DEVICE_SCHUR | STIGA_SETUP_CUSOLVER)) == 0, "stiga_fd_setup_ex: unknown flags");
+        const bool dev_schur = (flags & STIGA_SETUP_DEVICE_SCHUR) && device >= 0;
+        const bool use_cusolver = (flags & STIGA_SETUP_CUSOLVER) != 0;
+        require(!use_cusolver || device >= 0, "stiga_fd_setup_ex: the cuSOLVER eigensolver needs a device");
+        require(!(scaling && d_scaling), "stiga_fd_setup_ex: host and device scaling both given");
+        require(!d_scaling || (device >= 0 && !prepare), "stiga_fd_setup_ex: device scaling needs an unsharded device handle");
         require(n && K && M && Wt && Mt, "stiga_fd_setup: null input");
         require(n_t >= 1, "time_factorization: shape mismatch");
         std::vector<DenseMatrix> Ks, Ms;
@@ -203,10 +212,18 @@ stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* 
             Ms.push_back(from_colmajor(M[l], n[l]));
             n_s *= n[l];
         }
-        if (scaling)
+        if (scaling || d_scaling)
             require(scaling_len == n_s * n_t, "ExtendedFDPreconditioner: scaling vector length mismatch");
         auto h = std::make_unique<stiga_fd_s>();
-        h->F = fd_setup(Ks, Ms, from_colmajor(Wt, n_t), from_colmajor(Mt, n_t), gamma, nu, scaling);
+        {
+            std::unique_ptr<DeviceGuard> eg;
+            std::unique_ptr<ScopedSymEig> se;
+            if (use_cusolver) {  // every sym_eig of this setup (pencils, split halves, time embedding)
+                eg.reset(new DeviceGuard(device));
+                se.reset(new ScopedSymEig(&sym_eig_cusolver));
+            }
+            h->F = fd_setup(Ks, Ms, from_colmajor(Wt, n_t), from_colmajor(Mt, n_t), gamma, nu, scaling, !dev_schur);
+        }
         const FDFactors& F = h->F;
         h->device = device;
         h->d = d;
@@ -285,7 +302,51 @@ stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* 
         const int tKp = h->cand_ts.front().Kp;
         h->Jt_t.upload(pad_factor(F.time.U, true, trows, tKp));
         h->J_t.upload(pad_factor(F.time.U, false, trows, tKp));
-        h->S_inv.upload(F.S_inv_dev());
+        if (dev_schur) {  // Lambda_s and S^-1 on the device, bit-identical to the host loop (fdsolve.cpp:91-136)
+            gpu::SchurArgs sa;
+            sa.d = d;
+            for (int l = 0; l < d; ++l) {
+                sa.n[l] = F.n[l];
+                sa.lam[l] = h->lam[l]->p;  // device (fiber) order: S^-1 comes out in the device order
+            }
+            const int np = static_cast<int>(F.time.lambda.size());
+            std::vector<double> pcs(4 * std::max(np, 1), 0.0);
+            for (int j = 0; j < np; ++j) {
+                const double lam = F.time.lambda[j];
+                const double c1 = gamma / nu * lam;
+                pcs[4 * j] = gamma * gamma / nu * lam * lam;
+                pcs[4 * j + 1] = c1 * c1 / nu;
+                pcs[4 * j + 2] = F.time.g[2 * j] * F.time.g[2 * j];
+                pcs[4 * j + 3] = F.time.g[2 * j + 1] * F.time.g[2 * j + 1];
+            }
+            DBuf dpc;
+            dpc.upload(pcs);
+            sa.npairs = np;
+            sa.pc = dpc.p;
+            sa.gs = gamma * F.time.sigma;
+            sa.nu = nu;
+            sa.gg = gamma * gamma;
+            if (F.time.zero_count) {
+                const double gz = F.time.g[F.n_t - 2];
+                sa.cz = gamma * gamma * gz * gz / nu;
+                sa.zero_block = 1;
+            }
+            h->S_inv.alloc(static_cast<size_t>(F.n_s_total));
+            int* flag = nullptr;
+            ck(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
+            std::unique_ptr<int, decltype(&cudaFree)> fg(flag, &cudaFree);
+            ck(cudaMemset(flag, 0, sizeof(int)), "memset");
+            ck(gpu::launch_schur_inv(sa, F.n_s_total, h->S_inv.p, flag, nullptr), "device Schur diagonal");
+            int hf = 0;
+            ck(cudaMemcpy(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost), "download");
+            if (hf & 1)
+                throw std::runtime_error("ExtendedFDPreconditioner: spatial eigenvalues not positive "
+                                         "(stiffness pencil not positive definite)");
+            if (hf & 2) throw std::runtime_error("ExtendedFDPreconditioner: singular Schur complement");
+            h->schur_on_device = true;
+        } else {
+            h->S_inv.upload(F.S_inv_dev());
+        }
         std::vector<double> pc, pc1, pc1sq, pgg;
         for (size_t j = 0; j < F.time.lambda.size(); ++j) {
             const double lam = F.time.lambda[j];
@@ -309,7 +370,19 @@ stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* 
         std::vector<double> gg(F.time.g.begin(), F.time.g.end());
         if (gg.empty()) gg.push_back(0.0);
         h->g.upload(gg);
-        if (!F.d_inv_sqrt.empty()) h->dinv.upload(F.d_inv_sqrt);
+        if (!F.d_inv_sqrt.empty()) {
+            h->dinv.upload(F.d_inv_sqrt);
+        } else if (d_scaling) {  // D on the device: D^-1/2 there too (fdsolve.cpp:145-151, same rounding)
+            h->dinv.alloc(static_cast<size_t>(F.n_dof));
+            int* flag = nullptr;
+            ck(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
+            std::unique_ptr<int, decltype(&cudaFree)> fg(flag, &cudaFree);
+            ck(cudaMemset(flag, 0, sizeof(int)), "memset");
+            ck(gpu::launch_dinv_sqrt(d_scaling, h->dinv.p, F.n_dof, flag, nullptr), "device D^-1/2");
+            int hf = 0;
+            ck(cudaMemcpy(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost), "download");
+            if (hf) throw std::invalid_argument("ExtendedFDPreconditioner: scaling must be strictly positive");
+        }
         h->scratch.alloc(static_cast<size_t>(h->scratch_len));
 
         gpu::ArrowParams& ap = h->ap;
@@ -344,7 +417,19 @@ int stiga_fd_setup(int d, const int* n, const double* const* K, const double* co
     return guarded([&] {
         require(out != nullptr, "stiga_fd_setup: null handle output");
         *out = nullptr;
-        *out = fd_build(d, n, K, M, n_t, Wt, Mt, gamma, nu, scaling, scaling_len, device, nullptr);
+        *out = fd_build(d, n, K, M, n_t, Wt, Mt, gamma, nu, scaling, scaling_len, device, nullptr, 0, nullptr);
+    });
+}
+
+int stiga_fd_setup_ex(int d, const int* n, const double* const* K, const double* const* M, int n_t, const double* Wt,
+                      const double* Mt, double gamma, double nu, const double* scaling, long long scaling_len,
+                      const stiga_fd_setup_options* opts, int device, stiga_fd_t* out) {
+    return guarded([&] {
+        require(out != nullptr, "stiga_fd_setup_ex: null handle output");
+        *out = nullptr;
+        const int flags = opts ? opts->flags : 0;
+        const double* ds = opts ? opts->d_scaling : nullptr;
+        *out = fd_build(d, n, K, M, n_t, Wt, Mt, gamma, nu, scaling, scaling_len, device, nullptr, flags, ds);
     });
 }
 
@@ -398,7 +483,29 @@ int stiga_fd_export(stiga_fd_t P, int which, int l, double* out, long long out_l
             case 2: src = &F.time.U.a; break;
             case 3: tmp = F.time.lambda; src = &tmp; break;
             case 4: src = &F.time.g; break;
-            case 5: src = &F.S_inv; break;
+            case 5:
+                if (F.S_inv.empty() && P->schur_on_device) {  // device order -> the ascending (exported) order
+                    DeviceGuard dg(P->device);
+                    std::vector<double> dev(static_cast<size_t>(F.n_s_total));
+                    ck(cudaMemcpy(dev.data(), P->S_inv.p, sizeof(double) * dev.size(), cudaMemcpyDeviceToHost),
+                       "download");
+                    tmp.assign(dev.size(), 0.0);
+                    std::vector<Index> stride(F.d, 1);
+                    for (int k = 1; k < F.d; ++k) stride[k] = stride[k - 1] * F.n[k - 1];
+                    for (Index s = 0; s < static_cast<Index>(dev.size()); ++s) {
+                        Index rem = s, sa = 0;
+                        for (int k = 0; k < F.d; ++k) {
+                            const Index f = rem % F.n[k];
+                            rem /= F.n[k];
+                            sa += stride[k] * (F.fold[k].on ? F.fold[k].dev_order[f] : f);
+                        }
+                        tmp[sa] = dev[s];
+                    }
+                    src = &tmp;
+                } else {
+                    src = &F.S_inv;
+                }
+                break;
             default: throw std::invalid_argument("stiga_fd_export: unknown factor id");
         }
         require(out_len >= static_cast<long long>(src->size()), "stiga_fd_export: output too small");
@@ -1071,6 +1178,65 @@ int stiga_kronsum_diagonal(stiga_kronsum_t A, double* h_diag) {
             }
             for (long long i = 0; i < A->n_dof; ++i) h_diag[i] += A->coeffs[t] * acc[i];
         }
+    });
+}
+
+}  // extern "C"
+
+namespace {
+// diag(A) on the device (kronop.cpp:117-131 / the physical A_ of solver.cpp:67-70), or num / diag(A)
+// when num is set; same per-entry operation order as stiga_kronsum_diagonal (bit-identical).
+void ks_diag_device(stiga_kronsum_s* A, const double* num, double* out, cudaStream_t st) {
+    require(!A->kshard, "KronSumOperator::diagonal: sharded operator (use the slab's own diagonal)");
+    if (A->physical) {
+        const int d = A->D - 1;
+        const long long Ns = A->n_dof / A->dims[d];
+        DBuf dK, dM, W, M;
+        dK.alloc(static_cast<size_t>(Ns));
+        dM.alloc(static_cast<size_t>(Ns));
+        ck(gpu::launch_stencil_diag(A->pdesc, A->Kst.p, A->Mst.p, dK.p, dM.p, st), "stencil diag");
+        W.upload(A->time_W);
+        M.upload(A->time_M);
+        require(num == nullptr, "internal: physical diagonal as denominator");
+        ck(gpu::launch_physical_diag(dM.p, dK.p, W.p, M.p, Ns, A->dims[d], nullptr, out, st), "physical diagonal");
+        ck(cudaStreamSynchronize(st), "physical diagonal");
+        return;
+    }
+    const int D = A->D, nt = static_cast<int>(A->coeffs.size());
+    std::vector<std::unique_ptr<DBuf>> bufs;
+    std::vector<const double*> ptrs;
+    for (int t = 0; t < nt; ++t)
+        for (const DenseMatrix& F : A->factors[t]) {
+            std::vector<double> dg(static_cast<size_t>(F.rows));
+            for (Index j = 0; j < F.rows; ++j) dg[j] = F(j, j);
+            bufs.emplace_back(new DBuf);
+            bufs.back()->upload(dg);
+            ptrs.push_back(bufs.back()->p);
+        }
+    ck(gpu::launch_kron_diag(D, A->dims.data(), nt, A->coeffs.data(), ptrs.data(), num, out, A->n_dof, st),
+       "Kronecker-sum diagonal");
+    ck(cudaStreamSynchronize(st), "Kronecker-sum diagonal");
+}
+}  // namespace
+
+extern "C" {
+
+int stiga_kronsum_diagonal_device(stiga_kronsum_t A, double* d_diag, void* stream) {
+    return guarded([&] {
+        require(A && d_diag, "KronSumOperator::diagonal: null argument");
+        DeviceGuard dg(A->device);
+        ks_diag_device(A, nullptr, d_diag, as_stream(stream));
+    });
+}
+
+int stiga_geometry_scaling_device(stiga_kronsum_t A, stiga_kronsum_t Atilde, double* d_D, void* stream) {
+    return guarded([&] {
+        require(A && Atilde && d_D, "geometry scaling: null argument");
+        require(A->n_dof == Atilde->n_dof && A->device == Atilde->device, "geometry scaling: operator mismatch");
+        require(!Atilde->physical, "geometry scaling: A~ must be in Kronecker-sum form");
+        DeviceGuard dg(A->device);
+        ks_diag_device(A, nullptr, d_D, as_stream(stream));       // diag(A)
+        ks_diag_device(Atilde, d_D, d_D, as_stream(stream));      // / diag(A~)
     });
 }
 

@@ -91,38 +91,53 @@ struct RShape {
     static constexpr int FPL = (BN + 31) / 32;  // fibers per producer lane (L > 1)
 };
 
-// One 16-column chunk: KS k-steps of 4 over both matrices for this warp's NI fiber groups.
+// Fragments of k-step kk: A of both matrices (this warp's strips), B of both (forward: the fold).
+template <int MS, int NI, int NW, bool FWD>
+__device__ __forceinline__ void rfrag(const double* __restrict__ a1, const double* __restrict__ a2,
+                                      const double* __restrict__ xa, const double* __restrict__ xb, int LDA, int kk,
+                                      double (&av1)[MS], double (&av2)[MS], double (&b1)[NI], double (&b2)[NI]) {
+    using SH = RShape<NI, NW>;
+#pragma unroll
+    for (int mi = 0; mi < MS; ++mi) {
+        av1[mi] = a1[mi * 8 * LDA + kk * 4];
+        av2[mi] = a2[mi * 8 * LDA + kk * 4];
+    }
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+        const double u = xa[kk * 4 * SH::LDX + ni * 8];
+        if (FWD) {  // xb points at the mirrored row of k-step 0; rows run backwards
+            const double w = xb[-kk * 4 * SH::LDX + ni * 8];
+            b1[ni] = u + w;
+            b2[ni] = u - w;
+        } else {
+            b1[ni] = u;
+            b2[ni] = xb[kk * 4 * SH::LDX + ni * 8];
+        }
+    }
+}
+
+// One 16-column chunk: KS k-steps of 4 over both matrices for this warp's NI fiber groups; the
+// fragments of k-step kk + 1 are loaded (into the other register set) while k-step kk's DMMAs issue.
+// Strips past the matrix (mi >= S1 / S2: zero rows of the padded factor) are read but skipped.
 template <int MS, int NI, int NW, bool FWD, int KS>
 __device__ __forceinline__ void rchunk(const double* __restrict__ a1, const double* __restrict__ a2,
                                        const double* __restrict__ xa, const double* __restrict__ xb, int LDA,
                                        int S1, int S2, double (&c1)[MS][NI][2], double (&c2)[MS][NI][2]) {
-    using SH = RShape<NI, NW>;
+    double av1[2][MS], av2[2][MS], b1[2][NI], b2[2][NI];
+    rfrag<MS, NI, NW, FWD>(a1, a2, xa, xb, LDA, 0, av1[0], av2[0], b1[0], b2[0]);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
-        double b1[NI], b2[NI];
-#pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-            const double u = xa[kk * 4 * SH::LDX + ni * 8];
-            if (FWD) {  // xb points at the mirrored row of k-step 0; rows run backwards
-                const double w = xb[-kk * 4 * SH::LDX + ni * 8];
-                b1[ni] = u + w;
-                b2[ni] = u - w;
-            } else {
-                b1[ni] = u;
-                b2[ni] = xb[kk * 4 * SH::LDX + ni * 8];
-            }
-        }
+        const int cur = kk & 1, nxt = cur ^ 1;
+        if (kk + 1 < KS) rfrag<MS, NI, NW, FWD>(a1, a2, xa, xb, LDA, kk + 1, av1[nxt], av2[nxt], b1[nxt], b2[nxt]);
 #pragma unroll
         for (int mi = 0; mi < MS; ++mi) {
             if (mi < S1) {
-                const double av = a1[mi * 8 * LDA + kk * 4];
 #pragma unroll
-                for (int ni = 0; ni < NI; ++ni) rdmma(c1[mi][ni][0], c1[mi][ni][1], av, b1[ni]);
+                for (int ni = 0; ni < NI; ++ni) rdmma(c1[mi][ni][0], c1[mi][ni][1], av1[cur][mi], b1[cur][ni]);
             }
             if (mi < S2) {
-                const double av = a2[mi * 8 * LDA + kk * 4];
 #pragma unroll
-                for (int ni = 0; ni < NI; ++ni) rdmma(c2[mi][ni][0], c2[mi][ni][1], av, b2[ni]);
+                for (int ni = 0; ni < NI; ++ni) rdmma(c2[mi][ni][0], c2[mi][ni][1], av2[cur][mi], b2[cur][ni]);
             }
         }
     }
@@ -162,46 +177,86 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
     const int n = a.geo.n;
     if (warp == NW) {
         // ---------------- producer warp ----------------
+        // Address state per tile: L > 1: lane owns fibers lane + 32 u (pointer to row 0 of each);
+        // L == 1: lane owns chunk row lane % 16 of fibers fp, fp + 2, ... (one pointer, step 2 n).
+        // Interior chunks of full tiles take the unpredicated path (one 64-bit add per copy).
         unsigned seq = 0;
         for (long long tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
             const long long c0 = tile * SH::BN;
+            const bool full_tile = c0 + SH::BN <= ncols;
+            const double* fp0[SH::FPL];
+            bool fv[SH::FPL];
+            if (L != 1) {
+#pragma unroll
+                for (int u = 0; u < SH::FPL; ++u) {
+                    const long long cc = c0 + lane + 32 * u;
+                    fv[u] = cc < ncols && lane + 32 * u < SH::BN;
+                    fp0[u] = X + rbase(fv[u] ? cc : 0, L, n);
+                }
+            }
+            const int r16 = lane & 15, fpar = lane >> 4;
+            const double* f1 = X + (full_tile || c0 + fpar < ncols ? c0 + fpar : 0) * n;
             for (int q = 0; q < a.NQ; ++q, ++seq) {
                 const int s = seq % NS;
                 rmb_wait(&empty[s], ((seq / NS) & 1u) ^ 1u);
                 const unsigned sa = ru32(sX + s * SH::STAGE), sb = sa + 8u * SH::XB;
                 const int ra0 = q * kBK, rb0 = FWD ? n - q * kBK - kBK : a.F + q * kBK;
+                const bool rows_in = ra0 + kBK <= n && rb0 >= 0 && rb0 + kBK <= n;
                 if (L == 1) {
-                    // fibers contiguous: lane = (row r = lane % 16, fiber parity lane / 16)
-                    const int r = lane & 15, fp = lane >> 4;
-                    const int rowa = ra0 + r, rowb = rb0 + r;
-                    const bool va = rowa < n, vb = rowb >= 0 && rowb < n;
-#pragma unroll 4
-                    for (int f = fp; f < SH::BN; f += 2) {
-                        const long long cc = c0 + f;
-                        const bool fv = cc < ncols;
-                        const double* base = X + (fv ? cc : 0) * n;
-                        rcp8(sa + 8u * (r * SH::LDX + f), (va && fv) ? base + rowa : X, va && fv);
-                        rcp8(sb + 8u * (r * SH::LDX + f), (vb && fv) ? base + rowb : X, vb && fv);
+                    const int rowa = ra0 + r16, rowb = rb0 + r16;
+                    const double* pa = f1 + rowa;
+                    const double* pb = f1 + rowb;
+                    const long long step = 2LL * n;
+                    unsigned da = sa + 8u * (r16 * SH::LDX + fpar), db = sb + 8u * (r16 * SH::LDX + fpar);
+                    if (full_tile && rows_in) {
+#pragma unroll 8
+                        for (int f = 0; f < SH::BN; f += 2) {
+                            rcp8(da, pa, true);
+                            rcp8(db, pb, true);
+                            pa += step;
+                            pb += step;
+                            da += 16u;
+                            db += 16u;
+                        }
+                    } else {
+                        const bool va = rowa < n, vb = rowb >= 0 && rowb < n;
+                        for (int f = 0; f < SH::BN; f += 2) {
+                            const bool cv = c0 + fpar + f < ncols;
+                            rcp8(da, (va && cv) ? pa : X, va && cv);
+                            rcp8(db, (vb && cv) ? pb : X, vb && cv);
+                            pa += step;
+                            pb += step;
+                            da += 16u;
+                            db += 16u;
+                        }
                     }
                 } else {
-                    long long fb[SH::FPL];
-                    bool fv[SH::FPL];
 #pragma unroll
                     for (int u = 0; u < SH::FPL; ++u) {
-                        const long long cc = c0 + lane + 32 * u;
-                        fv[u] = cc < ncols && lane + 32 * u < SH::BN;
-                        fb[u] = rbase(fv[u] ? cc : 0, L, n);
-                    }
-#pragma unroll 4
-                    for (int r = 0; r < kBK; ++r) {
-                        const int rowa = ra0 + r, rowb = rb0 + r;
-                        const bool va = rowa < n, vb = rowb >= 0 && rowb < n;
-#pragma unroll
-                        for (int u = 0; u < SH::FPL; ++u) {
-                            const int f = lane + 32 * u;
-                            if (SH::BN % 32 != 0 && f >= SH::BN) continue;
-                            rcp8(sa + 8u * (r * SH::LDX + f), (va && fv[u]) ? X + fb[u] + L * rowa : X, va && fv[u]);
-                            rcp8(sb + 8u * (r * SH::LDX + f), (vb && fv[u]) ? X + fb[u] + L * rowb : X, vb && fv[u]);
+                        if (SH::BN % 32 != 0 && lane + 32 * u >= SH::BN) continue;
+                        const double* pa = fp0[u] + L * ra0;
+                        const double* pb = fp0[u] + L * rb0;
+                        unsigned da = sa + 8u * (lane + 32 * u), db = sb + 8u * (lane + 32 * u);
+                        if (fv[u] && rows_in) {
+#pragma unroll 8
+                            for (int r = 0; r < kBK; ++r) {
+                                rcp8(da, pa, true);
+                                rcp8(db, pb, true);
+                                pa += L;
+                                pb += L;
+                                da += 8u * SH::LDX;
+                                db += 8u * SH::LDX;
+                            }
+                        } else {
+                            for (int r = 0; r < kBK; ++r) {
+                                const bool va = fv[u] && ra0 + r < n, vb = fv[u] && rb0 + r >= 0 && rb0 + r < n;
+                                rcp8(da, va ? pa : X, va);
+                                rcp8(db, vb ? pb : X, vb);
+                                pa += L;
+                                pb += L;
+                                da += 8u * SH::LDX;
+                                db += 8u * SH::LDX;
+                            }
                         }
                     }
                 }

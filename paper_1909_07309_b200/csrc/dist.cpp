@@ -27,7 +27,8 @@ using namespace stiga::capi;
 namespace stiga {
 stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* const* M, int n_t, const double* Wt,
                      const double* Mt, double gamma, double nu, const double* scaling, long long scaling_len,
-                     int device, const std::function<void(stiga_fd_s&)>& prepare);  // capi.cpp
+                     int device, const std::function<void(stiga_fd_s&)>& prepare, int flags,
+                     const double* d_scaling);  // capi.cpp
 stiga_kronsum_s* ks_build_spacetime(int d, const int* n, const double* const* K, const double* const* M, int n_t,
                                     const double* Wt, const double* Mt, double gamma, double nu, int device);
 stiga_kronsum_s* ks_build_physical(stiga_problem_s* prob, int p, int n_el, int device);
@@ -467,7 +468,7 @@ int stiga_fd_setup_sharded(int d, const int* n, const double* const* K, const do
             T.b_shift = 0;
             h.shard = std::move(S);
         };
-        *out = fd_build(d, n, K, M, n_t, Wt, Mt, gamma, nu, nullptr, 0, comm->device, prepare);
+        *out = fd_build(d, n, K, M, n_t, Wt, Mt, gamma, nu, nullptr, 0, comm->device, prepare, 0, nullptr);
     });
 }
 

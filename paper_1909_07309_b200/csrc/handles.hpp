@@ -114,6 +114,7 @@ struct stiga_fd_s {
     DBuf Jt_t, J_t;
     std::vector<std::unique_ptr<DBuf>> lam;
     DBuf S_inv, pair_c, pair_c1, pair_c1sq, pair_gg, g, dinv;
+    bool schur_on_device = false;  // S_inv computed by the device setup (F.S_inv empty)
     DBuf scratch, scratch2;
     gpu::ArrowParams ap;
 

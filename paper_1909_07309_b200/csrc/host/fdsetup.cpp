@@ -171,7 +171,7 @@ Vector FDFactors::S_inv_dev() const {
 
 FDFactors fd_setup(const std::vector<DenseMatrix>& space_K, const std::vector<DenseMatrix>& space_M,
                    const DenseMatrix& Wt, const DenseMatrix& Mt, double gamma, double nu,
-                   const double* scaling) {
+                   const double* scaling, bool host_schur) {
     if (gamma <= 0.0) throw std::invalid_argument("ExtendedFDPreconditioner: gamma must be positive");
     if (nu <= 0.0) throw std::invalid_argument("ExtendedFDPreconditioner: nu must be positive");
     if (space_K.size() != space_M.size() || space_K.empty())
@@ -223,6 +223,16 @@ FDFactors fd_setup(const std::vector<DenseMatrix>& space_K, const std::vector<De
     F.gamma = gamma;
     F.nu = nu;
 
+    if (!host_schur) {  // Lambda_s, S^-1 and their checks on the device (capi.cpp fd_build)
+        if (scaling) {
+            F.d_inv_sqrt.resize(static_cast<size_t>(F.n_dof));
+            for (Index i = 0; i < F.n_dof; ++i)
+                if (!(scaling[i] > 0.0))
+                    throw std::invalid_argument("ExtendedFDPreconditioner: scaling must be strictly positive");
+            for (Index i = 0; i < F.n_dof; ++i) F.d_inv_sqrt[i] = 1.0 / std::sqrt(scaling[i]);
+        }
+        return F;
+    }
     const Vector lam_s = kron_sum_eigenvalues(F.lambda);
     for (double v : lam_s)
         if (v <= 0.0)

@@ -48,10 +48,11 @@ bool centrosymmetric(const DenseMatrix& A, double rtol);
 std::vector<double> fold_matrices(const FoldBasis& fb, bool forward, int Mp, int Kp);
 
 /// Throws std::invalid_argument / std::runtime_error exactly where the reference does.
-/// `scaling` (length N_dof) may be null.
+/// `scaling` (length N_dof) may be null.  host_schur = false leaves Lambda_s / S_inv (and their
+/// positivity / singularity checks) to the device setup (cuda/setup_kernels.cu): S_inv stays empty.
 FDFactors fd_setup(const std::vector<DenseMatrix>& space_K, const std::vector<DenseMatrix>& space_M,
                    const DenseMatrix& Wt, const DenseMatrix& Mt, double gamma, double nu,
-                   const double* scaling);
+                   const double* scaling, bool host_schur = true);
 
 /// Kronecker-sum spatial eigenvalues Lambda_s, left-to-right adds (fdsolve.cpp:91-99).
 Vector kron_sum_eigenvalues(const std::vector<Vector>& lambda);

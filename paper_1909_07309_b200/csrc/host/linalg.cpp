@@ -229,9 +229,23 @@ static void tridiagonal_ql(Vector& d, Vector& e, DenseMatrix& Z) {
     }
 }
 
+namespace {
+thread_local SymEigFn g_sym_eig_backend = nullptr;
+}
+
+SymEigFn set_sym_eig_backend(SymEigFn fn) {
+    const SymEigFn prev = g_sym_eig_backend;
+    g_sym_eig_backend = fn;
+    return prev;
+}
+
 void sym_eig(const DenseMatrix& A, Vector& w, DenseMatrix& Q) {
     const Index n = A.rows;
     if (A.cols != n) throw std::invalid_argument("sym_eig: matrix not square");
+    if (g_sym_eig_backend) {
+        g_sym_eig_backend(A, w, Q);
+        return;
+    }
     DenseMatrix T = A;
     // symmetrize defensively (the callers pass symmetric matrices)
     for (Index j = 0; j < n; ++j)

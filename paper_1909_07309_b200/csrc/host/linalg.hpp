@@ -53,4 +53,15 @@ void trsm_lower_t(const DenseMatrix& L, DenseMatrix& B);
 /// Throws std::runtime_error if the QL iteration does not converge.
 void sym_eig(const DenseMatrix& A, Vector& w, DenseMatrix& Q);
 
+/// Alternative symmetric eigensolver for sym_eig on the calling thread (nullptr: the host
+/// Householder + QL).  Used by the setup's cuSOLVER backend (host/eig_device.cpp) through
+/// ScopedSymEig; same contract: ascending w, orthonormal columns of Q.
+using SymEigFn = void (*)(const DenseMatrix& A, Vector& w, DenseMatrix& Q);
+SymEigFn set_sym_eig_backend(SymEigFn fn);
+struct ScopedSymEig {
+    SymEigFn prev;
+    explicit ScopedSymEig(SymEigFn fn) : prev(set_sym_eig_backend(fn)) {}
+    ~ScopedSymEig() { set_sym_eig_backend(prev); }
+};
+
 } // namespace stiga

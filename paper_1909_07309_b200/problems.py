@@ -111,19 +111,22 @@ class Problem:
                     "fields")
         return nu.value, gam.value
 
-    def geometry_pieces(self, p, n_el, want_D=True, device=None):
+    def geometry_pieces(self, p, n_el, want_D=True, device=None, D_on_device=False):
         """make_geometry_preconditioner inputs (solver.cpp:127-144): SpaceTimePieces with the
         separated-coefficient factors K~, M~, W_t, weighted M_t, plus D and phi/Phi.
 
         device=None: D = diag(A)/diag(A~) with diag(A) from the host quadrature of the physical
         diagonal.  device=k: diag(A) from the physical K_s, M_s assembled on GPU k (the operator the
         GMRES solve applies; `pc.A` keeps it) -- the same quadrature sums in another order, seconds
-        instead of the host's per-element loop at c4 sizes."""
+        instead of the host's per-element loop at c4 sizes.  The ratio itself is formed on the device
+        (stiga_geometry_scaling_device, bit-identical to the host division); D_on_device=True keeps D
+        there as a CUDA tensor (ExtendedFDPreconditioner.setup then forms D^-1/2 on the device)."""
         if want_D and device is not None:
             pc = self.geometry_pieces(p, n_el, want_D=False)
             A = stiga.KronSumOperator.physical(self, p, n_el, device=device)
-            den = kron_sum_diagonal(stiga.kron_sum_terms(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0))
-            pc.D = A.diagonal() / den
+            At = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=device)
+            Dd = stiga.geometry_scaling_device(A, At)
+            pc.D = Dd if D_on_device else Dd.cpu().numpy()
             pc.A = A
             return pc
         ns = stiga.space_dim(p, n_el)
@@ -256,7 +259,7 @@ class SpaceTimeSystem:
             self.Wt, self.Mt, self.Mt_plain = pc.Wt, pc.Mt, pc.Mt
             self.A = stiga.KronSumOperator.spacetime(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, device=device)
         else:
-            pc = self.problem.geometry_pieces(p, n_el, want_D=True, device=device)
+            pc = self.problem.geometry_pieces(p, n_el, want_D=True, device=device, D_on_device=True)
             self._pc = pc
             self.Wt, self.Mt = pc.Wt, pc.Mt
             _, self.Mt_plain = stiga.assemble_time_matrices(p, n_el, self.T)
@@ -290,10 +293,11 @@ class SpaceTimeSystem:
     def make_geometry_preconditioner(self):
         """A-hat-G (solver.cpp:127-144): separated factors, weighted M_t, D = diag(A)/diag(A~)."""
         if self._pc is None:
-            self._pc = self.problem.geometry_pieces(self.p, self.n_el, want_D=True, device=self.device)
+            self._pc = self.problem.geometry_pieces(self.p, self.n_el, want_D=True, device=self.device,
+                                                    D_on_device=True)
         pc = self._pc
         return stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=pc.D,
-                                                    device=self.device)
+                                                    device=self.device, device_schur=True)
 
     def solve(self, P=None, opts=None, b=None):
         """solver.cpp:146-155: left-preconditioned GMRES from x0 = 0 -> (DiscreteSolution, SolveReport)."""

@@ -258,9 +258,20 @@ class ExtendedFDPreconditioner:
         return self.offset, self.offset + self.n_local
 
     @staticmethod
-    def setup(space_K, space_M, Wt, Mt, gamma, nu, scaling=None, device=0, comm=None):
+    def setup(space_K, space_M, Wt, Mt, gamma, nu, scaling=None, device=0, comm=None, device_schur=False,
+              eig="host"):
         """fdsolve.cpp:67-153 (host factorizations, one upload of the factors).  With comm (a Comm):
-        the time-sharded handle of this rank (collective); `scaling` is then D on the local time slab."""
+        the time-sharded handle of this rank (collective); `scaling` is then D on the local time slab.
+
+        Device-side setup (stiga_fd_setup_ex): scaling may be a CUDA tensor (D^-1/2 formed on the
+        device); device_schur=True computes Lambda_s / S^-1 on the device (bit-identical);
+        eig="cusolver" runs the setup's symmetric eigenproblems with cuSOLVER."""
+        if eig not in ("host", "cusolver"):
+            raise ValueError("ExtendedFDPreconditioner: eig must be 'host' or 'cusolver'")
+        dev_scaling = scaling is not None and _is_torch(scaling) and scaling.is_cuda
+        if comm is None and (dev_scaling or device_schur or eig == "cusolver"):
+            return ExtendedFDPreconditioner._setup_ex(space_K, space_M, Wt, Mt, gamma, nu, scaling if dev_scaling else None,
+                                                      None if dev_scaling else scaling, device, device_schur, eig)
         if len(space_K) != len(space_M) or len(space_K) == 0:
             raise ValueError("ExtendedFDPreconditioner: per-direction matrices mismatch")
         Ks = [_colmajor(k) for k in space_K]
@@ -285,6 +296,28 @@ class ExtendedFDPreconditioner:
         check(lib().stiga_fd_setup(len(Ks), n, _ptr_array(Ks), _ptr_array(Ms), n_t, _ptr(W), _ptr(Mm),
                                    float(gamma), float(nu), _ptr(sc) if sc is not None else None,
                                    len(sc) if sc is not None else 0, int(device), ctypes.byref(h)), "fd_setup")
+        return ExtendedFDPreconditioner(h.value, device)
+
+    @staticmethod
+    def _setup_ex(space_K, space_M, Wt, Mt, gamma, nu, d_scaling, scaling, device, device_schur, eig):
+        if len(space_K) != len(space_M) or len(space_K) == 0:
+            raise ValueError("ExtendedFDPreconditioner: per-direction matrices mismatch")
+        Ks = [_colmajor(k) for k in space_K]
+        Ms = [_colmajor(m) for m in space_M]
+        n = (ctypes.c_int * len(Ks))(*[int(np.asarray(k).shape[0]) for k in space_K])
+        W = _colmajor(Wt)
+        Mm = _colmajor(Mt)
+        n_t = int(np.asarray(Wt).shape[0])
+        from ._lib import SETUP_CUSOLVER, SETUP_DEVICE_SCHUR, FdSetupOptions
+
+        opts = FdSetupOptions((SETUP_DEVICE_SCHUR if device_schur else 0) | (SETUP_CUSOLVER if eig == "cusolver" else 0),
+                              d_scaling.data_ptr() if d_scaling is not None else None)
+        sc = None if scaling is None else _f64(scaling)
+        length = d_scaling.numel() if d_scaling is not None else (len(sc) if sc is not None else 0)
+        h = ctypes.c_void_p()
+        check(lib().stiga_fd_setup_ex(len(Ks), n, _ptr_array(Ks), _ptr_array(Ms), n_t, _ptr(W), _ptr(Mm), float(gamma),
+                                      float(nu), _ptr(sc) if sc is not None else None, length, ctypes.byref(opts),
+                                      int(device), ctypes.byref(h)), "fd_setup_ex")
         return ExtendedFDPreconditioner(h.value, device)
 
     def __del__(self):
@@ -495,6 +528,28 @@ class KronSumOperator:
         d = np.zeros(self.n_dof)
         check(lib().stiga_kronsum_diagonal(self._h, _ptr(d)), "kronsum_diagonal")
         return d
+
+    def diagonal_device(self, out=None, stream=None):
+        """KronSumOperator::diagonal() into a CUDA tensor (bit-identical to diagonal())."""
+        import torch
+
+        if out is None:
+            out = torch.empty(self.n_dof, dtype=torch.float64, device=f"cuda:{self.device}")
+        check(lib().stiga_kronsum_diagonal_device(self._h, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)),
+              "kronsum_diagonal_device")
+        return out
+
+
+def geometry_scaling_device(A, Atilde, out=None, stream=None):
+    """D = diag(A) / diag(A~) (solver.cpp:138-142) on the device: A the system operator, A~ the
+    Kronecker-sum operator of the separated factors (gamma = nu = 1)."""
+    import torch
+
+    if out is None:
+        out = torch.empty(A.n_dof, dtype=torch.float64, device=f"cuda:{A.device}")
+    check(lib().stiga_geometry_scaling_device(A.handle, Atilde.handle, ctypes.c_void_p(out.data_ptr()),
+                                              _stream_handle(stream)), "geometry_scaling_device")
+    return out
 
 
 # ----------------------------------------------------------------------------------------

@@ -101,12 +101,51 @@ int main(int argc, char** argv) {
             diff += (x_native[i] - x_cb[i]) * (x_native[i] - x_cb[i]);
             nrm += x_native[i] * x_native[i];
         }
+        // SpaceTimeSystem on a curved geometry (solver.cpp:34-155): the physical A_, A-hat-G with D formed on
+        // the device, the device RHS, GMRES through the handles, compute_errors -- no host N_dof array
+        Problem prob("quarter-annulus-2d");
+        const int ps = 2, nels = 8;
+        KronSumOperator Aphys = KronSumOperator::physical(prob, ps, nels);
+        int nsd = 0, ntd = 0;
+        check(stiga_space_dim(ps, nels, 0, &nsd));
+        check(stiga_space_dim(ps, nels, 1, &ntd));
+        const size_t nn = static_cast<size_t>(nsd) * nsd;
+        std::vector<double> Kt(2 * nn), Mts(2 * nn);
+        Dense Wg(ntd), Mg(ntd);
+        check(stiga_geometry_preconditioner_pieces(prob.handle(), ps, nels, Kt.data(), Mts.data(), Wg.a.data(),
+                                                   Mg.a.data(), nullptr, nullptr, nullptr, nullptr, nullptr));
+        std::vector<Dense> Ks(2, Dense(nsd)), Ms(2, Dense(nsd));
+        for (int l = 0; l < 2; ++l) {
+            std::copy(Kt.begin() + l * nn, Kt.begin() + (l + 1) * nn, Ks[l].a.begin());
+            std::copy(Mts.begin() + l * nn, Mts.begin() + (l + 1) * nn, Ms[l].a.begin());
+        }
+        KronSumOperator Atil = KronSumOperator::spacetime(Ks, Ms, Wg, Mg, 1.0, 1.0);
+        const long long ns = Aphys.size();
+        double *d_D = nullptr, *d_bs = nullptr, *d_xs = nullptr;
+        cuck(cudaMalloc(&d_D, ns * sizeof(double)));
+        cuck(cudaMalloc(&d_bs, ns * sizeof(double)));
+        cuck(cudaMalloc(&d_xs, ns * sizeof(double)));
+        geometry_scaling_device(Aphys, Atil, d_D);
+        Preconditioner PG = Preconditioner::setup_device(Ks, Ms, Wg, Mg, 1.0, 1.0, d_D, ns);
+        assemble_rhs(prob, ps, nels, d_bs);
+        GmresOptions so;
+        so.tol = 1e-10;
+        so.max_krylov = 300;
+        const SolveReport sys = gmres(Aphys, &PG, d_bs, d_xs, so);
+        const Errors err = compute_errors(prob, ps, nels, d_xs, ps + 3);
+        const auto means = system_means(prob, ps, nels);
+        cudaFree(d_D);
+        cudaFree(d_bs);
+        cudaFree(d_xs);
         std::printf("{\"n\": %lld, \"invalid_argument\": %s, \"native_its\": %d, \"native_converged\": %s, "
                     "\"cb_its\": %d, \"cb_converged\": %s, \"cb_vs_native\": %.3e, \"shift_its\": %d, "
-                    "\"shift_converged\": %s, \"sigma\": %.17g}\n",
+                    "\"shift_converged\": %s, \"sigma\": %.17g, \"sys_n\": %lld, \"sys_its\": %d, "
+                    "\"sys_converged\": %s, \"err_l2l2\": %.17g, \"err_x\": %.17g, \"gamma_mean\": %.17g, "
+                    "\"nu_mean\": %.17g}\n",
                     n, threw ? "true" : "false", native.iterations, native.converged ? "true" : "false",
                     cb.iterations, cb.converged ? "true" : "false", std::sqrt(diff / nrm), sh.iterations,
-                    sh.converged ? "true" : "false", sigma);
+                    sh.converged ? "true" : "false", sigma, ns, sys.iterations, sys.converged ? "true" : "false",
+                    err.l2l2, err.x_upper, means.first, means.second);
         cudaFree(d_b);
         cudaFree(d_x);
         cudaFree(d_t);

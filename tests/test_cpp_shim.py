@@ -70,3 +70,14 @@ def test_cpp_shim_parity_and_gmres():
     xs, reps = ogm.gmres(lambda v: Ao.apply(v) + sigma * v, Pg.apply, g["r"], 1e-8, 200, 50)
     assert out["shift_converged"] and abs(out["shift_its"] - reps.iterations) <= 1
     assert rel(x_shift, xs) <= 1e-6
+    # SpaceTimeSystem through the C++ binding: annulus, A-hat-G with device D, device RHS, errors
+    from oracle import problems as opr
+
+    prob = opr.make_full_problem("quarter-annulus-2d")
+    sysm = opr.SpaceTimeSystem(prob, 2, 8)
+    x, rep = sysm.solve(sysm.make_geometry_preconditioner(), tol=1e-10, max_krylov=300)
+    eo = opr.compute_errors(x, sysm.spaces, sysm.tspace, prob, 5)
+    assert out["sys_n"] == sysm.n_dof and out["sys_converged"]
+    assert abs(out["sys_its"] - rep.iterations) <= 1
+    assert abs(out["err_l2l2"] - eo[0]) <= 1e-6 * eo[0] and abs(out["err_x"] - eo[1]) <= 1e-6 * eo[1]
+    assert abs(out["gamma_mean"] - sysm.gamma_mean) <= 1e-14 and abs(out["nu_mean"] - sysm.nu_mean) <= 1e-13
