@@ -187,6 +187,23 @@ int stiga_geometry_preconditioner_pieces(stiga_problem_t P, int p, int n_el, dou
 
 }  // extern "C"
 
+namespace {
+// Dense mode-product candidates; STIGA_DENSE_KERNEL=res / stream restricts them to the resident /
+// streaming kernels (tests), unset: both kinds go to the autotuner.
+std::vector<gpu::Tiling> dense_candidates(int m, int n) {
+    std::vector<gpu::Tiling> c = gpu::mode_tiling_candidates(m, n);
+    const char* k = std::getenv("STIGA_DENSE_KERNEL");
+    if (k && (std::string(k) == "res" || std::string(k) == "stream")) {
+        const bool want_res = std::string(k) == "res";
+        std::vector<gpu::Tiling> f;
+        for (const auto& t : c)
+            if ((t.res != 0) == want_res) f.push_back(t);
+        if (!f.empty()) c = f;
+    }
+    return c;
+}
+}  // namespace
+
 namespace stiga {
 // Host setup (fdsolve.cpp:67-153) + device upload + autotune of an FD handle.  `prepare` (sharded
 // handles, dist.cpp) runs after the host setup and before the uploads: it sets the stage spans, the
@@ -239,7 +256,7 @@ stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* 
         DeviceGuard dg(device);
         if (prepare) prepare(*h);
         for (int l = 0; l < d; ++l) {
-            std::vector<gpu::Tiling> dense = gpu::mode_tiling_candidates(F.n[l], F.n[l]);
+            std::vector<gpu::Tiling> dense = dense_candidates(F.n[l], F.n[l]);
             if (dense.empty()) throw std::runtime_error("internal: no mode-product tiling");
             int rows = 0;
             for (const auto& t : dense) rows = std::max(rows, t.Mp);
@@ -283,7 +300,7 @@ stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* 
             // has no such epilogue (folded WM = 2 tilings carry their own scatter epilogue)
             gpu::Tiling tdense = dense.front();
             for (const auto& t : dense)
-                if (t.WM == 1) {
+                if (t.WM == 1 && !t.res) {
                     tdense = t;
                     break;
                 }
@@ -294,7 +311,7 @@ stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* 
             h->lam.back()->upload(F.lambda_dev(l));
         }
         h->cand_time = gpu::time_tiling_candidates(F.n_t);
-        h->cand_ts = gpu::mode_tiling_candidates(F.n_t, F.n_t);
+        h->cand_ts = dense_candidates(F.n_t, F.n_t);
         if (h->cand_ts.empty()) throw std::runtime_error("internal: no time-product tiling");
         int trows = 0;
         for (const auto& t : h->cand_time) trows = std::max(trows, t.Mp);

@@ -81,6 +81,8 @@ struct Tiling {
     int nstage = 3;
     int fold = 0;     // 1: folded (centrosymmetric) product, fold_kernels.cu; 2: the resident-factor persistent
                       // folded kernel, fold_res.cu; MI/RB/Mp/Kp refer to the folded matrices
+    int res = 0;      // 1: dense resident-factor persistent kernel (dense_res.cu); MI = strips per warp,
+                      // WM = strip groups, WN = fiber groups, MpB = rows per row block
     size_t smem = 0;
     int ctas_per_sm = 1;
     int threads() const { return 32 * WM * WN; }
@@ -116,6 +118,12 @@ cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double
                                 bool forward, const double* post_scale, cudaStream_t stream,
                                 const double* pre_scale = nullptr, const Scatter* sc = nullptr);
 size_t fold_prescale_smem(const Tiling& t);
+/// Dense resident-factor persistent mode product (dense_res.cu, Tiling::res == 1), candidates
+/// for an m x n factor (the fused D^-1/2 pre-scale needs its own smem: prescale = true).
+std::vector<Tiling> mode_res_candidates(int m, int n, bool prescale);
+size_t mode_res_smem(const Tiling& t, bool prescale);
+cudaError_t launch_mode_res(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
+                            const double* post, const double* pre, cudaStream_t st);
 /// Resident-factor persistent folded product (fold_res.cu, Tiling::fold == 2): both folded matrices in
 /// shared memory for the whole launch, one CTA per SM, warp-specialised cp.async/mbarrier pipeline.
 /// Candidates for n with 4 <= ceil(ceil(n/2)/8) <= 11; no pre-scale / scatter epilogue.

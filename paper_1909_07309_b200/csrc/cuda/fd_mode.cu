@@ -17,6 +17,9 @@
 // time direction costs one HBM round trip instead of three.
 #include "fd_mode_impl.cuh"
 
+#include <cstdlib>
+#include <string>
+
 namespace stiga {
 namespace gpu {
 
@@ -100,6 +103,10 @@ std::vector<Tiling> mode_tiling_candidates(int m, int n) {
     }
     std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
     std::vector<Tiling> out;
+    // the dense resident-factor kernel (dense_res.cu) measured slower than the streaming kernel on every
+    // BASELINE shape (c4 modes 0.156 vs 0.118 ms, c5p5 time GEMM 9.9 vs 7.8 ms): opt-in only
+    const char* dk = std::getenv("STIGA_DENSE_KERNEL");
+    if (dk && std::string(dk) == "res") out = mode_res_candidates(m, n, false);
     for (auto& e : c) out.push_back(e.second);
     return out;
 }
@@ -107,12 +114,11 @@ std::vector<Tiling> mode_tiling_candidates(int m, int n) {
 Tiling choose_mode_tiling(int m, int n, bool prescale) {
     (void)prescale;  // the D^-1/2 pre-scale is a separate elementwise pass
     const std::vector<Tiling> c = mode_tiling_candidates(m, n);
-    if (c.empty()) {
-        Tiling t;
-        t.MI = 0;
-        return t;
-    }
-    return c.front();
+    for (const Tiling& t : c)
+        if (!t.res) return t;  // untuned callers take the streaming kernel's heuristic first choice
+    Tiling t;
+    t.MI = 0;
+    return t;
 }
 
 
@@ -121,6 +127,7 @@ size_t prescale_smem(const Tiling& t) {
 }
 
 bool prescale_fits(const Tiling& t) {
+    if (t.res) return mode_res_smem(t, true) + 1024 <= kSmemPerCTA;
     if (t.fold) return fold_prescale_smem(t) <= kSmemPerCTA;
     return t.WM == 1 && prescale_smem(t) <= kSmemPerCTA;
 }
@@ -129,6 +136,10 @@ cudaError_t launch_mode_product(const Tiling& t, const ModeGeom& g, const double
                                 const double* post_scale, cudaStream_t st, const double* pre_scale, const Scatter* sc) {
     if (g.ncols <= 0) return cudaSuccess;
     if (pre_scale && !prescale_fits(t)) return cudaErrorInvalidValue;
+    if (t.res) {
+        if (sc) return cudaErrorInvalidValue;  // no scatter epilogue on the resident kernel
+        return launch_mode_res(t, g, X, Y, Jpad, post_scale, pre_scale, st);
+    }
     if (sc && (pre_scale || post_scale || sc->G < 1 || sc->G > kMaxRanks)) return cudaErrorInvalidValue;
     return dispatch_mode(t, g, X, Y, Jpad, post_scale, pre_scale, st, nullptr, sc);
 }

@@ -21,6 +21,7 @@
 //  * DMMA.8x8x4 (FP64 tensor core) with A fragments from the resident factors (row stride == 4 mod 16
 //    doubles) and B fragments from the stage (row stride BN + 4): bank-conflict free.
 #include "fd_kernels.cuh"
+#include "res_common.cuh"
 
 #include <algorithm>
 #include <cstdint>
@@ -34,43 +35,7 @@ namespace {
 constexpr int kBK = 16;
 constexpr size_t kSmemPerCTA = 227 * 1024;
 
-__device__ __forceinline__ void rdmma(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(c0), "+d"(c1)
-                 : "d"(a), "d"(b));
-}
-__device__ __forceinline__ unsigned ru32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void rcp8(unsigned dst, const double* src, bool valid) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void rmb_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(ru32(bar)), "r"(count));
-}
-__device__ __forceinline__ void rmb_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(ru32(bar)) : "memory");
-}
-// arrive on `bar` when every cp.async issued so far by this thread has landed (counts against the
-// barrier's expected arrivals: .noinc)
-__device__ __forceinline__ void rmb_cp_arrive(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(ru32(bar)) : "memory");
-}
-__device__ __forceinline__ void rmb_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "RWAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra RWAIT_%=;\n"
-        "}\n" ::"r"(ru32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ long long rbase(long long cc, long long L, int n) {
-    if (L == 1) return cc * n;
-    const long long r = cc / L;
-    return (cc - r * L) + L * static_cast<long long>(n) * r;
-}
+using namespace resdev;
 
 struct RArgs {
     ModeGeom geo;
@@ -79,6 +44,7 @@ struct RArgs {
     int NQ;         // 16-column chunks per tile
     int S1, S2;     // live 8-row strips of the first / second matrix
     long long A2;   // offset of the second matrix in the global factor buffer (Mp * Kp)
+    int Mp;         // rows of each matrix in the global factor buffer
     long long ntiles;
 };
 
@@ -122,23 +88,21 @@ __device__ __forceinline__ void rfrag(const double* __restrict__ a1, const doubl
 template <int MS, int NI, int NW, bool FWD, int KS>
 __device__ __forceinline__ void rchunk(const double* __restrict__ a1, const double* __restrict__ a2,
                                        const double* __restrict__ xa, const double* __restrict__ xb, int LDA,
-                                       int S1, int S2, double (&c1)[MS][NI][2], double (&c2)[MS][NI][2]) {
+                                       double (&c1)[MS][NI][2], double (&c2)[MS][NI][2]) {
     double av1[2][MS], av2[2][MS], b1[2][NI], b2[2][NI];
     rfrag<MS, NI, NW, FWD>(a1, a2, xa, xb, LDA, 0, av1[0], av2[0], b1[0], b2[0]);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
         const int cur = kk & 1, nxt = cur ^ 1;
         if (kk + 1 < KS) rfrag<MS, NI, NW, FWD>(a1, a2, xa, xb, LDA, kk + 1, av1[nxt], av2[nxt], b1[nxt], b2[nxt]);
+        // every strip unconditionally: padded strips are zero rows of the resident factors (a predicated
+        // mma.sync costs a WARPSYNC + NOP per DMMA); their accumulators are never stored
 #pragma unroll
         for (int mi = 0; mi < MS; ++mi) {
-            if (mi < S1) {
 #pragma unroll
-                for (int ni = 0; ni < NI; ++ni) rdmma(c1[mi][ni][0], c1[mi][ni][1], av1[cur][mi], b1[cur][ni]);
-            }
-            if (mi < S2) {
+            for (int ni = 0; ni < NI; ++ni) rdmma(c1[mi][ni][0], c1[mi][ni][1], av1[cur][mi], b1[cur][ni]);
 #pragma unroll
-                for (int ni = 0; ni < NI; ++ni) rdmma(c2[mi][ni][0], c2[mi][ni][1], av2[cur][mi], b2[cur][ni]);
-            }
+            for (int ni = 0; ni < NI; ++ni) rdmma(c2[mi][ni][0], c2[mi][ni][1], av2[cur][mi], b2[cur][ni]);
         }
     }
 }
@@ -154,7 +118,7 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
     extern __shared__ __align__(16) double smem[];
     __shared__ uint64_t full[NS], empty[NS];
     const int LDA = a.LDA;
-    const int MR = 8 * MS;  // resident rows per matrix
+    constexpr int MR = 8 * MSW * WS;  // resident rows per matrix (strips past the factor: zero rows)
     double* sA = smem;                  // [2][MR][LDA]
     double* sX = smem + 2 * MR * LDA;   // [NS][STAGE]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -163,7 +127,7 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
     for (int i = tid; i < 2 * MR * a.Kp; i += blockDim.x) {
         const int m = i / (MR * a.Kp), rem = i - m * MR * a.Kp;
         const int row = rem / a.Kp, col = rem - row * a.Kp;
-        sA[(m * MR + row) * LDA + col] = J[m * a.A2 + static_cast<long long>(row) * a.Kp + col];
+        sA[(m * MR + row) * LDA + col] = row < a.Mp ? J[m * a.A2 + static_cast<long long>(row) * a.Kp + col] : 0.0;
     }
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -196,6 +160,20 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
             }
             const int r16 = lane & 15, fpar = lane >> 4;
             const double* f1 = X + (full_tile || c0 + fpar < ncols ? c0 + fpar : 0) * n;
+            if (POST) {  // the epilogue's D^-1/2 rows of this tile into L2, ~NQ chunks ahead of their use
+                if (L != 1) {
+#pragma unroll
+                    for (int u = 0; u < SH::FPL; ++u)
+                        if (fv[u] && (lane & 15) == 0)
+                            for (int r = 0; r < n; ++r)
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(post + (fp0[u] - X) + L * r));
+                } else {
+                    for (int f = lane; f < SH::BN; f += 32)
+                        if (c0 + f < ncols)
+                            for (int r = 0; r < n; r += 16)
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(post + (c0 + f) * n + r));
+                }
+            }
             for (int q = 0; q < a.NQ; ++q, ++seq) {
                 const int s = seq % NS;
                 rmb_wait(&empty[s], ((seq / NS) & 1u) ^ 1u);
@@ -273,7 +251,6 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
     const int so = ws * MSW;  // first strip of this warp
     const double* a1 = sA + (so * 8 + g) * LDA + t;
     const double* a2 = sA + MR * LDA + (so * 8 + g) * LDA + t;
-    const int S1w = min(MSW, a.S1 - so), S2w = min(MSW, a.S2 - so);
     const int fcol = wf * NI * 8 + g;  // this lane's B-fragment fiber column within the tile
     unsigned seq = 0;
     for (long long tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
@@ -291,10 +268,10 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
             const double* xb = st + SH::XB + (FWD ? (kBK - 1 - t) : t) * SH::LDX + fcol;
             const int k0 = q * kBK;
             const int ks = min(kBK, a.Kp - k0) >> 2;
-            if (ks == 4) rchunk<MSW, NI, WF, FWD, 4>(a1 + k0, a2 + k0, xa, xb, LDA, S1w, S2w, c1, c2);
-            else if (ks == 3) rchunk<MSW, NI, WF, FWD, 3>(a1 + k0, a2 + k0, xa, xb, LDA, S1w, S2w, c1, c2);
-            else if (ks == 2) rchunk<MSW, NI, WF, FWD, 2>(a1 + k0, a2 + k0, xa, xb, LDA, S1w, S2w, c1, c2);
-            else rchunk<MSW, NI, WF, FWD, 1>(a1 + k0, a2 + k0, xa, xb, LDA, S1w, S2w, c1, c2);
+            if (ks == 4) rchunk<MSW, NI, WF, FWD, 4>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
+            else if (ks == 3) rchunk<MSW, NI, WF, FWD, 3>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
+            else if (ks == 2) rchunk<MSW, NI, WF, FWD, 2>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
+            else rchunk<MSW, NI, WF, FWD, 1>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
             __syncwarp();
             if (lane == 0) rmb_arrive(&empty[s]);
         }
@@ -309,6 +286,41 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
                 cv[ni][v] = cc < ncols;
                 ob[ni][v] = rbase(cv[ni][v] ? cc : 0, L, n);
             }
+        if constexpr (POST) {
+            // D^-1/2 post-scale: every scale value of the tile is loaded (into the dead fragment
+            // registers) before the first store; the producer prefetched these rows into L2
+            double pl[MSW][NI][2], ph[MSW][NI][2];
+#pragma unroll
+            for (int mi = 0; mi < MSW; ++mi) {
+                const int i = (so + mi) * 8 + g;
+                const int ilo = i < a.F ? i : 0, ihi = i < a.h ? n - 1 - i : 0;
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        pl[mi][ni][v] = cv[ni][v] ? __ldg(post + ob[ni][v] + L * ilo) : 0.0;
+                        ph[mi][ni][v] = cv[ni][v] ? __ldg(post + ob[ni][v] + L * ihi) : 0.0;
+                    }
+            }
+#pragma unroll
+            for (int mi = 0; mi < MSW; ++mi) {
+                const int i = (so + mi) * 8 + g;
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        if (!cv[ni][v]) continue;
+                        double* y = Y + ob[ni][v];
+                        if (i < a.h) {
+                            y[L * i] = pl[mi][ni][v] * (c1[mi][ni][v] + c2[mi][ni][v]);
+                            y[L * (n - 1 - i)] = ph[mi][ni][v] * (c1[mi][ni][v] - c2[mi][ni][v]);
+                        } else if (i < a.F) {  // middle row (odd n)
+                            y[L * i] = pl[mi][ni][v] * c1[mi][ni][v];
+                        }
+                    }
+            }
+            continue;
+        }
 #pragma unroll
         for (int mi = 0; mi < MSW; ++mi) {
             const int i = (so + mi) * 8 + g;
@@ -341,9 +353,9 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
 
 int lda_of(int Kp) { return Kp + ((4 - Kp % 16) % 16 + 16) % 16; }
 
-size_t res_smem(int MS, int NI, int WF, int NS, int Kp) {
+size_t res_smem(int MSWS, int NI, int WF, int NS, int Kp) {  // MSWS = strips per warp x strip groups
     const int BN = 8 * NI * WF;
-    return sizeof(double) * (2 * 8 * static_cast<size_t>(MS) * lda_of(Kp) + static_cast<size_t>(NS) * 2 * kBK * (BN + 4));
+    return sizeof(double) * (2 * 8 * static_cast<size_t>(MSWS) * lda_of(Kp) + static_cast<size_t>(NS) * 2 * kBK * (BN + 4));
 }
 
 RArgs make_rargs(const Tiling& t, const ModeGeom& g) {
@@ -357,6 +369,7 @@ RArgs make_rargs(const Tiling& t, const ModeGeom& g) {
     a.S1 = (a.F + 7) / 8;
     a.S2 = (a.h + 7) / 8;
     a.A2 = static_cast<long long>(t.Mp) * t.Kp;
+    a.Mp = t.Mp;
     a.ntiles = (g.ncols + t.BN - 1) / t.BN;
     return a;
 }
@@ -370,7 +383,7 @@ cudaError_t res_launch_t(const Tiling& t, const ModeGeom& g, const double* X, do
     auto k = fwd ? fold_res_kernel<MS, MSW, NI, WS, WF, NS, true, false>
                  : (post ? fold_res_kernel<MS, MSW, NI, WS, WF, NS, false, true>
                          : fold_res_kernel<MS, MSW, NI, WS, WF, NS, false, false>);
-    const size_t smem = res_smem(MS, NI, WF, NS, t.Kp);
+    const size_t smem = res_smem(MSW * WS, NI, WF, NS, t.Kp);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -406,6 +419,10 @@ cudaError_t res_dispatch_ms(const Tiling& t, const ModeGeom& g, const double* X,
     // producer stay <= 8 warps (a 9-warp CTA caps the registers at 168).
     constexpr int H = (MS + 1) / 2;  // strips per warp with two strip groups
     if (t.WM == 1 && t.NI == 1 && t.WN == 7 && t.nstage == 4) return res_launch_t<MS, MS, 1, 1, 7, 4>(t, g, X, Y, J, fwd, post, st, occ);
+    // 8 consumer warps = two per SM sub-partition (a warp issues at most one DMMA.8x8x4 per 16 cycles,
+    // the sub-partition's DMMA unit accepts one per ~16: two ready warps per sub-partition keep it fed)
+    if (t.WM == 1 && t.NI == 1 && t.WN == 8 && t.nstage == 4) return res_launch_t<MS, MS, 1, 1, 8, 4>(t, g, X, Y, J, fwd, post, st, occ);
+    if (t.WM == 2 && t.NI == 1 && t.WN == 4 && t.nstage == 4) return res_launch_t<MS, H, 1, 2, 4, 4>(t, g, X, Y, J, fwd, post, st, occ);
     if (t.WM == 2 && t.NI == 2 && t.WN == 3 && t.nstage == 4) return res_launch_t<MS, H, 2, 2, 3, 4>(t, g, X, Y, J, fwd, post, st, occ);
     if (t.WM == 2 && t.NI == 1 && t.WN == 3 && t.nstage == 6) return res_launch_t<MS, H, 1, 2, 3, 6>(t, g, X, Y, J, fwd, post, st, occ);
     if constexpr (MS <= 8) {
@@ -438,7 +455,7 @@ std::vector<Tiling> fold_res_candidates(int n, int Mp_hint) {
     const int S = (F + 7) / 8;
     if (S < 4 || S > 11) return out;  // small factors: the streaming kernel; n > 176: factors exceed smem
     const int Kp = (F + 3) / 4 * 4;
-    const int variants[4][4] = {{2, 2, 3, 4}, {1, 1, 7, 4}, {2, 1, 3, 6}, {1, 2, 4, 4}};  // WM(WS), NI, WN(WF), NS
+    const int variants[5][4] = {{1, 1, 8, 4}, {2, 1, 4, 4}, {1, 1, 7, 4}, {2, 2, 3, 4}, {1, 2, 4, 4}};  // WM(WS), NI, WN(WF), NS
     for (const auto& v : variants) {
         Tiling t;
         t.fold = 2;
@@ -454,7 +471,7 @@ std::vector<Tiling> fold_res_candidates(int n, int Mp_hint) {
         t.Kp = Kp;
         t.BN = 8 * t.NI * t.WN;
         t.LDX = t.BN + 4;
-        t.smem = res_smem(S, t.NI, t.WN, t.nstage, Kp);
+        t.smem = res_smem(t.WM == 2 ? 2 * ((S + 1) / 2) : S, t.NI, t.WN, t.nstage, Kp);
         if (t.smem + 1024 > kSmemPerCTA) continue;
         if (t.WM == 1 && t.NI == 2 && S > 8) continue;  // 4 S NI accumulator doubles: spills beyond S = 8
         int occ = 0;

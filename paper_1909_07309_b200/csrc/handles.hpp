@@ -164,7 +164,7 @@ struct stiga_fd_s {
     }
     // best dense (unfolded) candidate of direction l (for stages the folded kernel cannot do)
     std::vector<gpu::Tiling> tl_dense;  // heuristic dense tiling per direction (J / Jt are padded for it)
-    const gpu::Tiling& dense_tiling(int l) const { return (tl[l].fold || tl[l].WM != 1) ? tl_dense[l] : tl[l]; }
+    const gpu::Tiling& dense_tiling(int l) const { return (tl[l].fold || tl[l].res || tl[l].WM != 1) ? tl_dense[l] : tl[l]; }
 
     // Profiling hook of the stage functions: when prof_ev is set, an event is recorded before every
     // launch (stiga_fd_apply_profiled on sharded handles).
@@ -236,7 +236,7 @@ struct stiga_fd_s {
             // the scattering product: the tuned tiling when it has a scatter epilogue (dense WM = 1 or
             // folded WM = 2), else the dense fallback
             const gpu::Tiling& tt = (l == 0 && fused_pre) ? first_tiling() : tl[l];
-            const bool scatter_ok = !(fused_pre && l == 0) && (tt.fold == 1 ? tt.WM == 2 : (tt.fold == 0 && tt.WM == 1));
+            const bool scatter_ok = !(fused_pre && l == 0) && (tt.fold == 1 ? tt.WM == 2 : (tt.fold == 0 && tt.WM == 1 && !tt.res));
             const gpu::Tiling& t = last ? (scatter_ok ? tt : dense_tiling(l)) : (l == 0 ? first_tiling() : tl[l]);
             mark(st);
             mprod(t, l, false, slab_geom(l, nt_local), src, dst, nullptr, st, (fused_pre && l == 0) ? dsl : nullptr,
@@ -257,9 +257,9 @@ struct stiga_fd_s {
             ck(gpu::launch_arrowhead(scratch.p, scratch2.p, ns_local, a2, st), "slab arrowhead");
             mark(st);
             gpu::Tiling tsc = tl_ts;
-            if (tsc.WM != 1)
+            if (tsc.WM != 1 || tsc.res)  // a streaming WM = 1 tiling carries the scatter epilogue
                 for (const auto& t : cand_ts)
-                    if (t.WM == 1) {
+                    if (t.WM == 1 && !t.res) {
                         tsc = t;
                         break;
                     }
@@ -512,7 +512,8 @@ struct stiga_fd_s {
             return t.fold ? 4.0 * Fh * Fh * Nsp / n : 2.0 * n * Nsp;
         };
         auto tag = [](const gpu::Tiling& t) {
-            return t.fold == 2 ? std::string("(folded,res)") : (t.fold ? std::string("(folded)") : std::string());
+            return t.fold == 2 ? std::string("(folded,res)")
+                               : (t.fold ? std::string("(folded)") : (t.res ? std::string("(res)") : std::string()));
         };
         for (int l = 0; l < d; ++l) {
             const gpu::Tiling& t = l == 0 ? (fused_pre ? tl_pre : tl[0]) : tl[l];
@@ -523,9 +524,9 @@ struct stiga_fd_s {
         if (sharded) L.emplace_back("exchange_barrier_1", 0.0);
         const double nt = dims[d];
         if (time_split) {
-            L.emplace_back("time_UtT", 2.0 * nt * Nt);
+            L.emplace_back("time_UtT" + tag(tl_ts), 2.0 * nt * Nt);
             L.emplace_back("arrowhead", 0.0);
-            L.emplace_back(std::string("time_Ut") + (sharded ? "+scatter" : ""), 2.0 * nt * Nt);
+            L.emplace_back(std::string("time_Ut") + (sharded ? "+scatter" : tag(tl_ts)), 2.0 * nt * Nt);
         } else {
             L.emplace_back(std::string("time_fused") + (sharded ? "+scatter" : ""), 4.0 * nt * Nt);
         }

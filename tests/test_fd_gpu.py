@@ -301,6 +301,40 @@ def test_fd_apply_parity_resident_fold(d, p, nel, scaled, monkeypatch):
     assert rel(s, s2) <= 1e-13
 
 
+@pytest.mark.parametrize("d,p,nel", [(3, 4, 9), (3, 4, 30), (2, 3, 96), (1, 5, 160), (2, 5, 160), (3, 2, 40)])
+@pytest.mark.parametrize("scaled", [False, True])
+def test_fd_apply_parity_dense_resident(d, p, nel, scaled, monkeypatch):
+    """STIGA_DENSE_KERNEL=res with folding off and the split time path: every spatial product and both
+    time GEMMs on the dense resident-factor kernel (dense_res.cu: row blocks of the factor in smem,
+    persistent CTAs, producer warp + mbarrier ring; the fused D^-1/2 pre-scale when the tuner picks
+    it), 1..3 row blocks, mode 0 and strided modes; <= 1e-11 vs the oracle, equal to the streaming
+    kernels to rounding."""
+    monkeypatch.setenv("STIGA_FOLD_KERNEL", "off")
+    monkeypatch.setenv("STIGA_TIME_VARIANT", "split")
+    monkeypatch.setenv("STIGA_DENSE_KERNEL", "res")
+    s, so, P, _, r = run_pair(d, p, nel, scaled)
+    names = [nm for nm, _ in P.launch_info()]
+    assert sum("(res)" in nm for nm in names) == 2 * d + 2, names
+    assert rel(s, so) <= TOL
+    monkeypatch.setenv("STIGA_DENSE_KERNEL", "stream")
+    s2, *_ = run_pair(d, p, nel, scaled)
+    assert rel(s, s2) <= 1e-13
+
+
+def test_fd_apply_parity_dense_resident_deformed(monkeypatch):
+    """The config-4 kind of factors (weighted, not mirror symmetric) with the real D^-1/2 on the dense
+    resident kernels."""
+    from paper_1909_07309_b200.problems import Problem
+
+    monkeypatch.setenv("STIGA_DENSE_KERNEL", "res")
+    pc = Problem("deformed-cube-3d").geometry_pieces(4, 20, want_D=True)
+    P = stiga.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=pc.D, device=0)
+    assert any("(res)" in nm for nm, _ in P.launch_info())
+    Po = ofd.ExtendedFDPreconditioner.setup(pc.K, pc.M, pc.Wt, pc.Mt, 1.0, 1.0, scaling=pc.D)
+    r = uniform_pm1(P.n_dof, 21)
+    assert rel(P.apply(torch.from_numpy(r).cuda()).cpu().numpy(), Po.apply(r)) <= TOL
+
+
 def test_fold_not_used_on_curved_geometry():
     """The A^G factors of the deformed cube are not centrosymmetric: dense kernels only."""
     from paper_1909_07309_b200.problems import Problem

@@ -6,3 +6,4 @@ ncu --set full --import-source on --clock-control none --profile-from-start off 
 ncu -i $O/r02c_c5p5.ncu-rep --page raw --csv > $O/r02c_c5p5_raw.csv 2>&1
 for i in 1 4 9; do ncu -i $O/r02c_c5p5.ncu-rep --page source --csv --launch-skip $i --launch-count 1 > $O/r02c_c5p5_src_$i.csv 2>&1; done
 ls -la $O | grep r02c
+rm -f $O/r02c_c5p5.ncu-rep
