@@ -199,13 +199,13 @@ __device__ __forceinline__ void issue_chunk(const KArgs& a, const Prod& p, unsig
 // strips are computed (warp-uniform predicate): strips wholly past the output rows are skipped, so
 // a row block that overhangs the matrix costs only its live strips; padded rows inside a live
 // strip are zero J rows and produce zeros that are never stored.
-template <class SH, int KS>
+template <class SH, int KS, bool FULL = false>
 __device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, int mact,
                                           double (&acc)[SH::MI][SH::NI][2]) {
     constexpr int MI = SH::MI, NI = SH::NI;
     double av[2][MI], bv[2][NI];
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi) av[0][mi] = mi < mact ? ja[mi * 8 * kLDJ] : 0.0;
+    for (int mi = 0; mi < MI; ++mi) av[0][mi] = (FULL || mi < mact) ? ja[mi * 8 * kLDJ] : 0.0;
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni) bv[0][ni] = SH::PS ? bb[ni * 8] * bb[SH::DOFF + ni * 8] : bb[ni * 8];
 #pragma unroll
@@ -213,7 +213,7 @@ __device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, in
         const int cur = kk & 1, nxt = cur ^ 1;
         if (kk + 1 < KS) {
 #pragma unroll
-            for (int mi = 0; mi < MI; ++mi) av[nxt][mi] = mi < mact ? ja[mi * 8 * kLDJ + (kk + 1) * 4] : 0.0;
+            for (int mi = 0; mi < MI; ++mi) av[nxt][mi] = (FULL || mi < mact) ? ja[mi * 8 * kLDJ + (kk + 1) * 4] : 0.0;
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni)
                 bv[nxt][ni] = SH::PS ? bb[(kk + 1) * 4 * SH::LDX + ni * 8] * bb[SH::DOFF + (kk + 1) * 4 * SH::LDX + ni * 8]
@@ -223,7 +223,7 @@ __device__ __forceinline__ void mma_chunk(const double* ja, const double* bb, in
         for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni)
-                if (mi < mact) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[cur][mi], bv[cur][ni]);
+                if (FULL || mi < mact) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], av[cur][mi], bv[cur][ni]);
     }
 }
 
@@ -392,7 +392,14 @@ __device__ __forceinline__ void gemm(const KArgs& a, double* stages, const Prod&
         const double* ja = st + ja_off;
         const double* bb = X_STREAM ? st + bb_off : Bres + q * kBK * SH::LDX + bb_off;
         const int ksteps = min(kBK, a.Kp - q * kBK) >> 2;
-        if (ksteps == 4) {
+        // all strips live (the usual case): the unpredicated chunk -- a runtime-predicated mma.sync
+        // costs a WARPSYNC + NOP per DMMA (folded-kernel analysis)
+        if (mact == SH::MI) {
+            if (ksteps == 4) mma_chunk<SH, 4, true>(ja, bb, mact, acc);
+            else if (ksteps == 3) mma_chunk<SH, 3, true>(ja, bb, mact, acc);
+            else if (ksteps == 2) mma_chunk<SH, 2, true>(ja, bb, mact, acc);
+            else mma_chunk<SH, 1, true>(ja, bb, mact, acc);
+        } else if (ksteps == 4) {
             mma_chunk<SH, 4>(ja, bb, mact, acc);
         } else if (ksteps == 3) {
             mma_chunk<SH, 3>(ja, bb, mact, acc);

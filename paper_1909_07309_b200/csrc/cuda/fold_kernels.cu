@@ -210,14 +210,14 @@ __device__ __forceinline__ void fissue(const FArgs& a, const FProd& p, unsigned 
     }
 }
 
-template <class SH, bool FWD>
+template <class SH, bool FWD, bool FULL = false>
 __device__ __forceinline__ void fload(const double* ja, const double* xa, const double* xb, int kk, int mact,
                                       double (&a1)[SH::MI], double (&a2)[SH::MI], double (&b1)[SH::NI],
                                       double (&b2)[SH::NI]) {
 #pragma unroll
     for (int mi = 0; mi < SH::MI; ++mi) {
-        a1[mi] = mi < mact ? ja[mi * 8 * kLDJ + kk * 4] : 0.0;
-        a2[mi] = mi < mact ? ja[(SH::J2 - SH::J1) + mi * 8 * kLDJ + kk * 4] : 0.0;
+        a1[mi] = (FULL || mi < mact) ? ja[mi * 8 * kLDJ + kk * 4] : 0.0;
+        a2[mi] = (FULL || mi < mact) ? ja[(SH::J2 - SH::J1) + mi * 8 * kLDJ + kk * 4] : 0.0;
     }
 #pragma unroll
     for (int ni = 0; ni < SH::NI; ++ni) {
@@ -237,11 +237,11 @@ __device__ __forceinline__ void fload(const double* ja, const double* xa, const 
 
 // WM = 2: one folded product per warp (matrix m = warp row): A fragments from J1 or J2, B fragments
 // x_k + x_{n-1-k} (m = 0) / x_k - x_{n-1-k} (m = 1) forward, the first / second half backward.
-template <class SH, bool FWD>
+template <class SH, bool FWD, bool FULL = false>
 __device__ __forceinline__ void fload1(const double* ja, const double* xa, const double* xb, int kk, int mact,
                                        double sgn, double (&a)[SH::MI], double (&b)[SH::NI]) {
 #pragma unroll
-    for (int mi = 0; mi < SH::MI; ++mi) a[mi] = mi < mact ? ja[mi * 8 * kLDJ + kk * 4] : 0.0;
+    for (int mi = 0; mi < SH::MI; ++mi) a[mi] = (FULL || mi < mact) ? ja[mi * 8 * kLDJ + kk * 4] : 0.0;
 #pragma unroll
     for (int ni = 0; ni < SH::NI; ++ni) {
         if (FWD) {
@@ -258,40 +258,40 @@ __device__ __forceinline__ void fload1(const double* ja, const double* xa, const
     }
 }
 
-template <class SH, bool FWD, int KS>
+template <class SH, bool FWD, int KS, bool FULL = false>
 __device__ __forceinline__ void fmma1(const double* ja, const double* xa, const double* xb, int mact, double sgn,
                                       double (&c)[SH::MI][SH::NI][2]) {
     constexpr int MI = SH::MI, NI = SH::NI;
     double a[2][MI], b[2][NI];
-    fload1<SH, FWD>(ja, xa, xb, 0, mact, sgn, a[0], b[0]);
+    fload1<SH, FWD, FULL>(ja, xa, xb, 0, mact, sgn, a[0], b[0]);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
         const int cur = kk & 1, nxt = cur ^ 1;
-        if (kk + 1 < KS) fload1<SH, FWD>(ja, xa, xb, kk + 1, mact, sgn, a[nxt], b[nxt]);
+        if (kk + 1 < KS) fload1<SH, FWD, FULL>(ja, xa, xb, kk + 1, mact, sgn, a[nxt], b[nxt]);
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni)
-                if (mi < mact) dmma(c[mi][ni][0], c[mi][ni][1], a[cur][mi], b[cur][ni]);
+                if (FULL || mi < mact) dmma(c[mi][ni][0], c[mi][ni][1], a[cur][mi], b[cur][ni]);
     }
 }
 
 // Both folded products over KS k-steps of 4, fragments double-buffered in registers.
-template <class SH, bool FWD, int KS>
+template <class SH, bool FWD, int KS, bool FULL = false>
 __device__ __forceinline__ void fmma(const double* ja, const double* xa, const double* xb, int mact,
                                      double (&c1)[SH::MI][SH::NI][2], double (&c2)[SH::MI][SH::NI][2]) {
     constexpr int MI = SH::MI, NI = SH::NI;
     double a1[2][MI], a2[2][MI], b1[2][NI], b2[2][NI];
-    fload<SH, FWD>(ja, xa, xb, 0, mact, a1[0], a2[0], b1[0], b2[0]);
+    fload<SH, FWD, FULL>(ja, xa, xb, 0, mact, a1[0], a2[0], b1[0], b2[0]);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
         const int cur = kk & 1, nxt = cur ^ 1;
-        if (kk + 1 < KS) fload<SH, FWD>(ja, xa, xb, kk + 1, mact, a1[nxt], a2[nxt], b1[nxt], b2[nxt]);
+        if (kk + 1 < KS) fload<SH, FWD, FULL>(ja, xa, xb, kk + 1, mact, a1[nxt], a2[nxt], b1[nxt], b2[nxt]);
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni)
-                if (mi < mact) {
+                if (FULL || mi < mact) {
                     dmma(c1[mi][ni][0], c1[mi][ni][1], a1[cur][mi], b1[cur][ni]);
                     dmma(c2[mi][ni][0], c2[mi][ni][1], a2[cur][mi], b2[cur][ni]);
                 }
@@ -341,7 +341,12 @@ __global__ void __launch_bounds__(32 * WN)
         commit();
         const double* sb = smem + stage * SH::STAGE;
         const int ks = min(kBK, a.Kp - q * kBK) >> 2;
-        if (ks == 4) fmma<SH, FWD, 4>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
+        if (mact == MI) {  // all strips live: unpredicated MMAs (no WARPSYNC per DMMA)
+            if (ks == 4) fmma<SH, FWD, 4, true>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
+            else if (ks == 3) fmma<SH, FWD, 3, true>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
+            else if (ks == 2) fmma<SH, FWD, 2, true>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
+            else fmma<SH, FWD, 1, true>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
+        } else if (ks == 4) fmma<SH, FWD, 4>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
         else if (ks == 3) fmma<SH, FWD, 3>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
         else if (ks == 2) fmma<SH, FWD, 2>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
         else fmma<SH, FWD, 1>(sb + ja_off, sb + xa_off, sb + xb_off, mact, c1, c2);
@@ -466,7 +471,12 @@ __global__ void __launch_bounds__(64 * WN)
         commit();
         const double* sb = smem + stage * SH::STAGE;
         const int ks = min(kBK, a.Kp - q * kBK) >> 2;
-        if (ks == 4) fmma1<SH, FWD, 4>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
+        if (mact == MI) {  // all strips live: unpredicated MMAs (no WARPSYNC per DMMA)
+            if (ks == 4) fmma1<SH, FWD, 4, true>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
+            else if (ks == 3) fmma1<SH, FWD, 3, true>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
+            else if (ks == 2) fmma1<SH, FWD, 2, true>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
+            else fmma1<SH, FWD, 1, true>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
+        } else if (ks == 4) fmma1<SH, FWD, 4>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
         else if (ks == 3) fmma1<SH, FWD, 3>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
         else if (ks == 2) fmma1<SH, FWD, 2>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
         else fmma1<SH, FWD, 1>(sb + ja_off, sb + xa_off, sb + xb_off, mact, sgn, c);
