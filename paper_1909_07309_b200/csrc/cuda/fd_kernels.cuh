@@ -129,7 +129,9 @@ cudaError_t launch_mode_res(const Tiling& t, const ModeGeom& g, const double* X,
 /// Candidates for n with 4 <= ceil(ceil(n/2)/8) <= 11; no pre-scale / scatter epilogue.
 std::vector<Tiling> fold_res_candidates(int n, int Mp_hint);
 cudaError_t launch_fold_res(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
-                            bool forward, const double* post_scale, cudaStream_t stream);
+                            bool forward, const double* post_scale, cudaStream_t stream,
+                            const double* pre_scale = nullptr);
+size_t fold_res_prescale_smem(const Tiling& t);
 
 /// Standalone block-arrowhead solve X = (gamma Delta_t (x) I + nu I (x) Lambda_s)^-1 Z on the
 /// time-eigen-coordinate tensor (N_s x n_t, time slowest); used when the time direction runs as

@@ -44,7 +44,8 @@ std::vector<Tiling> mode_tiling_candidates(int m, int n) {
         const int MI = (S + RB - 1) / RB;
         if (MI > 13 || MI < 1) continue;
         if (RB > rb0 && (S + rb0 - 1) / rb0 == MI) continue;  // same MI as a smaller RB
-        for (int WN : {4, 2}) {
+        for (int WN : {4, 2})
+        for (int ns : {3, 2}) {  // 2 stages: half the staging smem (the fused pre-scale doubles it)
             Tiling t;
             t.MI = MI;
             t.WM = 1;
@@ -57,7 +58,7 @@ std::vector<Tiling> mode_tiling_candidates(int m, int n) {
             t.Kp = Kp;
             t.BN = 16 * WN;
             t.LDX = t.BN + 4;
-            t.nstage = 3;
+            t.nstage = ns;
             t.smem = sizeof(double) * static_cast<size_t>(t.nstage) * (kBK * t.LDX + t.MpB * kLDJ);
             if (t.smem > kSmemPerCTA) continue;
             int occ = 0;
@@ -67,7 +68,7 @@ std::vector<Tiling> mode_tiling_candidates(int m, int n) {
             // strips past S are skipped, so padding costs only imbalance; each extra row block
             // re-stages the fiber tile
             const double eff = 0.85 + 0.15 * static_cast<double>(S) / (RB * MI);
-            c.emplace_back(std::min(occ * t.WN, 16) * eff + 0.02 * WN - 0.05 * RB, t);
+            c.emplace_back(std::min(occ * t.WN, 16) * eff + 0.02 * WN - 0.05 * RB - (ns == 2 ? 0.3 : 0.0), t);
         }
     }
     // two warp rows per CTA (WM = 2): twice the rows of one fiber tile per CTA at the same registers
@@ -128,6 +129,7 @@ size_t prescale_smem(const Tiling& t) {
 
 bool prescale_fits(const Tiling& t) {
     if (t.res) return mode_res_smem(t, true) + 1024 <= kSmemPerCTA;
+    if (t.fold == 2) return fold_res_prescale_smem(t) + 1024 <= kSmemPerCTA;
     if (t.fold) return fold_prescale_smem(t) <= kSmemPerCTA;
     return t.WM == 1 && prescale_smem(t) <= kSmemPerCTA;
 }

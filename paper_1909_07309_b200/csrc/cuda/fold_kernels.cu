@@ -776,8 +776,8 @@ cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double
                                 const Scatter* sc) {
     if (g.ncols <= 0) return cudaSuccess;
     if (t.fold == 2) {
-        if (pre_scale || sc) return cudaErrorInvalidValue;
-        return launch_fold_res(t, g, X, Y, Jfold, forward, post_scale, st);
+        if (sc) return cudaErrorInvalidValue;
+        return launch_fold_res(t, g, X, Y, Jfold, forward, post_scale, st, pre_scale);
     }
     if (!t.fold || g.m != g.n || g.n < 2 || (forward && post_scale) || (!forward && pre_scale))
         return cudaErrorInvalidValue;
@@ -789,7 +789,7 @@ cudaError_t launch_fold_product(const Tiling& t, const ModeGeom& g, const double
 }
 
 size_t fold_prescale_smem(const Tiling& t) {
-    if (t.fold == 2) return static_cast<size_t>(1) << 40;  // no pre-scale variant
+    if (t.fold == 2) return fold_res_prescale_smem(t);
     return t.smem + sizeof(double) * static_cast<size_t>(t.nstage) * 2 * kBK * t.LDX;
 }
 

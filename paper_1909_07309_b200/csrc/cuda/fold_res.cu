@@ -48,21 +48,22 @@ struct RArgs {
     long long ntiles;
 };
 
-template <int NI, int NW>  // NW = fiber-group warps (WF)
+template <int NI, int NW, bool PS = false>  // NW = fiber-group warps (WF)
 struct RShape {
     static constexpr int BN = 8 * NI * NW;   // fibers per tile
     static constexpr int LDX = BN + 4;       // == 4 mod 16 doubles
     static constexpr int XB = kBK * LDX;     // one 16-row chunk
-    static constexpr int STAGE = 2 * XB;     // chunk + mirror (forward) / + second half (backward)
+    static constexpr int DOFF = 2 * XB;      // PS: the D^-1/2 chunks of both, same layout
+    static constexpr int STAGE = 2 * XB * (PS ? 2 : 1);  // chunk + mirror (forward) / + second half (backward)
     static constexpr int FPL = (BN + 31) / 32;  // fibers per producer lane (L > 1)
 };
 
 // Fragments of k-step kk: A of both matrices (this warp's strips), B of both (forward: the fold).
-template <int MS, int NI, int NW, bool FWD>
+template <int MS, int NI, int NW, bool FWD, bool PS = false>
 __device__ __forceinline__ void rfrag(const double* __restrict__ a1, const double* __restrict__ a2,
                                       const double* __restrict__ xa, const double* __restrict__ xb, int LDA, int kk,
                                       double (&av1)[MS], double (&av2)[MS], double (&b1)[NI], double (&b2)[NI]) {
-    using SH = RShape<NI, NW>;
+    using SH = RShape<NI, NW, PS>;
 #pragma unroll
     for (int mi = 0; mi < MS; ++mi) {
         av1[mi] = a1[mi * 8 * LDA + kk * 4];
@@ -70,9 +71,11 @@ __device__ __forceinline__ void rfrag(const double* __restrict__ a1, const doubl
     }
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni) {
-        const double u = xa[kk * 4 * SH::LDX + ni * 8];
+        double u = xa[kk * 4 * SH::LDX + ni * 8];
+        if (PS) u *= xa[SH::DOFF + kk * 4 * SH::LDX + ni * 8];  // fused D^-1/2 pre-scale
         if (FWD) {  // xb points at the mirrored row of k-step 0; rows run backwards
-            const double w = xb[-kk * 4 * SH::LDX + ni * 8];
+            double w = xb[-kk * 4 * SH::LDX + ni * 8];
+            if (PS) w *= xb[SH::DOFF - kk * 4 * SH::LDX + ni * 8];
             b1[ni] = u + w;
             b2[ni] = u - w;
         } else {
@@ -85,16 +88,16 @@ __device__ __forceinline__ void rfrag(const double* __restrict__ a1, const doubl
 // One 16-column chunk: KS k-steps of 4 over both matrices for this warp's NI fiber groups; the
 // fragments of k-step kk + 1 are loaded (into the other register set) while k-step kk's DMMAs issue.
 // Strips past the matrix (mi >= S1 / S2: zero rows of the padded factor) are read but skipped.
-template <int MS, int NI, int NW, bool FWD, int KS>
+template <int MS, int NI, int NW, bool FWD, int KS, bool PS = false>
 __device__ __forceinline__ void rchunk(const double* __restrict__ a1, const double* __restrict__ a2,
                                        const double* __restrict__ xa, const double* __restrict__ xb, int LDA,
                                        double (&c1)[MS][NI][2], double (&c2)[MS][NI][2]) {
     double av1[2][MS], av2[2][MS], b1[2][NI], b2[2][NI];
-    rfrag<MS, NI, NW, FWD>(a1, a2, xa, xb, LDA, 0, av1[0], av2[0], b1[0], b2[0]);
+    rfrag<MS, NI, NW, FWD, PS>(a1, a2, xa, xb, LDA, 0, av1[0], av2[0], b1[0], b2[0]);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
         const int cur = kk & 1, nxt = cur ^ 1;
-        if (kk + 1 < KS) rfrag<MS, NI, NW, FWD>(a1, a2, xa, xb, LDA, kk + 1, av1[nxt], av2[nxt], b1[nxt], b2[nxt]);
+        if (kk + 1 < KS) rfrag<MS, NI, NW, FWD, PS>(a1, a2, xa, xb, LDA, kk + 1, av1[nxt], av2[nxt], b1[nxt], b2[nxt]);
         // every strip unconditionally: padded strips are zero rows of the resident factors (a predicated
         // mma.sync costs a WARPSYNC + NOP per DMMA); their accumulators are never stored
 #pragma unroll
@@ -109,12 +112,12 @@ __device__ __forceinline__ void rchunk(const double* __restrict__ a1, const doub
 
 // Consumer warps: WS strip groups x WF fiber groups; warp (ws, wf) owns strips [ws MSW, ws MSW + MSW) of
 // BOTH matrices and fiber groups [wf NI, wf NI + NI) of the tile.
-template <int MS, int MSW, int NI, int WS, int WF, int NS, bool FWD, bool POST>
+template <int MS, int MSW, int NI, int WS, int WF, int NS, bool FWD, bool POST, bool PS = false>
 __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
     fold_res_kernel(RArgs a, const double* __restrict__ X, double* __restrict__ Y, const double* __restrict__ J,
-                    const double* __restrict__ post) {
+                    const double* __restrict__ post, const double* __restrict__ pre) {
     constexpr int NW = WS * WF;
-    using SH = RShape<NI, WF>;
+    using SH = RShape<NI, WF, PS>;
     extern __shared__ __align__(16) double smem[];
     __shared__ uint64_t full[NS], empty[NS];
     const int LDA = a.LDA;
@@ -178,6 +181,8 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
                 const int s = seq % NS;
                 rmb_wait(&empty[s], ((seq / NS) & 1u) ^ 1u);
                 const unsigned sa = ru32(sX + s * SH::STAGE), sb = sa + 8u * SH::XB;
+                const unsigned dso = 8u * SH::DOFF;           // PS: D chunk bytes after its fiber chunk
+                const long long dofs = PS ? pre - X : 0;      // D^-1/2 element = X element + dofs
                 const int ra0 = q * kBK, rb0 = FWD ? n - q * kBK - kBK : a.F + q * kBK;
                 const bool rows_in = ra0 + kBK <= n && rb0 >= 0 && rb0 + kBK <= n;
                 if (L == 1) {
@@ -191,6 +196,10 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
                         for (int f = 0; f < SH::BN; f += 2) {
                             rcp8(da, pa, true);
                             rcp8(db, pb, true);
+                            if (PS) {
+                                rcp8(da + dso, pa + dofs, true);
+                                rcp8(db + dso, pb + dofs, true);
+                            }
                             pa += step;
                             pb += step;
                             da += 16u;
@@ -202,6 +211,10 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
                             const bool cv = c0 + fpar + f < ncols;
                             rcp8(da, (va && cv) ? pa : X, va && cv);
                             rcp8(db, (vb && cv) ? pb : X, vb && cv);
+                            if (PS) {
+                                rcp8(da + dso, (va && cv) ? pa + dofs : X, va && cv);
+                                rcp8(db + dso, (vb && cv) ? pb + dofs : X, vb && cv);
+                            }
                             pa += step;
                             pb += step;
                             da += 16u;
@@ -220,6 +233,10 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
                             for (int r = 0; r < kBK; ++r) {
                                 rcp8(da, pa, true);
                                 rcp8(db, pb, true);
+                                if (PS) {
+                                    rcp8(da + dso, pa + dofs, true);
+                                    rcp8(db + dso, pb + dofs, true);
+                                }
                                 pa += L;
                                 pb += L;
                                 da += 8u * SH::LDX;
@@ -230,6 +247,10 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
                                 const bool va = fv[u] && ra0 + r < n, vb = fv[u] && rb0 + r >= 0 && rb0 + r < n;
                                 rcp8(da, va ? pa : X, va);
                                 rcp8(db, vb ? pb : X, vb);
+                                if (PS) {
+                                    rcp8(da + dso, va ? pa + dofs : X, va);
+                                    rcp8(db + dso, vb ? pb + dofs : X, vb);
+                                }
                                 pa += L;
                                 pb += L;
                                 da += 8u * SH::LDX;
@@ -268,10 +289,10 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
             const double* xb = st + SH::XB + (FWD ? (kBK - 1 - t) : t) * SH::LDX + fcol;
             const int k0 = q * kBK;
             const int ks = min(kBK, a.Kp - k0) >> 2;
-            if (ks == 4) rchunk<MSW, NI, WF, FWD, 4>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
-            else if (ks == 3) rchunk<MSW, NI, WF, FWD, 3>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
-            else if (ks == 2) rchunk<MSW, NI, WF, FWD, 2>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
-            else rchunk<MSW, NI, WF, FWD, 1>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
+            if (ks == 4) rchunk<MSW, NI, WF, FWD, 4, PS>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
+            else if (ks == 3) rchunk<MSW, NI, WF, FWD, 3, PS>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
+            else if (ks == 2) rchunk<MSW, NI, WF, FWD, 2, PS>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
+            else rchunk<MSW, NI, WF, FWD, 1, PS>(a1 + k0, a2 + k0, xa, xb, LDA, c1, c2);
             __syncwarp();
             if (lane == 0) rmb_arrive(&empty[s]);
         }
@@ -353,9 +374,10 @@ __global__ void __launch_bounds__(32 * (WS * WF + 1), 1)
 
 int lda_of(int Kp) { return Kp + ((4 - Kp % 16) % 16 + 16) % 16; }
 
-size_t res_smem(int MSWS, int NI, int WF, int NS, int Kp) {  // MSWS = strips per warp x strip groups
+size_t res_smem(int MSWS, int NI, int WF, int NS, int Kp, bool ps = false) {  // MSWS = strips per warp x groups
     const int BN = 8 * NI * WF;
-    return sizeof(double) * (2 * 8 * static_cast<size_t>(MSWS) * lda_of(Kp) + static_cast<size_t>(NS) * 2 * kBK * (BN + 4));
+    return sizeof(double) *
+           (2 * 8 * static_cast<size_t>(MSWS) * lda_of(Kp) + static_cast<size_t>(NS) * 2 * kBK * (BN + 4) * (ps ? 2 : 1));
 }
 
 RArgs make_rargs(const Tiling& t, const ModeGeom& g) {
@@ -378,12 +400,13 @@ int g_sms = 0;
 
 template <int MS, int MSW, int NI, int WS, int WF, int NS>
 cudaError_t res_launch_t(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J, bool fwd,
-                         const double* post, cudaStream_t st, int* occ) {
+                         const double* post, const double* pre, cudaStream_t st, int* occ) {
     constexpr int NW = WS * WF;
-    auto k = fwd ? fold_res_kernel<MS, MSW, NI, WS, WF, NS, true, false>
+    auto k = fwd ? (pre ? fold_res_kernel<MS, MSW, NI, WS, WF, NS, true, false, true>
+                        : fold_res_kernel<MS, MSW, NI, WS, WF, NS, true, false>)
                  : (post ? fold_res_kernel<MS, MSW, NI, WS, WF, NS, false, true>
                          : fold_res_kernel<MS, MSW, NI, WS, WF, NS, false, false>);
-    const size_t smem = res_smem(MSW * WS, NI, WF, NS, t.Kp);
+    const size_t smem = res_smem(MSW * WS, NI, WF, NS, t.Kp, pre != nullptr);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -407,41 +430,42 @@ cudaError_t res_launch_t(const Tiling& t, const ModeGeom& g, const double* X, do
     }
     const RArgs ra = make_rargs(t, g);
     const long long grid = std::min<long long>(ra.ntiles, static_cast<long long>(g_sms) * std::max(1, t.ctas_per_sm));
-    k<<<static_cast<unsigned>(grid), 32 * (NW + 1), smem, st>>>(ra, X, Y, J, post);
+    k<<<static_cast<unsigned>(grid), 32 * (NW + 1), smem, st>>>(ra, X, Y, J, post, pre);
     return cudaGetLastError();
 }
 
 template <int MS>
 cudaError_t res_dispatch_ms(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J, bool fwd,
-                            const double* post, cudaStream_t st, int* occ) {
+                            const double* post, const double* pre, cudaStream_t st, int* occ) {
     // (NI, NW, NS) variants
     // Tiling fields: WM = strip groups (WS), WN = fiber groups (WF), NI, nstage.  Consumer warps + 1
     // producer stay <= 8 warps (a 9-warp CTA caps the registers at 168).
     constexpr int H = (MS + 1) / 2;  // strips per warp with two strip groups
-    if (t.WM == 1 && t.NI == 1 && t.WN == 7 && t.nstage == 4) return res_launch_t<MS, MS, 1, 1, 7, 4>(t, g, X, Y, J, fwd, post, st, occ);
+    if (t.WM == 1 && t.NI == 1 && t.WN == 7 && t.nstage == 4) return res_launch_t<MS, MS, 1, 1, 7, 4>(t, g, X, Y, J, fwd, post, pre, st, occ);
     // 8 consumer warps = two per SM sub-partition (a warp issues at most one DMMA.8x8x4 per 16 cycles,
     // the sub-partition's DMMA unit accepts one per ~16: two ready warps per sub-partition keep it fed)
-    if (t.WM == 1 && t.NI == 1 && t.WN == 8 && t.nstage == 4) return res_launch_t<MS, MS, 1, 1, 8, 4>(t, g, X, Y, J, fwd, post, st, occ);
-    if (t.WM == 2 && t.NI == 1 && t.WN == 4 && t.nstage == 4) return res_launch_t<MS, H, 1, 2, 4, 4>(t, g, X, Y, J, fwd, post, st, occ);
-    if (t.WM == 2 && t.NI == 2 && t.WN == 3 && t.nstage == 4) return res_launch_t<MS, H, 2, 2, 3, 4>(t, g, X, Y, J, fwd, post, st, occ);
-    if (t.WM == 2 && t.NI == 1 && t.WN == 3 && t.nstage == 6) return res_launch_t<MS, H, 1, 2, 3, 6>(t, g, X, Y, J, fwd, post, st, occ);
+    if (t.WM == 1 && t.NI == 1 && t.WN == 8 && t.nstage == 4) return res_launch_t<MS, MS, 1, 1, 8, 4>(t, g, X, Y, J, fwd, post, pre, st, occ);
+    if (t.WM == 1 && t.NI == 1 && t.WN == 8 && t.nstage == 2) return res_launch_t<MS, MS, 1, 1, 8, 2>(t, g, X, Y, J, fwd, post, pre, st, occ);
+    if (t.WM == 2 && t.NI == 1 && t.WN == 4 && t.nstage == 4) return res_launch_t<MS, H, 1, 2, 4, 4>(t, g, X, Y, J, fwd, post, pre, st, occ);
+    if (t.WM == 2 && t.NI == 2 && t.WN == 3 && t.nstage == 4) return res_launch_t<MS, H, 2, 2, 3, 4>(t, g, X, Y, J, fwd, post, pre, st, occ);
+    if (t.WM == 2 && t.NI == 1 && t.WN == 3 && t.nstage == 6) return res_launch_t<MS, H, 1, 2, 3, 6>(t, g, X, Y, J, fwd, post, pre, st, occ);
     if constexpr (MS <= 8) {
-        if (t.WM == 1 && t.NI == 2 && t.WN == 4 && t.nstage == 4) return res_launch_t<MS, MS, 2, 1, 4, 4>(t, g, X, Y, J, fwd, post, st, occ);
+        if (t.WM == 1 && t.NI == 2 && t.WN == 4 && t.nstage == 4) return res_launch_t<MS, MS, 2, 1, 4, 4>(t, g, X, Y, J, fwd, post, pre, st, occ);
     }
     return cudaErrorInvalidValue;
 }
 
 cudaError_t res_dispatch(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J, bool fwd,
-                         const double* post, cudaStream_t st, int* occ) {
+                         const double* post, const double* pre, cudaStream_t st, int* occ) {
     switch (t.MI) {
-        case 4: return res_dispatch_ms<4>(t, g, X, Y, J, fwd, post, st, occ);
-        case 5: return res_dispatch_ms<5>(t, g, X, Y, J, fwd, post, st, occ);
-        case 6: return res_dispatch_ms<6>(t, g, X, Y, J, fwd, post, st, occ);
-        case 7: return res_dispatch_ms<7>(t, g, X, Y, J, fwd, post, st, occ);
-        case 8: return res_dispatch_ms<8>(t, g, X, Y, J, fwd, post, st, occ);
-        case 9: return res_dispatch_ms<9>(t, g, X, Y, J, fwd, post, st, occ);
-        case 10: return res_dispatch_ms<10>(t, g, X, Y, J, fwd, post, st, occ);
-        case 11: return res_dispatch_ms<11>(t, g, X, Y, J, fwd, post, st, occ);
+        case 4: return res_dispatch_ms<4>(t, g, X, Y, J, fwd, post, pre, st, occ);
+        case 5: return res_dispatch_ms<5>(t, g, X, Y, J, fwd, post, pre, st, occ);
+        case 6: return res_dispatch_ms<6>(t, g, X, Y, J, fwd, post, pre, st, occ);
+        case 7: return res_dispatch_ms<7>(t, g, X, Y, J, fwd, post, pre, st, occ);
+        case 8: return res_dispatch_ms<8>(t, g, X, Y, J, fwd, post, pre, st, occ);
+        case 9: return res_dispatch_ms<9>(t, g, X, Y, J, fwd, post, pre, st, occ);
+        case 10: return res_dispatch_ms<10>(t, g, X, Y, J, fwd, post, pre, st, occ);
+        case 11: return res_dispatch_ms<11>(t, g, X, Y, J, fwd, post, pre, st, occ);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -455,7 +479,8 @@ std::vector<Tiling> fold_res_candidates(int n, int Mp_hint) {
     const int S = (F + 7) / 8;
     if (S < 4 || S > 11) return out;  // small factors: the streaming kernel; n > 176: factors exceed smem
     const int Kp = (F + 3) / 4 * 4;
-    const int variants[5][4] = {{1, 1, 8, 4}, {2, 1, 4, 4}, {1, 1, 7, 4}, {2, 2, 3, 4}, {1, 2, 4, 4}};  // WM(WS), NI, WN(WF), NS
+    // WM(WS), NI, WN(WF), NS; {1, 1, 8, 2}: the fused D^-1/2 pre-scale variant (doubled stages fit)
+    const int variants[6][4] = {{1, 1, 8, 4}, {2, 1, 4, 4}, {1, 1, 7, 4}, {2, 2, 3, 4}, {1, 2, 4, 4}, {1, 1, 8, 2}};
     for (const auto& v : variants) {
         Tiling t;
         t.fold = 2;
@@ -475,7 +500,7 @@ std::vector<Tiling> fold_res_candidates(int n, int Mp_hint) {
         if (t.smem + 1024 > kSmemPerCTA) continue;
         if (t.WM == 1 && t.NI == 2 && S > 8) continue;  // 4 S NI accumulator doubles: spills beyond S = 8
         int occ = 0;
-        res_dispatch(t, ModeGeom{}, nullptr, nullptr, nullptr, true, nullptr, nullptr, &occ);
+        res_dispatch(t, ModeGeom{}, nullptr, nullptr, nullptr, true, nullptr, nullptr, nullptr, &occ);
         if (occ < 1) continue;
         t.ctas_per_sm = 1;
         out.push_back(t);
@@ -484,10 +509,16 @@ std::vector<Tiling> fold_res_candidates(int n, int Mp_hint) {
 }
 
 cudaError_t launch_fold_res(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* Jfold,
-                            bool forward, const double* post_scale, cudaStream_t st) {
+                            bool forward, const double* post_scale, cudaStream_t st, const double* pre_scale) {
     if (g.ncols <= 0) return cudaSuccess;
-    if (t.fold != 2 || g.m != g.n || g.n < 2 || (forward && post_scale)) return cudaErrorInvalidValue;
-    return res_dispatch(t, g, X, Y, Jfold, forward, post_scale, st, nullptr);
+    if (t.fold != 2 || g.m != g.n || g.n < 2 || (forward && post_scale) || (!forward && pre_scale))
+        return cudaErrorInvalidValue;
+    if (pre_scale && fold_res_prescale_smem(t) + 1024 > kSmemPerCTA) return cudaErrorInvalidValue;
+    return res_dispatch(t, g, X, Y, Jfold, forward, post_scale, pre_scale, st, nullptr);
+}
+
+size_t fold_res_prescale_smem(const Tiling& t) {
+    return res_smem(t.WM == 2 ? 2 * ((t.MI + 1) / 2) : t.MI, t.NI, t.WN, t.nstage, t.Kp, true);
 }
 
 }  // namespace gpu

@@ -377,7 +377,7 @@ struct stiga_fd_s {
             size_t n_fold = 0, n_dense = 0;
             for (size_t c = 0; c < cand_space[l].size(); ++c) {
                 const gpu::Tiling& t = cand_space[l][c];
-                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : 2 * kMaxCand)) continue;
+                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : 3 * kMaxCand)) continue;
                 const float ms = time_once([&] {
                     mprod(t, l, false, geom(l), scratch.p, scratch2.p, nullptr, nullptr);
                 });
@@ -400,7 +400,7 @@ struct stiga_fd_s {
             size_t n_fold = 0, n_dense = 0;
             for (size_t c = 0; c < cand_space[l].size(); ++c) {
                 const gpu::Tiling& t = cand_space[l][c];
-                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : 2 * kMaxCand)) continue;
+                if ((t.fold ? n_fold : n_dense)++ >= (t.fold ? 4 * kMaxCand : 3 * kMaxCand)) continue;
                 const float ms = time_once([&] { mprod(t, l, true, geom(l), scratch.p, scratch2.p, post, nullptr); });
                 if (ms < 0.985f * best) { best = ms; tl_b[l] = t; pick_b[l] = static_cast<int>(c); }
                 if (debug_tune)
@@ -421,11 +421,12 @@ struct stiga_fd_s {
             for (size_t c = 0; c < cand_space[0].size(); ++c) {
                 const gpu::Tiling& t = cand_space[0][c];
                 if (!gpu::prescale_fits(t)) continue;
-                if ((t.fold ? n_fold : n_dense)++ >= kMaxCand) continue;
+                if ((t.fold ? n_fold : n_dense)++ >= 2 * kMaxCand) continue;
                 const float ms = time_once([&] { mprod(t, 0, false, geom(0), scratch.p, scratch2.p, nullptr, nullptr, dinv.p); });
                 if (ms < best_fus) { best_fus = ms; tl_pre = t; pick_pre = static_cast<int>(c); }
             }
-            use_fused_pre = pick_pre >= 0 && best_fus < sep;
+            static const bool force_pre = std::getenv("STIGA_FUSED_PRESCALE") != nullptr;  // tests
+            use_fused_pre = pick_pre >= 0 && (best_fus < sep || force_pre);
             if (debug_tune)
                 std::fprintf(stderr, "[stiga tune] pre-scale separate %.4f ms, fused %.4f ms (%s MI=%d RB=%d)\n", sep,
                              best_fus, tl_pre.fold ? "folded" : "dense", tl_pre.MI, tl_pre.RB);
@@ -449,7 +450,7 @@ struct stiga_fd_s {
             }
             if (!(force && std::string(force) == "fused")) {
                 float best_gemm = 1e30f;
-                for (size_t c = 0; c < std::min(2 * kMaxCand, cand_ts.size()); ++c) {
+                for (size_t c = 0; c < std::min(3 * kMaxCand, cand_ts.size()); ++c) {
                     const gpu::Tiling& t = cand_ts[c];
                     const float ms = time_once([&] {
                         ck(gpu::launch_mode_product(t, geom(d), scratch.p, scratch2.p, Jt_t.p, nullptr, nullptr), "tune");

@@ -301,6 +301,18 @@ def test_fd_apply_parity_resident_fold(d, p, nel, scaled, monkeypatch):
     assert rel(s, s2) <= 1e-13
 
 
+@pytest.mark.parametrize("d,p,nel", [(1, 3, 150), (2, 3, 96), (2, 5, 160), (3, 2, 64), (3, 3, 60)])
+def test_fd_apply_parity_resident_fold_prescale(d, p, nel, monkeypatch):
+    """The resident folded kernel with the fused D^-1/2 pre-scale (D chunks staged beside both fiber
+    chunks, B fragments scaled as the fold is formed): forced with STIGA_FUSED_PRESCALE."""
+    monkeypatch.setenv("STIGA_FOLD_KERNEL", "res")
+    monkeypatch.setenv("STIGA_FUSED_PRESCALE", "1")
+    s, so, P, _, r = run_pair(d, p, nel, True)
+    names = [nm for nm, _ in P.launch_info()]
+    assert names[0].startswith("fwd_mode0(folded,res)+pre_scale"), names
+    assert rel(s, so) <= TOL
+
+
 @pytest.mark.parametrize("d,p,nel", [(3, 4, 9), (3, 4, 30), (2, 3, 96), (1, 5, 160), (2, 5, 160), (3, 2, 40)])
 @pytest.mark.parametrize("scaled", [False, True])
 def test_fd_apply_parity_dense_resident(d, p, nel, scaled, monkeypatch):
