@@ -299,15 +299,16 @@ def test_fused_exchange_two_processes_cuda_ipc():
 
 
 def test_device_batched_gram_schmidt_ops():
-    """stiga_vec_multidot / stiga_vec_multiaxpy (the CGS2 building blocks) against torch, k up to 20."""
+    """stiga_vec_multidot / stiga_vec_multiaxpy (the CGS2 building blocks) against torch, k up to 130:
+    cycles longer than the kernels' 64-vector limit are chunked inside DeviceVec."""
     from paper_1909_07309_b200.distributed import DeviceVec
 
-    n = 1_000_003
+    n = 100_003
     g = torch.Generator(device="cuda").manual_seed(3)
-    V = [torch.rand(n, dtype=torch.float64, device="cuda", generator=g) - 0.5 for _ in range(20)]
+    V = [torch.rand(n, dtype=torch.float64, device="cuda", generator=g) - 0.5 for _ in range(130)]
     w = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) - 0.5
     vec = DeviceVec()
-    for k in (1, 7, 8, 9, 20):
+    for k in (1, 7, 8, 9, 20, 64, 65, 130):
         h = vec.multidot(V[:k], w)
         ref = np.array([float(torch.dot(v, w)) for v in V[:k]])
         assert np.abs(h - ref).max() <= 1e-12 * np.abs(ref).max()
