@@ -311,6 +311,13 @@ stiga_fd_s* fd_build(int d, const int* n, const double* const* K, const double* 
             h->lam.back()->upload(F.lambda_dev(l));
         }
         h->cand_time = gpu::time_tiling_candidates(F.n_t);
+        if (const char* tk = std::getenv("STIGA_TIME_KERNEL")) {  // tests: res / stream time-fused kernels only
+            const bool want_res = std::string(tk) == "res";
+            std::vector<gpu::Tiling> f;
+            for (const auto& t : h->cand_time)
+                if ((t.res == 2) == want_res) f.push_back(t);
+            if (!f.empty()) h->cand_time = f;
+        }
         h->cand_ts = dense_candidates(F.n_t, F.n_t);
         if (h->cand_ts.empty()) throw std::runtime_error("internal: no time-product tiling");
         int trows = 0;

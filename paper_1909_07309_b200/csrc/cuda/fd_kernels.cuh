@@ -81,7 +81,8 @@ struct Tiling {
     int nstage = 3;
     int fold = 0;     // 1: folded (centrosymmetric) product, fold_kernels.cu; 2: the resident-factor persistent
                       // folded kernel, fold_res.cu; MI/RB/Mp/Kp refer to the folded matrices
-    int res = 0;      // 1: dense resident-factor persistent kernel (dense_res.cu); MI = strips per warp,
+    int res = 0;      // 1: dense resident-factor persistent kernel (dense_res.cu); 2: resident time kernel
+                      // (time_res.cu); MI = strips per warp,
                       // WM = strip groups, WN = fiber groups, MpB = rows per row block
     size_t smem = 0;
     int ctas_per_sm = 1;
@@ -121,6 +122,11 @@ size_t fold_prescale_smem(const Tiling& t);
 /// Dense resident-factor persistent mode product (dense_res.cu, Tiling::res == 1), candidates
 /// for an m x n factor (the fused D^-1/2 pre-scale needs its own smem: prescale = true).
 std::vector<Tiling> mode_res_candidates(int m, int n, bool prescale);
+/// Resident-U_t persistent time kernel (time_res.cu, Tiling::res == 2): U_t^T -> arrowhead -> U_t
+/// with one resident copy of U_t, two CTAs per SM; n_t up to ~110.
+std::vector<Tiling> time_res_candidates(int n_t);
+cudaError_t launch_time_res(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J_pad,
+                            const ArrowParams& ap, cudaStream_t stream);
 size_t mode_res_smem(const Tiling& t, bool prescale);
 cudaError_t launch_mode_res(const Tiling& t, const ModeGeom& g, const double* X, double* Y, const double* J,
                             const double* post, const double* pre, cudaStream_t st);

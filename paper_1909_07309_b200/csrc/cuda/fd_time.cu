@@ -2,6 +2,9 @@
 // and launcher.
 #include "fd_time_impl.cuh"
 
+#include <cstdlib>
+#include <string>
+
 namespace stiga {
 namespace gpu {
 
@@ -61,18 +64,22 @@ std::vector<Tiling> time_tiling_candidates(int nt) {
     }
     std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
     std::vector<Tiling> out;
+    // the resident-U_t kernel (time_res.cu) measured slower than this streaming kernel on every
+    // BASELINE shape (c4 0.339 vs 0.282 ms, c3 3.48 vs 1.65 ms: the arrowhead phase leaves the DMMA
+    // pipe idle with one or two CTAs per SM): opt-in only
+    const char* tk = std::getenv("STIGA_TIME_KERNEL");
+    if (tk && std::string(tk) == "res" && !force_wm) out = time_res_candidates(nt);
     for (auto& e : c) out.push_back(e.second);
     return out;
 }
 
 Tiling choose_time_tiling(int nt) {
     const std::vector<Tiling> c = time_tiling_candidates(nt);
-    if (c.empty()) {
-        Tiling t;
-        t.MI = 0;
-        return t;
-    }
-    return c.front();
+    for (const Tiling& t : c)
+        if (!t.res) return t;
+    Tiling t;
+    t.MI = 0;
+    return t;
 }
 
 
@@ -80,6 +87,10 @@ cudaError_t launch_time_fused(const Tiling& t, const ModeGeom& g, const double* 
                               const double* J_pad, const ArrowParams& ap, cudaStream_t st, const Scatter* sc) {
     if (g.ncols <= 0) return cudaSuccess;
     if (sc && (sc->G < 1 || sc->G > kMaxRanks)) return cudaErrorInvalidValue;
+    if (t.res == 2) {
+        if (sc) return cudaErrorInvalidValue;  // no scatter epilogue on the resident kernel
+        return launch_time_res(t, g, X, Y, J_pad, ap, st);
+    }
     return dispatch_time(t, g, X, Y, Jt_pad, J_pad, ap, st, nullptr, sc);
 }
 

@@ -447,6 +447,9 @@ cudaError_t res_dispatch_ms(const Tiling& t, const ModeGeom& g, const double* X,
     if (t.WM == 1 && t.NI == 1 && t.WN == 8 && t.nstage == 4) return res_launch_t<MS, MS, 1, 1, 8, 4>(t, g, X, Y, J, fwd, post, pre, st, occ);
     if (t.WM == 1 && t.NI == 1 && t.WN == 8 && t.nstage == 2) return res_launch_t<MS, MS, 1, 1, 8, 2>(t, g, X, Y, J, fwd, post, pre, st, occ);
     if (t.WM == 2 && t.NI == 1 && t.WN == 4 && t.nstage == 4) return res_launch_t<MS, H, 1, 2, 4, 4>(t, g, X, Y, J, fwd, post, pre, st, occ);
+    // 12 consumer warps (three per sub-partition), half the strips each
+    if (t.WM == 2 && t.NI == 1 && t.WN == 6 && t.nstage == 4) return res_launch_t<MS, H, 1, 2, 6, 4>(t, g, X, Y, J, fwd, post, pre, st, occ);
+    if (t.WM == 2 && t.NI == 1 && t.WN == 6 && t.nstage == 2) return res_launch_t<MS, H, 1, 2, 6, 2>(t, g, X, Y, J, fwd, post, pre, st, occ);
     if (t.WM == 2 && t.NI == 2 && t.WN == 3 && t.nstage == 4) return res_launch_t<MS, H, 2, 2, 3, 4>(t, g, X, Y, J, fwd, post, pre, st, occ);
     if (t.WM == 2 && t.NI == 1 && t.WN == 3 && t.nstage == 6) return res_launch_t<MS, H, 1, 2, 3, 6>(t, g, X, Y, J, fwd, post, pre, st, occ);
     if constexpr (MS <= 8) {
@@ -480,7 +483,8 @@ std::vector<Tiling> fold_res_candidates(int n, int Mp_hint) {
     if (S < 4 || S > 11) return out;  // small factors: the streaming kernel; n > 176: factors exceed smem
     const int Kp = (F + 3) / 4 * 4;
     // WM(WS), NI, WN(WF), NS; {1, 1, 8, 2}: the fused D^-1/2 pre-scale variant (doubled stages fit)
-    const int variants[6][4] = {{1, 1, 8, 4}, {2, 1, 4, 4}, {1, 1, 7, 4}, {2, 2, 3, 4}, {1, 2, 4, 4}, {1, 1, 8, 2}};
+    const int variants[8][4] = {{1, 1, 8, 4}, {2, 1, 4, 4}, {1, 1, 7, 4}, {2, 2, 3, 4}, {1, 2, 4, 4}, {1, 1, 8, 2},
+                                {2, 1, 6, 4}, {2, 1, 6, 2}};
     for (const auto& v : variants) {
         Tiling t;
         t.fold = 2;

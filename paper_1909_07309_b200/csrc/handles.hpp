@@ -267,7 +267,14 @@ struct stiga_fd_s {
                "slab time U_t (scatter)");
         } else {
             mark(st);
-            ck(gpu::launch_time_fused(tl_t, g, in, nullptr, Jt_t.p, J_t.p, a2, st, &sc), "slab time fused (scatter)");
+            gpu::Tiling tf = tl_t;
+            if (tf.res)  // the scatter epilogue lives in the streaming time-fused kernel
+                for (const auto& t : cand_time)
+                    if (!t.res) {
+                        tf = t;
+                        break;
+                    }
+            ck(gpu::launch_time_fused(tf, g, in, nullptr, Jt_t.p, J_t.p, a2, st, &sc), "slab time fused (scatter)");
         }
     }
 
@@ -529,7 +536,7 @@ struct stiga_fd_s {
             L.emplace_back("arrowhead", 0.0);
             L.emplace_back(std::string("time_Ut") + (sharded ? "+scatter" : tag(tl_ts)), 2.0 * nt * Nt);
         } else {
-            L.emplace_back(std::string("time_fused") + (sharded ? "+scatter" : ""), 4.0 * nt * Nt);
+            L.emplace_back(std::string("time_fused") + (sharded ? "+scatter" : tag(tl_t)), 4.0 * nt * Nt);
         }
         if (sharded) L.emplace_back("exchange_barrier_2", 0.0);
         for (int l = 0; l < d; ++l)
