@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "matvec_fused.cuh"
 
@@ -69,6 +70,8 @@ struct Plane2Smem {
 //    register window of kR1 + 2P x rows; the coefficient rows (uniform per warp) are staged in smem.
 //  stage 2 (mode 0): thread = a fixed pair of columns i0 = 2 pi, 2 pi + 1 (their four coefficient rows stay
 //    in registers for the whole kernel) and rows g, g + G, ...; 16-byte window loads.
+// dbuf: a second x-tile buffer (after the coefficient rows) receives the NEXT tile's rows while the
+// current one is computed (cp.async groups: the wait before stage 1 leaves the prefetch in flight).
 template <int P>
 __global__ void __launch_bounds__(kPlaneThreads, 2) plane2_kernel(int n0, int n1, long long R,
                                                                   const double* __restrict__ x, double* __restrict__ a2,
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) plane2_kernel(int n0, int n1
                                                                   const double* __restrict__ m0,
                                                                   const double* __restrict__ k0,
                                                                   const double* __restrict__ m1,
-                                                                  const double* __restrict__ k1) {
+                                                                  const double* __restrict__ k1, int dbuf) {
     constexpr int W = 2 * P + 1;
     constexpr int B = kTR - 2 * P;
     constexpr int WP = (W + 1) & ~1;
@@ -110,21 +113,33 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) plane2_kernel(int n0, int n1
         const int row = rem / padw, c = rem - row * padw;
         (f ? bs : as)[row * L.ap + (c < P ? c : n0 + c)] = 0.0;
     }
+    // x rows j0 - P .. j0 + B + P - 1 of tile tt (zero rows outside [0, n1)) into buffer dst (the tile's x
+    // rows are one contiguous chunk of the colex vector; smem pitch = n0)
+    auto issue_x = [&](long long tt, double* dst) {
+        const long long rr = tt / tiles_j;
+        const int jj = static_cast<int>(tt - rr * tiles_j) * B;
+        const int jlo = max(jj - P, 0), jhi = min(jj + B + P, n1);  // rows that exist
+        const int e0 = (jlo - (jj - P)) * n0, e1 = (jhi - (jj - P)) * n0;
+        const double* src = x + static_cast<long long>(n0) * (n1 * rr + jlo) - e0;
+        for (int e = threadIdx.x; e < kTR * n0; e += blockDim.x) {
+            if (e >= e0 && e < e1) cpa8(dst + e, src + e);
+            else dst[e] = 0.0;
+        }
+    };
+    double* xbuf[2] = {xs, ck + L.c_elems()};
+    int cur = 0;
+    if (dbuf && blockIdx.x < ntiles) issue_x(blockIdx.x, xbuf[0]);
+    cpa_commit();
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const long long r = t / tiles_j;
         const int j0 = static_cast<int>(t - r * tiles_j) * B;
-        // x rows j0 - P .. j0 + B + P - 1 (zero rows outside [0, n1)) and the tile's mode-1 coefficient rows
-        // (the tile's x rows are one contiguous chunk of the colex vector; smem pitch = n0)
-        {
-            const int jlo = max(j0 - P, 0), jhi = min(j0 + B + P, n1);  // rows that exist
-            const int e0 = (jlo - (j0 - P)) * n0, e1 = (jhi - (j0 - P)) * n0;
-            const double* src = x + static_cast<long long>(n0) * (n1 * r + jlo) - e0;
-            for (int e = threadIdx.x; e < kTR * n0; e += blockDim.x) {
-                if (e >= e0 && e < e1) cpa8(xs + e, src + e);
-                else xs[e] = 0.0;
-            }
-            cpa_commit();
+        xs = dbuf ? xbuf[cur] : xbuf[0];
+        if (dbuf) {
+            if (t + gridDim.x < ntiles) issue_x(t + gridDim.x, xbuf[cur ^ 1]);
+        } else {
+            issue_x(t, xs);
         }
+        cpa_commit();
         for (int e = threadIdx.x; e < B * WP; e += blockDim.x) {
             const int q = e / WP, k = e - q * WP;
             const int j = j0 + q;
@@ -132,7 +147,8 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) plane2_kernel(int n0, int n1
             cm[q * WP + k] = ok ? __ldg(m1 + static_cast<long long>(j) * W + k) : 0.0;
             ck[q * WP + k] = ok ? __ldg(k1 + static_cast<long long>(j) * W + k) : 0.0;
         }
-        cpa_wait<0>();
+        if (dbuf) cpa_wait<1>();  // this tile's rows landed; the next tile's stay in flight
+        else cpa_wait<0>();
         __syncthreads();
         // ---- stage 1: mode 1 on the B interior rows ----
         {
@@ -205,7 +221,9 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) plane2_kernel(int n0, int n1
             }
         }
         __syncthreads();  // x, a1/b1 tiles and coefficient rows are rewritten by the next tile
+        cur ^= 1;
     }
+    cpa_wait<0>();
 }
 
 // ---- stream kernel ----------------------------------------------------------------------------
@@ -214,7 +232,7 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) plane2_kernel(int n0, int n1
 // columns per tile (one per thread), several CTAs per SM.
 __host__ __device__ constexpr int st_threads(bool mode2) { return 256; }
 __host__ __device__ constexpr int st_sq(bool mode2) { return mode2 ? 2 : 1; }
-constexpr int kNS = 3;    // cp.async ring depth over time slices
+constexpr int kNS = 4;    // cp.async ring depth over time slices (kNS - 2 ahead of the consumed one)
 
 struct StreamSmem {
     int rows_in, cols, cp, wp, nt;
@@ -225,7 +243,9 @@ struct StreamSmem {
     __host__ __device__ size_t stage() const { return 2 * static_cast<size_t>(rows_in) * cp; }
     __host__ __device__ size_t ring() const { return kNS * stage(); }
     __host__ __device__ size_t tcoef() const { return 2 * static_cast<size_t>(nt) * wp; }   // time columns
-    __host__ __device__ size_t bytes() const { return sizeof(double) * (ring() + tcoef()); }
+    // mode 2: the tile's coefficient rows (M_3, K_3 for the RPT output rows), read as warp broadcasts
+    __host__ __device__ size_t ccoef() const { return rows_in > 1 ? 2 * static_cast<size_t>(rows_in) * wp : 0; }
+    __host__ __device__ size_t bytes() const { return sizeof(double) * (ring() + tcoef() + ccoef()); }
 };
 
 // MODE2 = true: fields (L, n2, T) colex, tile = 32 consecutive l x 32 rows i2 (8 warps x kSQ rows).
@@ -235,7 +255,7 @@ struct StreamSmem {
 // cw / cm: band COLUMNS of gamma W_t and nu M_t, cw[t' * W + (d + P)] = gamma W_t(t' + d, t') (0 outside);
 // nt = rows of the time factors.
 template <int P, bool MODE2>
-__global__ void __launch_bounds__(st_threads(MODE2), 1) stream_kernel(long long Lc, int n2, int nt, int ti0, int nti, int to0, int nto,
+__global__ void __launch_bounds__(st_threads(MODE2), 2) stream_kernel(long long Lc, int n2, int nt, int ti0, int nti, int to0, int nto,
                                                      const double* __restrict__ a, const double* __restrict__ b,
                                                      double* __restrict__ y, const double* __restrict__ m2,
                                                      const double* __restrict__ k2, const double* __restrict__ cw,
@@ -249,6 +269,7 @@ __global__ void __launch_bounds__(st_threads(MODE2), 1) stream_kernel(long long 
     const size_t STAGE = S.stage();
     double* tcw = sm + S.ring();
     double* tcm = tcw + static_cast<size_t>(nt) * WP;
+    double* c2s = tcm + static_cast<size_t>(nt) * WP;  // MODE2: [RPT][2][WP] coefficient rows of the tile
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long slice = Lc * n2;  // entries per time slice
     const long long ncolb = (Lc + COLS - 1) / COLS;
@@ -293,17 +314,14 @@ __global__ void __launch_bounds__(st_threads(MODE2), 1) stream_kernel(long long 
             cpa_commit();
         };
         __syncthreads();  // previous tile done with the ring
-        // mode-2 coefficient rows of this thread's output rows (fixed for the tile) in registers
-        double c2m[MODE2 ? kSQ : 1][W], c2k[MODE2 ? kSQ : 1][W];
+        // mode-2 coefficient rows of the tile's output rows -> smem (warp-uniform rows: broadcast reads;
+        // in registers they cost 4 P + 2 doubles per thread and halved the occupancy); visible after the
+        // first streaming barrier
         if (MODE2) {
-#pragma unroll
-            for (int q = 0; q < kSQ; ++q) {
-                const int i2 = min(r0 + warp * kSQ + q, n2 - 1);  // rows past n2 are computed, not stored
-#pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    c2m[q][k] = __ldg(m2 + static_cast<long long>(i2) * W + k);
-                    c2k[q][k] = __ldg(k2 + static_cast<long long>(i2) * W + k);
-                }
+            for (int e = threadIdx.x; e < RPT * 2 * WP; e += blockDim.x) {
+                const int q = e / (2 * WP), rem = e - q * 2 * WP, f = rem / WP, k = rem - f * WP;
+                const int i2 = min(r0 + q, n2 - 1);  // rows past n2 are computed, not stored
+                c2s[e] = k < W ? __ldg((f ? k2 : m2) + static_cast<long long>(i2) * W + k) : 0.0;
             }
         }
         double acc[kSQ][W];
@@ -312,17 +330,23 @@ __global__ void __launch_bounds__(st_threads(MODE2), 1) stream_kernel(long long 
 #pragma unroll
             for (int s = 0; s < W; ++s) acc[q][s] = 0.0;
         for (int k = 0; k < kNS - 1; ++k) issue(ti0 + k);
-        // acc[q][k] accumulates output t = tp - P + k; after step tp, acc[q][0] (t = tp - P) is complete
-        // and the ring shifts by one (register moves, no dynamic indexing)
-        {
+        // Modular accumulator ring: at stream step tau = tp - ti0, output t = tp + kk - P accumulates into
+        // slot (tau + kk) mod W; the loop is unrolled by W so every slot index is a compile-time constant
+        // (no register shifting).  One barrier per step: stage (tau - 1) mod kNS is refilled only after it.
+        const int tot = te - ti0;
 #pragma unroll 1
-            for (int tp = ti0; tp < te; ++tp) {
+        for (int base = 0; base < tot; base += W) {
+#pragma unroll
+            for (int ph = 0; ph < W; ++ph) {
+                const int tau = base + ph;
+                if (tau >= tot) break;
+                const int tp = ti0 + tau;
+                cpa_wait<kNS - 2>();
+                __syncthreads();  // stage tau landed for all; everyone is done with step tau - 1
                 issue(tp + kNS - 1);
-                cpa_wait<kNS - 1>();
-                __syncthreads();
                 if (tp < ti0 + nti) {
                     double v3a[kSQ], v3b[kSQ];
-                    const double* st = sm + static_cast<size_t>((tp - ti0) % kNS) * STAGE;
+                    const double* st = sm + static_cast<size_t>(tau % kNS) * STAGE;
                     if (MODE2) {  // mode 2 on rows r0 + warp*kSQ + q, column lane
                         const int rw = warp * kSQ;
                         double aw[kSQ + 2 * P], bw[kSQ + 2 * P];
@@ -334,11 +358,13 @@ __global__ void __launch_bounds__(st_threads(MODE2), 1) stream_kernel(long long 
 #pragma unroll
                         for (int q = 0; q < kSQ; ++q) {
                             double sa = 0.0, sb = 0.0;
+                            const double* cmq = c2s + (rw + q) * 2 * WP;
 #pragma unroll
                             for (int k = 0; k < W; ++k) {
-                                sa = fma(c2m[q][k], aw[q + k], sa);
-                                sb = fma(c2k[q][k], aw[q + k], sb);
-                                sb = fma(c2m[q][k], bw[q + k], sb);
+                                const double cmk = cmq[k], ckk = cmq[WP + k];
+                                sa = fma(cmk, aw[q + k], sa);
+                                sb = fma(ckk, aw[q + k], sb);
+                                sb = fma(cmk, bw[q + k], sb);
                             }
                             v3a[q] = sa;
                             v3b[q] = sb;
@@ -350,7 +376,7 @@ __global__ void __launch_bounds__(st_threads(MODE2), 1) stream_kernel(long long 
                             v3b[q] = st[CP + threadIdx.x + kST * q];
                         }
                     }
-                    // time: output t = tp + dd receives cw(tp)[dd + P] a3 + cm(tp)[dd + P] b3
+                    // time: output t = tp + kk - P receives cw(tp)[kk] a3 + cm(tp)[kk] b3 (slot (ph + kk) mod W)
                     const double2* cwr = reinterpret_cast<const double2*>(tcw + static_cast<size_t>(tp) * WP);
                     const double2* cmr = reinterpret_cast<const double2*>(tcm + static_cast<size_t>(tp) * WP);
 #pragma unroll
@@ -358,42 +384,35 @@ __global__ void __launch_bounds__(st_threads(MODE2), 1) stream_kernel(long long 
                         const double2 w2 = cwr[k2], m2v = cmr[k2];
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            const int kk = 2 * k2 + h;  // dd = kk - P
+                            const int kk = 2 * k2 + h;
                             if (kk < W) {
                                 const double w = h ? w2.y : w2.x, m = h ? m2v.y : m2v.x;
-                                // output t = tp + kk - P sits in acc[.][kk]
+                                const int slot = (ph + kk) % W;
 #pragma unroll
-                                for (int q = 0; q < kSQ; ++q) acc[q][kk] = fma(m, v3b[q], fma(w, v3a[q], acc[q][kk]));
+                                for (int q = 0; q < kSQ; ++q)
+                                    acc[q][slot] = fma(m, v3b[q], fma(w, v3a[q], acc[q][slot]));
                             }
                         }
                     }
                 }
-                // output t = tp - P is complete
-                {
-                    const int tdone = tp - P;
-                    constexpr int s = 0;
-                    if (tdone >= to0 && tdone < to0 + nto) {
-                        double* yt = y + static_cast<long long>(tdone - to0) * slice;
-#pragma unroll
-                        for (int q = 0; q < kSQ; ++q) {
-                            if (MODE2) {
-                                const int i2 = r0 + warp * kSQ + q;
-                                const long long l = l0 + lane;
-                                if (i2 < n2 && l < Lc) yt[l + Lc * i2] = acc[q][s];
-                            } else {
-                                const long long l = l0 + threadIdx.x + kST * q;
-                                if (l < Lc) yt[l] = acc[q][s];
-                            }
-                        }
-                    }
+                // output t = tp - P is complete in slot ph
+                const int tdone = tp - P;
+                if (tdone >= to0 && tdone < to0 + nto) {
+                    double* yt = y + static_cast<long long>(tdone - to0) * slice;
 #pragma unroll
                     for (int q = 0; q < kSQ; ++q) {
-#pragma unroll
-                        for (int k = 0; k + 1 < W; ++k) acc[q][k] = acc[q][k + 1];
-                        acc[q][W - 1] = 0.0;
+                        if (MODE2) {
+                            const int i2 = r0 + warp * kSQ + q;
+                            const long long l = l0 + lane;
+                            if (i2 < n2 && l < Lc) yt[l + Lc * i2] = acc[q][ph];
+                        } else {
+                            const long long l = l0 + threadIdx.x + kST * q;
+                            if (l < Lc) yt[l] = acc[q][ph];
+                        }
                     }
                 }
-                __syncthreads();  // stage (tp - ti0) % kNS is refilled by the next iteration's issue
+#pragma unroll
+                for (int q = 0; q < kSQ; ++q) acc[q][ph] = 0.0;
             }
         }
         cpa_wait<0>();
@@ -410,8 +429,14 @@ cudaError_t launch_plane2(int n0, int n1, long long R, int P, const double* x, d
                           const double* m0, const double* k0, const double* m1, const double* k1, cudaStream_t st) {
     if (R <= 0 || n0 <= 0 || n1 <= 0) return cudaSuccess;
     if (P < 1 || P > kMaxFusedP || kTR - 2 * P < 2 || (n0 + 1) / 2 > kPlaneThreads) return cudaErrorInvalidValue;
-    const size_t sm = plane2_smem_bytes(n0, P);
-    if (sm > 227 * 1024) return cudaErrorInvalidValue;
+    const size_t sm1 = plane2_smem_bytes(n0, P);
+    if (sm1 > 227 * 1024) return cudaErrorInvalidValue;
+    // STIGA_PLANE2_DBUF=1: double-buffer the x tile when two CTAs per SM still fit (measured no faster:
+    // c3 1.95 vs 1.90 ms -- the two co-resident CTAs already overlap one tile's load with the other's work)
+    static const bool want_dbuf = std::getenv("STIGA_PLANE2_DBUF") != nullptr;
+    const size_t sm2 = sm1 + sizeof(double) * Plane2Smem(n0, P).x_elems();
+    const int dbuf = (want_dbuf && 2 * (sm2 + 1024) <= 228 * 1024) ? 1 : 0;
+    const size_t sm = dbuf ? sm2 : sm1;
     const int B = kTR - 2 * P;
     const long long ntiles = (n1 + B - 1) / B * R;
     const int per_sm = std::max(1, static_cast<int>((227 * 1024) / (sm + 1024)));
@@ -419,7 +444,7 @@ cudaError_t launch_plane2(int n0, int n1, long long R, int P, const double* x, d
 #define STIGA_P2(PP)                                                                                                 \
     case PP:                                                                                                         \
         cudaFuncSetAttribute(plane2_kernel<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)); \
-        plane2_kernel<PP><<<grid, kPlaneThreads, sm, st>>>(n0, n1, R, x, a2, b2, m0, k0, m1, k1);                    \
+        plane2_kernel<PP><<<grid, kPlaneThreads, sm, st>>>(n0, n1, R, x, a2, b2, m0, k0, m1, k1, dbuf);              \
         break;
     switch (P) {
         STIGA_P2(1)
@@ -445,7 +470,8 @@ cudaError_t launch_stream(bool mode2, long long Lc, int n2, int nt, int ti0, int
     if (sm > 227 * 1024) return cudaErrorInvalidValue;
     const int rpt = (st_threads(true) / 32) * st_sq(true);
     const long long ntiles = (Lc + S.cols - 1) / S.cols * (mode2 ? (n2 + rpt - 1) / rpt : 1);
-    const int per_sm = std::max(1, std::min(4, static_cast<int>((227 * 1024) / (sm + 1024))));
+    // mode 2: two CTAs per SM (<= 128 registers); time only: up to four
+    const int per_sm = std::max(1, std::min(mode2 ? 2 : 4, static_cast<int>((227 * 1024) / (sm + 1024))));
     const unsigned grid = static_cast<unsigned>(std::min<long long>(ntiles, 148LL * per_sm));
 #define STIGA_ST(PP)                                                                                                  \
     case PP:                                                                                                          \
