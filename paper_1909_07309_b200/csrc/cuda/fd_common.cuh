@@ -76,7 +76,8 @@ struct Shape {
     static constexpr int BN = 16 * WN;
     static constexpr int LDX = BN + 4;  // == 4 mod 16
     static constexpr int MPB = 8 * MI * WM;
-    static constexpr int XCNT = kBK * BN / NTHR;       // fiber-chunk elements per thread (8/WM)
+    static constexpr bool EXACT = (kBK * BN) % NTHR == 0;  // false for WM = 3: the last copy round is guarded
+    static constexpr int XCNT = (kBK * BN + NTHR - 1) / NTHR;  // fiber-chunk elements per thread (8/WM)
     static constexpr int JPIECES = MPB * (kBK / 2);    // 16-byte J pieces per chunk
     static constexpr int JROWSTEP = NTHR / 8;          // J rows between a thread's pieces
     static constexpr int JCNT = (JPIECES + NTHR - 1) / NTHR;
@@ -84,7 +85,7 @@ struct Shape {
     static constexpr int XCOLSTEP = NTHR / 16;         // fibers between elements (L == 1)
     static constexpr int DOFF = kBK * LDX + MPB * kLDJ;  // D chunk offset within a stage (PS)
     static constexpr int STAGE = DOFF + (PS ? kBK * LDX : 0);  // doubles per pipeline stage
-    static_assert(kBK * BN % NTHR == 0, "fiber chunk must split evenly over the CTA");
+    static_assert(NTHR % BN == 0 && NTHR % 16 == 0, "fiber-chunk copy rounds must be whole rows / fibers");
 };
 
 // Global offset of element 0 of fiber cc (colex: l + L*n*r).
@@ -129,7 +130,8 @@ __device__ __forceinline__ Prod make_prod(const KArgs& a, long long c0, const do
         p.xkstep = kBK;
 #pragma unroll
         for (int u = 0; u < SH::XCNT; ++u)
-            if (c0 + cf + u * SH::XCOLSTEP < a.geo.ncols) p.colmask |= 1u << u;
+            if (c0 + cf + u * SH::XCOLSTEP < a.geo.ncols && (SH::EXACT || cf + u * SH::XCOLSTEP < SH::BN))
+                p.colmask |= 1u << u;
     } else {
         const int c = tid & (SH::BN - 1), j0 = tid / SH::BN;
         const long long cc = c0 + c;
@@ -167,25 +169,30 @@ __device__ __forceinline__ void issue_chunk(const KArgs& a, const Prod& p, unsig
         if (p.contiguous) {
             if (p.full_tile && k0 + kBK <= a.geo.n) {
 #pragma unroll
-                for (int u = 0; u < SH::XCNT; ++u) cp_async8(xs + 8u * u * SH::XCOLSTEP, xg + u * p.xstep);
+                for (int u = 0; u < SH::XCNT; ++u)
+                    if (SH::EXACT || ((p.colmask >> u) & 1u)) cp_async8(xs + 8u * u * SH::XCOLSTEP, xg + u * p.xstep);
             } else {
                 const bool rowv = k0 + p.xrow0 < a.geo.n;
 #pragma unroll
                 for (int u = 0; u < SH::XCNT; ++u) {
                     const bool v = rowv && ((p.colmask >> u) & 1u);
-                    cp_async8_zfill(xs + 8u * u * SH::XCOLSTEP, v ? xg + u * p.xstep : X, v);
+                    if (SH::EXACT || static_cast<int>(threadIdx.x >> 4) + u * SH::XCOLSTEP < SH::BN)
+                        cp_async8_zfill(xs + 8u * u * SH::XCOLSTEP, v ? xg + u * p.xstep : X, v);
                 }
             }
         } else {
             if (p.full_tile && k0 + kBK <= a.geo.n) {
 #pragma unroll
-                for (int u = 0; u < SH::XCNT; ++u) cp_async8(xs + 8u * u * SH::XROWSTEP * SH::LDX, xg + u * p.xstep);
+                for (int u = 0; u < SH::XCNT; ++u)
+                    if (SH::EXACT || p.xrow0 + u * SH::XROWSTEP < kBK)
+                        cp_async8(xs + 8u * u * SH::XROWSTEP * SH::LDX, xg + u * p.xstep);
             } else {
                 const bool colv = p.colmask != 0u;
 #pragma unroll
                 for (int u = 0; u < SH::XCNT; ++u) {
                     const bool v = colv && (k0 + p.xrow0 + u * SH::XROWSTEP < a.geo.n);
-                    cp_async8_zfill(xs + 8u * u * SH::XROWSTEP * SH::LDX, v ? xg + u * p.xstep : X, v);
+                    if (SH::EXACT || p.xrow0 + u * SH::XROWSTEP < kBK)
+                        cp_async8_zfill(xs + 8u * u * SH::XROWSTEP * SH::LDX, v ? xg + u * p.xstep : X, v);
                 }
             }
         }
@@ -495,13 +502,14 @@ __device__ __forceinline__ void stage_arrow_consts(const ArrowParams& ap, double
 
 template <class SH>
 __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long long c0, const ArrowParams& ap,
-                                               const double* cs, const double* ccol) {
+                                               const double* cs, const double* ccol, double* red = nullptr) {
     const int NP = arrow_np(ap);
     constexpr int P = SH::NTHR / SH::BN;
-    static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "threads per column must be a power of two <= 32");
+    constexpr bool POW2 = (P & (P - 1)) == 0;  // WM = 3: P = 6, the Schur sum is reduced through smem (red)
+    static_assert(P >= 1 && P <= 32, "threads per column");
     const int tid = threadIdx.x;
-    const int c = tid / P;
-    const int p = tid - c * P;
+    const int c = POW2 ? tid / P : tid % SH::BN;
+    const int p = POW2 ? tid - c * P : tid / SH::BN;
     const double lam = ccol[c], linv = ccol[SH::BN + c];
     const double nu = ap.nu, inv_nu = ap.inv_nu, gam = ap.gamma;
     const double nulam = nu * lam;
@@ -525,8 +533,16 @@ __device__ __forceinline__ void arrowhead_tile(const KArgs& a, double* Zs, long 
         xz = linv * col[(nt - 2) * SH::LDX] * inv_nu;
         part += gam * __ldg(ap.g + nt - 2) * xz;
     }
+    if constexpr (POW2) {
 #pragma unroll
-    for (int off = P >> 1; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+        for (int off = P >> 1; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+    } else {  // the P partial sums of a column live in different warps: fixed-order sum through smem
+        red[p * SH::BN + c] = part;
+        __syncthreads();
+        part = 0.0;
+#pragma unroll
+        for (int q = 0; q < P; ++q) part += red[q * SH::BN + c];
+    }
     const double xlast = ccol[2 * SH::BN + c] * (slast + part);
     for (int j = p; j < ap.npairs; j += P) {
         double xa, xb;

@@ -26,7 +26,7 @@ std::vector<Tiling> time_tiling_candidates(int nt) {
         std::sscanf(f, "%d,%d,%d", &force_wm, &force_wn, &force_ns);
     const int S = (nt + 7) / 8;
     const int Kp = (nt + 3) / 4 * 4;
-    for (int WM : {1, 2, 4}) {
+    for (int WM : {1, 2, 3, 4}) {  // WM = 3: S = 9 (c4, c5p2) splits evenly into 3 x 3 strips
         const int MI = (S + WM - 1) / WM;
         if (MI > 13 || MI < 1) continue;
         for (int WN : {4, 2}) {
@@ -50,7 +50,8 @@ std::vector<Tiling> time_tiling_candidates(int nt) {
                 t.nstage = ns;
                 t.smem = sizeof(double) * (static_cast<size_t>(Kp) * t.LDX +
                                            static_cast<size_t>(ns) * (kBK * t.LDX + t.MpB * kLDJ) +
-                                           7 * static_cast<size_t>(nt / 2 + 1) + 3 * static_cast<size_t>(t.BN));
+                                           7 * static_cast<size_t>(nt / 2 + 1) + 3 * static_cast<size_t>(t.BN) +
+                                           (WM == 3 ? 6 * static_cast<size_t>(t.BN) : 0));
                 if (t.smem > kSmemPerCTA) continue;
                 int occ = 0;
                 ArrowParams ap;

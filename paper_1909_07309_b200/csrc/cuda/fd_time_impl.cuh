@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(32 * WM * WN)
     double* stages = smem + static_cast<size_t>(a.Zrows) * SH::LDX;  // nstage x stage
     double* cs = stages + static_cast<size_t>(a.nstage) * SH::STAGE;    // 7 x (n_t/2 + 1) pair constants
     double* ccol = cs + 7 * arrow_np(ap);                               // 3 x BN column constants
+    double* red = ccol + 3 * SH::BN;                                    // WM = 3 only: 6 x BN Schur partial sums
     const long long c0 = static_cast<long long>(blockIdx.x) * SH::BN;
     stage_arrow_consts(ap, cs);  // visible after the GEMM's first barrier
     stage_column_consts(ap, c0, a.geo.ncols, SH::BN, ccol);
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(32 * WM * WN)
             cp_commit();
         }
     }
-    if (!(ap.debug & 1)) arrowhead_tile<SH>(a, Zs, c0, ap, cs, ccol);
+    if (!(ap.debug & 1)) arrowhead_tile<SH>(a, Zs, c0, ap, cs, ccol, red);
     __syncthreads();
     zero_acc<SH>(acc);
     gemm<SH, false>(a, stages, p, X, Zs, true, 0, acc);  // y = U_t z
@@ -92,10 +93,12 @@ cudaError_t dispatch_time_v(const Tiling& t, const ModeGeom& g, const double* X,
     if (t.WN == 2) {
         if (t.WM == 1) return dispatch_time_w<SC, 1, 2>(t, g, X, Y, Jt, J, ap, st, occ, sc);
         if (t.WM == 2) return dispatch_time_w<SC, 2, 2>(t, g, X, Y, Jt, J, ap, st, occ, sc);
+        if (t.WM == 3) return dispatch_time_w<SC, 3, 2>(t, g, X, Y, Jt, J, ap, st, occ, sc);
         if (t.WM == 4) return dispatch_time_w<SC, 4, 2>(t, g, X, Y, Jt, J, ap, st, occ, sc);
     } else if (t.WN == 4) {
         if (t.WM == 1) return dispatch_time_w<SC, 1, 4>(t, g, X, Y, Jt, J, ap, st, occ, sc);
         if (t.WM == 2) return dispatch_time_w<SC, 2, 4>(t, g, X, Y, Jt, J, ap, st, occ, sc);
+        if (t.WM == 3) return dispatch_time_w<SC, 3, 4>(t, g, X, Y, Jt, J, ap, st, occ, sc);
     }
     return cudaErrorInvalidValue;
 }

@@ -204,6 +204,24 @@ def test_time_resident_kernel(d, p, nel, gamma, nu, monkeypatch):
     assert rel(s, P2.apply(torch.from_numpy(r).cuda()).cpu().numpy()) <= 1e-13
 
 
+@pytest.mark.parametrize("wn", [2, 4])
+@pytest.mark.parametrize("d,p,nel", [(3, 2, 64), (2, 4, 64), (2, 3, 40), (1, 3, 66), (2, 2, 9)])
+def test_time_fused_three_warp_rows(d, p, nel, wn, monkeypatch):
+    """Time-fused kernel with WM = 3 warp rows (fd_time.cu: n_t = 65..72 is 9 strips = 3 x 3, the c4 /
+    c5p2 shape; 96 WN threads, so the last fiber-copy round is guarded and the 6 Schur partial sums of a
+    column are reduced through shared memory): odd and even n_t, S not a multiple of 3, D^-1/2 scaled,
+    <= 1e-11 vs the oracle and equal to the tuned kernel to rounding."""
+    monkeypatch.setenv("STIGA_TIME_VARIANT", "fused")
+    monkeypatch.setenv("STIGA_FORCE_TIME_TILING", f"3,{wn},0")
+    s, so, P, Po, r = run_pair(d, p, nel, scaled=True, seed=33)
+    # only WM = 3 candidates exist under the forced tiling, so a fused launch is a WM = 3 launch
+    assert any(nm.startswith("time_fused") for nm, _ in P.launch_info())
+    assert rel(s, so) <= TOL
+    monkeypatch.delenv("STIGA_FORCE_TIME_TILING")
+    s2, *_ = run_pair(d, p, nel, scaled=True, seed=33)
+    assert rel(s, s2) <= 1e-13
+
+
 def _oracle_with_product_basis(Po, P, d, gamma=1.0, nu=1.0):
     """Rebuild the oracle's factors from the product's factorization (stiga_fd_export), so the
     comparison isolates the apply (fdsolve.cpp:155-164) from the eigensolver."""

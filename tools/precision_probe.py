@@ -1,6 +1,6 @@
 """Debugging aid: accuracy of the GPU FD apply and of the float64 oracle against an extended-
 precision (x87 long double) evaluation of the same apply on the product's exported factors, for a
-d = 1 shape (usage: python tools/debug_precision.py p n_el [scaled])."""
+d = 1 shape (usage: python tools/precision_probe.py p n_el [scaled])."""
 import os
 import sys
 
