@@ -358,6 +358,171 @@ __global__ void __launch_bounds__(32 * (2 * kMaxWarps + 1))
     stencil_store(sg, c, rb, acc, mat ? KX : MX);
 }
 
+// (c) Line-pair bricks (n even, <= 72 rows per line, d >= 2): the 8 MMA rows are 4 consecutive i_1 of
+// TWO neighbouring lines (i_2 = 2q, 2q + 1) instead of 8 consecutive i_1 of one line.  The union of the
+// 8 rows' neighbour windows is (4 + 2p) x (2p + 2) lines instead of (8 + 2p) x (2p + 1): for p = 4 the
+// band blocks are 9/12 * 9/10 = 67% dense instead of 9/16 = 56%, and 66 rows pad to 68 instead of 72 --
+// 17% fewer DMMAs per output row.  A CTA owns a line pair and <= 72 time columns and walks the
+// (2p + 2) * (2p + 1)^(d-2) neighbour lines j_2 = 2q - p + e; at step e line a uses offset plane o_2 = e - p
+// (e <= 2p), line b plane o_2 = e - p - 1 (e >= 1); the missing band of the first / last step is a zero
+// A-fragment half (warp-uniform flag).  Consumer warp = 3 row blocks x one matrix; same TMA ring.
+struct PairGeo {
+    int n, p, W, d;
+    long long Ns;
+    int n_t;
+    int nblk;            // 4-row blocks per line
+    int LDR, BR;         // X-window / band smem pitches (== 4 mod 16)
+    int nsteps;          // (W + 1) * W^(d-2)
+    int xstage, bstage;  // doubles per X stage / per (matrix, line) band stage
+    int shift, nst, boxt;
+};
+
+struct PairCtx {
+    int i2, i3, t0, tcols;
+    long long line_a;
+};
+
+__device__ __forceinline__ PairCtx pair_ctx(const PairGeo& sg) {
+    PairCtx c;
+    const int half = sg.n / 2;
+    c.i2 = 2 * static_cast<int>(blockIdx.x % half);
+    c.i3 = static_cast<int>(blockIdx.x / half);  // 0 for d = 2
+    c.line_a = c.i2 + static_cast<long long>(sg.n) * c.i3;
+    c.t0 = blockIdx.y * (8 * kTT);
+    c.tcols = min(8 * kTT, sg.n_t - c.t0);
+    return c;
+}
+
+// step s = e + (W + 1) o_3: neighbour line (j_2, j_3), -1 outside the patch
+__device__ __forceinline__ long long pair_nb_line(const PairGeo& sg, const PairCtx& c, int s) {
+    const int e = s % (sg.W + 1), o3 = s / (sg.W + 1);
+    const int j2 = c.i2 - sg.p + e;
+    if (j2 < 0 || j2 >= sg.n) return -1;
+    if (sg.d < 3) return j2;
+    const int j3 = c.i3 - sg.p + o3;
+    if (j3 < 0 || j3 >= sg.n) return -1;
+    return j2 + static_cast<long long>(sg.n) * j3;
+}
+__device__ __forceinline__ int pair_next_step(const PairGeo& sg, const PairCtx& c, int s) {
+    while (s < sg.nsteps && pair_nb_line(sg, c, s) < 0) ++s;
+    return s;
+}
+
+template <int KS, bool FULL>
+__device__ __forceinline__ void pair_step_t(const PairGeo& sg, const double* xs, const double* bm, int rb, bool va,
+                                            bool vb, int ntiles, double (&acc)[kTT][2]) {
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int ln = g >> 2, gi = g & 3;
+    const bool lv = ln ? vb : va;
+    const double* bs = xs + g * sg.LDR + sg.shift + 4 * rb + t4;
+    const double* br = bm + ln * sg.bstage + 4 * rb + gi;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+        const int o1 = 4 * kk + t4 - gi;
+        const bool av = lv && o1 >= 0 && o1 < sg.W;
+        const double a = av ? br[av ? o1 * sg.BR : 0] : 0.0;
+#pragma unroll
+        for (int tt = 0; tt < kTT; ++tt) {
+            if (FULL || tt < ntiles) sdmma(acc[tt][0], acc[tt][1], a, bs[tt * 8 * sg.LDR + 4 * kk]);
+        }
+    }
+}
+
+// Registers are allocated to warps in groups of four, so a 13th (producer) warp would cap the kernel at 128
+// registers and spill the 3 x 9 accumulator tiles: the producer is lane 0 of consumer warp 0 instead (it
+// issues the loads of step k + nst - 1 before computing step k), 12 warps, <= 168 registers.
+template <int KS, int RBW>
+__global__ void __launch_bounds__(32 * 2 * ((18 + RBW - 1) / RBW))
+    stencil_pair_kernel(PairGeo sg, const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapM,
+                        const __grid_constant__ CUtensorMap mapK, double* __restrict__ MX, double* __restrict__ KX) {
+    extern __shared__ __align__(128) double sx[];
+    const int nst = sg.nst;
+    double* xs = sx;                     // nst x xstage
+    double* bsm = xs + nst * sg.xstage;  // nst x (M, K) x (line a, line b) x bstage
+    uint64_t* full = reinterpret_cast<uint64_t*>(bsm + nst * 4 * sg.bstage);
+    uint64_t* empty = full + nst;
+    const int nwc = blockDim.x / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const PairCtx c = pair_ctx(sg);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            mb_init(full + s, 1);
+            mb_init(empty + s, nwc);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const bool producer = threadIdx.x == 0;
+    const int row0 = static_cast<int>(sg.n * c.line_a);
+    int sp = pair_next_step(sg, c, 0), kp = 0;  // producer cursor: next step to load, its ring index
+    auto produce = [&]() {                      // loads of step sp into stage kp % nst
+        const int st = kp % nst;
+        const int e = sp % (sg.W + 1), o3 = sp / (sg.W + 1);
+        const bool va = e < sg.W, vb = e >= 1;
+        if (kp >= nst) mb_wait(empty + st, ((kp / nst) - 1) & 1);
+        mb_expect(full + st, 8u * (sg.boxt * sg.LDR + 2 * ((va ? 1 : 0) + (vb ? 1 : 0)) * sg.W * sg.BR));
+        tma3(su32(xs + st * sg.xstage), &mapX, -sg.p - sg.shift, static_cast<int>(pair_nb_line(sg, c, sp)), c.t0,
+             full + st);
+        double* b0 = bsm + st * 4 * sg.bstage;
+        if (va) {
+            tma2(su32(b0), &mapM, row0, sg.W * (e + sg.W * o3), full + st);
+            tma2(su32(b0 + 2 * sg.bstage), &mapK, row0, sg.W * (e + sg.W * o3), full + st);
+        }
+        if (vb) {
+            tma2(su32(b0 + sg.bstage), &mapM, row0 + sg.n, sg.W * (e - 1 + sg.W * o3), full + st);
+            tma2(su32(b0 + 3 * sg.bstage), &mapK, row0 + sg.n, sg.W * (e - 1 + sg.W * o3), full + st);
+        }
+        sp = pair_next_step(sg, c, sp + 1);
+        ++kp;
+    };
+    if (producer)
+        for (int i = 0; i < nst - 1 && sp < sg.nsteps; ++i) produce();
+    const int nwm = nwc / 2, wi = warp % nwm, mat = warp / nwm;
+    const int ntiles = (c.tcols + 7) >> 3;
+    double acc[RBW][kTT][2];
+#pragma unroll
+    for (int r = 0; r < RBW; ++r)
+#pragma unroll
+        for (int t = 0; t < kTT; ++t) acc[r][t][0] = acc[r][t][1] = 0.0;
+    int k = 0;
+    for (int s = pair_next_step(sg, c, 0); s < sg.nsteps; s = pair_next_step(sg, c, s + 1), ++k) {
+        if (producer && sp < sg.nsteps) produce();  // step k + nst - 1 (waits until every warp released step k - 1)
+        __syncwarp();
+        const int st = k % nst;
+        const int e = s % (sg.W + 1);
+        const bool va = e < sg.W, vb = e >= 1;
+        mb_wait(full + st, (k / nst) & 1);
+        const double* xst = xs + st * sg.xstage;
+        const double* bm = bsm + (st * 4 + 2 * mat) * sg.bstage;
+#pragma unroll
+        for (int r = 0; r < RBW; ++r) {
+            const int rb = wi * RBW + r;
+            if (rb < sg.nblk) {
+                if (ntiles == kTT) pair_step_t<KS, true>(sg, xst, bm, rb, va, vb, ntiles, acc[r]);
+                else pair_step_t<KS, false>(sg, xst, bm, rb, va, vb, ntiles, acc[r]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mb_arrive(empty + st);
+    }
+    const int g = lane >> 2, t4 = lane & 3;
+    double* Y = mat ? KX : MX;
+#pragma unroll
+    for (int r = 0; r < RBW; ++r) {
+        const int i1 = 4 * (wi * RBW + r) + (g & 3);
+        if (i1 >= sg.n) continue;
+        const long long irow = i1 + sg.n * (c.line_a + (g >> 2));
+#pragma unroll
+        for (int tt = 0; tt < kTT; ++tt)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int tc = 8 * tt + 2 * t4 + v;
+                if (tc < c.tcols) Y[irow + sg.Ns * (c.t0 + tc)] = acc[r][tt][v];
+            }
+    }
+}
+
 // (b) cp.async staging by all threads (warp = column group, lane = rows), double buffered.
 template <int KS>
 __global__ void __launch_bounds__(32 * 2 * kMaxWarps)
@@ -504,9 +669,86 @@ cudaError_t launch_physical_assembly(const PhysicalDesc& g, double* Kst, double*
     }
 }
 
+template <int KS, int RBW>
+cudaError_t pair_launch(const PairGeo& sg, dim3 grid, const CUtensorMap* maps, double* MX, double* KX, cudaStream_t st) {
+    const size_t smem = sizeof(double) * sg.nst * (sg.xstage + 4 * sg.bstage) + 2 * sg.nst * sizeof(uint64_t);
+    cudaError_t e = cudaFuncSetAttribute(stencil_pair_kernel<KS, RBW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const int nwm = (sg.nblk + RBW - 1) / RBW;
+    stencil_pair_kernel<KS, RBW><<<grid, 32 * 2 * nwm, smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX);
+    return cudaGetLastError();
+}
+
+// Line-pair brick path (kernel (c)); returns cudaErrorNotSupported when the shape is not eligible.
+cudaError_t launch_stencil_pair(const PhysicalDesc& g, const double* Mst, const double* Kst, const double* X, double* MX,
+                                double* KX, long long n_t, cudaStream_t st) {
+    if (g.d < 2 || g.n % 2 != 0 || (g.n + 3) / 4 > 18 || std::getenv("STIGA_STENCIL_NO_TMA") ||
+        std::getenv("STIGA_STENCIL_NO_PAIR"))
+        return cudaErrorNotSupported;
+    if (((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Mst) | reinterpret_cast<uintptr_t>(Kst)) & 15u) != 0)
+        return cudaErrorNotSupported;
+    PairGeo sg;
+    sg.n = g.n;
+    sg.p = g.p;
+    sg.W = 2 * g.p + 1;
+    sg.d = g.d;
+    sg.Ns = 1;
+    long long pairs = g.n / 2;
+    sg.nsteps = sg.W + 1;
+    for (int l = 0; l < g.d; ++l) sg.Ns *= g.n;
+    for (int l = 2; l < g.d; ++l) {
+        pairs *= g.n;
+        sg.nsteps *= sg.W;
+    }
+    sg.n_t = static_cast<int>(n_t);
+    sg.nblk = (g.n + 3) / 4;
+    const int KS = (4 + 2 * g.p + 3) / 4;
+    sg.shift = g.p & 1;  // TMA boxes start on an even row
+    const int SR = 4 * (sg.nblk - 1) + 4 * KS + sg.shift;
+    sg.LDR = (SR + 11) / 16 * 16 + 4;
+    if (sg.LDR - 16 >= SR) sg.LDR -= 16;
+    sg.BR = (4 * sg.nblk + 11) / 16 * 16 + 4;
+    if (sg.BR - 16 >= 4 * sg.nblk) sg.BR -= 16;
+    sg.boxt = static_cast<int>(std::min<long long>(8 * kTT, n_t));
+    sg.xstage = (sg.boxt * sg.LDR + 15) / 16 * 16;
+    sg.bstage = (sg.W * sg.BR + 15) / 16 * 16;
+    const size_t per = sizeof(double) * (sg.xstage + 4 * sg.bstage) + 2 * sizeof(uint64_t);
+    sg.nst = static_cast<int>(std::min<size_t>(4, (227 * 1024) / per));
+    if (sg.nst < 2 || sg.LDR > 256 || sg.BR > 256) return cudaErrorNotSupported;
+    CUtensorMap maps[3];
+    const cuuint64_t dx[3] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(sg.Ns / g.n),
+                              static_cast<cuuint64_t>(n_t)};
+    const cuuint64_t sx[2] = {static_cast<cuuint64_t>(g.n) * 8, static_cast<cuuint64_t>(sg.Ns) * 8};
+    const cuuint32_t bx[3] = {static_cast<cuuint32_t>(sg.LDR), 1, static_cast<cuuint32_t>(sg.boxt)};
+    long long planes = 1;
+    for (int l = 0; l < g.d; ++l) planes *= sg.W;
+    const cuuint64_t db[2] = {static_cast<cuuint64_t>(sg.Ns), static_cast<cuuint64_t>(planes)};
+    const cuuint64_t sb[1] = {static_cast<cuuint64_t>(sg.Ns) * 8};
+    const cuuint32_t bb[2] = {static_cast<cuuint32_t>(sg.BR), static_cast<cuuint32_t>(sg.W)};
+    if (!(encode(&maps[0], X, 3, dx, sx, bx) && encode(&maps[1], Mst, 2, db, sb, bb) &&
+          encode(&maps[2], Kst, 2, db, sb, bb)))
+        return cudaErrorNotSupported;
+    dim3 grid(static_cast<unsigned>(pairs), static_cast<unsigned>((n_t + 8 * kTT - 1) / (8 * kTT)));
+#define STIGA_PAIR(KS_) \
+    case KS_: return pair_launch<KS_, 3>(sg, grid, maps, MX, KX, st);
+    switch (KS) {
+        STIGA_PAIR(2)
+        STIGA_PAIR(3)
+        STIGA_PAIR(4)
+        default: return cudaErrorNotSupported;
+    }
+#undef STIGA_PAIR
+}
+
 cudaError_t launch_stencil_apply2(const PhysicalDesc& g, const double* Mst, const double* Kst, const double* X,
                                   double* MX, double* KX, long long n_t, cudaStream_t st) {
     if (g.d < 1 || g.d > 3 || g.n <= 0 || n_t <= 0) return cudaErrorInvalidValue;
+    {
+        const cudaError_t pe = launch_stencil_pair(g, Mst, Kst, X, MX, KX, n_t, st);
+        if (pe != cudaErrorNotSupported) return pe;
+        if (std::getenv("STIGA_STENCIL_REQUIRE_PAIR")) return cudaErrorInvalidValue;  // tests: no silent fallback
+    }
     StencilGeo sg;
     sg.n = g.n;
     sg.p = g.p;

@@ -150,3 +150,32 @@ def test_physical_matvec_tiling_edges(pid, p, nel):
         y = A.apply(torch.from_numpy(x).cuda()).cpu().numpy()
         yo = Ad @ x
         assert np.linalg.norm(y - yo) <= 1e-12 * np.linalg.norm(yo)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pid,p,nel", [("deformed-cube-3d", 2, 4), ("deformed-cube-3d", 4, 6), ("deformed-cube-3d", 3, 5),
+                                        ("deformed-cube-3d", 5, 5), ("deformed-cube-3d", 1, 5), ("deformed-cube-3d", 2, 14),
+                                        ("quarter-annulus-2d", 4, 10), ("separable-nu-2d", 2, 30),
+                                        ("identity-square-2d", 3, 69), ("separable-nu-2d", 2, 72)])
+def test_physical_matvec_line_pair_bricks(pid, p, nel, monkeypatch):
+    """Line-pair brick stencil kernel (physical.cu kernel (c): MMA rows = 4 i_1 x 2 neighbouring lines, the c4
+    path): every band width KS = 2..4 (p = 1..5), d = 2 and 3, one to 18 row blocks, one and two time chunks,
+    against the oracle's assembled A (solver.cpp:67-70) and the one-line kernel.  STIGA_STENCIL_REQUIRE_PAIR
+    makes the launcher fail instead of falling back, so a pass means the brick kernel ran."""
+    torch = pytest.importorskip("torch")
+    from paper_1909_07309_b200 import stiga
+    from paper_1909_07309_b200.inputs import uniform_pm1
+
+    prob = Problem(pid)
+    ref = og.geometry_preconditioner_pieces(og.make_problem(pid), p, nel)
+    A = stiga.KronSumOperator.physical(prob, p, nel)
+    Ad = sp_kron(ref)
+    x = uniform_pm1(A.n_dof, 8)
+    yo = Ad @ x
+    monkeypatch.setenv("STIGA_STENCIL_REQUIRE_PAIR", "1")
+    y = A.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.linalg.norm(y - yo) <= 1e-12 * np.linalg.norm(yo)
+    monkeypatch.delenv("STIGA_STENCIL_REQUIRE_PAIR")
+    monkeypatch.setenv("STIGA_STENCIL_NO_PAIR", "1")
+    y1 = A.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.linalg.norm(y - y1) <= 1e-13 * np.linalg.norm(yo)
