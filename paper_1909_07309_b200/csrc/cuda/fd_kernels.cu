@@ -14,10 +14,11 @@ namespace {
 // the P warps in smem); second pass recomputes y_j from Z instead of storing it (24 B/DoF of HBM
 // traffic instead of 32) and writes x_j = y_j - H_j^-1 B_j x_last.
 template <int P>
-__device__ __forceinline__ void arrowhead_block(const double* __restrict__ Z, double* __restrict__ Xo, long long Ns,
-                                                const ArrowParams& ap, long long blk, double (*part_s)[32], int lane,
-                                                int w) {
-    const long long s0 = blk * 32 + lane;
+__global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restrict__ Z, double* __restrict__ Xo,
+                                                           long long Ns, ArrowParams ap) {
+    __shared__ double part_s[P][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long s0 = static_cast<long long>(blockIdx.x) * 32 + lane;
     const bool valid = s0 < Ns;
     const long long s = valid ? s0 : Ns - 1;
     double lam = 0.0;  // ((0 + lambda_1) + lambda_2) + ... (fdsolve.cpp:91-99)
@@ -53,7 +54,7 @@ __device__ __forceinline__ void arrowhead_block(const double* __restrict__ Z, do
 #pragma unroll
     for (int k = 0; k < P; ++k) srhs += part_s[k][lane];
     const double xlast = __ldg(ap.S_inv + ap.s_off + s) * srhs;
-    if (!valid) return;  // (no barrier follows within this block)
+    if (!valid) return;
     double* xo = Xo + s;
 #pragma unroll 4
     for (int j = w; j < ap.npairs; j += P) {
@@ -72,18 +73,6 @@ __device__ __forceinline__ void arrowhead_block(const double* __restrict__ Z, do
     }
 }
 
-template <int P>
-__global__ void __launch_bounds__(32 * P) arrowhead_kernel(const double* __restrict__ Z, double* __restrict__ Xo,
-                                                           long long Ns, ArrowParams ap) {
-    __shared__ double part_s[2][P][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const long long nblk = (Ns + 31) / 32;
-    int it = 0;
-    // grid-stride over the 32-column blocks (persistent launch: STIGA_ARROW_PERSISTENT); part_s is double
-    // buffered so one barrier per block suffices
-    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x, it ^= 1)
-        arrowhead_block<P>(Z, Xo, Ns, ap, blk, part_s[it], lane, w);
-}
 __global__ void scale_kernel(const double* __restrict__ a, const double* __restrict__ x, double* __restrict__ y,
                              long long n) {
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -111,9 +100,7 @@ __global__ void scale_kernel(const double* __restrict__ a, const double* __restr
 cudaError_t launch_arrowhead(const double* Z, double* X, long long Ns, const ArrowParams& ap, cudaStream_t st) {
     if (Ns <= 0) return cudaSuccess;
     constexpr int P = 8;
-    long long blocks = (Ns + 31) / 32;
-    static const bool persistent = std::getenv("STIGA_ARROW_PERSISTENT") != nullptr;
-    if (persistent) blocks = std::min<long long>(blocks, 148LL * 8);
+    const long long blocks = (Ns + 31) / 32;
     arrowhead_kernel<P><<<static_cast<unsigned>(blocks), 32 * P, 0, st>>>(Z, X, Ns, ap);
     return cudaGetLastError();
 }

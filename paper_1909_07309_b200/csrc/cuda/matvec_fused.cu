@@ -26,7 +26,6 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
-#include <mutex>
 
 #include "matvec_fused.cuh"
 
@@ -44,11 +43,6 @@ template <int N>
 __device__ __forceinline__ void cpa_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
-
-// Constant-bank copy of the warp-uniform band coefficients (STIGA_MATVEC_CONST, see launch_*): the kernels are
-// bound by shared-memory wavefronts and half of those are coefficient broadcasts.
-constexpr int kConstDoubles = 8000;
-__constant__ double c_coef[kConstDoubles];
 
 constexpr int kTR = 32;             // x rows per plane2 tile (outputs: the kTR - 2P interior rows)
 constexpr int kPlaneThreads = 256;  // 8 warps, two CTAs per SM where the tiles fit (n0 <= ~170)
@@ -78,15 +72,14 @@ struct Plane2Smem {
 //    in registers for the whole kernel) and rows g, g + G, ...; 16-byte window loads.
 // dbuf: a second x-tile buffer (after the coefficient rows) receives the NEXT tile's rows while the
 // current one is computed (cp.async groups: the wait before stage 1 leaves the prefetch in flight).
-template <int P, bool CB>
+template <int P>
 __global__ void __launch_bounds__(kPlaneThreads, 2) plane2_kernel(int n0, int n1, long long R,
                                                                   const double* __restrict__ x, double* __restrict__ a2,
                                                                   double* __restrict__ b2,
                                                                   const double* __restrict__ m0,
                                                                   const double* __restrict__ k0,
                                                                   const double* __restrict__ m1,
-                                                                  const double* __restrict__ k1, int dbuf, int om1,
-                                                                  int ok1) {
+                                                                  const double* __restrict__ k1, int dbuf) {
     constexpr int W = 2 * P + 1;
     constexpr int B = kTR - 2 * P;
     constexpr int WP = (W + 1) & ~1;
@@ -171,20 +164,9 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) plane2_kernel(int n0, int n1
 #pragma unroll
                 for (int q = 0; q < kR1; ++q) {
                     if (rs + q >= B) break;
-                    double sa = 0.0, sb = 0.0;
-                    if constexpr (CB) {  // warp-uniform coefficient rows from the constant bank
-                        const int jr = min(j0 + rs + q, n1 - 1) * W;
-#pragma unroll
-                        for (int k = 0; k < W; ++k) {
-                            sa = fma(c_coef[om1 + jr + k], xw[q + k], sa);
-                            sb = fma(c_coef[ok1 + jr + k], xw[q + k], sb);
-                        }
-                        as[(rs + q) * L.ap + P + col] = sa;
-                        bs[(rs + q) * L.ap + P + col] = sb;
-                        continue;
-                    }
                     const double2* mr = reinterpret_cast<const double2*>(cm + (rs + q) * WP);
                     const double2* kr = reinterpret_cast<const double2*>(ck + (rs + q) * WP);
+                    double sa = 0.0, sb = 0.0;
 #pragma unroll
                     for (int k2 = 0; k2 < WP / 2; ++k2) {
                         const double2 mk = mr[k2], kk = kr[k2];
@@ -272,12 +254,12 @@ struct StreamSmem {
 // [to0, to0 + nto) inside them (the caller passes base pointers of those slices).
 // cw / cm: band COLUMNS of gamma W_t and nu M_t, cw[t' * W + (d + P)] = gamma W_t(t' + d, t') (0 outside);
 // nt = rows of the time factors.
-template <int P, bool MODE2, bool CB>
+template <int P, bool MODE2>
 __global__ void __launch_bounds__(st_threads(MODE2), 2) stream_kernel(long long Lc, int n2, int nt, int ti0, int nti, int to0, int nto,
                                                      const double* __restrict__ a, const double* __restrict__ b,
                                                      double* __restrict__ y, const double* __restrict__ m2,
                                                      const double* __restrict__ k2, const double* __restrict__ cw,
-                                                     const double* __restrict__ cm, int om2, int ok2, int ocw, int ocm) {
+                                                     const double* __restrict__ cm) {
     constexpr int W = 2 * P + 1;
     constexpr int kST = st_threads(MODE2), kSQ = st_sq(MODE2);
     constexpr int RPT = (kST / 32) * kSQ;  // mode-2 output rows per tile
@@ -377,11 +359,9 @@ __global__ void __launch_bounds__(st_threads(MODE2), 2) stream_kernel(long long 
                         for (int q = 0; q < kSQ; ++q) {
                             double sa = 0.0, sb = 0.0;
                             const double* cmq = c2s + (rw + q) * 2 * WP;
-                            const int i2r = min(r0 + rw + q, n2 - 1) * W;
 #pragma unroll
                             for (int k = 0; k < W; ++k) {
-                                const double cmk = CB ? c_coef[om2 + i2r + k] : cmq[k];
-                                const double ckk = CB ? c_coef[ok2 + i2r + k] : cmq[WP + k];
+                                const double cmk = cmq[k], ckk = cmq[WP + k];
                                 sa = fma(cmk, aw[q + k], sa);
                                 sb = fma(ckk, aw[q + k], sb);
                                 sb = fma(cmk, bw[q + k], sb);
@@ -401,17 +381,12 @@ __global__ void __launch_bounds__(st_threads(MODE2), 2) stream_kernel(long long 
                     const double2* cmr = reinterpret_cast<const double2*>(tcm + static_cast<size_t>(tp) * WP);
 #pragma unroll
                     for (int k2 = 0; k2 < (W + 1) / 2; ++k2) {
-                        double2 w2, m2v;
-                        if constexpr (!CB) {
-                            w2 = cwr[k2];
-                            m2v = cmr[k2];
-                        }
+                        const double2 w2 = cwr[k2], m2v = cmr[k2];
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int kk = 2 * k2 + h;
                             if (kk < W) {
-                                const double w = CB ? c_coef[ocw + tp * W + kk] : (h ? w2.y : w2.x);
-                                const double m = CB ? c_coef[ocm + tp * W + kk] : (h ? m2v.y : m2v.x);
+                                const double w = h ? w2.y : w2.x, m = h ? m2v.y : m2v.x;
                                 const int slot = (ph + kk) % W;
 #pragma unroll
                                 for (int q = 0; q < kSQ; ++q)
@@ -446,72 +421,6 @@ __global__ void __launch_bounds__(st_threads(MODE2), 2) stream_kernel(long long 
 
 }  // namespace
 
-
-// ---- constant-bank ownership --------------------------------------------------------------------
-// c_coef is one per module: the coefficient sets of the last launch stay resident (key = the device
-// pointers of the set), a different set is uploaded on the launching stream after waiting for the
-// previous users; launches on other streams wait for the upload event.
-namespace {
-struct ConstBank {
-    std::mutex mu;
-    const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
-    int off[4] = {0, 0, 0, 0}, len[4] = {0, 0, 0, 0};
-    cudaEvent_t uploaded = nullptr, used = nullptr;
-};
-ConstBank& bank() {
-    static ConstBank b[16];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    return b[dev & 15];
-}
-// makes the n sets (device pointers ptr[i], len[i] doubles) resident; offsets in off[i]; false = does not fit
-bool const_resident(int n, const double* const* ptr, const int* len, int* off, cudaStream_t st) {
-    ConstBank& b = bank();
-    std::lock_guard<std::mutex> lk(b.mu);
-    if (!b.uploaded) {
-        cudaEventCreateWithFlags(&b.uploaded, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&b.used, cudaEventDisableTiming);
-        cudaEventRecord(b.uploaded, st);
-        cudaEventRecord(b.used, st);
-    }
-    bool all = true;
-    for (int i = 0; i < n; ++i) {
-        bool found = false;
-        for (int s = 0; s < 4; ++s)
-            if (b.key[s] == ptr[i] && b.len[s] == len[i]) {
-                off[i] = b.off[s];
-                found = true;
-            }
-        all = all && found;
-    }
-    if (!all) {  // replace the whole bank content by this launch's sets
-        int total = 0;
-        for (int i = 0; i < n; ++i) total += (len[i] + 1) & ~1;
-        if (n > 4 || total > kConstDoubles) return false;
-        cudaStreamWaitEvent(st, b.used, 0);
-        int o = 0;
-        for (int s = 0; s < 4; ++s) b.key[s] = nullptr;
-        for (int i = 0; i < n; ++i) {
-            cudaMemcpyToSymbolAsync(c_coef, ptr[i], sizeof(double) * len[i], sizeof(double) * o, cudaMemcpyDeviceToDevice, st);
-            b.key[i] = ptr[i];
-            b.off[i] = off[i] = o;
-            b.len[i] = len[i];
-            o += (len[i] + 1) & ~1;
-        }
-        cudaEventRecord(b.uploaded, st);
-    } else {
-        cudaStreamWaitEvent(st, b.uploaded, 0);
-    }
-    return true;
-}
-void const_used(cudaStream_t st) {
-    ConstBank& b = bank();
-    std::lock_guard<std::mutex> lk(b.mu);
-    cudaEventRecord(b.used, st);
-}
-bool want_const() { return std::getenv("STIGA_MATVEC_CONST") != nullptr; }
-}  // namespace
-
 // ---- host launchers ---------------------------------------------------------------------------
 
 size_t plane2_smem_bytes(int n0, int P) { return Plane2Smem(n0, P).bytes(); }
@@ -532,26 +441,10 @@ cudaError_t launch_plane2(int n0, int n1, long long R, int P, const double* x, d
     const long long ntiles = (n1 + B - 1) / B * R;
     const int per_sm = std::max(1, static_cast<int>((227 * 1024) / (sm + 1024)));
     const unsigned grid = static_cast<unsigned>(std::min<long long>(ntiles, 148LL * std::min(per_sm, 2)));
-    int off[2] = {0, 0};
-    bool cb = false;
-    if (want_const()) {
-        const double* ptr[2] = {m1, k1};
-        const int len[2] = {n1 * (2 * P + 1), n1 * (2 * P + 1)};
-        cb = const_resident(2, ptr, len, off, st);
-    }
 #define STIGA_P2(PP)                                                                                                 \
     case PP:                                                                                                         \
-        if (cb) {                                                                                                    \
-            cudaFuncSetAttribute(plane2_kernel<PP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
-                                 static_cast<int>(sm));                                                             \
-            plane2_kernel<PP, true><<<grid, kPlaneThreads, sm, st>>>(n0, n1, R, x, a2, b2, m0, k0, m1, k1, dbuf,    \
-                                                                      off[0], off[1]);                              \
-        } else {                                                                                                     \
-            cudaFuncSetAttribute(plane2_kernel<PP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,            \
-                                 static_cast<int>(sm));                                                             \
-            plane2_kernel<PP, false><<<grid, kPlaneThreads, sm, st>>>(n0, n1, R, x, a2, b2, m0, k0, m1, k1, dbuf,   \
-                                                                       0, 0);                                       \
-        }                                                                                                            \
+        cudaFuncSetAttribute(plane2_kernel<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)); \
+        plane2_kernel<PP><<<grid, kPlaneThreads, sm, st>>>(n0, n1, R, x, a2, b2, m0, k0, m1, k1, dbuf);              \
         break;
     switch (P) {
         STIGA_P2(1)
@@ -563,7 +456,6 @@ cudaError_t launch_plane2(int n0, int n1, long long R, int P, const double* x, d
         default: return cudaErrorInvalidValue;
     }
 #undef STIGA_P2
-    if (cb) const_used(st);
     return cudaGetLastError();
 }
 
@@ -581,31 +473,17 @@ cudaError_t launch_stream(bool mode2, long long Lc, int n2, int nt, int ti0, int
     // mode 2: two CTAs per SM (<= 128 registers); time only: up to four
     const int per_sm = std::max(1, std::min(mode2 ? 2 : 4, static_cast<int>((227 * 1024) / (sm + 1024))));
     const unsigned grid = static_cast<unsigned>(std::min<long long>(ntiles, 148LL * per_sm));
-    int off[4] = {0, 0, 0, 0};
-    bool cb = false;
-    if (want_const()) {
-        const int W = 2 * P + 1;
-        if (mode2) {
-            const double* ptr[4] = {m2, k2, cw, cm};
-            const int len[4] = {n2 * W, n2 * W, nt * W, nt * W};
-            cb = const_resident(4, ptr, len, off, st);
-        } else {
-            const double* ptr[2] = {cw, cm};
-            const int len[2] = {nt * W, nt * W};
-            cb = const_resident(2, ptr, len, off + 2, st);
-        }
-    }
-#define STIGA_ST_L(PP, M2, LC)                                                                                        \
-    cudaFuncSetAttribute(stream_kernel<PP, M2, LC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)); \
-    stream_kernel<PP, M2, LC><<<grid, st_threads(M2), sm, st>>>(Lc, M2 ? n2 : 1, nt, ti0, nti, to0, nto, a, b, y, m2, k2, cw, cm, \
-                                                                off[0], off[1], off[2], off[3]);
-#define STIGA_ST(PP)                                                     \
-    case PP:                                                             \
-        if (mode2) {                                                     \
-            if (cb) { STIGA_ST_L(PP, true, true) } else { STIGA_ST_L(PP, true, false) }   \
-        } else {                                                         \
-            if (cb) { STIGA_ST_L(PP, false, true) } else { STIGA_ST_L(PP, false, false) } \
-        }                                                                \
+#define STIGA_ST(PP)                                                                                                  \
+    case PP:                                                                                                          \
+        if (mode2) {                                                                                                  \
+            cudaFuncSetAttribute(stream_kernel<PP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                                 static_cast<int>(sm));                                                              \
+            stream_kernel<PP, true><<<grid, st_threads(true), sm, st>>>(Lc, n2, nt, ti0, nti, to0, nto, a, b, y, m2, k2, cw, cm);  \
+        } else {                                                                                                      \
+            cudaFuncSetAttribute(stream_kernel<PP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                                 static_cast<int>(sm));                                                              \
+            stream_kernel<PP, false><<<grid, st_threads(false), sm, st>>>(Lc, 1, nt, ti0, nti, to0, nto, a, b, y, m2, k2, cw, cm);  \
+        }                                                                                                             \
         break;
     switch (P) {
         STIGA_ST(1)
@@ -617,8 +495,6 @@ cudaError_t launch_stream(bool mode2, long long Lc, int n2, int nt, int ti0, int
         default: return cudaErrorInvalidValue;
     }
 #undef STIGA_ST
-#undef STIGA_ST_L
-    if (cb) const_used(st);
     return cudaGetLastError();
 }
 
