@@ -155,6 +155,8 @@ __global__ void __launch_bounds__(256) physical_assembly_kernel(PhysicalDesc g, 
 // per step (X box, M and K band boxes; out-of-range rows / t zero-filled by the TMA unit) into a
 // kStages ring guarded by full / empty mbarriers, consumers never meet a CTA barrier;
 // (b) otherwise every thread stages with 8-byte cp.async (double buffered, one CTA barrier a step).
+// A third kernel, (c) further down, takes the 8 MMA rows from two neighbouring lines (line-pair bricks:
+// denser band blocks); it is the one selected for d >= 2, n even, n <= 72 (BASELINE configs[3]).
 constexpr int kTT = 9;          // 8-column time tiles per chunk (72 columns)
 constexpr int kMaxWarps = 12;   // row blocks per CTA (96 rows); two consumer warps (M, K) each
 constexpr int kStages = 3;
@@ -393,21 +395,6 @@ __device__ __forceinline__ PairCtx pair_ctx(const PairGeo& sg) {
     return c;
 }
 
-// step s = e + (W + 1) o_3: neighbour line (j_2, j_3), -1 outside the patch
-__device__ __forceinline__ long long pair_nb_line(const PairGeo& sg, const PairCtx& c, int s) {
-    const int e = s % (sg.W + 1), o3 = s / (sg.W + 1);
-    const int j2 = c.i2 - sg.p + e;
-    if (j2 < 0 || j2 >= sg.n) return -1;
-    if (sg.d < 3) return j2;
-    const int j3 = c.i3 - sg.p + o3;
-    if (j3 < 0 || j3 >= sg.n) return -1;
-    return j2 + static_cast<long long>(sg.n) * j3;
-}
-__device__ __forceinline__ int pair_next_step(const PairGeo& sg, const PairCtx& c, int s) {
-    while (s < sg.nsteps && pair_nb_line(sg, c, s) < 0) ++s;
-    return s;
-}
-
 template <int KS, bool FULL>
 __device__ __forceinline__ void pair_step_t(const PairGeo& sg, const double* xs, const double* bm, int rb, bool va,
                                             bool vb, int ntiles, double (&acc)[kTT][2]) {
@@ -425,6 +412,44 @@ __device__ __forceinline__ void pair_step_t(const PairGeo& sg, const double* xs,
 #pragma unroll
         for (int tt = 0; tt < kTT; ++tt) {
             if (FULL || tt < ntiles) sdmma(acc[tt][0], acc[tt][1], a, bs[tt * 8 * sg.LDR + 4 * kk]);
+        }
+    }
+}
+
+// All RBW consecutive row blocks of a warp in one pass: row block r and contraction chunk kk read window
+// columns 4 (rb0 + r + kk) .., so the RBW * KS (block, chunk) pairs share RBW + KS - 1 distinct B fragments
+// per time tile (5 instead of 9 loads for RBW = KS = 3).  Per accumulator the chunks are still added in
+// ascending kk, i.e. the same order as pair_step_t.  NR = live row blocks (RBW, or fewer for the last warp).
+template <int KS, int RBW, int NR, bool FULL>
+__device__ __forceinline__ void pair_step_all(const PairGeo& sg, const double* xs, const double* bm, int rb0, bool va,
+                                              bool vb, int ntiles, double (&acc)[RBW][kTT][2]) {
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int ln = g >> 2, gi = g & 3;
+    const bool lv = ln ? vb : va;
+    const double* bs = xs + g * sg.LDR + sg.shift + 4 * rb0 + t4;
+    const double* br = bm + ln * sg.bstage + 4 * rb0 + gi;
+    double a[NR][KS];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+        const int o1 = 4 * kk + t4 - gi;
+        const bool av = lv && o1 >= 0 && o1 < sg.W;
+        const int off = av ? o1 * sg.BR : 0;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) a[r][kk] = av ? br[off + 4 * r] : 0.0;
+    }
+#pragma unroll
+    for (int tt = 0; tt < kTT; ++tt) {
+        if (FULL || tt < ntiles) {
+#pragma unroll
+            for (int cc = 0; cc < NR + KS - 1; ++cc) {
+                const double b = bs[tt * 8 * sg.LDR + 4 * cc];
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    const int kk = cc - r;
+                    if (kk >= 0 && kk < KS) sdmma(acc[r][tt][0], acc[r][tt][1], a[r][kk], b);
+                }
+            }
         }
     }
 }
@@ -453,31 +478,39 @@ __global__ void __launch_bounds__(32 * 2 * ((18 + RBW - 1) / RBW))
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    // Valid steps = the rectangle of neighbour offsets inside the patch: e in [e_lo, e_hi] (j_2 = i_2 - p + e),
+    // o_3 in [o_lo, o_hi] (j_3 = i_3 - p + o_3); walked with incremental counters (an integer division per
+    // step and warp showed up as ~15% of the issue slots in the first version).
+    const int e_lo = max(0, sg.p - c.i2), e_hi = min(sg.W, sg.n - 1 - c.i2 + sg.p);
+    const int o_lo = sg.d < 3 ? 0 : max(0, sg.p - c.i3), o_hi = sg.d < 3 ? 0 : min(sg.W - 1, sg.n - 1 - c.i3 + sg.p);
+    const int nvalid = (e_hi - e_lo + 1) * (o_hi - o_lo + 1);
     const bool producer = threadIdx.x == 0;
     const int row0 = static_cast<int>(sg.n * c.line_a);
-    int sp = pair_next_step(sg, c, 0), kp = 0;  // producer cursor: next step to load, its ring index
-    auto produce = [&]() {                      // loads of step sp into stage kp % nst
+    int pe = e_lo, po = o_lo, kp = 0;  // producer cursor: next step to load, its ring index
+    auto produce = [&]() {             // loads of step (pe, po) into stage kp % nst
         const int st = kp % nst;
-        const int e = sp % (sg.W + 1), o3 = sp / (sg.W + 1);
-        const bool va = e < sg.W, vb = e >= 1;
+        const bool va = pe < sg.W, vb = pe >= 1;
+        const int nbl = (c.i2 - sg.p + pe) + (sg.d < 3 ? 0 : sg.n * (c.i3 - sg.p + po));
         if (kp >= nst) mb_wait(empty + st, ((kp / nst) - 1) & 1);
         mb_expect(full + st, 8u * (sg.boxt * sg.LDR + 2 * ((va ? 1 : 0) + (vb ? 1 : 0)) * sg.W * sg.BR));
-        tma3(su32(xs + st * sg.xstage), &mapX, -sg.p - sg.shift, static_cast<int>(pair_nb_line(sg, c, sp)), c.t0,
-             full + st);
+        tma3(su32(xs + st * sg.xstage), &mapX, -sg.p - sg.shift, nbl, c.t0, full + st);
         double* b0 = bsm + st * 4 * sg.bstage;
         if (va) {
-            tma2(su32(b0), &mapM, row0, sg.W * (e + sg.W * o3), full + st);
-            tma2(su32(b0 + 2 * sg.bstage), &mapK, row0, sg.W * (e + sg.W * o3), full + st);
+            tma2(su32(b0), &mapM, row0, sg.W * (pe + sg.W * po), full + st);
+            tma2(su32(b0 + 2 * sg.bstage), &mapK, row0, sg.W * (pe + sg.W * po), full + st);
         }
         if (vb) {
-            tma2(su32(b0 + sg.bstage), &mapM, row0 + sg.n, sg.W * (e - 1 + sg.W * o3), full + st);
-            tma2(su32(b0 + 3 * sg.bstage), &mapK, row0 + sg.n, sg.W * (e - 1 + sg.W * o3), full + st);
+            tma2(su32(b0 + sg.bstage), &mapM, row0 + sg.n, sg.W * (pe - 1 + sg.W * po), full + st);
+            tma2(su32(b0 + 3 * sg.bstage), &mapK, row0 + sg.n, sg.W * (pe - 1 + sg.W * po), full + st);
         }
-        sp = pair_next_step(sg, c, sp + 1);
+        if (++pe > e_hi) {
+            pe = e_lo;
+            ++po;
+        }
         ++kp;
     };
     if (producer)
-        for (int i = 0; i < nst - 1 && sp < sg.nsteps; ++i) produce();
+        for (int i = 0; i < nst - 1 && kp < nvalid; ++i) produce();
     const int nwm = nwc / 2, wi = warp % nwm, mat = warp / nwm;
     const int ntiles = (c.tcols + 7) >> 3;
     double acc[RBW][kTT][2];
@@ -485,26 +518,33 @@ __global__ void __launch_bounds__(32 * 2 * ((18 + RBW - 1) / RBW))
     for (int r = 0; r < RBW; ++r)
 #pragma unroll
         for (int t = 0; t < kTT; ++t) acc[r][t][0] = acc[r][t][1] = 0.0;
-    int k = 0;
-    for (int s = pair_next_step(sg, c, 0); s < sg.nsteps; s = pair_next_step(sg, c, s + 1), ++k) {
-        if (producer && sp < sg.nsteps) produce();  // step k + nst - 1 (waits until every warp released step k - 1)
+    const int nr = min(RBW, sg.nblk - wi * RBW);  // live row blocks of this warp (<= 0: none)
+    int ce = e_lo, st = 0, ph = 0;  // consumer cursor: offset e of step k, its stage and mbarrier phase
+    for (int k = 0; k < nvalid; ++k) {
+        if (producer && kp < nvalid) produce();  // step k + nst - 1 (waits until every warp released step k - 1)
         __syncwarp();
-        const int st = k % nst;
-        const int e = s % (sg.W + 1);
-        const bool va = e < sg.W, vb = e >= 1;
-        mb_wait(full + st, (k / nst) & 1);
+        const bool va = ce < sg.W, vb = ce >= 1;
+        mb_wait(full + st, ph);
         const double* xst = xs + st * sg.xstage;
         const double* bm = bsm + (st * 4 + 2 * mat) * sg.bstage;
+        if (nr == RBW && ntiles == kTT) {  // the usual case: every row block and time tile live
+            pair_step_all<KS, RBW, RBW, true>(sg, xst, bm, wi * RBW, va, vb, ntiles, acc);
+        } else {
 #pragma unroll
-        for (int r = 0; r < RBW; ++r) {
-            const int rb = wi * RBW + r;
-            if (rb < sg.nblk) {
-                if (ntiles == kTT) pair_step_t<KS, true>(sg, xst, bm, rb, va, vb, ntiles, acc[r]);
-                else pair_step_t<KS, false>(sg, xst, bm, rb, va, vb, ntiles, acc[r]);
+            for (int r = 0; r < RBW; ++r) {
+                if (r < nr) {
+                    if (ntiles == kTT) pair_step_t<KS, true>(sg, xst, bm, wi * RBW + r, va, vb, ntiles, acc[r]);
+                    else pair_step_t<KS, false>(sg, xst, bm, wi * RBW + r, va, vb, ntiles, acc[r]);
+                }
             }
         }
         __syncwarp();
         if (lane == 0) mb_arrive(empty + st);
+        if (++ce > e_hi) ce = e_lo;
+        if (++st == nst) {
+            st = 0;
+            ph ^= 1;
+        }
     }
     const int g = lane >> 2, t4 = lane & 3;
     double* Y = mat ? KX : MX;
