@@ -240,24 +240,38 @@ __device__ __forceinline__ LineCtx line_ctx(const StencilGeo& sg) {
     return c;
 }
 
-// neighbour line of step s (offsets o_2 + W o_3), -1 when it falls outside the patch
-__device__ __forceinline__ long long nb_line(const StencilGeo& sg, const LineCtx& c, int s) {
-    long long nl = 0, stride = 1;
-    int rem = s;
-    for (int l = 0; l < sg.d - 1; ++l) {
-        const int o = rem % sg.W;
-        rem /= sg.W;
-        const int j = c.lc[l] + o - sg.p;
-        if (j < 0 || j >= sg.n) return -1;
-        nl += j * stride;
-        stride *= sg.n;
+// The valid steps of a line are the rectangle of neighbour offsets inside the patch; StepIter walks it with
+// counters (nb_line / next_step cost an integer division per step and warp, ~15% of the issue slots of the
+// line-pair kernel before it switched to counters).
+struct StepIter {
+    int o2, o3, lo2, hi2, hi3;
+    long long base;  // neighbour line of (o2, o3) = base + o2 + n o3
+    int n, W;
+    __device__ __forceinline__ StepIter(const StencilGeo& sg, const LineCtx& c) : n(sg.n), W(sg.W) {
+        if (sg.d == 1) {
+            lo2 = hi2 = 0;
+            o3 = hi3 = 0;
+            base = 0;
+        } else {
+            lo2 = max(0, sg.p - c.lc[0]);
+            hi2 = min(sg.W - 1, sg.n - 1 - c.lc[0] + sg.p);
+            const int lo3 = sg.d < 3 ? 0 : max(0, sg.p - c.lc[1]);
+            hi3 = sg.d < 3 ? 0 : min(sg.W - 1, sg.n - 1 - c.lc[1] + sg.p);
+            o3 = lo3;
+            base = (c.lc[0] - sg.p) + (sg.d < 3 ? 0LL : static_cast<long long>(sg.n) * (c.lc[1] - sg.p));
+        }
+        o2 = lo2;
     }
-    return nl;
-}
-__device__ __forceinline__ int next_step(const StencilGeo& sg, const LineCtx& c, int s) {
-    while (s < sg.nsteps && nb_line(sg, c, s) < 0) ++s;
-    return s;
-}
+    __device__ __forceinline__ bool valid() const { return o3 <= hi3; }
+    __device__ __forceinline__ int step() const { return o2 + W * o3; }  // offset-plane group index
+    __device__ __forceinline__ long long line() const { return base + o2 + static_cast<long long>(n) * o3; }
+    __device__ __forceinline__ void next() {
+        if (++o2 > hi2) {
+            o2 = lo2;
+            ++o3;
+        }
+    }
+};
 
 // One step of a consumer warp: accumulate the band of offset step into (accm, acck).
 // One step of consumer warp (row block rb, matrix mat): acc += band(mat) x staged window.
@@ -333,14 +347,13 @@ __global__ void __launch_bounds__(32 * (2 * kMaxWarps + 1))
         const unsigned bytes = 8u * (sg.boxt * sg.LDR + 2 * sg.W * sg.BR);
         const int row0 = static_cast<int>(c.seg0 + sg.n * c.line);
         int k = 0;
-        for (int s = next_step(sg, c, 0); s < sg.nsteps; s = next_step(sg, c, s + 1), ++k) {
+        for (StepIter it(sg, c); it.valid(); it.next(), ++k) {
             const int st = k % nst;
             if (k >= nst) mb_wait(empty + st, ((k / nst) - 1) & 1);
             mb_expect(full + st, bytes);
-            tma3(su32(xs + st * sg.xstage), &mapX, c.seg0 - sg.p - sg.shift, static_cast<int>(nb_line(sg, c, s)), c.t0,
-                 full + st);
-            tma2(su32(bsm + (st * 2) * sg.bstage), &mapM, row0, sg.W * s, full + st);
-            tma2(su32(bsm + (st * 2 + 1) * sg.bstage), &mapK, row0, sg.W * s, full + st);
+            tma3(su32(xs + st * sg.xstage), &mapX, c.seg0 - sg.p - sg.shift, static_cast<int>(it.line()), c.t0, full + st);
+            tma2(su32(bsm + (st * 2) * sg.bstage), &mapM, row0, sg.W * it.step(), full + st);
+            tma2(su32(bsm + (st * 2 + 1) * sg.bstage), &mapK, row0, sg.W * it.step(), full + st);
         }
         return;
     }
@@ -350,7 +363,7 @@ __global__ void __launch_bounds__(32 * (2 * kMaxWarps + 1))
 #pragma unroll
     for (int t = 0; t < kTT; ++t) acc[t][0] = acc[t][1] = 0.0;
     int k = 0;
-    for (int s = next_step(sg, c, 0); s < sg.nsteps; s = next_step(sg, c, s + 1), ++k) {
+    for (StepIter it(sg, c); it.valid(); it.next(), ++k) {
         const int st = k % nst;
         mb_wait(full + st, (k / nst) & 1);
         stencil_step<KS>(sg, xs + st * sg.xstage, bsm + (st * 2 + mat) * sg.bstage, rb, ntiles, acc);
@@ -457,10 +470,15 @@ __device__ __forceinline__ void pair_step_all(const PairGeo& sg, const double* x
 // Registers are allocated to warps in groups of four, so a 13th (producer) warp would cap the kernel at 128
 // registers and spill the 3 x 9 accumulator tiles: the producer is lane 0 of consumer warp 0 instead (it
 // issues the loads of step k + nst - 1 before computing step k), 12 warps, <= 168 registers.
-template <int KS, int RBW>
+// TF (single time chunk, n_t <= 72): the banded time pass y = MX W_t^T + KX M_t^T (solver.cpp:67-70) runs in
+// the epilogue on the CTA's (2 lines x all time columns) results, staged through the then idle ring -- MX and
+// KX never go to HBM and the separate time kernel disappears.  tw / tm: row band storage of gamma W_t, nu M_t
+// (half-bandwidth pt); the result goes to MX.
+template <int KS, int RBW, bool TF>
 __global__ void __launch_bounds__(32 * 2 * ((18 + RBW - 1) / RBW))
     stencil_pair_kernel(PairGeo sg, const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapM,
-                        const __grid_constant__ CUtensorMap mapK, double* __restrict__ MX, double* __restrict__ KX) {
+                        const __grid_constant__ CUtensorMap mapK, double* __restrict__ MX, double* __restrict__ KX,
+                        const double* __restrict__ tw, const double* __restrict__ tm, int pt) {
     extern __shared__ __align__(128) double sx[];
     const int nst = sg.nst;
     double* xs = sx;                     // nst x xstage
@@ -547,6 +565,40 @@ __global__ void __launch_bounds__(32 * 2 * ((18 + RBW - 1) / RBW))
         }
     }
     const int g = lane >> 2, t4 = lane & 3;
+    if constexpr (TF) {
+        // results -> smem [matrix][line * RP + i_1][t] (pitch TP odd: conflict-free both ways), then the time bands
+        const int RP = 4 * sg.nblk, TP = 8 * kTT + 1;
+        __syncthreads();  // every stage of the ring has been consumed
+        double* zs = sx + static_cast<size_t>(mat) * 2 * RP * TP;
+#pragma unroll
+        for (int r = 0; r < RBW; ++r) {
+            const int rb = wi * RBW + r;
+            if (rb >= sg.nblk) continue;
+            double* zr = zs + ((g >> 2) * RP + 4 * rb + (g & 3)) * TP + 2 * t4;
+#pragma unroll
+            for (int tt = 0; tt < kTT; ++tt) {
+                zr[8 * tt] = acc[r][tt][0];
+                zr[8 * tt + 1] = acc[r][tt][1];
+            }
+        }
+        __syncthreads();
+        const double* zm = sx;
+        const double* zk = sx + static_cast<size_t>(2) * RP * TP;
+        const int wt = 2 * pt + 1, nt = sg.n_t;
+        for (int idx = threadIdx.x; idx < 2 * RP * nt; idx += blockDim.x) {
+            const int t = idx / (2 * RP), rr = idx - t * (2 * RP);
+            const int ln = rr >= RP ? 1 : 0, i1 = rr - ln * RP;
+            if (i1 >= sg.n) continue;
+            const int jlo = max(0, t - pt), jhi = min(nt - 1, t + pt);
+            const double* rw = tw + static_cast<long long>(t) * wt + (pt - t);
+            const double* rm = tm + static_cast<long long>(t) * wt + (pt - t);
+            double sa = 0.0, sb = 0.0;  // out = A a + B b, each summed over ascending t' (launch_banded_pass order)
+            for (int j = jlo; j <= jhi; ++j) sa += __ldg(rw + j) * zm[rr * TP + j];
+            for (int j = jlo; j <= jhi; ++j) sb += __ldg(rm + j) * zk[rr * TP + j];
+            MX[i1 + sg.n * (c.line_a + ln) + sg.Ns * static_cast<long long>(t)] = sa + sb;
+        }
+        return;
+    }
     double* Y = mat ? KX : MX;
 #pragma unroll
     for (int r = 0; r < RBW; ++r) {
@@ -575,8 +627,7 @@ __global__ void __launch_bounds__(32 * 2 * kMaxWarps)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const LineCtx c = line_ctx(sg);
     const int rows_seg = min(sg.seg_rows, sg.n - c.seg0);
-    auto issue = [&](int s, int buf) {
-        const long long nl = nb_line(sg, c, s);
+    auto issue = [&](int s, long long nl, int buf) {
         const double* src = X + (c.seg0 - sg.p) + sg.n * nl + sg.Ns * c.t0;
         const unsigned dst = su32(xs + buf * sg.xstage);
         for (int col = warp; col < c.tcols; col += nw) {
@@ -602,16 +653,15 @@ __global__ void __launch_bounds__(32 * 2 * kMaxWarps)
     double acc[kTT][2];
 #pragma unroll
     for (int t = 0; t < kTT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    int s = next_step(sg, c, 0);
-    if (s < sg.nsteps) issue(s, 0);
+    StepIter it(sg, c);
+    if (it.valid()) issue(it.step(), it.line(), 0);
     int buf = 0;
-    while (s < sg.nsteps) {
-        const int sn = next_step(sg, c, s + 1);
+    while (it.valid()) {
+        it.next();
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();  // stage buf landed for all; the other buffer is free again
-        if (sn < sg.nsteps) issue(sn, buf ^ 1);
+        if (it.valid()) issue(it.step(), it.line(), buf ^ 1);
         stencil_step<KS>(sg, xs + buf * sg.xstage, bsm + (buf * 2 + mat) * sg.bstage, rb, ntiles, acc);
-        s = sn;
         buf ^= 1;
     }
     stencil_store(sg, c, rb, acc, mat ? KX : MX);
@@ -710,19 +760,33 @@ cudaError_t launch_physical_assembly(const PhysicalDesc& g, double* Kst, double*
 }
 
 template <int KS, int RBW>
-cudaError_t pair_launch(const PairGeo& sg, dim3 grid, const CUtensorMap* maps, double* MX, double* KX, cudaStream_t st) {
+cudaError_t pair_launch(const PairGeo& sg, dim3 grid, const CUtensorMap* maps, double* MX, double* KX, const double* tw,
+                        const double* tm, int pt, cudaStream_t st) {
     const size_t smem = sizeof(double) * sg.nst * (sg.xstage + 4 * sg.bstage) + 2 * sg.nst * sizeof(uint64_t);
-    cudaError_t e = cudaFuncSetAttribute(stencil_pair_kernel<KS, RBW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const int nwm = (sg.nblk + RBW - 1) / RBW;
+    if (tw) {  // fused time bands: the epilogue stages 2 matrices x 2 lines x 4 nblk rows x (72 + 1) columns
+        if (sizeof(double) * 4 * 4 * sg.nblk * (8 * kTT + 1) > sizeof(double) * sg.nst * (sg.xstage + 4 * sg.bstage))
+            return cudaErrorNotSupported;
+        cudaError_t e = cudaFuncSetAttribute(stencil_pair_kernel<KS, RBW, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        stencil_pair_kernel<KS, RBW, true><<<grid, 32 * 2 * nwm, smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX, tw,
+                                                                                 tm, pt);
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaFuncSetAttribute(stencil_pair_kernel<KS, RBW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    const int nwm = (sg.nblk + RBW - 1) / RBW;
-    stencil_pair_kernel<KS, RBW><<<grid, 32 * 2 * nwm, smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX);
+    stencil_pair_kernel<KS, RBW, false><<<grid, 32 * 2 * nwm, smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX, nullptr,
+                                                                              nullptr, 0);
     return cudaGetLastError();
 }
 
 // Line-pair brick path (kernel (c)); returns cudaErrorNotSupported when the shape is not eligible.
 cudaError_t launch_stencil_pair(const PhysicalDesc& g, const double* Mst, const double* Kst, const double* X, double* MX,
-                                double* KX, long long n_t, cudaStream_t st) {
+                                double* KX, long long n_t, cudaStream_t st, const double* tw = nullptr,
+                                const double* tm = nullptr, int pt = 0) {
+    if (tw && (n_t > 8 * kTT || std::getenv("STIGA_STENCIL_NO_TIME_FUSION"))) return cudaErrorNotSupported;
     if (g.d < 2 || g.n % 2 != 0 || (g.n + 3) / 4 > 18 || std::getenv("STIGA_STENCIL_NO_TMA") ||
         std::getenv("STIGA_STENCIL_NO_PAIR"))
         return cudaErrorNotSupported;
@@ -771,7 +835,7 @@ cudaError_t launch_stencil_pair(const PhysicalDesc& g, const double* Mst, const 
         return cudaErrorNotSupported;
     dim3 grid(static_cast<unsigned>(pairs), static_cast<unsigned>((n_t + 8 * kTT - 1) / (8 * kTT)));
 #define STIGA_PAIR(KS_) \
-    case KS_: return pair_launch<KS_, 3>(sg, grid, maps, MX, KX, st);
+    case KS_: return pair_launch<KS_, 3>(sg, grid, maps, MX, KX, tw, tm, pt, st);
     switch (KS) {
         STIGA_PAIR(2)
         STIGA_PAIR(3)
@@ -779,6 +843,13 @@ cudaError_t launch_stencil_pair(const PhysicalDesc& g, const double* Mst, const 
         default: return cudaErrorNotSupported;
     }
 #undef STIGA_PAIR
+}
+
+cudaError_t launch_stencil_apply_time(const PhysicalDesc& g, const double* Mst, const double* Kst, const double* X,
+                                      double* Y, long long n_t, const double* tw, const double* tm, int pt,
+                                      cudaStream_t st) {
+    if (g.d < 1 || g.d > 3 || g.n <= 0 || n_t <= 0 || !tw || !tm) return cudaErrorInvalidValue;
+    return launch_stencil_pair(g, Mst, Kst, X, Y, nullptr, n_t, st, tw, tm, pt);
 }
 
 cudaError_t launch_stencil_apply2(const PhysicalDesc& g, const double* Mst, const double* Kst, const double* X,
