@@ -470,15 +470,10 @@ __device__ __forceinline__ void pair_step_all(const PairGeo& sg, const double* x
 // Registers are allocated to warps in groups of four, so a 13th (producer) warp would cap the kernel at 128
 // registers and spill the 3 x 9 accumulator tiles: the producer is lane 0 of consumer warp 0 instead (it
 // issues the loads of step k + nst - 1 before computing step k), 12 warps, <= 168 registers.
-// TF (single time chunk, n_t <= 72): the banded time pass y = MX W_t^T + KX M_t^T (solver.cpp:67-70) runs in
-// the epilogue on the CTA's (2 lines x all time columns) results, staged through the then idle ring -- MX and
-// KX never go to HBM and the separate time kernel disappears.  tw / tm: row band storage of gamma W_t, nu M_t
-// (half-bandwidth pt); the result goes to MX.
-template <int KS, int RBW, bool TF>
+template <int KS, int RBW>
 __global__ void __launch_bounds__(32 * 2 * ((18 + RBW - 1) / RBW))
     stencil_pair_kernel(PairGeo sg, const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapM,
-                        const __grid_constant__ CUtensorMap mapK, double* __restrict__ MX, double* __restrict__ KX,
-                        const double* __restrict__ tw, const double* __restrict__ tm, int pt) {
+                        const __grid_constant__ CUtensorMap mapK, double* __restrict__ MX, double* __restrict__ KX) {
     extern __shared__ __align__(128) double sx[];
     const int nst = sg.nst;
     double* xs = sx;                     // nst x xstage
@@ -565,40 +560,6 @@ __global__ void __launch_bounds__(32 * 2 * ((18 + RBW - 1) / RBW))
         }
     }
     const int g = lane >> 2, t4 = lane & 3;
-    if constexpr (TF) {
-        // results -> smem [matrix][line * RP + i_1][t] (pitch TP odd: conflict-free both ways), then the time bands
-        const int RP = 4 * sg.nblk, TP = 8 * kTT + 1;
-        __syncthreads();  // every stage of the ring has been consumed
-        double* zs = sx + static_cast<size_t>(mat) * 2 * RP * TP;
-#pragma unroll
-        for (int r = 0; r < RBW; ++r) {
-            const int rb = wi * RBW + r;
-            if (rb >= sg.nblk) continue;
-            double* zr = zs + ((g >> 2) * RP + 4 * rb + (g & 3)) * TP + 2 * t4;
-#pragma unroll
-            for (int tt = 0; tt < kTT; ++tt) {
-                zr[8 * tt] = acc[r][tt][0];
-                zr[8 * tt + 1] = acc[r][tt][1];
-            }
-        }
-        __syncthreads();
-        const double* zm = sx;
-        const double* zk = sx + static_cast<size_t>(2) * RP * TP;
-        const int wt = 2 * pt + 1, nt = sg.n_t;
-        for (int idx = threadIdx.x; idx < 2 * RP * nt; idx += blockDim.x) {
-            const int t = idx / (2 * RP), rr = idx - t * (2 * RP);
-            const int ln = rr >= RP ? 1 : 0, i1 = rr - ln * RP;
-            if (i1 >= sg.n) continue;
-            const int jlo = max(0, t - pt), jhi = min(nt - 1, t + pt);
-            const double* rw = tw + static_cast<long long>(t) * wt + (pt - t);
-            const double* rm = tm + static_cast<long long>(t) * wt + (pt - t);
-            double sa = 0.0, sb = 0.0;  // out = A a + B b, each summed over ascending t' (launch_banded_pass order)
-            for (int j = jlo; j <= jhi; ++j) sa += __ldg(rw + j) * zm[rr * TP + j];
-            for (int j = jlo; j <= jhi; ++j) sb += __ldg(rm + j) * zk[rr * TP + j];
-            MX[i1 + sg.n * (c.line_a + ln) + sg.Ns * static_cast<long long>(t)] = sa + sb;
-        }
-        return;
-    }
     double* Y = mat ? KX : MX;
 #pragma unroll
     for (int r = 0; r < RBW; ++r) {
@@ -760,33 +721,19 @@ cudaError_t launch_physical_assembly(const PhysicalDesc& g, double* Kst, double*
 }
 
 template <int KS, int RBW>
-cudaError_t pair_launch(const PairGeo& sg, dim3 grid, const CUtensorMap* maps, double* MX, double* KX, const double* tw,
-                        const double* tm, int pt, cudaStream_t st) {
+cudaError_t pair_launch(const PairGeo& sg, dim3 grid, const CUtensorMap* maps, double* MX, double* KX, cudaStream_t st) {
     const size_t smem = sizeof(double) * sg.nst * (sg.xstage + 4 * sg.bstage) + 2 * sg.nst * sizeof(uint64_t);
-    const int nwm = (sg.nblk + RBW - 1) / RBW;
-    if (tw) {  // fused time bands: the epilogue stages 2 matrices x 2 lines x 4 nblk rows x (72 + 1) columns
-        if (sizeof(double) * 4 * 4 * sg.nblk * (8 * kTT + 1) > sizeof(double) * sg.nst * (sg.xstage + 4 * sg.bstage))
-            return cudaErrorNotSupported;
-        cudaError_t e = cudaFuncSetAttribute(stencil_pair_kernel<KS, RBW, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        stencil_pair_kernel<KS, RBW, true><<<grid, 32 * 2 * nwm, smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX, tw,
-                                                                                 tm, pt);
-        return cudaGetLastError();
-    }
-    cudaError_t e = cudaFuncSetAttribute(stencil_pair_kernel<KS, RBW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(stencil_pair_kernel<KS, RBW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    stencil_pair_kernel<KS, RBW, false><<<grid, 32 * 2 * nwm, smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX, nullptr,
-                                                                              nullptr, 0);
+    const int nwm = (sg.nblk + RBW - 1) / RBW;
+    stencil_pair_kernel<KS, RBW><<<grid, 32 * 2 * nwm, smem, st>>>(sg, maps[0], maps[1], maps[2], MX, KX);
     return cudaGetLastError();
 }
 
 // Line-pair brick path (kernel (c)); returns cudaErrorNotSupported when the shape is not eligible.
 cudaError_t launch_stencil_pair(const PhysicalDesc& g, const double* Mst, const double* Kst, const double* X, double* MX,
-                                double* KX, long long n_t, cudaStream_t st, const double* tw = nullptr,
-                                const double* tm = nullptr, int pt = 0) {
-    if (tw && (n_t > 8 * kTT || std::getenv("STIGA_STENCIL_NO_TIME_FUSION"))) return cudaErrorNotSupported;
+                                double* KX, long long n_t, cudaStream_t st) {
     if (g.d < 2 || g.n % 2 != 0 || (g.n + 3) / 4 > 18 || std::getenv("STIGA_STENCIL_NO_TMA") ||
         std::getenv("STIGA_STENCIL_NO_PAIR"))
         return cudaErrorNotSupported;
@@ -835,7 +782,7 @@ cudaError_t launch_stencil_pair(const PhysicalDesc& g, const double* Mst, const 
         return cudaErrorNotSupported;
     dim3 grid(static_cast<unsigned>(pairs), static_cast<unsigned>((n_t + 8 * kTT - 1) / (8 * kTT)));
 #define STIGA_PAIR(KS_) \
-    case KS_: return pair_launch<KS_, 3>(sg, grid, maps, MX, KX, tw, tm, pt, st);
+    case KS_: return pair_launch<KS_, 3>(sg, grid, maps, MX, KX, st);
     switch (KS) {
         STIGA_PAIR(2)
         STIGA_PAIR(3)
@@ -843,13 +790,6 @@ cudaError_t launch_stencil_pair(const PhysicalDesc& g, const double* Mst, const 
         default: return cudaErrorNotSupported;
     }
 #undef STIGA_PAIR
-}
-
-cudaError_t launch_stencil_apply_time(const PhysicalDesc& g, const double* Mst, const double* Kst, const double* X,
-                                      double* Y, long long n_t, const double* tw, const double* tm, int pt,
-                                      cudaStream_t st) {
-    if (g.d < 1 || g.d > 3 || g.n <= 0 || n_t <= 0 || !tw || !tm) return cudaErrorInvalidValue;
-    return launch_stencil_pair(g, Mst, Kst, X, Y, nullptr, n_t, st, tw, tm, pt);
 }
 
 cudaError_t launch_stencil_apply2(const PhysicalDesc& g, const double* Mst, const double* Kst, const double* X,

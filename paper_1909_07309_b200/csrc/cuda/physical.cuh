@@ -44,13 +44,6 @@ struct PhysicalDesc {
 cudaError_t launch_physical_assembly(const PhysicalDesc& desc, double* Kst, double* Mst, cudaStream_t st);
 
 /// MX = M_s X and KX = K_s X, X / MX / KX (N_s x n_t) colex (space fastest), on the FP64 tensor cores.
-/// The whole physical mat-vec Y = M_s X (gamma W_t)^T + K_s X (nu M_t)^T in one kernel: the line-pair stencil
-/// kernel with the banded time pass in its epilogue (tw, tm: row band storage, half-bandwidth pt).  Only for a
-/// single time chunk (n_t <= 72) and pair-eligible shapes; cudaErrorNotSupported otherwise (the caller then
-/// runs launch_stencil_apply2 + the banded time pass).
-cudaError_t launch_stencil_apply_time(const PhysicalDesc& desc, const double* Mst, const double* Kst, const double* X,
-                                      double* Y, long long n_t, const double* tw, const double* tm, int pt,
-                                      cudaStream_t st);
 cudaError_t launch_stencil_apply2(const PhysicalDesc& desc, const double* Mst, const double* Kst, const double* X,
                                   double* MX, double* KX, long long n_t, cudaStream_t st);
 

@@ -726,14 +726,8 @@ struct stiga_kronsum_s {
         if (physical) {  // y = M_s X W_t^T + K_s X M_t^T  (solver.cpp:67-70)
             // spatial stencils first, as the reference's mode order (kronop.cpp:75-89): MX = M_s X,
             // KX = K_s X on the tensor cores, then y = MX W_t^T + KX M_t^T in one banded time pass
-            const int d = D - 1;
-            if (band(0).p == band(1).p && x != y) {  // one kernel when the shape allows (time bands in the epilogue)
-                const cudaError_t fe = gpu::launch_stencil_apply_time(pdesc, Mst.p, Kst.p, x, y, dims[d], band(0).band,
-                                                                      band(1).band, band(0).p, st);
-                if (fe == cudaSuccess) return;
-                if (fe != cudaErrorNotSupported) ck(fe, "stencil apply + time bands");
-            }
             ensure_scratch(2);
+            const int d = D - 1;
             ck(gpu::launch_stencil_apply2(pdesc, Mst.p, Kst.p, x, t0.p, t1.p, dims[d], st), "stencil apply");
             ck(gpu::launch_banded_pass(geom(d), t0.p, t1.p, y, nullptr, band(0), band(1), none, none, 0.0, st),
                "time bands");
