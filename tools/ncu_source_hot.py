@@ -1,20 +1,43 @@
 """Summarise an `ncu --page source --csv --print-source sass` export: per-instruction stall samples
-for the first kernel in the file, top-N instructions and the stall mix by opcode."""
+for the K-th kernel in the file (default the first; `all` = every kernel, stall mix only), top-N
+instructions and the stall mix by opcode.
+
+    python tools/ncu_source_hot.py file.csv [top] [kernel index | all]"""
 import collections
 import csv
 import sys
 
 
-def main(path, top=40):
-    rows = list(csv.reader(open(path)))
-    name = rows[0][1] if len(rows[0]) > 1 else "?"
-    hdr = rows[1]
+def split_kernels(rows):
+    """[(name, header, body rows)]: a kernel section starts with a short name row followed by the header."""
+    out, i = [], 0
+    while i < len(rows):
+        if i + 1 < len(rows) and "Source" in rows[i + 1] and "Source" not in rows[i]:
+            name = rows[i][1] if len(rows[i]) > 1 else "?"
+            hdr = rows[i + 1]
+            j = i + 2
+            body = []
+            while j < len(rows) and len(rows[j]) == len(hdr) and "Source" not in rows[j]:
+                body.append(rows[j])
+                j += 1
+            out.append((name, hdr, body))
+            i = j
+        else:
+            i += 1
+    return out
+
+
+def main(path, top=40, which=0):
+    ks = split_kernels(list(csv.reader(open(path))))
+    if which == "all":
+        for k in range(len(ks)):
+            report(*ks[k], top=0)
+        return
+    report(*ks[int(which)], top=top)
+
+
+def report(name, hdr, body, top=40):
     idx = {h: i for i, h in enumerate(hdr)}
-    body = []
-    for r in rows[2:]:
-        if len(r) != len(hdr):
-            break  # next kernel
-        body.append(r)
     stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
     tot = collections.Counter()
     byop = collections.defaultdict(collections.Counter)
@@ -37,6 +60,8 @@ def main(path, top=40):
     for op, c in ops[:15]:
         n = sum(c.values())
         print(f"  {op:10s} {n:8d} {100*n/T:5.1f}%  " + ", ".join(f"{k[6:]}={v}" for k, v in c.most_common(4) if v))
+    if not top:
+        return
     print("hot instructions:")
     hot = sorted(body, key=lambda r: -int(r[idx["Warp Stall Sampling (All Samples)"]] or 0))[:top]
     for r in hot:
@@ -47,4 +72,4 @@ def main(path, top=40):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40, sys.argv[3] if len(sys.argv) > 3 else 0)
